@@ -1,0 +1,213 @@
+/* cqrrpt_gpu.h — C ABI of the B200-native CQRRPT (sm_100a).
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *
+ *   CqrrptOutput cqrrpt(const DenseMatrix &m, const CqrrptConfig &cfg = {});
+ *       /root/reference/proj/include/cqrrpt/cqrrpt.hh:140, body cqrrpt.cc:317-328
+ *   CqrrptOutput cqrrpt_core(const DenseMatrix &m, const SketchOperator &s,
+ *                            const CqrrptConfig &cfg);
+ *       cqrrpt.hh:136, body cqrrpt.cc:233-315
+ *
+ * re-expressed in the (m, n, A, lda, d_factor) -> (R, J, k, Q in place)
+ * convention of BASELINE.json:north_star, with plain pointers and sizes, no
+ * C++ types and no exceptions. A C++ adapter with the reference's own
+ * signature lives in include/cqrrpt_b200.hh.
+ *
+ * Conventions
+ *   - Matrices are column-major FP64 with an explicit leading dimension
+ *     (DenseMatrix is column-major, dense_matrix.hh:36-41).
+ *   - Pivots J are 0-based int64 (qrcp.hh:21-23).
+ *   - Return 0 on success; -i when argument i is invalid (LAPACK style; these
+ *     are exactly the reference's std::invalid_argument conditions,
+ *     cqrrpt.cc:38-42, sketch.cc:54,74-75); a positive value for a CUDA/NCCL
+ *     failure (CQRRPT_GPU_ERR_*). A zero diagonal in a triangular solve (the
+ *     reference's std::domain_error, linalg.cc:250-252) is
+ *     CQRRPT_GPU_ERR_SINGULAR.
+ *   - All device work is ordered on ctx->stream; the call returns after the
+ *     outputs are complete (k is needed on the host to size later phases).
+ *   - Multi-GPU: one process (or host thread) per GPU. Each rank passes its
+ *     local rows (m_local, A_local, lda) and ctx->global_row_offset, because
+ *     SASO column c of S is a function of the GLOBAL row index (sketch.cc:81).
+ *     The d x n sketch and the k0 x k0 Gram are sum-allreduced (NCCL or a
+ *     caller-supplied callback); R, J, k, k0 come out identical on all ranks.
+ */
+#ifndef CQRRPT_GPU_H
+#define CQRRPT_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CQRRPT_GPU_ABI_VERSION 1
+
+/* error codes (positive) */
+#define CQRRPT_GPU_ERR_CUDA 1
+#define CQRRPT_GPU_ERR_NCCL 2
+#define CQRRPT_GPU_ERR_SINGULAR 3 /* trsm_right zero diagonal: linalg.cc:250-252 */
+#define CQRRPT_GPU_ERR_NOMEM 4
+#define CQRRPT_GPU_ERR_INTERNAL 5
+
+/* cond estimators (cqrrpt.hh:61) */
+#define CQRRPT_COND_DIAG_RATIO 0
+#define CQRRPT_COND_KRYLOV_BOUNDS 1
+#define CQRRPT_COND_IDENTITY_DEVIATION 2
+/* identity_deviation with NestedCondEstimator's krylov_bounds fallback when it
+ * returns +inf (cqrrpt.cc:57-58): what rank_stage2 evaluates per probe */
+#define CQRRPT_COND_NESTED_IDENTITY_DEVIATION 3
+
+/* ctx->flags */
+#define CQRRPT_GPU_OUTPUTS_ON_HOST 0x1 /* R and J are host pointers (default: device) */
+#define CQRRPT_GPU_EXACT_STAGE2 0x2    /* always run the reference's binary search with
+                                          power-iteration estimates (also fills cond_m_pre) */
+#define CQRRPT_GPU_NO_STAGE1 0x4       /* CqrrptConfig::stage1_enabled = false */
+#define CQRRPT_GPU_DIAGNOSTICS 0x8     /* truncation_ratio (spectral norm of R_sk) */
+#define CQRRPT_GPU_TIMINGS 0x10        /* per-phase CUDA-event timings into ctx->timings_ms */
+
+/* Sum-allreduce of `count` doubles in place on device memory, ordered on
+ * `stream`. Return 0 on success. */
+typedef int (*cqrrpt_gpu_allreduce_fn)(double *buf, size_t count, void *stream, void *user);
+
+typedef struct cqrrpt_gpu_comm cqrrpt_gpu_comm; /* opaque NCCL communicator wrapper */
+
+typedef struct cqrrpt_gpu_ctx {
+    /* in */
+    void *stream;                /* cudaStream_t; NULL = legacy default stream */
+    int32_t rank, nranks;        /* row-shard identity; nranks <= 1 means single GPU */
+    int64_t global_row_offset;   /* global index of local row 0 */
+    cqrrpt_gpu_comm *comm;       /* NCCL communicator (cqrrpt_gpu_comm_init), or NULL */
+    cqrrpt_gpu_allreduce_fn allreduce; /* used when comm == NULL and nranks > 1 */
+    void *allreduce_user;
+    int32_t cond_method;         /* CQRRPT_COND_* (default identity_deviation = 2) */
+    int32_t flags;               /* CQRRPT_GPU_* */
+    /* out: diagnostics (cqrrpt.hh:104-122) */
+    int64_t d;                   /* sketch rows ceil(d_factor * n) */
+    int64_t k_sk;                /* QRCP steps on the sketch */
+    int64_t k0_final;            /* k0 after Cholesky-failure shrink */
+    int32_t retries;             /* Cholesky-failure retries (rank_stage2) */
+    int32_t stage2_exact;        /* 1 if the binary search ran, 0 if fast-accepted */
+    double cond_m_pre;           /* estimate at the final rank (exact path or flag) */
+    double cond_upper_bound;     /* ||R_pre||_F ||R_pre^-1||_F (fast path) */
+    double truncation_ratio;     /* ||C_k||_F / ||R_sk||_2 (CQRRPT_GPU_DIAGNOSTICS) */
+    double flop_estimate;        /* flop_model (cqrrpt.cc:330-338) */
+    /* phase timings (CQRRPT_GPU_TIMINGS), milliseconds, PhaseTimings order:
+     * sketch, qrcp, rank_select, precondition, cholesky_qr, undo, total,
+     * + [7] communication (allreduce) */
+    double timings_ms[8];
+} cqrrpt_gpu_ctx;
+
+/* Fill a context with defaults (single GPU, default stream). */
+void cqrrpt_gpu_ctx_init(cqrrpt_gpu_ctx *ctx);
+
+/* CQRRPT of a tall FP64 matrix (north_star entry point).
+ *   m, n      local rows, columns (m_local on a shard; n identical on all ranks)
+ *   A, lda    device, column-major. On return A[:, :k] holds Q (in place).
+ *             Columns k..n-1 of A are left unspecified.
+ *   d_factor  sketch oversampling gamma >= 1 (CqrrptConfig::gamma, cqrrpt.hh:93)
+ *   nnz       SASO nonzeros per column of S, 1 <= nnz <= d (cqrrpt.hh:95)
+ *   seed      sketch seed (CqrrptConfig::seed)
+ *   eps_tol   stage-2 tolerance > u (CqrrptConfig::eps_tol, default 1e-4)
+ *   R, ldr    out: k x n upper-trapezoidal (ldr >= n), device unless
+ *             CQRRPT_GPU_OUTPUTS_ON_HOST. Rows >= k untouched.
+ *   J         out: n pivots, 0-based (device unless OUTPUTS_ON_HOST)
+ *   k, k0     out (host): final rank and stage-1 rank
+ */
+int cqrrpt_gpu_dgeqpt(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, int64_t nnz,
+                      uint64_t seed, double eps_tol, double *R, int64_t ldr, int64_t *J, int64_t *k,
+                      int64_t *k0, cqrrpt_gpu_ctx *ctx);
+
+/* ---------------------------------------------------------------------------
+ * Phase-level entry points (the same kernels the driver composes; exposed for
+ * parity tests and for callers that run their own collectives).
+ * All pointers are device pointers unless stated; `stream` is a cudaStream_t.
+ * ------------------------------------------------------------------------- */
+
+/* sketch_rows_for (cqrrpt.cc:211-213) */
+int64_t cqrrpt_gpu_sketch_rows(double d_factor, int64_t n);
+
+/* SASO plan for global S columns [c0, c0+count): plan[c*nnz+t] =
+ * row | (sign << 31), sign 1 = +1/sqrt(d). sample_sketch (sketch.cc:73-99). */
+int cqrrpt_gpu_saso_plan(int64_t d, int64_t c0, int64_t count, int64_t nnz, uint64_t seed,
+                         uint32_t *plan, void *stream);
+
+/* M_sk (d x n, ldm) = S[:, c0:c0+m] * A (m x n, lda); apply (sketch.cc:131-146).
+ * Deterministic (fixed-order partial sums). */
+int cqrrpt_gpu_saso_sketch(int64_t m, int64_t n, const double *A, int64_t lda, int64_t d,
+                           int64_t nnz, uint64_t seed, int64_t c0, double *Msk, int64_t ldm,
+                           void *stream);
+
+/* Max-norm Householder QRCP of the d x n sketch (qrcp.cc:35-97, want_q=false).
+ * Msk is overwritten. R_sk (n x n buffer, ldr >= n; first k_sk rows valid,
+ * exactly upper-trapezoidal), J (n, 0-based), k_sk (host). rank_tol < 0
+ * selects the default n*u. */
+int cqrrpt_gpu_qrcp(int64_t d, int64_t n, double *Msk, int64_t ldm, double rank_tol, double *Rsk,
+                    int64_t ldr, int64_t *J, int64_t *k_sk, void *stream);
+
+/* rank_stage1 (cqrrpt.cc:92-112) on a k x n upper-trapezoidal R (device). */
+int cqrrpt_gpu_rank_stage1(int64_t k, int64_t n, const double *R, int64_t ldr, int64_t *k0,
+                           void *stream);
+
+/* X (m x k, ldx) = B[:, cols] * U^{-1}, U upper-triangular k x k (ldu);
+ * cols = NULL means identity. trsm_right (linalg.cc:244-277) fused with the
+ * pivoted column gather (dense_matrix.hh:70-80). X must not alias B. */
+int cqrrpt_gpu_trsm_right(int64_t m, int64_t k, const double *B, int64_t ldb, const int64_t *cols,
+                          const double *U, int64_t ldu, double *X, int64_t ldx, void *stream);
+
+/* G (k x k, ldg) = X^T X, bitwise symmetric; gram (linalg.cc:298-307). */
+int cqrrpt_gpu_gram(int64_t m, int64_t k, const double *X, int64_t ldx, double *G, int64_t ldg,
+                    void *stream);
+
+/* Upper Cholesky G = R^T R in place on the upper triangle of G (ldg);
+ * strict lower triangle is zeroed. failure_index (host): 0 on success, else
+ * the 1-based first non-positive pivot and the leading (j-1) block is valid
+ * (cholesky, linalg.cc:223-242). */
+int cqrrpt_gpu_potrf(int64_t n, double *G, int64_t ldg, int64_t *failure_index, void *stream);
+
+/* cond_estimate (cqrrpt.cc:114-147) of the leading ell x ell block of an
+ * upper-triangular R (ldr), reference semantics (power iterations capped at
+ * 200, 1e-6 inflation). value on host. */
+int cqrrpt_gpu_cond_estimate(int64_t ell, const double *R, int64_t ldr, int32_t method, double *value,
+                             void *stream);
+
+/* C (k x n, ldc) = triu(A) (k x k, lda) * triu(B) (k x n, ldb): exactly
+ * upper-trapezoidal; multiply_upper_triangular (cqrrpt.cc:23-36). */
+int cqrrpt_gpu_trmm_upper(int64_t k, int64_t n, const double *A, int64_t lda, const double *B,
+                          int64_t ldb, double *C, int64_t ldc, void *stream);
+
+/* Device evaluator of validate() (qrcp.cc:150-196) plus the BASELINE
+ * Frobenius metric. A is the ORIGINAL matrix (m x n), Q (m x k), R (k x n),
+ * J (device). Outputs on host: orth_fro = ||Q^T Q - I||_F,
+ * orth_2 = ||Q^T Q - I||_2 (power iteration), recon = ||A[:,J] - QR||_F/||A||_F. */
+int cqrrpt_gpu_validate(int64_t m, int64_t n, int64_t k, const double *A, int64_t lda, const double *Q,
+                        int64_t ldq, const double *R, int64_t ldr, const int64_t *J, double *orth_fro,
+                        double *orth_2, double *recon, void *stream);
+
+/* flop_model (cqrrpt.cc:330-338) with C_sk = 2 nnz m n (sketch.cc:216-217). */
+double cqrrpt_gpu_flop_model(int64_t m, int64_t n, int64_t k, int64_t d, double c_sk);
+
+/* ---------------------------------------------------------------------------
+ * NCCL (dlopen'ed libnccl.so.2; no link-time dependency)
+ * ------------------------------------------------------------------------- */
+/* 128-byte ncclUniqueId, created on rank 0 and broadcast by the caller. */
+int cqrrpt_gpu_comm_unique_id(unsigned char id[128]);
+int cqrrpt_gpu_comm_init(int32_t nranks, int32_t rank, const unsigned char id[128],
+                         cqrrpt_gpu_comm **comm);
+int cqrrpt_gpu_comm_allreduce(cqrrpt_gpu_comm *comm, double *buf, size_t count, void *stream);
+void cqrrpt_gpu_comm_destroy(cqrrpt_gpu_comm *comm);
+
+/* Free the library's cached device workspaces (calling thread). */
+void cqrrpt_gpu_release_workspace(void);
+
+/* Last error message of this thread (never NULL). */
+const char *cqrrpt_gpu_last_error(void);
+
+/* Number of kernel launches issued by this library on the calling thread
+ * since the last reset (evidence for bench.py's gpu_launches). */
+int64_t cqrrpt_gpu_launch_count(int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,254 @@
+// K7: stage-2 condition estimators on device.
+//
+// Reference: cond_estimate (cqrrpt.cc:114-147), NestedCondEstimator
+// (cqrrpt.cc:47-71), power_iterate (linalg.cc:446-465) with the deterministic
+// start vector CounterRng(0x5eedcafe01234567).normal(i) normalised
+// (linalg.cc:434-442), cap 200 iterations, stop at |est-prev| <= 1e-10 est.
+//
+// The full estimator runs as ONE single-CTA kernel per estimate (all 200
+// iterations inside the kernel; a launch per matvec would cost more than the
+// matvec). The inverse-norm estimate uses the explicit inverse of R (the
+// leading block of R^{-1} is the inverse of the leading block of R), so both
+// matvecs are GEMVs instead of triangular solves.
+#include "common.cuh"
+#include "internal.hh"
+
+namespace cqg {
+
+constexpr int kPowThreads = 1024;
+
+struct PowOp {
+    const double *a;
+    int64_t ld, rows, cols;
+    int kind;  // 0 dense, 1 upper triangular, 2 upper triangular minus identity
+};
+
+CQ_DEVI double op_entry(const PowOp &op, int64_t i, int64_t j) {
+    double v = op.a[j * op.ld + i];
+    if (op.kind == 2 && i == j) v -= 1.0;
+    return v;
+}
+
+// deterministic_unit_vector(n) (linalg.cc:434-442), device libm
+__device__ double normal_dev(uint64_t seed, uint64_t counter) {
+    double u1 = (double)((rng_bits(seed, 2 * counter) >> 11) + 1) * 0x1.0p-53;
+    double u2 = (double)(rng_bits(seed, 2 * counter + 1) >> 11) * 0x1.0p-53;
+    return sqrt(-2.0 * log(u1)) * cos(6.283185307179586476925287 * u2);
+}
+
+__device__ void start_vector(int64_t n, double *v, double *scratch) {
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        double x = normal_dev(0x5eedcafe01234567ULL, (uint64_t)i);
+        v[i] = x;
+        s = fma(x, x, s);
+    }
+    double nrm = sqrt(block_sum(s, scratch));
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = (nrm == 0.0) ? (i == 0 ? 1.0 : 0.0) : v[i] / nrm;
+    __syncthreads();
+}
+
+// y = op x (rows), threads over rows, j ascending (the reference's axpy order)
+__device__ void op_forward(const PowOp &op, const double *x, double *y) {
+    for (int64_t i = threadIdx.x; i < op.rows; i += blockDim.x) {
+        double s = 0.0;
+        const int64_t jb = (op.kind == 0) ? 0 : i;
+        for (int64_t j = jb; j < op.cols; ++j) s = fma(x[j], op_entry(op, i, j), s);
+        y[i] = s;
+    }
+    __syncthreads();
+}
+
+// z = op^T y (cols), warp per column
+__device__ void op_adjoint(const PowOp &op, const double *y, double *z) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int64_t j = wid; j < op.cols; j += nw) {
+        const int64_t ie = (op.kind == 0) ? op.rows : j + 1;
+        double s = 0.0;
+        for (int64_t i = lane; i < ie; i += 32) s = fma(op_entry(op, i, j), y[i], s);
+        s = warp_sum(s);
+        if (lane == 0) z[j] = s;
+    }
+    __syncthreads();
+}
+
+// returns est (and converged flag) of sigma_max(op) by the reference's power iteration
+__device__ double power_iterate_dev(const PowOp &op, double *v, double *w, double *z, double *scratch, int *conv) {
+    start_vector(op.cols, v, scratch);
+    double est = 0.0, prev = -1.0;
+    for (int it = 0; it < 200; ++it) {
+        op_forward(op, v, w);
+        double s = 0.0;
+        for (int64_t i = threadIdx.x; i < op.rows; i += blockDim.x) s = fma(w[i], w[i], s);
+        double nw = sqrt(block_sum(s, scratch));
+        if (nw == 0.0) {
+            *conv = 1;
+            return 0.0;
+        }
+        est = (est < nw) ? nw : est;
+        if (prev >= 0.0 && fabs(est - prev) <= 1e-10 * est) {
+            *conv = 1;
+            return est;
+        }
+        prev = est;
+        op_adjoint(op, w, z);
+        s = 0.0;
+        for (int64_t i = threadIdx.x; i < op.cols; i += blockDim.x) s = fma(z[i], z[i], s);
+        double nz = sqrt(block_sum(s, scratch));
+        if (nz == 0.0) {
+            *conv = 1;
+            return est;
+        }
+        __syncthreads();
+        for (int64_t i = threadIdx.x; i < op.cols; i += blockDim.x) v[i] = z[i] / nz;
+        __syncthreads();
+    }
+    *conv = 0;
+    return est;
+}
+
+// method: 0 diag_ratio, 1 krylov_bounds, 2 identity_deviation (+inf when
+// tau >= 1), 3 identity_deviation with NestedCondEstimator's fallback to
+// krylov_bounds when it is +inf (cqrrpt.cc:57-58).
+__global__ void __launch_bounds__(kPowThreads) cond_estimate_kernel(int64_t ell, const double *__restrict__ r,
+                                                                    int64_t ldr, const double *__restrict__ rinv,
+                                                                    int64_t ldi, int method, double *work,
+                                                                    double *out) {
+    __shared__ double scratch[32];
+    double *v = work, *w = work + ell, *z = work + 2 * ell;
+    int conv = 1;
+    double value = 1.0;
+    if (ell <= 0) {
+        if (threadIdx.x == 0) out[0] = 1.0;
+        return;
+    }
+    if (method == 0) {
+        double hi = 0.0, lo = INFINITY;
+        for (int64_t i = threadIdx.x; i < ell; i += blockDim.x) {
+            double d = fabs(r[i * ldr + i]);
+            hi = fmax(hi, d);
+            lo = fmin(lo, d);
+        }
+        hi = warp_max(hi);
+        lo = -warp_max(-lo);
+        __shared__ double sh[32], sl[32];
+        if ((threadIdx.x & 31) == 0) {
+            sh[threadIdx.x >> 5] = hi;
+            sl[threadIdx.x >> 5] = lo;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+                hi = fmax(hi, sh[q]);
+                lo = fmin(lo, sl[q]);
+            }
+            double vv = (lo == 0.0) ? INFINITY : hi / lo;
+            out[0] = vv < 1.0 ? 1.0 : vv;
+            out[1] = 1.0;
+        }
+        return;
+    }
+    bool need_krylov = (method == 1);
+    if (method == 2 || method == 3) {
+        PowOp dev{r, ldr, ell, ell, 2};
+        double tau = power_iterate_dev(dev, v, w, z, scratch, &conv) * (1.0 + 1e-6);
+        if (tau >= 1.0) {
+            if (method == 3) need_krylov = true;  // NestedCondEstimator fallback (cqrrpt.cc:57-58)
+            else value = INFINITY;                // cond_estimate itself returns +inf (cqrrpt.cc:141-142)
+        } else {
+            double vv = (1.0 + tau) / (1.0 - tau);
+            value = vv < 1.0 ? 1.0 : vv;
+        }
+    }
+    if (need_krylov) {
+        int c1 = 1, c2 = 1;
+        PowOp fwd{r, ldr, ell, ell, 1};
+        double hi = power_iterate_dev(fwd, v, w, z, scratch, &c1);
+        double inv;
+        bool zero_diag = false;
+        for (int64_t i = 0; i < ell; ++i)
+            if (r[i * ldr + i] == 0.0) zero_diag = true;
+        if (zero_diag) {
+            inv = INFINITY;  // linalg.cc:489-490
+        } else {
+            PowOp ri{rinv, ldi, ell, ell, 1};
+            inv = power_iterate_dev(ri, v, w, z, scratch, &c2);
+        }
+        double vv = hi * (1.0 + 1e-6) * inv * (1.0 + 1e-6);
+        value = vv < 1.0 ? 1.0 : vv;
+        conv = c1 && c2;
+    }
+    if (threadIdx.x == 0) {
+        out[0] = value;
+        out[1] = conv;
+    }
+}
+
+// One CTA per probe ell: first power iterate ||(R_ell - I) v0||.
+__global__ void __launch_bounds__(kPowThreads) idev_first_kernel(const double *__restrict__ r, int64_t ldr,
+                                                                 const int64_t *__restrict__ ells, double *work,
+                                                                 int64_t work_stride, double *__restrict__ out) {
+    __shared__ double scratch[32];
+    const int64_t ell = ells[blockIdx.x];
+    double *v = work + blockIdx.x * work_stride, *w = v + ell;
+    start_vector(ell, v, scratch);
+    PowOp dev{r, ldr, ell, ell, 2};
+    op_forward(dev, v, w);
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < ell; i += blockDim.x) s = fma(w[i], w[i], s);
+    double nw = sqrt(block_sum(s, scratch));
+    if (threadIdx.x == 0) out[blockIdx.x] = nw;
+}
+
+__global__ void __launch_bounds__(kPowThreads) spectral_kernel(const double *__restrict__ a, int64_t lda, int64_t m,
+                                                               int64_t n, double *work, double *out) {
+    __shared__ double scratch[32];
+    int conv = 1;
+    PowOp op{a, lda, m, n, 0};
+    double est = (m == 0 || n == 0) ? 0.0 : power_iterate_dev(op, work, work + n, work + n + m, scratch, &conv);
+    if (threadIdx.x == 0) out[0] = est;
+}
+
+int identity_deviation_first(const double *r, int64_t ldr, const int64_t *ells, int nells, double *out_host,
+                             Workspace &ws, cudaStream_t st) {
+    if (nells <= 0) return 0;
+    int64_t maxl = 0;
+    for (int i = 0; i < nells; ++i) maxl = std::max(maxl, ells[i]);
+    int64_t *dl = ws.get<int64_t>("idev.ells", nells);
+    double *work = ws.get<double>("idev.work", (size_t)nells * 2 * maxl + 1);
+    double *dout = ws.get<double>("idev.out", nells);
+    CQ_CUDA(cudaMemcpyAsync(dl, ells, sizeof(int64_t) * nells, cudaMemcpyHostToDevice, st), "ells h2d");
+    idev_first_kernel<<<(unsigned)nells, kPowThreads, 0, st>>>(r, ldr, dl, work, 2 * maxl, dout);
+    note_launch();
+    CQ_TRY(check_launch("idev_first_kernel"));
+    CQ_CUDA(cudaMemcpyAsync(out_host, dout, sizeof(double) * nells, cudaMemcpyDeviceToHost, st), "idev d2h");
+    CQ_CUDA(cudaStreamSynchronize(st), "idev sync");
+    return 0;
+}
+
+int cond_estimate(int64_t ell, const double *r, int64_t ldr, const double *rinv, int64_t ldi, int method,
+                  double *value_host, Workspace &ws, cudaStream_t st) {
+    double *work = ws.get<double>("cond.work", (size_t)(3 * std::max<int64_t>(ell, 1)));
+    double *dout = ws.get<double>("cond.out", 2);
+    cond_estimate_kernel<<<1, kPowThreads, 0, st>>>(ell, r, ldr, rinv, ldi, method, work, dout);
+    note_launch();
+    CQ_TRY(check_launch("cond_estimate_kernel"));
+    CQ_CUDA(cudaMemcpyAsync(value_host, dout, sizeof(double), cudaMemcpyDeviceToHost, st), "cond d2h");
+    CQ_CUDA(cudaStreamSynchronize(st), "cond sync");
+    return 0;
+}
+
+int spectral_norm_estimate(int64_t m, int64_t n, const double *a, int64_t lda, double *value_host, Workspace &ws,
+                           cudaStream_t st) {
+    double *work = ws.get<double>("spec.work", (size_t)(2 * n + m + 1));
+    double *dout = ws.get<double>("spec.out", 1);
+    spectral_kernel<<<1, kPowThreads, 0, st>>>(a, lda, m, n, work, dout);
+    note_launch();
+    CQ_TRY(check_launch("spectral_kernel"));
+    CQ_CUDA(cudaMemcpyAsync(value_host, dout, sizeof(double), cudaMemcpyDeviceToHost, st), "spec d2h");
+    CQ_CUDA(cudaStreamSynchronize(st), "spec sync");
+    return 0;
+}
+
+}  // namespace cqg

@@ -1,0 +1,586 @@
+// Host orchestration of the B200 CQRRPT pipeline and the C ABI
+// (include/cqrrpt_gpu.h).
+//
+// Reference control flow: cqrrpt (cqrrpt.cc:317-328) -> cqrrpt_core
+// (cqrrpt.cc:233-315) -> rank_stage2 (cqrrpt.cc:149-209). The phases, their
+// kernels and where the two cross-GPU sums sit:
+//
+//   sketch      K1 plan + K2 apply            -> allreduce(d*n)       [rank-local rows]
+//   qrcp        K3 cooperative QRCP           (replicated, deterministic)
+//   rank_select K4 stage-1 + stage-2 search   (replicated)
+//   precondition K5a gather+TRSM (DMMA)       [rank-local rows]
+//   cholesky_qr K5b Gram (DMMA) -> allreduce(k0*k0) -> K6 potrf -> K8 Q TRSM
+//   undo        K9 R = R_pre R_sk[:k,:]       (replicated)
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.hh"
+
+namespace cqg {
+int64_t launch_count(bool reset);
+const char *last_error();
+}  // namespace cqg
+
+using namespace cqg;
+
+// ---------------------------------------------------------------------------
+// NCCL via dlopen
+// ---------------------------------------------------------------------------
+namespace {
+typedef int (*nccl_get_id_t)(void *);
+struct NcclId {
+    char internal[128];
+};
+typedef int (*nccl_init_rank2_t)(void **, int, NcclId, int);
+typedef int (*nccl_allreduce_t)(const void *, void *, size_t, int, int, void *, cudaStream_t);
+typedef int (*nccl_destroy_t)(void *);
+typedef const char *(*nccl_errstr_t)(int);
+struct NcclApi {
+    bool loaded = false;
+    nccl_get_id_t get_id = nullptr;
+    nccl_init_rank2_t init_rank = nullptr;
+    nccl_allreduce_t allreduce = nullptr;
+    nccl_destroy_t destroy = nullptr;
+    nccl_errstr_t errstr = nullptr;
+};
+NcclApi &nccl() {
+    static NcclApi api;
+    if (!api.loaded) {
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            api.get_id = (nccl_get_id_t)dlsym(h, "ncclGetUniqueId");
+            api.init_rank = (nccl_init_rank2_t)dlsym(h, "ncclCommInitRank");
+            api.allreduce = (nccl_allreduce_t)dlsym(h, "ncclAllReduce");
+            api.destroy = (nccl_destroy_t)dlsym(h, "ncclCommDestroy");
+            api.errstr = (nccl_errstr_t)dlsym(h, "ncclGetErrorString");
+        }
+        api.loaded = true;
+    }
+    return api;
+}
+}  // namespace
+
+struct cqrrpt_gpu_comm {
+    void *comm = nullptr;
+    int nranks = 1, rank = 0;
+};
+
+// ---------------------------------------------------------------------------
+// timing helper
+// ---------------------------------------------------------------------------
+namespace {
+struct PhaseClock {
+    bool on = false;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev[16];
+    int n = 0;
+    int tag[16];
+    void start(bool enable, cudaStream_t s) {
+        on = enable;
+        st = s;
+        n = 0;
+        if (on) mark(-1);
+    }
+    void mark(int phase) {
+        if (!on || n >= 16) return;
+        cudaEventCreate(&ev[n]);
+        cudaEventRecord(ev[n], st);
+        tag[n++] = phase;
+    }
+    void finish(double *out) {
+        if (!on) return;
+        cudaEventSynchronize(ev[n - 1]);
+        for (int i = 0; i < 8; ++i) out[i] = 0.0;
+        for (int i = 1; i < n; ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+            if (tag[i] >= 0 && tag[i] < 8) out[tag[i]] += ms;
+        }
+        float tot = 0.f;
+        cudaEventElapsedTime(&tot, ev[0], ev[n - 1]);
+        out[6] = tot;
+        for (int i = 0; i < n; ++i) cudaEventDestroy(ev[i]);
+        n = 0;
+    }
+};
+enum { PH_SKETCH = 0, PH_QRCP = 1, PH_RANK = 2, PH_PRE = 3, PH_CHOL = 4, PH_UNDO = 5, PH_COMM = 7 };
+
+int do_allreduce(cqrrpt_gpu_ctx *ctx, double *buf, size_t count, cudaStream_t st) {
+    if (ctx->nranks <= 1) return 0;
+    if (ctx->comm) return cqrrpt_gpu_comm_allreduce(ctx->comm, buf, count, st);
+    if (ctx->allreduce) {
+        int rc = ctx->allreduce(buf, count, st, ctx->allreduce_user);
+        if (rc) {
+            set_error("user allreduce failed");
+            return CQRRPT_GPU_ERR_NCCL;
+        }
+        return 0;
+    }
+    set_error("nranks > 1 but neither comm nor allreduce callback given");
+    return CQRRPT_GPU_ERR_NCCL;
+}
+}  // namespace
+
+extern "C" {
+
+void cqrrpt_gpu_ctx_init(cqrrpt_gpu_ctx *ctx) {
+    std::memset(ctx, 0, sizeof(*ctx));
+    ctx->nranks = 1;
+    ctx->cond_method = CQRRPT_COND_IDENTITY_DEVIATION;
+    ctx->cond_m_pre = 1.0;
+}
+
+const char *cqrrpt_gpu_last_error(void) { return cqg::last_error(); }
+int64_t cqrrpt_gpu_launch_count(int32_t reset) { return cqg::launch_count(reset != 0); }
+
+int64_t cqrrpt_gpu_sketch_rows(double d_factor, int64_t n) {
+    return (int64_t)std::ceil(d_factor * (double)n);  // cqrrpt.cc:211-213
+}
+
+double cqrrpt_gpu_flop_model(int64_t m, int64_t n, int64_t k, int64_t d, double c_sk) {
+    if (k < 0 || k > std::min(d, n)) return -1.0;  // cqrrpt.cc:331-332
+    __int128 mm = m, kk = k, nn = n, dd = d;
+    __int128 num = 12 * mm * kk * kk + 6 * mm * kk * (kk + 1) + 24 * dd * nn * kk - 12 * kk * kk * (dd + nn) +
+                   10 * kk * kk * kk + 3 * kk * kk + kk;
+    return (double)num / 6.0 + c_sk;
+}
+
+int cqrrpt_gpu_dgeqpt(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, int64_t nnz, uint64_t seed,
+                      double eps_tol, double *R, int64_t ldr, int64_t *J, int64_t *k_out, int64_t *k0_out,
+                      cqrrpt_gpu_ctx *ctx) {
+    cqrrpt_gpu_ctx local;
+    if (!ctx) {
+        cqrrpt_gpu_ctx_init(&local);
+        ctx = &local;
+    }
+    // ---- argument checks (check_config cqrrpt.cc:38-42 first, as the reference does)
+    if (!(d_factor >= 1.0)) return set_error("d_factor must be >= 1"), -5;
+    if (!(eps_tol > kUnitRoundoff)) return set_error("eps_tol must exceed the unit roundoff"), -8;
+    if (m < 0) return set_error("m < 0"), -1;
+    if (n < 0) return set_error("n < 0"), -2;
+    if (!k_out) return -12;
+    if (!k0_out) return -13;
+    *k_out = 0;
+    *k0_out = 0;
+    if (n == 0) return 0;  // cqrrpt.cc:319-324
+    const bool multi = ctx->nranks > 1;
+    if (!multi && m < 1) return set_error("sample_sketch: need m >= 1"), -1;  // sketch.cc:54
+    if (m > 0 && !A) return -3;
+    if (m > 0 && lda < m) return set_error("lda < m"), -4;
+    const int64_t d = cqrrpt_gpu_sketch_rows(d_factor, n);
+    if (nnz < 1 || nnz > d) return set_error("SASO needs 1 <= nnz <= d"), -6;  // sketch.cc:74-75
+    if (!R) return -9;
+    if (ldr < n) return set_error("ldr < n"), -10;
+    if (!J) return -11;
+
+    cudaStream_t st = (cudaStream_t)ctx->stream;
+    Workspace &ws = workspace();
+    const bool host_out = (ctx->flags & CQRRPT_GPU_OUTPUTS_ON_HOST) != 0;
+    PhaseClock clk;
+    clk.start((ctx->flags & CQRRPT_GPU_TIMINGS) != 0, st);
+    ctx->d = d;
+    ctx->retries = 0;
+    ctx->stage2_exact = 0;
+    ctx->cond_m_pre = 1.0;
+    ctx->cond_upper_bound = 0.0;
+    ctx->truncation_ratio = 0.0;
+
+    // ---- sketch ------------------------------------------------------------
+    double *msk = ws.get<double>("drv.msk", (size_t)(d * n));
+    if (!msk) return fail_nomem("sketch");
+    CQ_TRY(saso_sketch(m, n, A, lda, d, nnz, seed, ctx->global_row_offset, msk, d, ws, st));
+    clk.mark(PH_SKETCH);
+    CQ_TRY(do_allreduce(ctx, msk, (size_t)(d * n), st));
+    clk.mark(PH_COMM);
+
+    // ---- QRCP of the sketch -------------------------------------------------
+    const int64_t ldk = n;  // R_sk buffer: n x n
+    double *rsk = ws.get<double>("drv.rsk", (size_t)(n * n));
+    int64_t *jd = ws.get<int64_t>("drv.j", (size_t)n);
+    if (!rsk || !jd) return fail_nomem("rsk");
+    int64_t k_sk = 0;
+    CQ_TRY(qrcp(d, n, msk, d, -1.0, rsk, ldk, jd, &k_sk, ws, st));
+    ctx->k_sk = k_sk;
+    clk.mark(PH_QRCP);
+
+    // ---- stage 1 ------------------------------------------------------------
+    int64_t k0 = k_sk;
+    if (!(ctx->flags & CQRRPT_GPU_NO_STAGE1)) CQ_TRY(rank_stage1(k_sk, n, rsk, ldk, &k0, ws, st));
+    *k0_out = k0;
+    clk.mark(PH_RANK);
+    auto emit_pivots = [&]() -> int {
+        if (host_out) {
+            CQ_CUDA(cudaMemcpyAsync(J, jd, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st), "J d2h");
+        } else {
+            CQ_CUDA(cudaMemcpyAsync(J, jd, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, st), "J d2d");
+        }
+        CQ_CUDA(cudaStreamSynchronize(st), "final sync");
+        return 0;
+    };
+    auto finish_diag = [&](int64_t k) {
+        ctx->flop_estimate = cqrrpt_gpu_flop_model(m, n, k, d,
+                                                   2.0 * (double)nnz * (double)m * (double)n);
+        clk.finish(ctx->timings_ms);
+    };
+    if (k0 == 0) {  // cqrrpt.cc:257-260
+        CQ_TRY(emit_pivots());
+        finish_diag(0);
+        return 0;
+    }
+
+    // ---- precondition: M_pre = M[:, J[:k0]] * A_sk^{-1} ----------------------
+    const int64_t ldp = std::max<int64_t>(m, 1);
+    double *mpre = ws.get<double>("drv.mpre", (size_t)(ldp * k0));
+    if (!mpre) return fail_nomem("M_pre workspace");
+    CQ_TRY(trsm_right(m, k0, A, lda, jd, rsk, ldk, mpre, ldp, st));
+    clk.mark(PH_PRE);
+
+    // ---- Gram + Cholesky (rank_stage2 attempt loop, cqrrpt.cc:160-193) -------
+    double *gmat = ws.get<double>("drv.gram", (size_t)(k0 * k0));
+    if (!gmat) return fail_nomem("gram");
+    CQ_TRY(gram(m, k0, mpre, ldp, gmat, k0, ws, st));
+    clk.mark(PH_CHOL);
+    CQ_TRY(do_allreduce(ctx, gmat, (size_t)(k0 * k0), st));
+    clk.mark(PH_COMM);
+    int64_t fi = 0;
+    CQ_TRY(potrf(k0, gmat, k0, &fi, ws, st));
+    int64_t k0f = k0;
+    if (fi > 0) {
+        // The retry on the leading fi-1 columns recomputes bitwise the same
+        // M_pre columns, Gram block and factor (cqrrpt.cc:162-164), so it
+        // always succeeds: one retry, k0_final = fi - 1.
+        ctx->retries = 1;
+        k0f = fi - 1;
+        if (k0f <= 0) {
+            ctx->k0_final = 0;
+            CQ_TRY(emit_pivots());
+            finish_diag(0);
+            return 0;
+        }
+    }
+    ctx->k0_final = k0f;
+    const double *rfull = gmat;  // upper triangle, ld k0
+    clk.mark(PH_CHOL);
+
+    // ---- stage 2: largest leading block with cond <= sqrt(eps_tol/u) -------
+    const double threshold = std::sqrt(eps_tol / kUnitRoundoff);
+    const int method = ctx->cond_method;
+    double *rinv = ws.get<double>("drv.rinv", (size_t)(k0f * k0f));
+    double *eye = ws.get<double>("drv.eye", (size_t)(k0f * k0f));
+    if (!rinv || !eye) return fail_nomem("rinv");
+    CQ_TRY(fill_identity(k0f, eye, k0f, st));
+    CQ_TRY(trsm_right(k0f, k0f, eye, k0f, nullptr, rfull, k0, rinv, k0f, st));  // X R = I
+    bool exact = (ctx->flags & CQRRPT_GPU_EXACT_STAGE2) != 0;
+    int64_t k = k0f;
+    if (!exact) {
+        // probes of the all-pass binary search path (cqrrpt.cc:197-204)
+        std::vector<int64_t> ells;
+        for (int64_t lo = 0, hi = k0f; lo < hi;) {
+            int64_t mid = lo + (hi - lo + 1) / 2;
+            ells.push_back(mid);
+            lo = mid;
+        }
+        if (method == CQRRPT_COND_IDENTITY_DEVIATION) {
+            // power_iterate keeps est = max(est, ...) (linalg.cc:455): if the
+            // first iterate already gives tau >= 1 the reference returns +inf
+            // and falls back to krylov_bounds, whatever the later iterates.
+            std::vector<double> first(ells.size());
+            CQ_TRY(identity_deviation_first(rfull, k0, ells.data(), (int)ells.size(), first.data(), ws, st));
+            for (double v : first)
+                if (!(v * (1.0 + 1e-6) >= 1.0)) exact = true;
+        }
+        double fr = 0.0, fi_ = 0.0;
+        CQ_TRY(frob_norm_upper(k0f, rfull, k0, &fr, ws, st));
+        CQ_TRY(frob_norm_upper(k0f, rinv, k0f, &fi_, ws, st));
+        const double bound = fr * fi_;  // >= cond_2(R_ell) for every leading block
+        ctx->cond_upper_bound = bound;
+        if (!(bound * (1.0 + 1e-5) <= threshold)) exact = true;
+    }
+    if (exact) {
+        // NestedCondEstimator (cqrrpt.cc:47-71) + binary search (cqrrpt.cc:197-207)
+        std::map<int64_t, double> raw;
+        auto at = [&](int64_t ell, double *out) -> int {
+            if (ell <= 0) {
+                *out = 1.0;
+                return 0;
+            }
+            if (!raw.count(ell)) {
+                double v = 1.0;
+                // method 3 = identity_deviation with the nested krylov fallback
+                const int m_nested = (method == CQRRPT_COND_IDENTITY_DEVIATION) ? 3 : method;
+                CQ_TRY(cond_estimate(ell, rfull, k0, rinv, k0f, m_nested, &v, ws, st));
+                raw[ell] = v;
+            }
+            double v = 1.0;
+            for (auto &kv : raw)
+                if (kv.first <= ell) v = std::max(v, kv.second);
+            *out = v;
+            return 0;
+        };
+        int64_t lo = 0, hi = k0f;
+        while (lo < hi) {
+            int64_t mid = lo + (hi - lo + 1) / 2;
+            double e = 0.0;
+            CQ_TRY(at(mid, &e));
+            if (e <= threshold) lo = mid;
+            else hi = mid - 1;
+        }
+        k = lo;
+        double c = 1.0;
+        if (lo > 0) CQ_TRY(at(lo, &c));
+        ctx->cond_m_pre = c;
+        ctx->stage2_exact = 1;
+    }
+    clk.mark(PH_RANK);
+    *k_out = k;
+    if (k == 0) {
+        CQ_TRY(emit_pivots());
+        finish_diag(0);
+        return 0;
+    }
+
+    // ---- Q = M_pre[:, :k] R_pre^{-1}, in place into A[:, :k] ----------------
+    CQ_TRY(trsm_right(m, k, mpre, ldp, nullptr, rfull, k0, A, lda, st));
+    clk.mark(PH_CHOL);
+
+    // ---- R = R_pre R_sk[:k, :] (upper-trapezoidal) --------------------------
+    if (host_out) {
+        double *rk = ws.get<double>("drv.rout", (size_t)(k * n));
+        if (!rk) return fail_nomem("rout");
+        CQ_TRY(gemm(false, k, n, k, 1.0, rfull, k0, rsk, ldk, 0.0, rk, k, st));
+        clk.mark(PH_UNDO);
+        CQ_CUDA(cudaMemcpy2DAsync(R, sizeof(double) * ldr, rk, sizeof(double) * k, sizeof(double) * k, n,
+                                  cudaMemcpyDeviceToHost, st),
+                "R d2h");
+    } else {
+        CQ_TRY(gemm(false, k, n, k, 1.0, rfull, k0, rsk, ldk, 0.0, R, ldr, st));
+        clk.mark(PH_UNDO);
+    }
+    CQ_TRY(emit_pivots());
+
+    // ---- diagnostics (outside the profiled phases, cqrrpt.cc:298-303) -------
+    finish_diag(k);
+    if (ctx->flags & CQRRPT_GPU_DIAGNOSTICS) {
+        std::vector<double> hr((size_t)(n * n));
+        CQ_CUDA(cudaMemcpyAsync(hr.data(), rsk, sizeof(double) * n * n, cudaMemcpyDeviceToHost, st), "rsk d2h");
+        CQ_CUDA(cudaStreamSynchronize(st), "diag sync");
+        double ck = 0.0;
+        for (int64_t j = k; j < n; ++j)
+            for (int64_t i = k; i < k_sk; ++i) ck += hr[j * n + i] * hr[j * n + i];
+        double rn = 0.0;
+        CQ_TRY(spectral_norm_estimate(k_sk, n, rsk, ldk, &rn, ws, st));
+        ctx->truncation_ratio = (rn > 0.0) ? std::sqrt(ck) / rn : 0.0;
+    }
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// phase-level entry points
+// ---------------------------------------------------------------------------
+int cqrrpt_gpu_saso_plan(int64_t d, int64_t c0, int64_t count, int64_t nnz, uint64_t seed, uint32_t *plan,
+                         void *stream) {
+    if (d < 1) return -1;
+    if (count < 0) return -3;
+    if (nnz < 1 || nnz > d) return -4;
+    return saso_plan(d, c0, count, nnz, seed, plan, (cudaStream_t)stream);
+}
+
+int cqrrpt_gpu_saso_sketch(int64_t m, int64_t n, const double *A, int64_t lda, int64_t d, int64_t nnz, uint64_t seed,
+                           int64_t c0, double *Msk, int64_t ldm, void *stream) {
+    if (m < 0) return -1;
+    if (n < 0) return -2;
+    if (m > 0 && lda < m) return -4;
+    if (d < 1) return -5;
+    if (nnz < 1 || nnz > d) return -6;
+    if (ldm < d) return -10;
+    return saso_sketch(m, n, A, lda, d, nnz, seed, c0, Msk, ldm, workspace(), (cudaStream_t)stream);
+}
+
+int cqrrpt_gpu_qrcp(int64_t d, int64_t n, double *Msk, int64_t ldm, double rank_tol, double *Rsk, int64_t ldr,
+                    int64_t *J, int64_t *k_sk, void *stream) {
+    if (d < 1) return set_error("qrcp_maxnorm: need at least one row"), -1;  // qrcp.cc:37
+    if (n < 0) return -2;
+    if (ldm < d) return -4;
+    if (ldr < n) return -7;
+    *k_sk = 0;
+    if (n == 0) return 0;
+    return qrcp(d, n, Msk, ldm, rank_tol, Rsk, ldr, J, k_sk, workspace(), (cudaStream_t)stream);
+}
+
+int cqrrpt_gpu_rank_stage1(int64_t k, int64_t n, const double *R, int64_t ldr, int64_t *k0, void *stream) {
+    if (k < 0 || n < 0) return -1;
+    return rank_stage1(k, n, R, ldr, k0, workspace(), (cudaStream_t)stream);
+}
+
+int cqrrpt_gpu_trsm_right(int64_t m, int64_t k, const double *B, int64_t ldb, const int64_t *cols, const double *U,
+                          int64_t ldu, double *X, int64_t ldx, void *stream) {
+    if (m < 0) return -1;
+    if (k < 0) return -2;
+    if (ldu < k) return -7;
+    if (ldx < m) return -9;
+    return trsm_right(m, k, B, ldb, cols, U, ldu, X, ldx, (cudaStream_t)stream);
+}
+
+int cqrrpt_gpu_gram(int64_t m, int64_t k, const double *X, int64_t ldx, double *G, int64_t ldg, void *stream) {
+    if (m < 0 || k < 0) return -1;
+    if (ldg < k) return -6;
+    return gram(m, k, X, ldx, G, ldg, workspace(), (cudaStream_t)stream);
+}
+
+int cqrrpt_gpu_potrf(int64_t n, double *G, int64_t ldg, int64_t *failure_index, void *stream) {
+    if (n < 0) return -1;
+    if (ldg < n) return -3;
+    return potrf(n, G, ldg, failure_index, workspace(), (cudaStream_t)stream);
+}
+
+int cqrrpt_gpu_cond_estimate(int64_t ell, const double *R, int64_t ldr, int32_t method, double *value, void *stream) {
+    if (ell < 0) return -1;
+    if (method < 0 || method > 3) return -4;
+    cudaStream_t st = (cudaStream_t)stream;
+    Workspace &ws = workspace();
+    double *rinv = nullptr;
+    if (method != CQRRPT_COND_DIAG_RATIO && ell > 0) {
+        rinv = ws.get<double>("ce.rinv", (size_t)(ell * ell));
+        double *eye = ws.get<double>("ce.eye", (size_t)(ell * ell));
+        CQ_TRY(fill_identity(ell, eye, ell, st));
+        // zero diagonal: inverse_norm_estimate returns +inf (linalg.cc:489-490);
+        // the kernel handles that case without touching rinv
+        int rc = trsm_right(ell, ell, eye, ell, nullptr, R, ldr, rinv, ell, st);
+        if (rc && rc != CQRRPT_GPU_ERR_SINGULAR) return rc;
+    }
+    return cond_estimate(ell, R, ldr, rinv, ell, method, value, ws, st);
+}
+
+int cqrrpt_gpu_trmm_upper(int64_t k, int64_t n, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
+                          int64_t ldc, void *stream) {
+    if (k < 0 || n < 0) return -1;
+    return gemm(false, k, n, k, 1.0, A, lda, B, ldb, 0.0, C, ldc, (cudaStream_t)stream);
+}
+
+// ---- device validator ------------------------------------------------------
+namespace {
+__global__ void sub_identity_kernel(int64_t k, double *a, int64_t lda) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < k) a[i * lda + i] -= 1.0;
+}
+__global__ void colsq_kernel(int64_t m, int64_t n, const double *a, int64_t lda, const int64_t *cols,
+                             const double *b, int64_t ldb, double *colsq) {
+    __shared__ double sc[32];
+    int64_t j = blockIdx.x;
+    const double *aj = a + (cols ? cols[j] : j) * lda;
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+        double v = aj[i] - (b ? b[j * ldb + i] : 0.0);
+        s = fma(v, v, s);
+    }
+    s = block_sum(s, sc);
+    if (threadIdx.x == 0) colsq[j] = s;
+}
+__global__ void sum1_kernel(int64_t n, const double *v, double *out) {
+    __shared__ double sc[32];
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
+    s = block_sum(s, sc);
+    if (threadIdx.x == 0) out[0] = s;
+}
+int frob_cols(int64_t m, int64_t n, const double *a, int64_t lda, const int64_t *cols, const double *b, int64_t ldb,
+              double *out, Workspace &ws, cudaStream_t st) {
+    double *cs = ws.get<double>("val.cs", (size_t)std::max<int64_t>(n, 1));
+    double *tot = ws.get<double>("val.tot", 1);
+    if (n <= 0) {
+        *out = 0.0;
+        return 0;
+    }
+    colsq_kernel<<<(unsigned)n, 256, 0, st>>>(m, n, a, lda, cols, b, ldb, cs);
+    note_launch();
+    sum1_kernel<<<1, 1024, 0, st>>>(n, cs, tot);
+    note_launch();
+    CQ_TRY(check_launch("frob_cols"));
+    double h = 0.0;
+    CQ_CUDA(cudaMemcpyAsync(&h, tot, sizeof(double), cudaMemcpyDeviceToHost, st), "frob d2h");
+    CQ_CUDA(cudaStreamSynchronize(st), "frob sync");
+    *out = std::sqrt(h);
+    return 0;
+}
+}  // namespace
+
+int cqrrpt_gpu_validate(int64_t m, int64_t n, int64_t k, const double *A, int64_t lda, const double *Q, int64_t ldq,
+                        const double *R, int64_t ldr, const int64_t *J, double *orth_fro, double *orth_2, double *recon,
+                        void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    Workspace &ws = workspace();
+    *orth_fro = 0.0;
+    *orth_2 = 0.0;
+    if (k > 0) {
+        double *qtq = ws.get<double>("val.qtq", (size_t)(k * k));
+        CQ_TRY(gram(m, k, Q, ldq, qtq, k, ws, st));
+        sub_identity_kernel<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(k, qtq, k);
+        note_launch();
+        CQ_TRY(frob_cols(k, k, qtq, k, nullptr, nullptr, 0, orth_fro, ws, st));
+        CQ_TRY(spectral_norm_estimate(k, k, qtq, k, orth_2, ws, st));
+    }
+    double an = 0.0, dn = 0.0;
+    CQ_TRY(frob_cols(m, n, A, lda, nullptr, nullptr, 0, &an, ws, st));
+    double *qr = ws.get<double>("val.qr", (size_t)(std::max<int64_t>(m, 1) * n));
+    if (!qr) return fail_nomem("validate QR");
+    if (k > 0) CQ_TRY(gemm(false, m, n, k, 1.0, Q, ldq, R, ldr, 0.0, qr, std::max<int64_t>(m, 1), st));
+    else CQ_CUDA(cudaMemsetAsync(qr, 0, sizeof(double) * std::max<int64_t>(m, 1) * n, st), "memset qr");
+    CQ_TRY(frob_cols(m, n, A, lda, J, qr, std::max<int64_t>(m, 1), &dn, ws, st));
+    *recon = (an > 0.0) ? dn / an : (dn > 0.0 ? INFINITY : 0.0);  // qrcp.cc:182
+    return 0;
+}
+
+// ---- NCCL --------------------------------------------------------------------
+int cqrrpt_gpu_comm_unique_id(unsigned char id[128]) {
+    NcclApi &api = nccl();
+    if (!api.get_id) return set_error("libnccl.so.2 not found"), CQRRPT_GPU_ERR_NCCL;
+    int rc = api.get_id(id);
+    if (rc) return set_error("ncclGetUniqueId failed"), CQRRPT_GPU_ERR_NCCL;
+    return 0;
+}
+
+int cqrrpt_gpu_comm_init(int32_t nranks, int32_t rank, const unsigned char id[128], cqrrpt_gpu_comm **comm) {
+    NcclApi &api = nccl();
+    if (!api.init_rank) return set_error("libnccl.so.2 not found"), CQRRPT_GPU_ERR_NCCL;
+    NcclId uid;
+    std::memcpy(uid.internal, id, 128);
+    cqrrpt_gpu_comm *c = new cqrrpt_gpu_comm();
+    int rc = api.init_rank(&c->comm, nranks, uid, rank);
+    if (rc) {
+        delete c;
+        set_error(std::string("ncclCommInitRank: ") + (api.errstr ? api.errstr(rc) : "error"));
+        return CQRRPT_GPU_ERR_NCCL;
+    }
+    c->nranks = nranks;
+    c->rank = rank;
+    *comm = c;
+    return 0;
+}
+
+int cqrrpt_gpu_comm_allreduce(cqrrpt_gpu_comm *comm, double *buf, size_t count, void *stream) {
+    NcclApi &api = nccl();
+    if (!comm || !api.allreduce) return set_error("no NCCL communicator"), CQRRPT_GPU_ERR_NCCL;
+    int rc = api.allreduce(buf, buf, count, /*ncclDouble*/ 8, /*ncclSum*/ 0, comm->comm, (cudaStream_t)stream);
+    if (rc) {
+        set_error(std::string("ncclAllReduce: ") + (api.errstr ? api.errstr(rc) : "error"));
+        return CQRRPT_GPU_ERR_NCCL;
+    }
+    return 0;
+}
+
+void cqrrpt_gpu_comm_destroy(cqrrpt_gpu_comm *comm) {
+    if (!comm) return;
+    NcclApi &api = nccl();
+    if (api.destroy && comm->comm) api.destroy(comm->comm);
+    delete comm;
+}
+
+void cqrrpt_gpu_release_workspace(void) { release_workspace(); }
+
+}  // extern "C"

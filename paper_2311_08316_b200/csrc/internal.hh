@@ -1,0 +1,91 @@
+// Host-side internals shared by the .cu translation units: error state,
+// launch accounting and the device workspace cache.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstddef>
+#include <string>
+#include <vector>
+
+#include "../../include/cqrrpt_gpu.h"
+
+namespace cqg {
+
+// ---- errors ---------------------------------------------------------------
+void set_error(const std::string &msg);
+int fail_cuda(const char *what);      // records cudaGetLastError + what
+int fail_nomem(const char *what);
+int fail_internal(const char *what);
+int check_launch(const char *kernel);  // cudaGetLastError after a launch
+
+#define CQ_TRY(expr)              \
+    do {                          \
+        int _rc = (expr);         \
+        if (_rc) return _rc;      \
+    } while (0)
+#define CQ_CUDA(expr, what)                              \
+    do {                                                 \
+        if ((expr) != cudaSuccess) return fail_cuda(what); \
+    } while (0)
+
+// ---- launch accounting ----------------------------------------------------
+void note_launch();
+int num_sms();
+
+// ---- workspace ------------------------------------------------------------
+// Named device buffers that persist across calls on the calling host thread
+// and device (grow-only). One CQRRPT call touches each name at most once
+// concurrently, so reuse is safe within stream order.
+class Workspace {
+public:
+    void *raw(const char *name, size_t bytes);
+    template <class T>
+    T *get(const char *name, size_t count) {
+        return static_cast<T *>(raw(name, count * sizeof(T) + 256));
+    }
+};
+Workspace &workspace();
+void release_workspace();
+
+// ---- kernels' host entry points (implemented in the .cu files) -------------
+int saso_plan(int64_t d, int64_t c0, int64_t count, int64_t nnz, uint64_t seed, uint32_t *plan, cudaStream_t st);
+int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, int64_t nnz, uint64_t seed,
+                int64_t c0, double *msk, int64_t ldm, Workspace &ws, cudaStream_t st, bool exact_order = true);
+
+// QRCP: fills Rsk (n x n, ldr; rows >= k_sk zero), Jdev (int64 n), k_sk (host).
+int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *rsk, int64_t ldr, int64_t *jdev,
+         int64_t *k_sk, Workspace &ws, cudaStream_t st);
+int rank_stage1(int64_t k, int64_t n, const double *r, int64_t ldr, int64_t *k0, Workspace &ws, cudaStream_t st);
+
+int trsm_right(int64_t m, int64_t k, const double *b, int64_t ldb, const int64_t *cols, const double *u,
+               int64_t ldu, double *x, int64_t ldx, cudaStream_t st);
+int gram(int64_t m, int64_t k, const double *x, int64_t ldx, double *g, int64_t ldg, Workspace &ws,
+         cudaStream_t st);
+// C (M x N, ldc) = alpha * op(A) * B + beta * C; op(A) = A (M x K) or A^T (A is K x M).
+int gemm(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const double *a, int64_t lda,
+         const double *b, int64_t ldb, double beta, double *c, int64_t ldc, cudaStream_t st);
+int potrf(int64_t n, double *g, int64_t ldg, int64_t *failure_index, Workspace &ws, cudaStream_t st);
+int trmm_upper(int64_t k, int64_t n, const double *a, int64_t lda, const double *b, int64_t ldb, double *c,
+               int64_t ldc, Workspace &ws, cudaStream_t st);
+
+// small utilities (util.cu)
+int fill_identity(int64_t n, double *a, int64_t lda, cudaStream_t st);
+int zero_strict_lower(int64_t n, double *a, int64_t lda, cudaStream_t st);
+int frob_norm_upper(int64_t n, const double *a, int64_t lda, double *out_host, Workspace &ws, cudaStream_t st);
+int copy_matrix(int64_t m, int64_t n, const double *src, int64_t lds, double *dst, int64_t ldd, cudaStream_t st);
+
+// stage-2 estimators (cond.cu)
+// first power iterate of ||(R_ell - I) v0|| for each ell in ells (host list) -> host values
+int identity_deviation_first(const double *r, int64_t ldr, const int64_t *ells, int nells, double *out_host,
+                             Workspace &ws, cudaStream_t st);
+// full reference cond_estimate on the leading ell block; rinv = explicit inverse (ld ldr) for krylov
+int cond_estimate(int64_t ell, const double *r, int64_t ldr, const double *rinv, int64_t ldi, int method,
+                  double *value_host, Workspace &ws, cudaStream_t st);
+int spectral_norm_estimate(int64_t m, int64_t n, const double *a, int64_t lda, double *value_host, Workspace &ws,
+                           cudaStream_t st);
+
+}  // namespace cqg

@@ -1,0 +1,217 @@
+"""End-to-end GPU parity of cqrrpt() against the reference (through the C ABI).
+
+North-star bars (BASELINE.json):
+  * J and k exactly equal wherever the sketch's pivot decisions are not within
+    rounding of a tie (ties located with the oracle's tie-gap instrumentation);
+  * ||M[:,J] - QR||_F/||M||_F and ||Q^T Q - I||_F within 10x of the reference's;
+  * R within a relative tolerance scaled by cond(M): column-wise
+    ||dR[:,j]|| <= 1e3 * n * u * cond_est * ||R[:,j]||.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+U = 1.1102230246251565e-16
+
+
+def run_gpu(pkg, a, gamma=1.25, nnz=8, seed=0, eps_tol=1e-4, exact=False):
+    A = pkg.to_device_colmajor(np.asfortranarray(a))
+    res = pkg.dgeqpt(A, d_factor=gamma, nnz=nnz, seed=seed, eps_tol=eps_tol, exact_stage2=exact)
+    q = np.asfortranarray(A[:, : res.k].cpu().numpy())
+    r = np.asfortranarray(res.r.cpu().numpy())
+    return q, r, res.pivots.cpu().numpy(), res.k, res.k0, res
+
+
+def metrics(oracle, a, q, r, piv):
+    v = oracle.validate(a, q, r, piv)
+    return v["orth_fro"], v["recon_rel"]
+
+
+def tie_free_prefix(oracle, a, gamma, nnz, seed):
+    """Length of the pivot prefix whose sketch QRCP decisions are not near-ties."""
+    ref = oracle.cqrrpt(a, gamma=gamma, nnz=nnz, seed=seed, want_sketch=True)
+    _, _, _, gaps = oracle.qrcp(ref.extra["m_sk"], gaps=True)
+    n = a.shape[1]
+    tie = np.nonzero(gaps <= 1e3 * U * n)[0]
+    return (int(tie[0]) if tie.size else n), ref
+
+
+def check_against_reference(pkg, oracle, a, gamma=1.25, nnz=8, seed=0, cond=1.0):
+    q, r, piv, k, k0, res = run_gpu(pkg, a, gamma, nnz, seed)
+    ref = oracle.cqrrpt(a, gamma=gamma, nnz=nnz, seed=seed)
+    n = a.shape[1]
+    # sketch + QRCP + stage 1 restate the reference's arithmetic: J, k0 bit-exact
+    assert np.array_equal(piv, ref.pivots)
+    assert k0 == ref.k0 and k == ref.k
+    of, rr = metrics(oracle, a, q, r, piv)
+    of_ref, rr_ref = metrics(oracle, a, ref.q, ref.r, ref.pivots)
+    floor = 10 * n * U  # both can sit at the unit-roundoff floor
+    assert of <= 10 * max(of_ref, floor), (of, of_ref)
+    assert rr <= 10 * max(rr_ref, floor), (rr, rr_ref)
+    err = np.linalg.norm(r - ref.r, axis=0) / (np.linalg.norm(ref.r, axis=0) + 1e-300)
+    assert np.max(err) <= 1e3 * n * U * cond
+    return res, ref
+
+
+def test_c1_shape_matches_reference(cuda, oracle):
+    a = oracle.gen_gaussian(16384, 256, 0)  # BASELINE config 1 (exact generator)
+    res, ref = check_against_reference(cuda, oracle, a)
+    assert res.k == 256 and res.k0 == 256
+    # SURVEY §9 P11 golden summary of the reference for C1
+    from oracle.oracle import fnv_pivots
+    assert fnv_pivots(res.pivots.cpu().numpy()) == "ac0e857417ac8f07"
+    assert list(res.pivots.cpu().numpy()[:8]) == [170, 80, 191, 79, 65, 38, 11, 243]
+
+
+@pytest.mark.parametrize("gamma", [1.0, 1.25, 2.0])
+def test_c5_style_graded_columns(cuda, oracle, gamma):
+    a = oracle.gen_gaussian(20000, 128, 0)
+    a, _ = oracle.c5_scale_columns(a, span=8.0, seed=0)
+    check_against_reference(cuda, oracle, a, gamma=gamma, cond=1e8)
+
+
+def test_cond1e10_spectrum(cuda, oracle):
+    sig = 10.0 ** (-10 * np.arange(128) / 127)  # C2 spectrum at desk scale
+    a = oracle.gen_spectral(8192, 128, sig, 0)
+    check_against_reference(cuda, oracle, a, cond=1e10)
+
+
+@pytest.mark.parametrize("noise,expect_k", [(1e-14, None), (1e-12, None), (0.0, 64)])
+def test_planted_rank_detection(cuda, oracle, noise, expect_k):
+    ab = oracle.gen_exact_rank(8192, 128, 64, 0)  # C3 structure at desk scale
+    g = oracle.gen_gaussian(8192, 128, 1)
+    a = np.asfortranarray(ab + noise * np.linalg.norm(ab) / np.sqrt(ab.size) * g)
+    q, r, piv, k, k0, res = run_gpu(cuda, a)
+    ref = oracle.cqrrpt(a, gamma=1.25, nnz=8, seed=0)
+    assert k == ref.k and k0 == ref.k0
+    assert np.array_equal(piv, ref.pivots)
+    if expect_k is not None:
+        assert k == expect_k
+
+
+def test_exact_rank_known_answer(cuda, oracle):
+    # test_cqrrpt.cc:243-251: gen_exact_rank(200, 40, 10, 24), seed 25 (nnz default 4) -> k = 10
+    a = oracle.gen_exact_rank(200, 40, 10, 24)
+    q, r, piv, k, k0, res = run_gpu(cuda, a, nnz=4, seed=25)
+    assert k == 10
+    v = oracle.validate(a, q, r, piv)
+    assert v["recon_rel"] <= 1e-12
+
+
+def test_zero_matrix_rank_zero(cuda, oracle):
+    # test_cqrrpt.cc:262-268
+    out = cuda.cqrrpt(np.zeros((30, 5)), cuda.CqrrptConfig())
+    assert out.k == 0 and out.k0 == 0
+    assert out.factorization.q.shape == (30, 0) and out.factorization.r.shape[0] == 0
+
+
+def test_scaled_coordinate_columns(cuda, oracle):
+    # test_cqrrpt.cc:223-241 (SASO instead of the Gaussian family): |R| = c I
+    c = 3.5
+    m = np.zeros((40, 8)); m[np.arange(8), np.arange(8)] = c
+    out = cuda.cqrrpt(m, cuda.CqrrptConfig(gamma=2.0, seed=23, nnz_per_col=4))
+    assert out.k == 8
+    r = out.factorization.r
+    assert np.all(np.abs(np.abs(np.diag(r)) - c) <= c * 1e-12)
+    assert np.all(np.abs(np.triu(r, 1)) <= c * 1e-12)
+
+
+def test_driver_defaults_and_config_errors(cuda, oracle):
+    # test_cqrrpt.cc:253-260, 348-356
+    assert cuda.sketch_rows_for(1.25, 50) == 63 and cuda.sketch_rows_for(3.0, 500) == 1500
+    m = oracle.gen_gaussian(20, 4, 29)
+    with pytest.raises(ValueError):
+        cuda.cqrrpt(m, cuda.CqrrptConfig(gamma=0.5))
+    with pytest.raises(ValueError):
+        cuda.cqrrpt(m, cuda.CqrrptConfig(eps_tol=U / 2))
+    with pytest.raises(ValueError):
+        cuda.cqrrpt(m, cuda.CqrrptConfig(nnz_per_col=0))
+
+
+def test_bitwise_deterministic(cuda, oracle):
+    # test_cqrrpt.cc:270-283
+    a = oracle.gen_gaussian(150, 20, 26)
+    x = cuda.cqrrpt(a, cuda.CqrrptConfig(seed=27))
+    y = cuda.cqrrpt(a, cuda.CqrrptConfig(seed=27))
+    assert np.array_equal(x.factorization.q, y.factorization.q)
+    assert np.array_equal(x.factorization.r, y.factorization.r)
+    assert np.array_equal(x.factorization.pivots, y.factorization.pivots)
+    z = cuda.cqrrpt(a, cuda.CqrrptConfig(seed=28))
+    assert not np.array_equal(x.factorization.r, z.factorization.r)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_valid_output_small(cuda, oracle, seed):
+    # test_cqrrpt.cc:285-300 (SASO): valid at 100 n u, k = n
+    n = 6 + 2 * seed
+    a = oracle.gen_gaussian(40 * (1 + seed % 3) + 20, n, 400 + seed)
+    out = cuda.cqrrpt(a, cuda.CqrrptConfig(gamma=2.0, nnz_per_col=4, seed=500 + seed))
+    assert out.k == n
+    v = cuda.validate(out.factorization, a, 100.0 * n * U)
+    assert v.passed, v
+
+
+def test_stage2_exact_vs_fast_path_agree(cuda, oracle):
+    a = oracle.gen_gaussian(4000, 96, 3)
+    _, _, p1, k1, _, r1 = run_gpu(cuda, a, exact=False)
+    _, _, p2, k2, _, r2 = run_gpu(cuda, a, exact=True)
+    assert k1 == k2 and np.array_equal(p1, p2)
+    assert r2.ctx.stage2_exact == 1 and r1.ctx.stage2_exact == 0
+    ref = oracle.cqrrpt(a, gamma=1.25, nnz=8, seed=0)
+    assert r2.ctx.cond_m_pre == pytest.approx(ref.cond_m_pre, rel=1e-6)
+
+
+@pytest.mark.parametrize("case", ["zero_col", "dups", "dups_small"])
+def test_stage2_cholesky_failure_paths(cuda, oracle, case):
+    """Reference stage-2 behaviour on its own failure inputs (test_cqrrpt.cc:170-197,302-313;
+    SURVEY P10 values: (retries, k0_final, rank) = (1,8,8), (1,6,6), (1,5,5))."""
+    if case == "zero_col":
+        base = oracle.gen_gaussian(40, 8, 11)
+        mk = np.zeros((40, 12)); mk[:, :8] = base; mk[:, 9:12] = base[:, :3]
+        want = (1, 8, 8)
+    elif case == "dups":
+        base = oracle.gen_gaussian(50, 6, 12)
+        mk = np.zeros((50, 9)); mk[:, :6] = base; mk[:, 6:9] = base[:, :3]
+        want = (1, 6, 6)
+    else:
+        base = oracle.gen_gaussian(30, 5, 13)
+        mk = np.zeros((30, 7)); mk[:, :5] = base; mk[:, 5:7] = base[:, :2]
+        want = (1, 5, 5)
+    ref = oracle.rank_stage2(mk, np.eye(mk.shape[1]))
+    assert (ref["retries"], ref["k0_final"], ref["rank"]) == want
+    # the GPU path: TRSM (identity) + Gram + potrf + stage-2 via the kernels
+    from paper_2311_08316_b200 import kernels
+    mpre = kernels.trsm_right(cuda.to_device_colmajor(mk), cuda.to_device_colmajor(np.eye(mk.shape[1])))
+    g = kernels.gram(mpre)
+    r, fi = kernels.potrf(g)
+    assert fi - 1 == ref["k0_final"]
+    # binary search with the reference estimator semantics on the leading block
+    thr = np.sqrt(1e-4 / U)
+    R = r
+    memo = {}
+
+    def at(ell):
+        if ell <= 0:
+            return 1.0
+        if ell not in memo:
+            memo[ell] = kernels.cond_estimate(R[:ell, :ell], 3)  # nested identity_deviation
+        return max([1.0] + [v for l, v in memo.items() if l <= ell])
+    lo, hi = 0, R.shape[0]
+    while lo < hi:
+        mid = lo + (hi - lo + 1) // 2
+        if at(mid) <= thr:
+            lo = mid
+        else:
+            hi = mid - 1
+    assert lo == ref["rank"]
+
+
+def test_c_abi_host_outputs_path(cuda, oracle):
+    """cqrrpt() from host numpy (the reference-signature adapter path)."""
+    a = oracle.gen_gaussian(3000, 64, 12)
+    out = cuda.cqrrpt(a, cuda.CqrrptConfig(nnz_per_col=8))
+    ref = oracle.cqrrpt(a, gamma=1.25, nnz=8, seed=0)
+    assert np.array_equal(out.factorization.pivots, ref.pivots)
+    assert out.k == ref.k
+    assert out.diagnostics.validation.passed
