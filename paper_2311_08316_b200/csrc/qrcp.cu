@@ -18,26 +18,48 @@
 // the stop test sqrt(max(w_p,0)) <= n*u*max_j ||col_j|| (qrcp.cc:52-62).
 // Every CTA recomputes the pivot column's reflector redundantly (same code,
 // same order -> identical bits), so one grid barrier per step suffices.
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.hh"
 
 namespace cqg {
 
-constexpr int kQrcpThreads = 256;  // 64 quads of 4 lanes
+constexpr int kQrcpThreads = 256;  // 8 warps; a warp owns one column at a time
 
-// The reference's dot (linalg.cc:36-50) as compiled (oracle/cqrrpt_oracle.c
+// ---------------------------------------------------------------------------
+// The reference's dot (linalg.cc:36-50) as compiled (see oracle/cqrrpt_oracle.c
 // orc_dot): four interleaved accumulators s_q over the 4-aligned body with
 // separately rounded products, (s0 + s1) + (s2 + s3), then the <4-element
-// tail with the last term of an odd count fused. Lane q of a 4-lane quad
-// owns s_q; the result is returned in all 4 lanes. This file is compiled
-// with --fmad=false: every FMA below is an explicit fma().
+// tail with the last term of an odd count fused. Lanes 0..3 of a warp own
+// s_0..s_3 (the ordered chains); the other lanes stage operands. This file is
+// compiled with --fmad=false: every FMA below is an explicit fma().
+// ---------------------------------------------------------------------------
+
+// lanes 0..3: accumulate body elements [b0, b0+len) of a.b into s (e = lane mod 4)
+CQ_DEVI double chain_chunk(double s, const double *a, const double *b, int64_t len, int lane) {
+    int64_t e = lane;
+    for (; e + 28 < len; e += 32) {
+        double av[8], bv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            av[u] = a[e + 4 * u];
+            bv[u] = b[e + 4 * u];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s = s + av[u] * bv[u];
+    }
+    for (; e < len; e += 4) s = s + a[e] * b[e];
+    return s;
+}
+
+// lanes 0..3: (s0+s1)+(s2+s3), then the tail (elements body..c-1 via fa/fb)
 template <class FA, class FB>
-CQ_DEVI double quad_dot(unsigned qmask, int q, int64_t c, FA fa, FB fb) {
+CQ_DEVI double chain_finish(double s, int64_t c, FA fa, FB fb) {
     const int64_t body = c & ~(int64_t)3;
-    double s = 0.0;
-    for (int64_t e = q; e < body; e += 4) s = s + fa(e) * fb(e);
-    double pair = s + __shfl_xor_sync(qmask, s, 1);
-    double tot = pair + __shfl_xor_sync(qmask, pair, 2);
+    double pair = s + __shfl_xor_sync(0xfu, s, 1);
+    double tot = pair + __shfl_xor_sync(0xfu, pair, 2);
     int64_t e = body, rem = c - body;
     if (rem >= 2) {
         tot = tot + fa(e) * fb(e);
@@ -49,6 +71,29 @@ CQ_DEVI double quad_dot(unsigned qmask, int q, int64_t c, FA fa, FB fb) {
     return tot;
 }
 
+// Warp-cooperative reference dot of sa[0..c) (shared, or nullptr = the column
+// itself) with the global column g[0..c): the column is staged through the
+// warp's shared buffer wb (WB doubles) with coalesced loads; lanes 0..3 run
+// the ordered chains from shared memory. Result broadcast to all lanes.
+CQ_DEVI double warp_ref_dot(const double *sa, const double *g, int64_t c, double *wb, int WB, int lane) {
+    const int64_t body = c & ~(int64_t)3;
+    double s = 0.0;
+    for (int64_t b0 = 0; b0 < body; b0 += WB) {
+        const int len = (int)cmin<int64_t>(WB, body - b0);
+#pragma unroll 4
+        for (int e = lane; e < len; e += 32) wb[e] = ld_cg(g + b0 + e);
+        __syncwarp();
+        if (lane < 4) s = chain_chunk(s, sa ? sa + b0 : wb, wb, len, lane);
+        __syncwarp();
+    }
+    double tot = 0.0;
+    if (lane < 4) {
+        tot = chain_finish(s, c, [&](int64_t x) { return sa ? sa[x] : ld_cg(g + x); },
+                           [&](int64_t x) { return ld_cg(g + x); });
+    }
+    return __shfl_sync(0xffffffffu, tot, 0);
+}
+
 struct QrcpArgs {
     int64_t d, n, ld;
     double *b;
@@ -57,63 +102,106 @@ struct QrcpArgs {
     int32_t *cmap[2];
     int32_t *piv;     // physical pivot chosen at each step
     double *alpha;    // R(i,i)
-    double *pv[2];    // per-CTA argmax partials
+    double *pv[2];    // per-CTA argmax partials: value, logical index, physical column
     int32_t *pi[2];
+    int32_t *pp[2];
     unsigned int *bar;
     int64_t *k_out;
     int32_t *final_buf;  // which cmap buffer holds positions >= k
     double rank_tol;
     int64_t steps;
+    int wb;              // per-warp staging buffer (doubles, multiple of 32)
+    unsigned long long *trace;  // optional per-step phase timestamps (CTA 0)
 };
 
+CQ_DEVI void trace_mark(unsigned long long *tr, int64_t i, int slot) {
+    if (tr && blockIdx.x == 0 && threadIdx.x == 0 && i < 512) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        tr[i * 6 + slot] = t;
+    }
+}
+
+// Lanes of a warp stage g[0..len) into wb (coalesced).
+CQ_DEVI void warp_stage(double *wb, const double *g, int64_t len, int lane) {
+#pragma unroll 4
+    for (int64_t e = lane; e < len; e += 32) wb[e] = ld_cg(g + e);
+}
+
 __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
-    extern __shared__ double s_v[];  // pivot column rows i..d-1, then scaled reflector
+    extern __shared__ double smem[];
     __shared__ double s_av[kQrcpThreads / 32];
-    __shared__ int32_t s_ai[kQrcpThreads / 32];
+    __shared__ int32_t s_ai[kQrcpThreads / 32], s_ap[kQrcpThreads / 32];
     __shared__ double s_bc[4];
     const int G = gridDim.x, cta = blockIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kQrcpThreads / 32;
-    const int q = lane & 3;
-    const int quad = threadIdx.x >> 2;  // 0..63
-    const unsigned qmask = 0xfu << (lane & ~3);
     const int64_t d = A.d, n = A.n, ld = A.ld;
+    const int WB = A.wb;
+    double *wb = smem + wid * WB;   // warp staging buffer: the warp's column tail
+    double *s_v = smem + nw * WB;   // pivot column / scaled reflector (d+1)
     const double sqrt_u = sqrt(kUnitRoundoff);
 
-    auto block_argmax = [&](ArgMax a) -> ArgMax {
-        a = warp_argmax(a);
+    // block argmax carrying the physical column of the winner
+    auto block_argmax = [&](ArgMax a, int32_t phys, int32_t *phys_out) -> ArgMax {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            ArgMax b;
+            b.v = __shfl_xor_sync(0xffffffffu, a.v, o);
+            b.i = __shfl_xor_sync(0xffffffffu, a.i, o);
+            int32_t bp = __shfl_xor_sync(0xffffffffu, phys, o);
+            ArgMax c = argmax_combine(a, b);
+            if (c.i != a.i || c.v != a.v) phys = bp;
+            a = c;
+        }
         __syncthreads();
         if (lane == 0) {
             s_av[wid] = a.v;
             s_ai[wid] = a.i;
+            s_ap[wid] = phys;
         }
         __syncthreads();
         ArgMax r{-INFINITY, 0x7fffffff};
-        if (lane < nw) r = ArgMax{s_av[lane], s_ai[lane]};
-        return warp_argmax(r);
+        int32_t rp = 0;
+        if (lane < nw) {
+            r = ArgMax{s_av[lane], s_ai[lane]};
+            rp = s_ap[lane];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            ArgMax b;
+            b.v = __shfl_xor_sync(0xffffffffu, r.v, o);
+            b.i = __shfl_xor_sync(0xffffffffu, r.i, o);
+            int32_t bp = __shfl_xor_sync(0xffffffffu, rp, o);
+            ArgMax c = argmax_combine(r, b);
+            if (c.i != r.i || c.v != r.v) rp = bp;
+            r = c;
+        }
+        *phys_out = rp;
+        return r;
     };
 
     // ---- initial squared norms w_j = dot(col_j, col_j) (qrcp.cc:48-51) ----
     ArgMax loc{-INFINITY, 0x7fffffff};
-    {
-        const int64_t nper = (n + G - 1) / G;  // positions cta, cta+G, ...
-        for (int64_t t0 = 0; t0 < nper; t0 += kQrcpThreads / 4) {
-            const int64_t j = cta + (t0 + quad) * G;
-            const bool act = (t0 + quad) < nper && j < n;
-            const double *col = A.b + (act ? j : 0) * ld;
-            double s = quad_dot(qmask, q, act ? d : 0, [&](int64_t e) { return col[e]; },
-                                [&](int64_t e) { return col[e]; });
-            if (act && q == 0) {
-                A.w[0][j] = s;
-                A.wref[j] = s;
-                A.cmap[0][j] = (int32_t)j;
-                loc = argmax_combine(loc, ArgMax{s, (int32_t)j});
-            }
+    int32_t locp = 0;
+    for (int64_t j = cta + (int64_t)wid * G; j < n; j += (int64_t)nw * G) {
+        double s = warp_ref_dot(nullptr, A.b + j * ld, d, wb, WB, lane);
+        if (lane == 0) {
+            A.w[0][j] = s;
+            A.wref[j] = s;
+            A.cmap[0][j] = (int32_t)j;
         }
+        ArgMax c = argmax_combine(loc, ArgMax{s, (int32_t)j});
+        if (c.i != loc.i) locp = (int32_t)j;
+        loc = c;
     }
-    loc = block_argmax(loc);
-    if (threadIdx.x == 0) {
-        A.pv[0][cta] = loc.v;
-        A.pi[0][cta] = loc.i;
+    {
+        int32_t bp;
+        loc = block_argmax(loc, locp, &bp);
+        if (threadIdx.x == 0) {
+            A.pv[0][cta] = loc.v;
+            A.pi[0][cta] = loc.i;
+            A.pp[0][cta] = bp;
+        }
     }
     grid_barrier(A.bar, G);
 
@@ -122,26 +210,50 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
     int64_t i = 0;
     for (; i < A.steps; ++i) {
         const int cur = (int)(i & 1), nxt = cur ^ 1;
+        const int64_t c = d - i - 1;  // rows below the diagonal
+        const bool fits = c <= WB;
+        trace_mark(A.trace, i, 0);
+
+        // ---- prefetch this warp's first owned column (independent of the pivot)
+        const int64_t jfirst = i + 1 + ((cta - (i + 1)) % G + G) % G;
+        const int64_t j_w = jfirst + (int64_t)wid * G;
+        int32_t pj0 = 0;
+        double wj0 = 0.0, wrefj0 = 0.0, t0 = 0.0;
+        if (j_w < n) {
+            pj0 = ld_cg(A.cmap[cur] + j_w);
+            wj0 = ld_cg(A.w[cur] + j_w);
+            wrefj0 = ld_cg(A.wref + j_w);
+            const double *col = A.b + (int64_t)pj0 * ld;
+            t0 = ld_cg(col + i);
+            if (fits) warp_stage(wb, col + i + 1, c, lane);
+        }
+        const int32_t phys_i = ld_cg(A.cmap[cur] + i);
+        const double w_i = ld_cg(A.w[cur] + i), wref_i = ld_cg(A.wref + i);
+
         // ---- pivot: lowest index attaining the max (qrcp.cc:26-31) -------
         ArgMax g{-INFINITY, 0x7fffffff};
-        if (threadIdx.x < G) g = ArgMax{ld_cg(A.pv[cur] + threadIdx.x), ld_cg(A.pi[cur] + threadIdx.x)};
-        g = block_argmax(g);
+        int32_t gp = 0;
+        if (threadIdx.x < G) {
+            g = ArgMax{ld_cg(A.pv[cur] + threadIdx.x), ld_cg(A.pi[cur] + threadIdx.x)};
+            gp = ld_cg(A.pp[cur] + threadIdx.x);
+        }
+        int32_t phys_p;
+        g = block_argmax(g, gp, &phys_p);
         if (i == 0) stop = A.rank_tol * sqrt(fmax(g.v, 0.0));  // max_norm0 (qrcp.cc:52-55)
         const double wp = g.v;
         const int64_t p = g.i;
         if (sqrt(wp > 0.0 ? wp : 0.0) <= stop) break;  // qrcp.cc:62
-        const int32_t phys_p = ld_cg(A.cmap[cur] + p);
-        const int32_t phys_i = ld_cg(A.cmap[cur] + i);
         const double *x = A.b + (int64_t)phys_p * ld;
-        const int64_t c = d - i - 1;  // rows below the diagonal
+        trace_mark(A.trace, i, 1);
 
-        // ---- make_reflector (linalg.cc:110-124) ---------------------------
+        // ---- make_reflector (linalg.cc:110-124), redundantly per CTA ------
         for (int64_t r = threadIdx.x; r < d - i; r += kQrcpThreads) s_v[r] = ld_cg(x + i + r);
         __syncthreads();
         if (wid == 0 && lane < 4) {
-            double tail_sq = quad_dot(0xfu, q, c, [&](int64_t e) { return s_v[1 + e]; },
-                                      [&](int64_t e) { return s_v[1 + e]; });
-            if (q == 0) {
+            double s = chain_chunk(0.0, s_v + 1, s_v + 1, c & ~(int64_t)3, lane);
+            double tail_sq = chain_finish(s, c, [&](int64_t e) { return s_v[1 + e]; },
+                                          [&](int64_t e) { return s_v[1 + e]; });
+            if (lane == 0) {
                 double x0 = s_v[0];
                 double norm_x = sqrt(fma(x0, x0, tail_sq));
                 double alpha = x0, v0 = 1.0, beta = 0.0;
@@ -162,56 +274,108 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
             for (int64_t r = threadIdx.x; r < c; r += kQrcpThreads) s_v[1 + r] = s_v[1 + r] / v0;  // colj[i] /= v0
         __syncthreads();
         const double *sv = s_v + 1;
+        trace_mark(A.trace, i, 2);
 
-        // ---- apply_reflector + norm downdate on owned positions j > i ----
+        // ---- apply_reflector + norm downdate, one owned column per warp --
         ArgMax mine{-INFINITY, 0x7fffffff};
-        const int64_t jfirst = i + 1 + ((cta - (i + 1)) % G + G) % G;
-        const int64_t nown = (jfirst < n) ? (n - jfirst + G - 1) / G : 0;
-        for (int64_t t0 = 0; t0 < nown; t0 += kQrcpThreads / 4) {
-            const bool act = (t0 + quad) < nown;
-            const int64_t j = jfirst + (t0 + quad) * G;
-            const bool isp = act && (j == p);
-            const int32_t pj = !act ? 0 : (isp ? phys_i : ld_cg(A.cmap[cur] + j));
-            const double wj = !act ? 0.0 : (isp ? ld_cg(A.w[cur] + i) : ld_cg(A.w[cur] + j));
-            const double wrefj = !act ? 0.0 : (isp ? ld_cg(A.wref + i) : ld_cg(A.wref + j));
+        int32_t minep = 0;
+        bool first = true;
+        for (int64_t j = j_w; j < n; j += (int64_t)nw * G, first = false) {
+            const bool isp = (j == p);
+            int32_t pj;
+            double wj, wrefj, t;
+            bool staged = false;
+            if (first && !isp) {
+                pj = pj0;
+                wj = wj0;
+                wrefj = wrefj0;
+                t = t0;
+                staged = fits;
+            } else {
+                pj = isp ? phys_i : ld_cg(A.cmap[cur] + j);
+                wj = isp ? w_i : ld_cg(A.w[cur] + j);
+                wrefj = isp ? wref_i : ld_cg(A.wref + j);
+                t = ld_cg(A.b + (int64_t)pj * ld + i);
+                if (fits) {
+                    __syncwarp();
+                    warp_stage(wb, A.b + (int64_t)pj * ld + i + 1, c, lane);
+                    staged = true;
+                }
+            }
             double *col = A.b + (int64_t)pj * ld;
-            const int64_t cc = act ? c : 0;
-            double t = act ? ld_cg(col + i) : 0.0;
-            if (beta != 0.0) {
-                double dot = quad_dot(qmask, q, cc, [&](int64_t e) { return sv[e]; },
-                                      [&](int64_t e) { return ld_cg(col + i + 1 + e); });
-                double tau = t;  // linalg.cc:131-135
+            double *tail = col + i + 1;
+            if (staged) __syncwarp();
+            if (beta != 0.0) {  // apply_reflector (linalg.cc:126-136)
+                double dot;
+                if (staged) {
+                    double s = 0.0;
+                    if (lane < 4) {
+                        s = chain_chunk(0.0, sv, wb, c & ~(int64_t)3, lane);
+                        s = chain_finish(s, c, [&](int64_t e) { return sv[e]; }, [&](int64_t e) { return wb[e]; });
+                    }
+                    dot = __shfl_sync(0xffffffffu, s, 0);
+                } else {
+                    dot = warp_ref_dot(sv, tail, c, wb, WB, lane);
+                }
+                double tau = t;
                 tau += dot;
                 tau *= beta;
                 t = t - tau;
-                for (int64_t e = q; e < cc; e += 4) __stcg(col + i + 1 + e, fma(-tau, sv[e], ld_cg(col + i + 1 + e)));
-                __syncwarp(qmask);
+                if (staged) {
+#pragma unroll 4
+                    for (int64_t e = lane; e < c; e += 32) {
+                        double nv = fma(-tau, sv[e], wb[e]);
+                        wb[e] = nv;
+                        __stcg(tail + e, nv);
+                    }
+                } else {
+#pragma unroll 4
+                    for (int64_t e = lane; e < c; e += 32) __stcg(tail + e, fma(-tau, sv[e], ld_cg(tail + e)));
+                }
+                __syncwarp();
             }
             double updated = fma(-t, t, wj);  // qrcp.cc:77-78
             double newref = wrefj;
-            if (updated <= sqrt_u * wrefj) {   // qrcp.cc:82-86 (uniform within the quad)
-                updated = quad_dot(qmask, q, cc, [&](int64_t e) { return ld_cg(col + i + 1 + e); },
-                                   [&](int64_t e) { return ld_cg(col + i + 1 + e); });
+            if (updated <= sqrt_u * wrefj) {  // qrcp.cc:82-86 (warp-uniform)
+                if (staged) {
+                    double s = 0.0;
+                    if (lane < 4) {
+                        s = chain_chunk(0.0, wb, wb, c & ~(int64_t)3, lane);
+                        s = chain_finish(s, c, [&](int64_t e) { return wb[e]; }, [&](int64_t e) { return wb[e]; });
+                    }
+                    updated = __shfl_sync(0xffffffffu, s, 0);
+                } else {
+                    updated = warp_ref_dot(nullptr, tail, c, wb, WB, lane);
+                }
                 newref = updated;
             }
-            if (act && q == 0) {
+            if (lane == 0) {
                 __stcg(col + i, t);
                 __stcg(A.w[nxt] + j, updated);
                 __stcg(A.wref + j, newref);
                 __stcg(A.cmap[nxt] + j, pj);
-                mine = argmax_combine(mine, ArgMax{updated, (int32_t)j});
             }
+            ArgMax cnd = argmax_combine(mine, ArgMax{updated, (int32_t)j});
+            if (cnd.i != mine.i) minep = pj;
+            mine = cnd;
+            __syncwarp();
         }
-        mine = block_argmax(mine);
-        if (threadIdx.x == 0) {
-            __stcg(A.pv[nxt] + cta, mine.v);
-            __stcg(A.pi[nxt] + cta, mine.i);
-            if (cta == 0) {
-                __stcg(A.piv + i, phys_p);
-                __stcg(A.alpha + i, alpha);
+        trace_mark(A.trace, i, 3);
+        {
+            int32_t bp;
+            mine = block_argmax(mine, minep, &bp);
+            if (threadIdx.x == 0) {
+                __stcg(A.pv[nxt] + cta, mine.v);
+                __stcg(A.pi[nxt] + cta, mine.i);
+                __stcg(A.pp[nxt] + cta, bp);
+                if (cta == 0) {
+                    __stcg(A.piv + i, phys_p);
+                    __stcg(A.alpha + i, alpha);
+                }
             }
         }
         k = i + 1;
+        trace_mark(A.trace, i, 4);
         grid_barrier(A.bar, G);
     }
     if (cta == 0 && threadIdx.x == 0) {
@@ -293,11 +457,16 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     if (d < 1) return fail_internal("qrcp: need at least one row");
     if (rank_tol < 0.0) rank_tol = (double)n * kUnitRoundoff;  // qrcp.cc:17,38
     const int sms = num_sms();
+    // shared memory: 8 warp staging buffers + the pivot column (d+1 doubles)
+    const int64_t budget = (200 * 1024) / (int64_t)sizeof(double);
+    if (d + 1 + 8 * 128 > budget) return fail_internal("qrcp: d too large for the shared-memory reflector");
+    const int WB = (int)std::min<int64_t>(4096, ((budget - (d + 1)) / 8) & ~(int64_t)31);
+    const size_t smem = sizeof(double) * (size_t)(8 * WB + d + 1);
+    CQ_CUDA(cudaFuncSetAttribute(qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "qrcp smem");
+    // one owned column per warp per step at the start (8 warps per CTA)
     int G = (int)std::min<int64_t>(std::min<int64_t>(sms, kQrcpThreads), std::max<int64_t>(1, (n + 7) / 8));
     int maxb = 0;
-    CQ_CUDA(cudaFuncSetAttribute(qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "qrcp smem");
-    CQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, qrcp_kernel, kQrcpThreads, sizeof(double) * (d + 1)),
-            "occupancy");
+    CQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, qrcp_kernel, kQrcpThreads, smem), "occupancy");
     G = std::min(G, std::max(1, maxb) * sms);
     QrcpArgs a;
     a.d = d;
@@ -315,6 +484,8 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     a.pv[1] = ws.get<double>("qrcp.pv1", 256);
     a.pi[0] = ws.get<int32_t>("qrcp.pi0", 256);
     a.pi[1] = ws.get<int32_t>("qrcp.pi1", 256);
+    a.pp[0] = ws.get<int32_t>("qrcp.pp0", 256);
+    a.pp[1] = ws.get<int32_t>("qrcp.pp1", 256);
     a.bar = ws.get<unsigned int>("qrcp.bar", 4);
     a.k_out = ws.get<int64_t>("qrcp.k", 2);
     a.final_buf = ws.get<int32_t>("qrcp.fb", 2);
@@ -322,9 +493,10 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     a.steps = std::min(d, n);
     if (!a.w[0] || !a.bar || !a.k_out) return fail_nomem("qrcp workspace");
     CQ_CUDA(cudaMemsetAsync(a.bar, 0, 4 * sizeof(unsigned int), st), "memset bar");
-    const size_t smem = sizeof(double) * (size_t)(d + 1);
-    if (smem > 200 * 1024) return fail_internal("qrcp: d too large for the shared-memory reflector (d <= 25600)");
-    CQ_CUDA(cudaFuncSetAttribute(qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "qrcp smem");
+    a.wb = WB;
+    static const bool tracing = getenv("CQRRPT_QRCP_TRACE") != nullptr;
+    a.trace = tracing ? ws.get<unsigned long long>("qrcp.trace", 512 * 6) : nullptr;
+    if (a.trace) CQ_CUDA(cudaMemsetAsync(a.trace, 0, 512 * 6 * sizeof(unsigned long long), st), "trace memset");
     void *args[] = {&a};
     CQ_CUDA(cudaLaunchCooperativeKernel((void *)qrcp_kernel, dim3(G), dim3(kQrcpThreads), args, smem, st),
             "qrcp cooperative launch");
@@ -335,6 +507,21 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     CQ_TRY(check_launch("qrcp_extract_kernel"));
     CQ_CUDA(cudaMemcpyAsync(k_sk, a.k_out, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "k_sk d2h");
     CQ_CUDA(cudaStreamSynchronize(st), "qrcp sync");
+    if (a.trace) {  // debug: mean per-phase ns over the first steps
+        std::vector<unsigned long long> h(512 * 6);
+        cudaMemcpy(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost);
+        double acc[5] = {0, 0, 0, 0, 0};
+        int cnt = 0;
+        for (int s2 = 0; s2 + 1 < 512 && s2 + 1 < *k_sk; ++s2) {
+            for (int q = 0; q < 4; ++q) acc[q] += (double)(h[s2 * 6 + q + 1] - h[s2 * 6 + q]);
+            acc[4] += (double)(h[(s2 + 1) * 6] - h[s2 * 6 + 4]);
+            ++cnt;
+        }
+        if (cnt)
+            fprintf(stderr, "qrcp trace (G=%d, d=%lld, n=%lld, %d steps): argmax %.0f ns, reflector %.0f ns, "
+                    "columns %.0f ns, partials %.0f ns, barrier %.0f ns\n", G, (long long)d, (long long)n, cnt,
+                    acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt);
+    }
     return 0;
 }
 
