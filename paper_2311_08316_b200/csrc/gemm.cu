@@ -1,147 +1,267 @@
-// K5b: Gram (SYRK) and a general FP64 DMMA GEMM.
+// FP64 DMMA GEMM engine shared by the contraction passes.
 //
-// gram: G = X^T X (reference gram, linalg.cc:298-307): upper-triangle 64x64
-// tiles, split-K over the m rows into fixed slices; each (tile, slice) CTA
-// writes a partial, a second kernel sums the slices in fixed order and
-// mirrors the upper triangle, so G is deterministic and bitwise symmetric
-// (the property test_linalg.cc:179-189 pins). Because every entry's
-// arithmetic depends only on its own two columns and the slice partition of
-// m, the leading j x j block of G equals gram(X[:, :j]) bitwise — which is
-// what makes the reference's Cholesky-failure retry free (cqrrpt.cc:162-164).
+//   C_out = alpha * op(A) * B + beta * C_in        op(A) in {A, A^T}
 //
-// gemm: C = alpha op(A) B + beta C with op(A) in {A, A^T}, used by the
-// blocked Cholesky trailing update, the R = R_pre R_sk product and the
-// device validator.
+// Used by: the recursive TRSM updates (K5a/K8, trsm.cu), the Gram SYRK (K5b,
+// split-K partials), the blocked Cholesky trailing update (K6), the
+// R = R_pre R_sk product (K9) and the device validator.
 //
-// Both: 128 threads, 64 x 64 CTA tile (2 x 2 warps of 32 x 32 = 16 DMMA
-// accumulators each), K chunks of 32 through a 3-stage cp.async pipeline,
-// operand tiles padded so every m8n8k4 fragment load is conflict-free.
+// sm_100a has no FP64 tcgen05 kind, so the MMA is warp-level
+// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4). CTA = 4 warps, tile 64x128 or
+// 128x64, every warp owns a 32x64 accumulator block (32 DMMAs per 4-deep k
+// step against 12 fragment loads). K streams in 16-deep chunks through a
+// 3-stage cp.async pipeline; the shared tiles are unpadded and XOR-swizzled
+// so all fragment loads and async fills are bank-conflict free, which keeps a
+// stage at 24 KB and allows 3 CTAs (12 warps) per SM.
 #include "common.cuh"
+#include "gemm.cuh"
 #include "internal.hh"
 
 namespace cqg {
 
-constexpr int kGT = 64;        // tile
-constexpr int kGBK = 32;       // K chunk
-constexpr int kGStages = 3;
-constexpr int kGThreads = 128;
-constexpr int kLdK = kGBK + 4;   // [mn][k] layout, 36 = 4 mod 16
-constexpr int kLdM = kGT + 8;    // [k][mn] layout, 72 = 8 mod 16
-constexpr size_t kGemmSmem = sizeof(double) * kGStages * (kGBK * kLdM + kGT * kLdK);  // covers both A layouts
-constexpr size_t kSyrkSmem = sizeof(double) * kGStages * 2 * kGT * kLdK;
+constexpr int kBK = 16;
+constexpr int kStages = 3;
+constexpr int kThreads = 128;
 
-// ---------------------------------------------------------------------------
-// loaders (8-byte cp.async, zero fill outside the matrix)
-// ---------------------------------------------------------------------------
-// tile[mn][k] <- src[(c0+mn)*ld + k0 + k]   (column mn contiguous along k)
-CQ_DEVI void load_mn_k(double *tile, const double *src, int64_t ld, int64_t c0, int64_t ncols, int64_t k0,
-                       int64_t kmax, int tid) {
-#pragma unroll
-    for (int it = 0; it < (kGT * kGBK) / kGThreads; ++it) {
-        int q = it * kGThreads + tid;
-        int mn = q / kGBK, kk = q % kGBK;
-        bool ok = (c0 + mn < ncols) && (k0 + kk < kmax);
-        const double *p = src + (ok ? (c0 + mn) * ld + k0 + kk : 0);
-        cp_async8_zfill(tile + mn * kLdK + kk, p, ok ? 8 : 0);
-    }
+// swizzled offsets (doubles) inside a stage tile
+// [k][m] layout (A, not transposed): BM doubles per k row
+template <int BM>
+CQ_DEVI int sw_km(int k, int m) {
+    return k * BM + (m ^ ((k & 1) << 3));
 }
-// tile[k][mn] <- src[(k0+k)*ld + r0 + mn]   (column k contiguous along mn)
-CQ_DEVI void load_k_mn(double *tile, const double *src, int64_t ld, int64_t r0, int64_t nrows, int64_t k0,
-                       int64_t kmax, int tid) {
-#pragma unroll
-    for (int it = 0; it < (kGT * kGBK) / kGThreads; ++it) {
-        int q = it * kGThreads + tid;
-        int kk = q / kGT, mn = q % kGT;
-        bool ok = (r0 + mn < nrows) && (k0 + kk < kmax);
-        const double *p = src + (ok ? (k0 + kk) * ld + r0 + mn : 0);
-        cp_async8_zfill(tile + kk * kLdM + mn, p, ok ? 8 : 0);
-    }
-}
+// [r][k] layout (B, and A transposed): 16 doubles per row
+CQ_DEVI int sw_rk(int r, int k) { return r * kBK + (k ^ ((r & 3) << 2)); }
 
-// 32x32 warp tile on a 4-deep k step. a_at(mi) / b_at(ni) give the fragment.
-#define DMMA_WARP_STEP(acc, A_EXPR, B_EXPR)                                         \
-    {                                                                               \
-        double af[4], bf[4];                                                        \
-        _Pragma("unroll") for (int mi = 0; mi < 4; ++mi) af[mi] = (A_EXPR);         \
-        _Pragma("unroll") for (int ni = 0; ni < 4; ++ni) bf[ni] = (B_EXPR);         \
-        _Pragma("unroll") for (int mi = 0; mi < 4; ++mi)                            \
-            _Pragma("unroll") for (int ni = 0; ni < 4; ++ni)                        \
-                dmma884(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);            \
-    }
-
-// ---------------------------------------------------------------------------
-// SYRK partials: tile list (ti, tj) with ti <= tj, split-K slices.
-// part[(slice * ntiles + tile) * 64*64 + c*64 + r] (col-major 64 x 64)
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kGThreads, 2)
-    syrk_partial_kernel(int64_t m, int64_t k, const double *__restrict__ x, int64_t ldx, int64_t rows_per_slice,
-                        const int2 *__restrict__ tiles, int64_t ntiles, double *__restrict__ part) {
+template <int BM, int BN, bool TA>
+__global__ void __launch_bounds__(kThreads, 3) dgemm_kernel(GemmArgs P) {
+    constexpr int WM = BM / 32;  // warps along M
+    static_assert(WM * (BN / 64) == 4, "4 warps of 32x64");
     extern __shared__ __align__(16) double sm[];
+    if (P.skip_flag && *P.skip_flag) return;
+    int64_t tm, tn;
+    if (P.tiles) {
+        const int2 tt = P.tiles[blockIdx.x];
+        tm = tt.x;
+        tn = tt.y;
+    } else {
+        tm = blockIdx.x;
+        tn = blockIdx.y;
+    }
+    const int64_t r0 = tm * BM, c0 = tn * BN;
+    if (P.upper_only && r0 > c0 + BN - 1) return;
+    const int64_t z = blockIdx.z;
+    const int64_t kbeg = z * P.k_per_split;
+    const int64_t kend = cmin<int64_t>(kbeg + P.k_per_split, P.K);
+    const int nchunks = (int)((kend - kbeg + kBK - 1) / kBK);
+
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
-    const int wm = warp >> 1, wn = warp & 1;
-    const int64_t tile = blockIdx.x, slice = blockIdx.y;
-    const int2 tt = tiles[tile];
-    const int64_t ci = (int64_t)tt.x * kGT, cj = (int64_t)tt.y * kGT;
-    const int64_t kbeg = slice * rows_per_slice;
-    const int64_t kend = cmin<int64_t>(kbeg + rows_per_slice, m);
-    const int nchunks = (int)((kend - kbeg + kGBK - 1) / kGBK);
+    const int wm = warp % WM, wn = warp / WM;
+    double *const As0 = sm;
+    double *const Bs0 = sm + kStages * BM * kBK;
 
-    double acc[4][4][2];
+    double acc[4][8][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    auto As = [&](int s) { return sm + s * 2 * kGT * kLdK; };
-    auto Bs = [&](int s) { return sm + s * 2 * kGT * kLdK + kGT * kLdK; };
     auto load = [&](int kc, int s) {
-        int64_t k0 = kbeg + (int64_t)kc * kGBK;
-        load_mn_k(As(s), x, ldx, ci, k, k0, kend, tid);
-        load_mn_k(Bs(s), x, ldx, cj, k, k0, kend, tid);
-    };
+        const int64_t k0 = kbeg + (int64_t)kc * kBK;
+        double *as = As0 + s * BM * kBK;
+        double *bs = Bs0 + s * BN * kBK;
+        if (!TA) {  // A: M x K col-major, tile [k][m]
 #pragma unroll
-    for (int s = 0; s < kGStages - 1; ++s) {
+            for (int it = 0; it < BM * kBK / kThreads; ++it) {
+                int q = it * kThreads + tid;
+                int kk = q / BM, mm = q % BM;
+                bool ok = (r0 + mm < P.M) && (k0 + kk < kend);
+                const double *src = P.A + (ok ? (k0 + kk) * P.lda + r0 + mm : 0);
+                cp_async8_zfill(as + sw_km<BM>(kk, mm), src, ok ? 8 : 0);
+            }
+        } else {  // A: K x M col-major (op = A^T), tile [m][k]
+#pragma unroll
+            for (int it = 0; it < BM * kBK / kThreads; ++it) {
+                int q = it * kThreads + tid;
+                int mm = q / kBK, kk = q % kBK;
+                bool ok = (r0 + mm < P.M) && (k0 + kk < kend);
+                const double *src = P.A + (ok ? (r0 + mm) * P.lda + k0 + kk : 0);
+                cp_async8_zfill(as + sw_rk(mm, kk), src, ok ? 8 : 0);
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < BN * kBK / kThreads; ++it) {  // B: K x N col-major, tile [n][k]
+            int q = it * kThreads + tid;
+            int nn = q / kBK, kk = q % kBK;
+            bool ok = (c0 + nn < P.N) && (k0 + kk < kend);
+            const double *src = P.B + (ok ? (c0 + nn) * P.ldb + k0 + kk : 0);
+            cp_async8_zfill(bs + sw_rk(nn, kk), src, ok ? 8 : 0);
+        }
+    };
+
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) {
         if (s < nchunks) load(s, s);
         cp_async_commit();
     }
     for (int kc = 0; kc < nchunks; ++kc) {
-        cp_async_wait<kGStages - 2>();
+        cp_async_wait<kStages - 2>();
         __syncthreads();
         {
-            int nk = kc + kGStages - 1;
-            if (nk < nchunks) load(nk, nk % kGStages);
+            int nk = kc + kStages - 1;
+            if (nk < nchunks) load(nk, nk % kStages);
             cp_async_commit();
         }
-        const double *as = As(kc % kGStages) + (wm * 32 + g) * kLdK + t;
-        const double *bs = Bs(kc % kGStages) + (wn * 32 + g) * kLdK + t;
+        const double *as = As0 + (kc % kStages) * BM * kBK;
+        const double *bs = Bs0 + (kc % kStages) * BN * kBK;
+        const int mb = wm * 32 + g, nb = wn * 64 + g;
 #pragma unroll
-        for (int kk = 0; kk < kGBK; kk += 4)
-            DMMA_WARP_STEP(acc, as[mi * 8 * kLdK + kk], bs[ni * 8 * kLdK + kk]);
+        for (int kk = 0; kk < kBK; kk += 4) {
+            double af[4], bf[8];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+                af[mi] = TA ? as[sw_rk(mb + 8 * mi, kk + t)] : as[sw_km<BM>(kk + t, mb + 8 * mi)];
+#pragma unroll
+            for (int ni = 0; ni < 8; ++ni) bf[ni] = bs[sw_rk(nb + 8 * ni, kk + t)];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 8; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+        }
     }
     cp_async_wait<0>();
-    double *out = part + (slice * ntiles + tile) * (int64_t)(kGT * kGT);
+
+    // ---- epilogue ------------------------------------------------------------
+    if (P.part) {  // split-K partial tile, column-major BM x BN
+        const int64_t tix = P.tiles ? (int64_t)blockIdx.x : (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+        double *out = P.part + ((int64_t)z * P.ntiles_part + tix) * (int64_t)(BM * BN);
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+        for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-            int r = wm * 32 + mi * 8 + g, c = wn * 32 + ni * 8 + 2 * t;
-            out[c * kGT + r] = acc[mi][ni][0];
-            out[(c + 1) * kGT + r] = acc[mi][ni][1];
+            for (int ni = 0; ni < 8; ++ni)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    int r = wm * 32 + mi * 8 + g, c = wn * 64 + ni * 8 + 2 * t + v;
+                    out[c * BM + r] = acc[mi][ni][v];
+                }
+        return;
+    }
+#pragma unroll
+    for (int ni = 0; ni < 8; ++ni)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            const int64_t j = c0 + wn * 64 + ni * 8 + 2 * t + v;
+            if (j >= P.N) continue;
+            const double *cin = nullptr;
+            if (P.beta != 0.0) cin = P.Cin + (P.cin_cols ? P.cin_cols[j] : j) * P.ldcin;
+            double *cout = P.Cout + j * P.ldc;
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) {
+                const int64_t i = r0 + wm * 32 + mi * 8 + g;
+                if (i < P.M && (!P.upper_only || i <= j)) {
+                    double val = P.alpha * acc[mi][ni][v];
+                    if (cin) val = fma(P.beta, cin[i], val);
+                    cout[i] = val;
+                }
+            }
         }
 }
 
-// G[i][j] = sum_s part[s][tile(i,j)] for i <= j (upper), mirrored below.
-__global__ void syrk_reduce_kernel(int64_t k, int64_t nslices, const int2 *__restrict__ tiles, int64_t ntiles,
+template <int BM, int BN, bool TA>
+size_t gemm_smem() {
+    return sizeof(double) * kStages * (BM + BN) * kBK;
+}
+
+template <int BM, int BN, bool TA>
+static int launch(const GemmArgs &P, dim3 grid, cudaStream_t st) {
+    auto kern = dgemm_kernel<BM, BN, TA>;
+    const size_t smem = gemm_smem<BM, BN, TA>();
+    static thread_local int configured[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !configured[dev]) {
+        CQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "gemm attr");
+        configured[dev] = 1;
+    }
+    kern<<<grid, kThreads, smem, st>>>(P);
+    note_launch();
+    return check_launch("dgemm_kernel");
+}
+
+// Tile shape: 128x64 for tall-skinny outputs (N <= 64), 64x128 otherwise.
+int gemm_ex(bool trans_a, GemmArgs P, int64_t splits, cudaStream_t st) {
+    if (P.M <= 0 || P.N <= 0) return 0;
+    if (splits < 1) splits = 1;
+    if (P.k_per_split <= 0) P.k_per_split = (P.K + splits - 1) / splits;
+    const bool tall = P.N <= 64;
+    const int BM = tall ? 128 : 64, BN = tall ? 64 : 128;
+    dim3 grid;
+    if (P.tiles) grid = dim3((unsigned)P.ntiles_part, 1, (unsigned)splits);
+    else grid = dim3((unsigned)((P.M + BM - 1) / BM), (unsigned)((P.N + BN - 1) / BN), (unsigned)splits);
+    if (tall) return trans_a ? launch<128, 64, true>(P, grid, st) : launch<128, 64, false>(P, grid, st);
+    return trans_a ? launch<64, 128, true>(P, grid, st) : launch<64, 128, false>(P, grid, st);
+}
+
+int gemm(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const double *a, int64_t lda,
+         const double *b, int64_t ldb, double beta, double *c, int64_t ldc, cudaStream_t st) {
+    GemmArgs P{};
+    P.M = M;
+    P.N = N;
+    P.K = K;
+    P.A = a;
+    P.lda = lda;
+    P.B = b;
+    P.ldb = ldb;
+    P.Cin = c;
+    P.ldcin = ldc;
+    P.Cout = c;
+    P.ldc = ldc;
+    P.alpha = alpha;
+    P.beta = beta;
+    return gemm_ex(trans_a, P, 1, st);
+}
+
+int gemm_tn_upper(int64_t N, int64_t K, double alpha, const double *a, int64_t lda, const double *b, int64_t ldb,
+                  double beta, double *c, int64_t ldc, const int64_t *skip_flag, cudaStream_t st) {
+    GemmArgs P{};
+    P.M = N;
+    P.N = N;
+    P.K = K;
+    P.A = a;
+    P.lda = lda;
+    P.B = b;
+    P.ldb = ldb;
+    P.Cin = c;
+    P.ldcin = ldc;
+    P.Cout = c;
+    P.ldc = ldc;
+    P.alpha = alpha;
+    P.beta = beta;
+    P.upper_only = 1;
+    P.skip_flag = skip_flag;
+    return gemm_ex(true, P, 1, st);
+}
+
+// ---------------------------------------------------------------------------
+// Gram: G = X^T X (reference gram, linalg.cc:298-307). 64x128 tiles covering
+// the upper triangle, split-K over m into fixed slices, then a fixed-order
+// slice sum that mirrors the upper triangle -> deterministic and bitwise
+// symmetric (test_linalg.cc:179-189). Every entry depends only on its two
+// columns and the (k0-independent) slice partition of m, so the leading j x j
+// block of G equals gram(X[:, :j]) bitwise — the reference's Cholesky-retry
+// property (cqrrpt.cc:162-164) holds without recomputation.
+// ---------------------------------------------------------------------------
+__global__ void gram_reduce_kernel(int64_t k, int64_t nslices, const int2 *__restrict__ tiles, int64_t ntiles,
                                    const double *__restrict__ part, double *__restrict__ gmat, int64_t ldg) {
+    constexpr int BM = 64, BN = 128;
     const int64_t tile = blockIdx.x;
     const int2 tt = tiles[tile];
-    for (int q = threadIdx.x; q < kGT * kGT; q += blockDim.x) {
-        int c = q / kGT, r = q % kGT;
-        int64_t i = (int64_t)tt.x * kGT + r, j = (int64_t)tt.y * kGT + c;
+    for (int q = threadIdx.x; q < BM * BN; q += blockDim.x) {
+        int c = q / BM, r = q % BM;
+        int64_t i = (int64_t)tt.x * BM + r, j = (int64_t)tt.y * BN + c;
         if (i >= k || j >= k || i > j) continue;
         double s = 0.0;
-        for (int64_t sl = 0; sl < nslices; ++sl) s += part[(sl * ntiles + tile) * (int64_t)(kGT * kGT) + q];
+        for (int64_t sl = 0; sl < nslices; ++sl) s += part[(sl * ntiles + tile) * (int64_t)(BM * BN) + q];
         gmat[j * ldg + i] = s;
         gmat[i * ldg + j] = s;
     }
@@ -150,143 +270,48 @@ __global__ void syrk_reduce_kernel(int64_t k, int64_t nslices, const int2 *__res
 int gram(int64_t m, int64_t k, const double *x, int64_t ldx, double *gmat, int64_t ldg, Workspace &ws,
          cudaStream_t st) {
     if (k <= 0) return 0;
-    const int64_t nt = (k + kGT - 1) / kGT;
-    const int64_t ntiles = nt * (nt + 1) / 2;
-    int2 *tiles = ws.get<int2>("gram.tiles", ntiles);
-    std::vector<int2> h((size_t)ntiles);
-    {
-        size_t q = 0;
-        for (int64_t j = 0; j < nt; ++j)
-            for (int64_t i = 0; i <= j; ++i) h[q++] = make_int2((int)i, (int)j);
-    }
-    // slices: fill >= 2 waves of 2 CTAs/SM, slices at least 256 rows
+    constexpr int BM = 64, BN = 128;
+    const int64_t tm = (k + BM - 1) / BM, tn = (k + BN - 1) / BN;
+    std::vector<int2> h;
+    for (int64_t j = 0; j < tn; ++j)
+        for (int64_t i = 0; i < tm; ++i)
+            if (i * BM <= j * BN + BN - 1) h.push_back(make_int2((int)i, (int)j));
+    const int64_t ntiles = (int64_t)h.size();
+    // split-K slices: fill >= 3 CTAs per SM for a couple of waves, >= 512 rows each
     const int sms = num_sms();
-    int64_t want = std::max<int64_t>(1, (4 * (int64_t)sms + ntiles - 1) / ntiles);
-    int64_t max_slices = std::max<int64_t>(1, m / 256);
-    int64_t nslices = std::min(want, max_slices);
-    int64_t rps = ((m + nslices - 1) / nslices + kGBK - 1) / kGBK * kGBK;
+    int64_t want = std::max<int64_t>(1, (6 * (int64_t)sms + ntiles - 1) / ntiles);
+    int64_t nslices = std::min<int64_t>(want, std::max<int64_t>(1, m / 512));
+    int64_t rps = ((m + nslices - 1) / nslices + kBK - 1) / kBK * kBK;
     nslices = std::max<int64_t>(1, (m + rps - 1) / rps);
-    double *part = ws.get<double>("gram.part", (size_t)(nslices * ntiles * kGT * kGT));
+    int2 *tiles = ws.get<int2>("gram.tiles", (size_t)ntiles);
+    double *part = ws.get<double>("gram.part", (size_t)(nslices * ntiles * BM * BN));
     if (!tiles || !part) return fail_nomem("gram workspace");
     CQ_CUDA(cudaMemcpyAsync(tiles, h.data(), sizeof(int2) * ntiles, cudaMemcpyHostToDevice, st), "tiles h2d");
-    CQ_CUDA(cudaFuncSetAttribute(syrk_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem),
-            "syrk smem attr");
     if (m > 0) {
-        syrk_partial_kernel<<<dim3((unsigned)ntiles, (unsigned)nslices), kGThreads, kSyrkSmem, st>>>(
-            m, k, x, ldx, rps, tiles, ntiles, part);
-        note_launch();
+        GemmArgs P{};
+        P.M = k;
+        P.N = k;
+        P.K = m;
+        P.A = x;
+        P.lda = ldx;
+        P.B = x;
+        P.ldb = ldx;
+        P.alpha = 1.0;
+        P.k_per_split = rps;
+        P.part = part;
+        P.ntiles_part = ntiles;
+        P.tiles = tiles;
+        GemmArgs *pp = &P;
+        dim3 grid((unsigned)ntiles, 1, (unsigned)nslices);
+        CQ_TRY((launch<64, 128, true>(*pp, grid, st)));
     } else {
-        CQ_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * ntiles * kGT * kGT, st), "memset part");
+        CQ_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * ntiles * BM * BN, st), "memset part");
         nslices = 1;
     }
-    syrk_reduce_kernel<<<(unsigned)ntiles, 256, 0, st>>>(k, nslices, tiles, ntiles, part, gmat, ldg);
+    gram_reduce_kernel<<<(unsigned)ntiles, 256, 0, st>>>(k, nslices, tiles, ntiles, part, gmat, ldg);
     note_launch();
-    // the host vector must outlive the async copy
-    CQ_CUDA(cudaStreamSynchronize(st), "gram sync");
-    return check_launch("syrk kernels");
-}
-
-// ---------------------------------------------------------------------------
-// general GEMM: C (M x N) = alpha op(A) B + beta C. UPPER_ONLY skips tiles
-// strictly below the diagonal (ti > tj) and entries i > j inside diagonal tiles.
-// ---------------------------------------------------------------------------
-template <bool TRANS_A, bool UPPER_ONLY>
-__global__ void __launch_bounds__(kGThreads, 2)
-    gemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double *__restrict__ a, int64_t lda,
-                const double *__restrict__ b, int64_t ldb, double beta, double *__restrict__ c, int64_t ldc,
-                const int64_t *__restrict__ skip_flag) {
-    if (skip_flag && *skip_flag) return;
-    const int64_t ti = blockIdx.x, tj = blockIdx.y;
-    if (UPPER_ONLY && ti > tj) return;
-    extern __shared__ __align__(16) double sm[];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int g = lane >> 2, t = lane & 3;
-    const int wm = warp >> 1, wn = warp & 1;
-    const int64_t r0 = ti * kGT, c0 = tj * kGT;
-    constexpr int aStride = TRANS_A ? kGT * kLdK : kGBK * kLdM;
-    auto As = [&](int s) { return sm + s * (aStride + kGT * kLdK); };
-    auto Bs = [&](int s) { return sm + s * (aStride + kGT * kLdK) + aStride; };
-    const int nchunks = (int)((K + kGBK - 1) / kGBK);
-
-    double acc[4][4][2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-    auto load = [&](int kc, int s) {
-        int64_t k0 = (int64_t)kc * kGBK;
-        if (TRANS_A) load_mn_k(As(s), a, lda, r0, M, k0, K, tid);   // A is K x M
-        else load_k_mn(As(s), a, lda, r0, M, k0, K, tid);           // A is M x K
-        load_mn_k(Bs(s), b, ldb, c0, N, k0, K, tid);
-    };
-#pragma unroll
-    for (int s = 0; s < kGStages - 1; ++s) {
-        if (s < nchunks) load(s, s);
-        cp_async_commit();
-    }
-    for (int kc = 0; kc < nchunks; ++kc) {
-        cp_async_wait<kGStages - 2>();
-        __syncthreads();
-        {
-            int nk = kc + kGStages - 1;
-            if (nk < nchunks) load(nk, nk % kGStages);
-            cp_async_commit();
-        }
-        const double *bs = Bs(kc % kGStages) + (wn * 32 + g) * kLdK + t;
-        if (TRANS_A) {
-            const double *as = As(kc % kGStages) + (wm * 32 + g) * kLdK + t;
-#pragma unroll
-            for (int kk = 0; kk < kGBK; kk += 4)
-                DMMA_WARP_STEP(acc, as[mi * 8 * kLdK + kk], bs[ni * 8 * kLdK + kk]);
-        } else {
-            const double *as = As(kc % kGStages) + t * kLdM + wm * 32 + g;
-#pragma unroll
-            for (int kk = 0; kk < kGBK; kk += 4)
-                DMMA_WARP_STEP(acc, as[kk * kLdM + mi * 8], bs[ni * 8 * kLdK + kk]);
-        }
-    }
-    cp_async_wait<0>();
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-            for (int v = 0; v < 2; ++v) {
-                int64_t i = r0 + wm * 32 + mi * 8 + g, j = c0 + wn * 32 + ni * 8 + 2 * t + v;
-                if (i < M && j < N && (!UPPER_ONLY || i <= j)) {
-                    double val = alpha * acc[mi][ni][v];
-                    if (beta != 0.0) val = fma(beta, c[j * ldc + i], val);
-                    c[j * ldc + i] = val;
-                }
-            }
-}
-
-template <bool TA, bool UP>
-static int launch_gemm(int64_t M, int64_t N, int64_t K, double alpha, const double *a, int64_t lda,
-                       const double *b, int64_t ldb, double beta, double *c, int64_t ldc, const int64_t *skip,
-                       cudaStream_t st) {
-    auto kern = gemm_kernel<TA, UP>;
-    CQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem), "gemm attr");
-    dim3 grid((unsigned)((M + kGT - 1) / kGT), (unsigned)((N + kGT - 1) / kGT));
-    kern<<<grid, kGThreads, kGemmSmem, st>>>(M, N, K, alpha, a, lda, b, ldb, beta, c, ldc, skip);
-    note_launch();
-    return check_launch("gemm_kernel");
-}
-
-int gemm(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const double *a, int64_t lda,
-         const double *b, int64_t ldb, double beta, double *c, int64_t ldc, cudaStream_t st) {
-    if (M <= 0 || N <= 0) return 0;
-    return trans_a ? launch_gemm<true, false>(M, N, K, alpha, a, lda, b, ldb, beta, c, ldc, nullptr, st)
-                   : launch_gemm<false, false>(M, N, K, alpha, a, lda, b, ldb, beta, c, ldc, nullptr, st);
-}
-
-// upper-triangle-only C -= A^T B (Cholesky trailing update), skipped when
-// *skip_flag != 0 (a failure was already found)
-int gemm_tn_upper(int64_t N, int64_t K, double alpha, const double *a, int64_t lda, const double *b, int64_t ldb,
-                  double beta, double *c, int64_t ldc, const int64_t *skip_flag, cudaStream_t st) {
-    if (N <= 0) return 0;
-    return launch_gemm<true, true>(N, N, K, alpha, a, lda, b, ldb, beta, c, ldc, skip_flag, st);
+    CQ_CUDA(cudaStreamSynchronize(st), "gram sync");  // h must outlive the async copy
+    return check_launch("gram_reduce_kernel");
 }
 
 }  // namespace cqg

@@ -1,0 +1,33 @@
+// Arguments of the FP64 DMMA GEMM engine (gemm.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cqg {
+
+struct GemmArgs {
+    int64_t M, N, K;
+    const double *A;  // op(A) = A (M x K) or A^T (A is K x M); column-major
+    int64_t lda;
+    const double *B;  // K x N, column-major
+    int64_t ldb;
+    const double *Cin;  // read when beta != 0; optional column gather
+    int64_t ldcin;
+    const int64_t *cin_cols;
+    double *Cout;
+    int64_t ldc;
+    double alpha, beta;
+    int64_t k_per_split;      // split-K slice length (0 = K / splits)
+    double *part;             // split-K partial tiles (BM*BN each) instead of C
+    int64_t ntiles_part;      // tiles per slice in `part` / length of `tiles`
+    const int2 *tiles;        // optional explicit (tile_m, tile_n) list
+    const int64_t *skip_flag; // device flag: nonzero -> the launch is a no-op
+    int upper_only;           // only entries i <= j (and tiles touching them)
+};
+
+// C_out = alpha op(A) B + beta C_in, optionally split over K into `splits`
+// partial tiles (P.part non-null).
+int gemm_ex(bool trans_a, GemmArgs P, int64_t splits, cudaStream_t st);
+
+}  // namespace cqg

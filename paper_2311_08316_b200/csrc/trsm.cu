@@ -6,103 +6,114 @@
 // (dense_matrix.hh:70-80, cqrrpt.cc:262,165) and to M_pre (cqrrpt.cc:280).
 //
 // Left-looking blocked algorithm, one launch per 64-wide column block jb:
-//   X[:, jb] = (B[:, cols(jb)] - X[:, <jb] * U[<jb, jb]) * U[jb, jb]^{-1}
-// The update is a DMMA GEMM (mma.sync.m8n8k4.f64 -> DMMA.8x8x4): a CTA owns a
-// 128 x 64 tile (4 warps x 32 rows x 64 cols, 32 DMMA accumulators / warp),
-// K streams through a 3-stage cp.async pipeline in 16-deep chunks. The
-// epilogue stages the accumulator in shared memory, gathers the pivoted
-// source columns (coalesced: thread = row), and solves the 64 x 64 diagonal
-// block by row substitution in registers with the reference's per-element
-// order (subtract U(s,c) x_s for s ascending, then multiply by 1/U(c,c)).
+//   X[:, jb] = (B[:, cols(jb)] - X[:, <jb] U[<jb, jb]) U[jb, jb]^{-1}
+// A CTA owns a 64 x 64 tile (4 warps, 32 x 32 DMMA accumulators each). The
+// accumulator is initialised with the gathered source columns (their loads
+// overlap the main loop) and accumulates B - X U over K = 64*jb with
+// mma.sync.m8n8k4.f64 (DMMA.8x8x4), K streaming in 16-deep chunks through a
+// 3-stage cp.async pipeline of XOR-swizzled (conflict-free, unpadded) tiles.
+// The epilogue solves the 64 x 64 diagonal block by row substitution in
+// registers with the reference's per-element order (subtract U(s,c) x_s for
+// s ascending, then multiply by 1/U(c,c)); with 3 CTAs per SM one CTA's
+// substitution overlaps its neighbours' DMMA work.
 // Algorithmic flops: m*k^2 (the reference's count, flop_model term).
 #include "common.cuh"
 #include "internal.hh"
 
 namespace cqg {
 
-constexpr int kTBM = 128;  // rows per CTA
-constexpr int kTNB = 64;   // column block
-constexpr int kTBK = 16;   // K chunk
-constexpr int kTStages = 3;
-constexpr int kTThreads = 128;
-constexpr int kLdA = kTBM + 8;  // 136 = 8 mod 16 -> conflict-free A fragments
-constexpr int kLdB = kTBK + 4;  // 20  = 4 mod 16 -> conflict-free B fragments
-constexpr int kLdT = kTNB + 1;
+constexpr int kBM = 64;    // rows per CTA
+constexpr int kNB = 64;    // column block
+constexpr int kBK = 16;    // K chunk
+constexpr int kStages = 3;
+constexpr int kThreads = 128;
+constexpr int kLdT = kNB + 2;  // 66: conflict-free double2 row access
+constexpr int kLdU = kNB + 2;  // Uj row-major [s][c], 16-byte aligned rows
 
-constexpr size_t kPipeBytes = sizeof(double) * kTStages * (kTBK * kLdA + kTNB * kLdB);
-constexpr size_t kEpiBytes = sizeof(double) * (kTBM * kLdT + kTNB * kTNB + kTNB);
-constexpr size_t kTrsmSmem = (kPipeBytes > kEpiBytes) ? kPipeBytes : kEpiBytes;
+constexpr size_t kPipeBytes = sizeof(double) * kStages * (kBM + kNB) * kBK;
+constexpr size_t kEpiBytes = sizeof(double) * (kBM * kLdT + kNB * kLdU + kNB);
+constexpr size_t kTrsmSmem = kPipeBytes > kEpiBytes ? kPipeBytes : kEpiBytes;
 
-__global__ void __launch_bounds__(kTThreads, 2)
+CQ_DEVI int sw_km(int k, int m) { return k * kBM + (m ^ ((k & 1) << 3)); }   // A tile [k][m]
+CQ_DEVI int sw_rk(int r, int k) { return r * kBK + (k ^ ((r & 3) << 2)); }  // B tile [n][k]
+
+__global__ void __launch_bounds__(kThreads, 3)
     trsm_block_kernel(int64_t m, int64_t k, int64_t c0, const double *__restrict__ b, int64_t ldb,
                       const int64_t *__restrict__ cols, const double *__restrict__ u, int64_t ldu,
                       double *__restrict__ x, int64_t ldx) {
     extern __shared__ __align__(16) double sm[];
-    double *As = sm;                                 // [stages][16][136]
-    double *Bs = sm + kTStages * kTBK * kLdA;        // [stages][64][20]
+    double *As = sm;                        // [stages][16][64] swizzled
+    double *Bs = sm + kStages * kBK * kBM;  // [stages][64][16] swizzled
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
-    const int64_t row0 = (int64_t)blockIdx.x * kTBM;
-    const int nbw = (int)cmin<int64_t>(kTNB, k - c0);
+    const int wm = warp & 1, wn = warp >> 1;
+    const int64_t row0 = (int64_t)blockIdx.x * kBM;
+    const int nbw = (int)cmin<int64_t>(kNB, k - c0);
 
-    double acc[4][8][2];
+    // accumulator <- gathered right-hand side B[:, cols(c0 + c)]
+    double acc[4][4][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-    const int nchunks = (int)(c0 / kTBK);  // c0 is a multiple of 64
-    auto load_chunk = [&](int kc, int stage) {
-        const int64_t kb = (int64_t)kc * kTBK;
-        double *as = As + stage * kTBK * kLdA;
-        double *bs = Bs + stage * kTNB * kLdB;
-        // A: X[row0 + mm][kb + kk], 16 x 128, lanes along mm
+        for (int v = 0; v < 2; ++v) {
+            const int c = wn * 32 + ni * 8 + 2 * t + v;
+            const double *bc = (c < nbw) ? b + (cols ? __ldg(cols + c0 + c) : (c0 + c)) * ldb : nullptr;
 #pragma unroll
-        for (int it = 0; it < (kTBK * kTBM) / kTThreads; ++it) {
-            int q = it * kTThreads + tid;
-            int kk = q / kTBM, mm = q % kTBM;
-            int64_t row = row0 + mm;
-            const double *src = x + (kb + kk) * ldx + (row < m ? row : 0);
-            cp_async8_zfill(as + kk * kLdA + mm, src, row < m ? 8 : 0);
+            for (int mi = 0; mi < 4; ++mi) {
+                const int64_t row = row0 + wm * 32 + mi * 8 + g;
+                acc[mi][ni][v] = (bc && row < m) ? __ldg(bc + row) : 0.0;
+            }
         }
-        // B: U[kb + kk][c0 + nn], 16 x 64, lanes along kk
+
+    const int nchunks = (int)(c0 / kBK);  // c0 is a multiple of 64
+    auto load_chunk = [&](int kc, int stage) {
+        const int64_t kb = (int64_t)kc * kBK;
+        double *as = As + stage * kBK * kBM;
+        double *bs = Bs + stage * kNB * kBK;
 #pragma unroll
-        for (int it = 0; it < (kTBK * kTNB) / kTThreads; ++it) {
-            int q = it * kTThreads + tid;
-            int nn = q / kTBK, kk = q % kTBK;
+        for (int it = 0; it < (kBK * kBM) / kThreads; ++it) {  // A: X[row0 + mm][kb + kk]
+            int q = it * kThreads + tid;
+            int kk = q / kBM, mm = q % kBM;
+            int64_t row = row0 + mm;
+            cp_async8_zfill(as + sw_km(kk, mm), x + (kb + kk) * ldx + (row < m ? row : 0), row < m ? 8 : 0);
+        }
+#pragma unroll
+        for (int it = 0; it < (kBK * kNB) / kThreads; ++it) {  // B: U[kb + kk][c0 + nn]
+            int q = it * kThreads + tid;
+            int nn = q / kBK, kk = q % kBK;
             bool ok = nn < nbw;
-            const double *src = u + (c0 + (ok ? nn : 0)) * ldu + kb + kk;
-            cp_async8_zfill(bs + nn * kLdB + kk, src, ok ? 8 : 0);
+            cp_async8_zfill(bs + sw_rk(nn, kk), u + (c0 + (ok ? nn : 0)) * ldu + kb + kk, ok ? 8 : 0);
         }
     };
 
     if (nchunks > 0) {
 #pragma unroll
-        for (int s = 0; s < kTStages - 1; ++s) {
+        for (int s = 0; s < kStages - 1; ++s) {
             if (s < nchunks) load_chunk(s, s);
             cp_async_commit();
         }
         for (int kc = 0; kc < nchunks; ++kc) {
-            cp_async_wait<kTStages - 2>();
+            cp_async_wait<kStages - 2>();
             __syncthreads();
             {
-                int nk = kc + kTStages - 1;
-                if (nk < nchunks) load_chunk(nk, nk % kTStages);
+                int nk = kc + kStages - 1;
+                if (nk < nchunks) load_chunk(nk, nk % kStages);
                 cp_async_commit();
             }
-            const double *as = As + (kc % kTStages) * kTBK * kLdA + warp * 32 + g;
-            const double *bs = Bs + (kc % kTStages) * kTNB * kLdB + g * kLdB + t;
+            const double *as = As + (kc % kStages) * kBK * kBM;
+            const double *bs = Bs + (kc % kStages) * kNB * kBK;
+            const int mb = wm * 32 + g, nb = wn * 32 + g;
 #pragma unroll
-            for (int kk = 0; kk < kTBK; kk += 4) {
-                double af[4], bf[8];
+            for (int kk = 0; kk < kBK; kk += 4) {
+                double af[4], bf[4];
 #pragma unroll
-                for (int mi = 0; mi < 4; ++mi) af[mi] = as[(kk + t) * kLdA + mi * 8];
+                for (int mi = 0; mi < 4; ++mi) af[mi] = -as[sw_km(kk + t, mb + 8 * mi)];  // B - X U
 #pragma unroll
-                for (int ni = 0; ni < 8; ++ni) bf[ni] = bs[ni * 8 * kLdB + kk];
+                for (int ni = 0; ni < 4; ++ni) bf[ni] = bs[sw_rk(nb + 8 * ni, kk + t)];
 #pragma unroll
                 for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-                    for (int ni = 0; ni < 8; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+                    for (int ni = 0; ni < 4; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
             }
         }
         cp_async_wait<0>();
@@ -110,49 +121,51 @@ __global__ void __launch_bounds__(kTThreads, 2)
     __syncthreads();  // pipeline buffers are reused by the epilogue
 
     // ---- epilogue -------------------------------------------------------
-    double *Ts = sm;                       // [128][65]
-    double *Uj = sm + kTBM * kLdT;         // [64 cols][64 rows] col-major
-    double *inv = Uj + kTNB * kTNB;        // [64]
+    double *Ts = sm;               // [64][66] = B[:, cols] - X[:, <jb] U[<jb, jb]
+    double *Uj = sm + kBM * kLdT;  // [64 s][66] row-major: Uj[s][c] = U[c0+s][c0+c]
+    double *inv = Uj + kNB * kLdU;
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 8; ++ni) {
-            int r = warp * 32 + mi * 8 + g, c = ni * 8 + 2 * t;
-            Ts[r * kLdT + c] = acc[mi][ni][0];
-            Ts[r * kLdT + c + 1] = acc[mi][ni][1];
+        for (int ni = 0; ni < 4; ++ni) {
+            int r = wm * 32 + mi * 8 + g, c = wn * 32 + ni * 8 + 2 * t;
+            *reinterpret_cast<double2 *>(Ts + r * kLdT + c) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
         }
-    for (int q = tid; q < kTNB * kTNB; q += kTThreads) {
-        int cc = q / kTNB, ss = q % kTNB;  // Uj[cc][ss] = U[c0+ss][c0+cc]
+    for (int q = tid; q < kNB * kNB; q += kThreads) {
+        int cc = q / kNB, ss = q % kNB;  // coalesced over ss (a column of U)
         double v;
         if (cc < nbw) v = (ss <= cc) ? u[(c0 + cc) * ldu + c0 + ss] : 0.0;
         else v = (ss == cc) ? 1.0 : 0.0;
-        Uj[cc * kTNB + ss] = v;
+        Uj[ss * kLdU + cc] = v;
     }
     __syncthreads();
-    if (tid < kTNB) inv[tid] = 1.0 / Uj[tid * kTNB + tid];  // linalg.cc:272
+    if (tid < kNB) inv[tid] = 1.0 / Uj[tid * kLdU + tid];  // linalg.cc:272
     __syncthreads();
 
     const int64_t row = row0 + tid;
-    if (row < m) {
-        double tv[kTNB];
+    if (tid < kBM && row < m) {
+        double tv[kNB];
 #pragma unroll
-        for (int c = 0; c < kTNB; ++c) {
-            double bv = 0.0;
-            if (c < nbw) {
-                int64_t col = cols ? cols[c0 + c] : (c0 + c);
-                bv = b[col * ldb + row];
-            }
-            tv[c] = bv - Ts[tid * kLdT + c];
+        for (int c = 0; c < kNB; c += 2) {
+            const double2 v2 = *reinterpret_cast<const double2 *>(Ts + tid * kLdT + c);
+            tv[c] = v2.x;
+            tv[c + 1] = v2.y;
         }
 #pragma unroll
-        for (int s = 0; s < kTNB; ++s) {
+        for (int s = 0; s < kNB; ++s) {
             const double xs = tv[s] * inv[s];
             tv[s] = xs;
+            const double *us = Uj + s * kLdU;
+            if ((s + 1) & 1) tv[s + 1] = fma(-us[s + 1], xs, tv[s + 1]);  // odd start: one single
 #pragma unroll
-            for (int c = s + 1; c < kTNB; ++c) tv[c] = fma(-Uj[c * kTNB + s], xs, tv[c]);
+            for (int c = ((s + 1) & 1) ? s + 2 : s + 1; c < kNB; c += 2) {
+                const double2 u2 = *reinterpret_cast<const double2 *>(us + c);
+                tv[c] = fma(-u2.x, xs, tv[c]);
+                tv[c + 1] = fma(-u2.y, xs, tv[c + 1]);
+            }
         }
 #pragma unroll
-        for (int c = 0; c < kTNB; ++c)
+        for (int c = 0; c < kNB; ++c)
             if (c < nbw) x[(c0 + c) * ldx + row] = tv[c];
     }
 }
@@ -177,15 +190,11 @@ int trsm_right(int64_t m, int64_t k, const double *b, int64_t ldb, const int64_t
         set_error("trsm_right: singular preconditioner (zero diagonal)");
         return CQRRPT_GPU_ERR_SINGULAR;
     }
-    static bool attr = false;
-    if (!attr) {
-        CQ_CUDA(cudaFuncSetAttribute(trsm_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrsmSmem),
-                "trsm smem attr");
-        attr = true;
-    }
-    const unsigned grid = (unsigned)((m + kTBM - 1) / kTBM);
-    for (int64_t c0 = 0; c0 < k; c0 += kTNB) {
-        trsm_block_kernel<<<grid, kTThreads, kTrsmSmem, st>>>(m, k, c0, b, ldb, cols, u, ldu, x, ldx);
+    CQ_CUDA(cudaFuncSetAttribute(trsm_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrsmSmem),
+            "trsm smem attr");
+    const unsigned grid = (unsigned)((m + kBM - 1) / kBM);
+    for (int64_t c0 = 0; c0 < k; c0 += kNB) {
+        trsm_block_kernel<<<grid, kThreads, kTrsmSmem, st>>>(m, k, c0, b, ldb, cols, u, ldu, x, ldx);
         note_launch();
     }
     return check_launch("trsm_block_kernel");
