@@ -56,6 +56,9 @@ CQ_DEVI void cp_async8_zfill(void *smem, const void *gmem, int src_bytes) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
                  "r"(src_bytes));
 }
+CQ_DEVI void cp_async4(void *smem, const void *gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem)), "l"(gmem));
+}
 CQ_DEVI void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 CQ_DEVI void cp_async_wait() {
@@ -88,6 +91,22 @@ CQ_DEVI void grid_barrier(unsigned int *bar, unsigned int nblocks) {
             }
         }
         __threadfence();
+    }
+    __syncthreads();
+}
+
+// Monotonic-counter barrier: one atomic per CTA, completion = the counter
+// reaching `target` (= number of barriers so far x nblocks). The counter is
+// zeroed by the host before the launch.
+CQ_DEVI void grid_barrier_mono(unsigned long long *counter, unsigned long long target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(counter, 1ULL);
+        unsigned long long v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(counter) : "memory");
+        } while (v < target);
     }
     __syncthreads();
 }

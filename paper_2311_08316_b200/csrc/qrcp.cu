@@ -4,20 +4,29 @@
 // apply_reflector (linalg.cc:110-136), extract_upper (linalg.cc:177-183);
 // rank_stage1 (cqrrpt.cc:92-112).
 //
+// Bit-exact restatement: every floating-point operation of the reference is
+// performed in the reference's order (dot products with its fixed 4-way
+// reassociation, its FMA contractions as built), so R_sk, J and k_sk are
+// bit-identical to the reference's on the same sketch.
+//
 // One cooperative persistent kernel runs all n steps (the QRCP is a chain of
-// n dependent steps; launching per step would cost more than the step).
-// Columns never move in memory: a logical->physical column map (ping-pong per
-// step) implements the reference's column swaps, and the physical index of
-// the column finally at logical position j is exactly J[j] (the pivots are
-// the original column indices). Logical position j is owned by CTA j % G;
-// a warp applies the step's reflector to one column and downdates its
-// squared norm with the reference's cancellation safeguard
-// (updated <= sqrt(u) * w_ref -> recompute from the updated column,
-// qrcp.cc:76-88). The pivot search uses the reference's rule: largest
-// downdated squared norm, lowest logical index on ties (qrcp.cc:26-31), and
-// the stop test sqrt(max(w_p,0)) <= n*u*max_j ||col_j|| (qrcp.cc:52-62).
-// Every CTA recomputes the pivot column's reflector redundantly (same code,
-// same order -> identical bits), so one grid barrier per step suffices.
+// n dependent steps). Columns never move in memory: a logical->physical
+// column map (ping-pong per step) implements the reference's swaps, and the
+// physical index of the column finally at logical position j is J[j].
+// Logical position j is owned by CTA j % G and, inside it, by one warp. Per
+// step:
+//   * every CTA reduces the per-CTA argmax partials (largest downdated squared
+//     norm, lowest index on ties, qrcp.cc:26-31) and tests the stop rule
+//     sqrt(max(w_p,0)) <= n*u*max_j||col_j|| (qrcp.cc:52-62);
+//   * every CTA builds the pivot column's reflector redundantly (same code,
+//     same order -> identical bits), so one grid barrier per step suffices;
+//   * each warp applies it to its column and downdates the squared norm with
+//     the cancellation safeguard (qrcp.cc:76-88).
+// Columns are staged into shared memory with L2-coherent cp.async while the
+// pivot is decided; the products of each dot are formed by all 32 lanes in
+// parallel and only the ordered additions (lanes 0..3, one per reference
+// accumulator) stay serial. Grid barrier: one atomic per CTA on a monotonic
+// counter.
 #include <cstdio>
 #include <cstdlib>
 
@@ -27,34 +36,31 @@
 namespace cqg {
 
 constexpr int kQrcpThreads = 256;  // 8 warps; a warp owns one column at a time
+constexpr int kQrcpWarps = kQrcpThreads / 32;
 
 // ---------------------------------------------------------------------------
 // The reference's dot (linalg.cc:36-50) as compiled (see oracle/cqrrpt_oracle.c
-// orc_dot): four interleaved accumulators s_q over the 4-aligned body with
+// orc_dot): accumulators s_q (q = e mod 4) over the 4-aligned body with
 // separately rounded products, (s0 + s1) + (s2 + s3), then the <4-element
-// tail with the last term of an odd count fused. Lanes 0..3 of a warp own
-// s_0..s_3 (the ordered chains); the other lanes stage operands. This file is
-// compiled with --fmad=false: every FMA below is an explicit fma().
+// tail: products added in order, the last term of an odd count fused.
+// This file is compiled with --fmad=false: every FMA below is an explicit fma().
 // ---------------------------------------------------------------------------
 
-// lanes 0..3: accumulate body elements [b0, b0+len) of a.b into s (e = lane mod 4)
-CQ_DEVI double chain_chunk(double s, const double *a, const double *b, int64_t len, int lane) {
+// lanes 0..3: add the precomputed products p[e] (e = lane mod 4, e < body) to s
+CQ_DEVI double chain_sum(double s, const double *p, int64_t body, int lane) {
     int64_t e = lane;
-    for (; e + 28 < len; e += 32) {
-        double av[8], bv[8];
+    for (; e + 28 < body; e += 32) {
+        double v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            av[u] = a[e + 4 * u];
-            bv[u] = b[e + 4 * u];
-        }
+        for (int u = 0; u < 8; ++u) v[u] = p[e + 4 * u];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) s = s + av[u] * bv[u];
+        for (int u = 0; u < 8; ++u) s = s + v[u];
     }
-    for (; e < len; e += 4) s = s + a[e] * b[e];
+    for (; e < body; e += 4) s = s + p[e];
     return s;
 }
 
-// lanes 0..3: (s0+s1)+(s2+s3), then the tail (elements body..c-1 via fa/fb)
+// lanes 0..3: (s0+s1)+(s2+s3), then the tail elements body..c-1 of a.b
 template <class FA, class FB>
 CQ_DEVI double chain_finish(double s, int64_t c, FA fa, FB fb) {
     const int64_t body = c & ~(int64_t)3;
@@ -71,26 +77,84 @@ CQ_DEVI double chain_finish(double s, int64_t c, FA fa, FB fb) {
     return tot;
 }
 
-// Warp-cooperative reference dot of sa[0..c) (shared, or nullptr = the column
-// itself) with the global column g[0..c): the column is staged through the
-// warp's shared buffer wb (WB doubles) with coalesced loads; lanes 0..3 run
-// the ordered chains from shared memory. Result broadcast to all lanes.
-CQ_DEVI double warp_ref_dot(const double *sa, const double *g, int64_t c, double *wb, int WB, int lane) {
+// Async L2-coherent copy of g[0..len) into shared memory. The copy starts at
+// the 16-byte aligned address at or below g; returns the element offset of
+// g[0] inside dst (0 or 1). Only bytes inside [g-1, g+len) are read.
+CQ_DEVI int stage_async(double *dst, const double *g, int64_t len, int tid, int nthreads) {
+    const int off = (int)((reinterpret_cast<uintptr_t>(g) >> 3) & 1);
+    const double *base = g - off;
+    const int64_t total = len + off;
+    for (int64_t q = tid; 2 * q < total; q += nthreads) {
+        const int64_t rem = total - 2 * q;
+        cp_async16_zfill(dst + 2 * q, base + 2 * q, rem >= 2 ? 16 : 8);
+    }
+    return off;
+}
+
+// Reference dot of sa[0..c) . g[0..c) (sa == nullptr: g . g) for a column that
+// is not staged: the warp streams it through wb in WB-sized chunks, forming
+// the products in parallel; lanes 0..3 carry the four ordered chains.
+CQ_DEVI double warp_ref_dot_chunked(const double *sa, const double *g, int64_t c, double *wb, int WB, int lane) {
     const int64_t body = c & ~(int64_t)3;
     double s = 0.0;
     for (int64_t b0 = 0; b0 < body; b0 += WB) {
-        const int len = (int)cmin<int64_t>(WB, body - b0);
-#pragma unroll 4
-        for (int e = lane; e < len; e += 32) wb[e] = ld_cg(g + b0 + e);
+        const int len = (int)cmin<int64_t>(WB, body - b0);  // multiple of 4 (WB is)
+        for (int e = lane; e < len; e += 32) {
+            const double xv = ld_cg(g + b0 + e);
+            wb[e] = (sa ? sa[b0 + e] : xv) * xv;
+        }
         __syncwarp();
-        if (lane < 4) s = chain_chunk(s, sa ? sa + b0 : wb, wb, len, lane);
+        if (lane < 4) s = chain_sum(s, wb, len, lane);
         __syncwarp();
     }
     double tot = 0.0;
-    if (lane < 4) {
+    if (lane < 4)
+        tot = chain_finish(s, c, [&](int64_t xx) { return sa ? sa[xx] : ld_cg(g + xx); },
+                           [&](int64_t xx) { return ld_cg(g + xx); });
+    return __shfl_sync(0xffffffffu, tot, 0);
+}
+
+// Warp-level reference dot of sa[0..c) (shared memory; nullptr = the column
+// with itself) and the global column g[0..c). g streams through the warp's two
+// half-buffers b0/b1 (CHD data doubles each, a multiple of 4) with
+// double-buffered L2-coherent cp.async; all lanes form the products, lanes
+// 0..3 add them in the reference's order. `pre0`: chunk 0 is already in flight
+// into b0 (prefetched). When the whole column fits in one chunk the products
+// go to b1, so b0 keeps the column (*kept = true) for the update pass.
+CQ_DEVI double stream_dot(const double *sa, const double *g, int64_t c, double *b0, double *b1, int CHD, bool pre0,
+                          bool *kept, int lane) {
+    const int off = (int)((reinterpret_cast<uintptr_t>(g) >> 3) & 1);  // same for every chunk
+    const int64_t body = c & ~(int64_t)3;
+    const int64_t nch = (c + CHD - 1) / CHD;
+    *kept = (nch == 1);
+    double s = 0.0;
+    if (nch > 0 && !pre0) {
+        stage_async(b0, g, cmin<int64_t>(CHD, c), lane, 32);
+        cp_async_commit();
+    }
+    for (int64_t k = 0; k < nch; ++k) {
+        if (k + 1 < nch) {
+            stage_async(((k + 1) & 1) ? b1 : b0, g + (k + 1) * CHD, cmin<int64_t>(CHD, c - (k + 1) * CHD), lane, 32);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncwarp();
+        double *buf = ((k & 1) ? b1 : b0) + off;
+        const int64_t base = k * CHD;
+        const int64_t bl = cmax<int64_t>(0, cmin<int64_t>(CHD, body - base));
+        double *prod = (nch == 1) ? b1 : buf;
+#pragma unroll 8
+        for (int64_t e = lane; e < bl; e += 32) prod[e] = (sa ? sa[base + e] : buf[e]) * buf[e];
+        __syncwarp();
+        if (lane < 4) s = chain_sum(s, prod, bl, lane);
+        __syncwarp();
+    }
+    double tot = 0.0;
+    if (lane < 4)
         tot = chain_finish(s, c, [&](int64_t x) { return sa ? sa[x] : ld_cg(g + x); },
                            [&](int64_t x) { return ld_cg(g + x); });
-    }
     return __shfl_sync(0xffffffffu, tot, 0);
 }
 
@@ -105,12 +169,13 @@ struct QrcpArgs {
     double *pv[2];    // per-CTA argmax partials: value, logical index, physical column
     int32_t *pi[2];
     int32_t *pp[2];
-    unsigned int *bar;
+    unsigned long long *bar;
     int64_t *k_out;
     int32_t *final_buf;  // which cmap buffer holds positions >= k
     double rank_tol;
     int64_t steps;
-    int wb;              // per-warp staging buffer (doubles, multiple of 32)
+    int wb;                     // per-warp buffer (doubles, multiple of 32)
+    int xlen;                   // pivot buffer length (doubles, >= d + 2, even)
     unsigned long long *trace;  // optional per-step phase timestamps (CTA 0)
 };
 
@@ -122,24 +187,23 @@ CQ_DEVI void trace_mark(unsigned long long *tr, int64_t i, int slot) {
     }
 }
 
-// Lanes of a warp stage g[0..len) into wb (coalesced).
-CQ_DEVI void warp_stage(double *wb, const double *g, int64_t len, int lane) {
-#pragma unroll 4
-    for (int64_t e = lane; e < len; e += 32) wb[e] = ld_cg(g + e);
-}
-
 __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
-    extern __shared__ double smem[];
-    __shared__ double s_av[kQrcpThreads / 32];
-    __shared__ int32_t s_ai[kQrcpThreads / 32], s_ap[kQrcpThreads / 32];
+    extern __shared__ __align__(16) double smem[];
+    __shared__ double s_av[kQrcpWarps];
+    __shared__ int32_t s_ai[kQrcpWarps], s_ap[kQrcpWarps];
     __shared__ double s_bc[4];
+    __shared__ int s_poff;
     const int G = gridDim.x, cta = blockIdx.x;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kQrcpThreads / 32;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t d = A.d, n = A.n, ld = A.ld;
     const int WB = A.wb;
-    double *wb = smem + wid * WB;   // warp staging buffer: the warp's column tail
-    double *s_v = smem + nw * WB;   // pivot column / scaled reflector (d+1)
+    double *wb = smem + wid * WB;                // warp buffer: two halves b0/b1
+    double *b0 = wb, *b1 = wb + WB / 2;
+    const int CHD = ((WB / 2) - 2) & ~3;         // data doubles per chunk (alignment slack 2)
+    double *s_x = smem + kQrcpWarps * WB;        // pivot column rows i..d-1 (+ alignment slack)
+    double *s_sv = s_x + A.xlen;                 // products, then the scaled reflector (d doubles)
     const double sqrt_u = sqrt(kUnitRoundoff);
+    unsigned long long nbar = 0;
 
     // block argmax carrying the physical column of the winner
     auto block_argmax = [&](ArgMax a, int32_t phys, int32_t *phys_out) -> ArgMax {
@@ -162,7 +226,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         __syncthreads();
         ArgMax r{-INFINITY, 0x7fffffff};
         int32_t rp = 0;
-        if (lane < nw) {
+        if (lane < kQrcpWarps) {
             r = ArgMax{s_av[lane], s_ai[lane]};
             rp = s_ap[lane];
         }
@@ -183,8 +247,9 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
     // ---- initial squared norms w_j = dot(col_j, col_j) (qrcp.cc:48-51) ----
     ArgMax loc{-INFINITY, 0x7fffffff};
     int32_t locp = 0;
-    for (int64_t j = cta + (int64_t)wid * G; j < n; j += (int64_t)nw * G) {
-        double s = warp_ref_dot(nullptr, A.b + j * ld, d, wb, WB, lane);
+    for (int64_t j = cta + (int64_t)wid * G; j < n; j += (int64_t)kQrcpWarps * G) {
+        bool kept;
+        double s = stream_dot(nullptr, A.b + j * ld, d, b0, b1, CHD, false, &kept, lane);
         if (lane == 0) {
             A.w[0][j] = s;
             A.wref[j] = s;
@@ -203,7 +268,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
             A.pp[0][cta] = bp;
         }
     }
-    grid_barrier(A.bar, G);
+    grid_barrier_mono(A.bar, (++nbar) * (unsigned long long)G);
 
     double stop = 0.0;
     int64_t k = 0;
@@ -211,21 +276,23 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
     for (; i < A.steps; ++i) {
         const int cur = (int)(i & 1), nxt = cur ^ 1;
         const int64_t c = d - i - 1;  // rows below the diagonal
-        const bool fits = c <= WB;
+        const int64_t body = c & ~(int64_t)3;
         trace_mark(A.trace, i, 0);
 
-        // ---- prefetch this warp's first owned column (independent of the pivot)
+        // ---- prefetch chunk 0 of this warp's first owned column (async,
+        // independent of the pivot decision)
         const int64_t jfirst = i + 1 + ((cta - (i + 1)) % G + G) % G;
         const int64_t j_w = jfirst + (int64_t)wid * G;
         int32_t pj0 = 0;
         double wj0 = 0.0, wrefj0 = 0.0, t0 = 0.0;
         if (j_w < n) {
             pj0 = ld_cg(A.cmap[cur] + j_w);
+            const double *col = A.b + (int64_t)pj0 * ld;
+            stage_async(b0, col + i + 1, cmin<int64_t>(CHD, c), lane, 32);
+            cp_async_commit();
             wj0 = ld_cg(A.w[cur] + j_w);
             wrefj0 = ld_cg(A.wref + j_w);
-            const double *col = A.b + (int64_t)pj0 * ld;
             t0 = ld_cg(col + i);
-            if (fits) warp_stage(wb, col + i + 1, c, lane);
         }
         const int32_t phys_i = ld_cg(A.cmap[cur] + i);
         const double w_i = ld_cg(A.w[cur] + i), wref_i = ld_cg(A.wref + i);
@@ -242,19 +309,31 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         if (i == 0) stop = A.rank_tol * sqrt(fmax(g.v, 0.0));  // max_norm0 (qrcp.cc:52-55)
         const double wp = g.v;
         const int64_t p = g.i;
-        if (sqrt(wp > 0.0 ? wp : 0.0) <= stop) break;  // qrcp.cc:62
+        if (sqrt(wp > 0.0 ? wp : 0.0) <= stop) {
+            cp_async_wait<0>();
+            break;  // qrcp.cc:62
+        }
         const double *x = A.b + (int64_t)phys_p * ld;
         trace_mark(A.trace, i, 1);
 
         // ---- make_reflector (linalg.cc:110-124), redundantly per CTA ------
-        for (int64_t r = threadIdx.x; r < d - i; r += kQrcpThreads) s_v[r] = ld_cg(x + i + r);
+        {
+            const int off = stage_async(s_x, x + i, d - i, threadIdx.x, kQrcpThreads);
+            if (threadIdx.x == 0) s_poff = off;
+            cp_async_commit();
+            cp_async_wait<0>();  // also completes this warp's column prefetch
+            __syncthreads();
+        }
+        const double *xs = s_x + s_poff;  // xs[0] = x_i, xs[1 + e] = tail element e
+#pragma unroll 8
+        for (int64_t e = threadIdx.x; e < body; e += kQrcpThreads) s_sv[e] = xs[1 + e] * xs[1 + e];
         __syncthreads();
         if (wid == 0 && lane < 4) {
-            double s = chain_chunk(0.0, s_v + 1, s_v + 1, c & ~(int64_t)3, lane);
-            double tail_sq = chain_finish(s, c, [&](int64_t e) { return s_v[1 + e]; },
-                                          [&](int64_t e) { return s_v[1 + e]; });
+            double s = chain_sum(0.0, s_sv, body, lane);
+            double tail_sq = chain_finish(s, c, [&](int64_t e) { return xs[1 + e]; },
+                                          [&](int64_t e) { return xs[1 + e]; });
             if (lane == 0) {
-                double x0 = s_v[0];
+                double x0 = xs[0];
                 double norm_x = sqrt(fma(x0, x0, tail_sq));
                 double alpha = x0, v0 = 1.0, beta = 0.0;
                 if (norm_x != 0.0) {
@@ -270,82 +349,101 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         }
         __syncthreads();
         const double alpha = s_bc[0], v0 = s_bc[1], beta = s_bc[2];
-        if (beta != 0.0)
-            for (int64_t r = threadIdx.x; r < c; r += kQrcpThreads) s_v[1 + r] = s_v[1 + r] / v0;  // colj[i] /= v0
+#pragma unroll 8
+        for (int64_t r = threadIdx.x; r < c; r += kQrcpThreads)
+            s_sv[r] = (beta != 0.0) ? xs[1 + r] / v0 : xs[1 + r];  // colj[i] /= v0
         __syncthreads();
-        const double *sv = s_v + 1;
+        const double *sv = s_sv;
         trace_mark(A.trace, i, 2);
 
         // ---- apply_reflector + norm downdate, one owned column per warp --
         ArgMax mine{-INFINITY, 0x7fffffff};
         int32_t minep = 0;
         bool first = true;
-        for (int64_t j = j_w; j < n; j += (int64_t)nw * G, first = false) {
+        for (int64_t j = j_w; j < n; j += (int64_t)kQrcpWarps * G, first = false) {
             const bool isp = (j == p);
             int32_t pj;
             double wj, wrefj, t;
-            bool staged = false;
+            bool pre = false;
             if (first && !isp) {
                 pj = pj0;
                 wj = wj0;
                 wrefj = wrefj0;
                 t = t0;
-                staged = fits;
+                pre = true;  // chunk 0 of this column is already in flight into b0
             } else {
+                if (first) {  // the prefetched column was the swapped one: drain it
+                    cp_async_wait<0>();
+                    __syncwarp();
+                }
                 pj = isp ? phys_i : ld_cg(A.cmap[cur] + j);
                 wj = isp ? w_i : ld_cg(A.w[cur] + j);
                 wrefj = isp ? wref_i : ld_cg(A.wref + j);
                 t = ld_cg(A.b + (int64_t)pj * ld + i);
-                if (fits) {
-                    __syncwarp();
-                    warp_stage(wb, A.b + (int64_t)pj * ld + i + 1, c, lane);
-                    staged = true;
-                }
             }
             double *col = A.b + (int64_t)pj * ld;
             double *tail = col + i + 1;
-            if (staged) __syncwarp();
+            const int off = (int)((reinterpret_cast<uintptr_t>(tail) >> 3) & 1);
+            bool kept = false;
+            __syncwarp();
             if (beta != 0.0) {  // apply_reflector (linalg.cc:126-136)
-                double dot;
-                if (staged) {
-                    double s = 0.0;
-                    if (lane < 4) {
-                        s = chain_chunk(0.0, sv, wb, c & ~(int64_t)3, lane);
-                        s = chain_finish(s, c, [&](int64_t e) { return sv[e]; }, [&](int64_t e) { return wb[e]; });
-                    }
-                    dot = __shfl_sync(0xffffffffu, s, 0);
-                } else {
-                    dot = warp_ref_dot(sv, tail, c, wb, WB, lane);
-                }
+                const double dot = stream_dot(sv, tail, c, b0, b1, CHD, pre, &kept, lane);
                 double tau = t;
                 tau += dot;
                 tau *= beta;
                 t = t - tau;
-                if (staged) {
-#pragma unroll 4
+                if (kept) {  // column still in b0: update from shared memory
+                    double *cb = b0 + off;
+#pragma unroll 8
                     for (int64_t e = lane; e < c; e += 32) {
-                        double nv = fma(-tau, sv[e], wb[e]);
-                        wb[e] = nv;
+                        const double nv = fma(-tau, sv[e], cb[e]);
+                        cb[e] = nv;
                         __stcg(tail + e, nv);
                     }
-                } else {
-#pragma unroll 4
-                    for (int64_t e = lane; e < c; e += 32) __stcg(tail + e, fma(-tau, sv[e], ld_cg(tail + e)));
+                } else {  // restream the column (double-buffered)
+                    const int64_t nch = (c + CHD - 1) / CHD;
+                    stage_async(b0, tail, cmin<int64_t>(CHD, c), lane, 32);
+                    cp_async_commit();
+                    for (int64_t kk = 0; kk < nch; ++kk) {
+                        if (kk + 1 < nch) {
+                            stage_async(((kk + 1) & 1) ? b1 : b0, tail + (kk + 1) * CHD,
+                                        cmin<int64_t>(CHD, c - (kk + 1) * CHD), lane, 32);
+                            cp_async_commit();
+                            cp_async_wait<1>();
+                        } else {
+                            cp_async_wait<0>();
+                        }
+                        __syncwarp();
+                        const double *buf = ((kk & 1) ? b1 : b0) + off;
+                        const int64_t base = kk * CHD, len = cmin<int64_t>(CHD, c - base);
+#pragma unroll 8
+                        for (int64_t e = lane; e < len; e += 32)
+                            __stcg(tail + base + e, fma(-tau, sv[base + e], buf[e]));
+                        __syncwarp();
+                    }
                 }
+                __syncwarp();
+            } else if (pre) {
+                cp_async_wait<0>();  // drain the prefetch before b0 is reused
                 __syncwarp();
             }
             double updated = fma(-t, t, wj);  // qrcp.cc:77-78
             double newref = wrefj;
             if (updated <= sqrt_u * wrefj) {  // qrcp.cc:82-86 (warp-uniform)
-                if (staged) {
+                if (kept) {                   // updated column is in b0
+                    const double *cb = b0 + off;
+                    for (int64_t e = lane; e < body; e += 32) b1[e] = cb[e] * cb[e];
+                    __syncwarp();
                     double s = 0.0;
                     if (lane < 4) {
-                        s = chain_chunk(0.0, wb, wb, c & ~(int64_t)3, lane);
-                        s = chain_finish(s, c, [&](int64_t e) { return wb[e]; }, [&](int64_t e) { return wb[e]; });
+                        s = chain_sum(0.0, b1, body, lane);
+                        s = chain_finish(s, c, [&](int64_t e) { return cb[e]; }, [&](int64_t e) { return cb[e]; });
                     }
                     updated = __shfl_sync(0xffffffffu, s, 0);
+                    __syncwarp();
                 } else {
-                    updated = warp_ref_dot(nullptr, tail, c, wb, WB, lane);
+                    bool k2;
+                    updated = stream_dot(nullptr, tail, c, b0, b1, CHD, false, &k2, lane);
                 }
                 newref = updated;
             }
@@ -376,7 +474,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         }
         k = i + 1;
         trace_mark(A.trace, i, 4);
-        grid_barrier(A.bar, G);
+        grid_barrier_mono(A.bar, (++nbar) * (unsigned long long)G);
     }
     if (cta == 0 && threadIdx.x == 0) {
         *A.k_out = k;
@@ -415,8 +513,19 @@ __global__ void row_stats_kernel(int64_t k, int64_t n, const double *__restrict_
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool act = i < k;
     double acc = 0.0, mx = 0.0;
-    for (int64_t j = 0; j < n; ++j) {  // all lanes walk j together: coalesced over rows
-        double v = act ? r[j * ldr + i] : 0.0;
+    int64_t j = 0;
+    for (; j + 8 <= n; j += 8) {  // all lanes walk j together: coalesced over rows
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = act ? __ldg(r + (j + u) * ldr + i) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            mx = fmax(mx, fabs(v[u]));
+            if (j + u >= i) acc = acc + v[u] * v[u];
+        }
+    }
+    for (; j < n; ++j) {
+        double v = act ? __ldg(r + j * ldr + i) : 0.0;
         mx = fmax(mx, fabs(v));
         if (j >= i) acc = acc + v * v;
     }
@@ -457,11 +566,14 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     if (d < 1) return fail_internal("qrcp: need at least one row");
     if (rank_tol < 0.0) rank_tol = (double)n * kUnitRoundoff;  // qrcp.cc:17,38
     const int sms = num_sms();
-    // shared memory: 8 warp staging buffers + the pivot column (d+1 doubles)
-    const int64_t budget = (200 * 1024) / (int64_t)sizeof(double);
-    if (d + 1 + 8 * 128 > budget) return fail_internal("qrcp: d too large for the shared-memory reflector");
-    const int WB = (int)std::min<int64_t>(4096, ((budget - (d + 1)) / 8) & ~(int64_t)31);
-    const size_t smem = sizeof(double) * (size_t)(8 * WB + d + 1);
+    // shared memory: pivot buffer (d+2, even) + reflector (d) + 8 warp buffers
+    const int64_t budget = (212 * 1024) / (int64_t)sizeof(double);
+    const int xlen = (int)(((d + 2) + 1) & ~(int64_t)1);
+    const int64_t room = budget - xlen - d;
+    if (room < 8 * 128) return fail_internal("qrcp: d too large for the shared-memory reflector");
+    // per warp: two halves; one half holds a whole column when it fits
+    const int WB = (int)std::min<int64_t>(2 * (((d + 2 + 31) / 32) * 32), (room / 8) & ~(int64_t)63);
+    const size_t smem = sizeof(double) * (size_t)(8 * (int64_t)WB + xlen + d);
     CQ_CUDA(cudaFuncSetAttribute(qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "qrcp smem");
     // one owned column per warp per step at the start (8 warps per CTA)
     int G = (int)std::min<int64_t>(std::min<int64_t>(sms, kQrcpThreads), std::max<int64_t>(1, (n + 7) / 8));
@@ -486,14 +598,15 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     a.pi[1] = ws.get<int32_t>("qrcp.pi1", 256);
     a.pp[0] = ws.get<int32_t>("qrcp.pp0", 256);
     a.pp[1] = ws.get<int32_t>("qrcp.pp1", 256);
-    a.bar = ws.get<unsigned int>("qrcp.bar", 4);
+    a.bar = ws.get<unsigned long long>("qrcp.bar", 2);
     a.k_out = ws.get<int64_t>("qrcp.k", 2);
     a.final_buf = ws.get<int32_t>("qrcp.fb", 2);
     a.rank_tol = rank_tol;
     a.steps = std::min(d, n);
-    if (!a.w[0] || !a.bar || !a.k_out) return fail_nomem("qrcp workspace");
-    CQ_CUDA(cudaMemsetAsync(a.bar, 0, 4 * sizeof(unsigned int), st), "memset bar");
     a.wb = WB;
+    a.xlen = xlen;
+    if (!a.w[0] || !a.bar || !a.k_out) return fail_nomem("qrcp workspace");
+    CQ_CUDA(cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned long long), st), "memset bar");
     static const bool tracing = getenv("CQRRPT_QRCP_TRACE") != nullptr;
     a.trace = tracing ? ws.get<unsigned long long>("qrcp.trace", 512 * 6) : nullptr;
     if (a.trace) CQ_CUDA(cudaMemsetAsync(a.trace, 0, 512 * 6 * sizeof(unsigned long long), st), "trace memset");
@@ -518,9 +631,11 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
             ++cnt;
         }
         if (cnt)
-            fprintf(stderr, "qrcp trace (G=%d, d=%lld, n=%lld, %d steps): argmax %.0f ns, reflector %.0f ns, "
-                    "columns %.0f ns, partials %.0f ns, barrier %.0f ns\n", G, (long long)d, (long long)n, cnt,
-                    acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt);
+            fprintf(stderr,
+                    "qrcp trace (G=%d, d=%lld, n=%lld, WB=%d, %d steps): argmax %.0f ns, reflector %.0f ns, "
+                    "columns %.0f ns, partials %.0f ns, barrier %.0f ns\n",
+                    G, (long long)d, (long long)n, WB, cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt,
+                    acc[4] / cnt);
     }
     return 0;
 }
@@ -533,7 +648,7 @@ int rank_stage1(int64_t k, int64_t n, const double *r, int64_t ldr, int64_t *k0,
     double *mass = ws.get<double>("s1.mass", k);
     double *rmax = ws.get<double>("s1.rmax", k);
     int64_t *kd = ws.get<int64_t>("s1.k0", 1);
-    row_stats_kernel<<<(unsigned)((k + 127) / 128), 128, 0, st>>>(k, n, r, ldr, mass, rmax);
+    row_stats_kernel<<<(unsigned)((k + 31) / 32), 32, 0, st>>>(k, n, r, ldr, mass, rmax);
     note_launch();
     stage1_kernel<<<1, 1024, 0, st>>>(k, mass, rmax, kUnitRoundoff, kd);
     note_launch();

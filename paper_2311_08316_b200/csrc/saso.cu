@@ -142,7 +142,9 @@ __global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d
 
 // ---------------------------------------------------------------------------
 // K2: apply. A accumulators per lane (template), 16 warps -> 16*A sketch rows
-// per CTA. Writes part[split][r][j] (row-major, coalesced over lanes).
+// per CTA. Tiles of 256 rows x 32 columns of A plus the tile's CSR slice are
+// double-buffered in shared memory with cp.async (the copy of tile t+1 runs
+// under the FMAs of tile t). Writes part[split][r][j] (row-major).
 // ---------------------------------------------------------------------------
 template <int A>
 __global__ void __launch_bounds__(kApplyWarps * 32, 1)
@@ -152,10 +154,13 @@ __global__ void __launch_bounds__(kApplyWarps * 32, 1)
                       double *__restrict__ part) {
     constexpr int RB = kApplyWarps * A;
     constexpr int LD = 33;
+    constexpr int NT = kApplyWarps * 32;
+    constexpr int PTRW = ((RB + 1 + 1) / 2 + 1 + 3) & ~3;  // 32-bit words per ptr buffer (16B multiple)
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double *s_tile = reinterpret_cast<double *>(smem_raw);                       // [256][33]
-    uint16_t *s_ptr = reinterpret_cast<uint16_t *>(s_tile + kTileRows * LD);     // [RB+1]
-    uint16_t *s_ent = s_ptr + ((RB + 1 + 7) & ~7);                                // [256*nnz]
+    double *s_tile = reinterpret_cast<double *>(smem_raw);                     // [2][256][33]
+    uint32_t *s_ptrw = reinterpret_cast<uint32_t *>(s_tile + 2 * kTileRows * LD);  // [2][PTRW]
+    const int entw = ((kTileRows * nnz + 1) / 2 + 3) & ~3;                    // words per entry buffer
+    uint32_t *s_entw = s_ptrw + 2 * PTRW;                                      // [2][entw]
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t j0 = (int64_t)blockIdx.x * 32;
@@ -169,51 +174,79 @@ __global__ void __launch_bounds__(kApplyWarps * 32, 1)
 #pragma unroll
     for (int i = 0; i < A; ++i) acc[i] = 0.0;
 
-    // register prefetch of one 256x32 tile: element e = it*512 + tid ->
-    // column e/256, row e%256 (a warp reads 256 contiguous bytes of a column)
-    constexpr int PER = kTileRows * 32 / (kApplyWarps * 32);  // 16
-    double pre[PER];
-    auto load_tile = [&](int64_t tile) {
+    // async copy of tile `tile` into buffer `bf`:
+    //   A rows [256*tile, +256) x cols [j0, j0+32) -> s_tile[bf][row][col] (8-byte copies,
+    //   a warp covers 256 contiguous bytes of one column)
+    //   tptr[tile][r0 .. r0+rows_here] (absolute offsets) -> ptr buffer (4-byte copies from
+    //   the 4-byte aligned start; odd start recorded by the parity of the address)
+    //   tent[tile][0 .. 256*nnz) -> entry buffer (4-byte copies)
+    auto issue = [&](int64_t tile, int bf) {
         const int64_t row0 = tile * kTileRows;
-#pragma unroll
-        for (int it = 0; it < PER; ++it) {
-            int e = it * (kApplyWarps * 32) + threadIdx.x;
+        double *dt = s_tile + bf * kTileRows * LD;
+#pragma unroll 4
+        for (int it = 0; it < kTileRows * 32 / NT; ++it) {
+            int e = it * NT + threadIdx.x;
             int jj = e / kTileRows, cc = e % kTileRows;
             int64_t row = row0 + cc, col = j0 + jj;
-            pre[it] = (row < m && col < n) ? __ldg(a + col * lda + row) : 0.0;
+            bool ok = row < m && col < n;
+            cp_async8_zfill(dt + cc * LD + jj, a + (ok ? col * lda + row : 0), ok ? 8 : 0);
         }
+        const uint16_t *gp = tptr + tile * (d + 1) + r0;
+        const uint32_t *gpw = reinterpret_cast<const uint32_t *>(reinterpret_cast<uintptr_t>(gp) & ~(uintptr_t)3);
+        const int nw = (int)(((reinterpret_cast<uintptr_t>(gp + rows_here + 1) + 3) - reinterpret_cast<uintptr_t>(gpw)) / 4);
+        for (int w = threadIdx.x; w < nw; w += NT) cp_async4(s_ptrw + bf * PTRW + w, gpw + w);
+        const uint32_t *gew = reinterpret_cast<const uint32_t *>(tent + tile * (int64_t)(kTileRows * nnz));
+        const int nent_w = (kTileRows * nnz + 1) / 2;  // tile entry arrays start 4-byte aligned (256*nnz even)
+        for (int w = threadIdx.x; w < nent_w; w += NT) cp_async4(s_entw + bf * entw + w, gew + w);
+        cp_async_commit();
     };
-    if (t_begin < t_end) load_tile(t_begin);
+    if (t_begin < t_end) issue(t_begin, 0);
 
     for (int64_t tile = t_begin; tile < t_end; ++tile) {
-        __syncthreads();  // previous tile fully consumed
-#pragma unroll
-        for (int it = 0; it < PER; ++it) {
-            int e = it * (kApplyWarps * 32) + threadIdx.x;
-            s_tile[(e % kTileRows) * LD + e / kTileRows] = pre[it];
+        const int bf = (int)((tile - t_begin) & 1);
+        if (tile + 1 < t_end) {
+            issue(tile + 1, bf ^ 1);  // buffer bf^1 was released by the barrier below (previous iteration)
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
-        const uint16_t *gp = tptr + tile * (d + 1);
-        const int e_lo = gp[r0];
-        const int e_hi = gp[r0 + rows_here];
-        for (int i = threadIdx.x; i <= RB; i += blockDim.x)
-            s_ptr[i] = (uint16_t)((i <= rows_here ? gp[r0 + i] : e_hi) - e_lo);
-        const uint16_t *ge = tent + tile * (int64_t)(kTileRows * nnz) + e_lo;
-        for (int i = threadIdx.x; i < e_hi - e_lo; i += blockDim.x) s_ent[i] = ge[i];
         __syncthreads();
-        if (tile + 1 < t_end) load_tile(tile + 1);  // overlaps the compute below
+        const double *st = s_tile + bf * kTileRows * LD;
+        const uint16_t *sp = reinterpret_cast<const uint16_t *>(s_ptrw + bf * PTRW) +
+                             ((reinterpret_cast<uintptr_t>(tptr + tile * (d + 1) + r0) >> 1) & 1);
+        const uint16_t *se = reinterpret_cast<const uint16_t *>(s_entw + bf * entw);
 
+        // Each sketch row's entries in c order (sketch.cc:137-143); IL rows
+        // interleaved for instruction-level parallelism.
+        constexpr int IL = A < 4 ? A : 4;
 #pragma unroll
-        for (int i = 0; i < A; ++i) {
-            const int rl = wid * A + i;
-            const int beg = s_ptr[rl], end = s_ptr[rl + 1];
-            double s = acc[i];
-            for (int e = beg; e < end; ++e) {
-                const uint32_t w = s_ent[e];
-                const double v = (w & 0x8000u) ? val : -val;
-                s = fma(v, s_tile[(w & 0x7fffu) * LD + lane], s);  // sketch.cc:142
+        for (int i0 = 0; i0 < A; i0 += IL) {
+            int beg[IL], end[IL];
+            double s[IL];
+            int nmax = 0;
+#pragma unroll
+            for (int q = 0; q < IL; ++q) {
+                const int rl = min(wid * A + i0 + q, rows_here);
+                beg[q] = sp[rl];
+                end[q] = sp[min(rl + 1, rows_here)];
+                s[q] = acc[i0 + q];
+                nmax = max(nmax, end[q] - beg[q]);
             }
-            acc[i] = s;
+            for (int jj = 0; jj < nmax; ++jj) {
+#pragma unroll
+                for (int q = 0; q < IL; ++q) {
+                    const int e = beg[q] + jj;
+                    if (e < end[q]) {
+                        const uint32_t w = se[e];
+                        const double v = (w & 0x8000u) ? val : -val;
+                        s[q] = fma(v, st[(w & 0x7fffu) * LD + lane], s[q]);  // sketch.cc:142
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < IL; ++q) acc[i0 + q] = s[q];
         }
+        __syncthreads();  // buffer bf fully consumed before it is refilled
     }
     // write the partial: part[split][r][j]
     const int64_t col = j0 + lane;
@@ -265,7 +298,10 @@ static int launch_apply(int64_t m, int64_t n, const double *a, int64_t lda, int6
                         int64_t ntiles, const uint16_t *tptr, const uint16_t *tent, double *part,
                         int64_t nsplit, int64_t tps, int64_t rblocks, cudaStream_t st) {
     constexpr int RB = kApplyWarps * A;
-    size_t smem = sizeof(double) * kTileRows * 33 + sizeof(uint16_t) * (((RB + 1 + 7) & ~7) + kTileRows * nnz);
+    constexpr int PTRW = ((RB + 1 + 1) / 2 + 1 + 3) & ~3;
+    const int entw = ((kTileRows * nnz + 1) / 2 + 3) & ~3;
+    size_t smem = sizeof(double) * 2 * kTileRows * 33 + sizeof(uint32_t) * 2 * (PTRW + entw);
+    if (smem > 220 * 1024) return fail_internal("saso_apply: nnz too large for the shared-memory CSR");
     auto kern = saso_apply_kernel<A>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return fail_cuda("saso_apply smem attr");
@@ -308,13 +344,21 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
         // One pass over all rows per CTA keeps the reference's per-entry sum
         // order (c ascending, sketch.cc:137-143) -> bit-identical sketch.
         // Parallelism comes from finer sketch-row blocks instead.
+        // Every CTA streams all m rows of its 32 columns (a fixed staging cost,
+        // ~ the entry work of 256 sketch rows) plus work proportional to its
+        // row-block height 16*A; CTAs run one per SM: minimise
+        // waves(A) * (256 + 16*A).
         const int cand[] = {20, 16, 12, 8, 4, 2, 1};
-        A = 1;
-        for (int a : cand)
-            if (cgroups * ((d + 16 * a - 1) / (16 * a)) >= sms) {
+        double best = 1e300;
+        for (int a : cand) {
+            const int64_t ctas = cgroups * ((d + 16 * a - 1) / (16 * a));
+            const int64_t waves = (ctas + sms - 1) / sms;
+            const double cost = (double)waves * (256.0 + (double)std::min<int64_t>(16 * a, d));
+            if (cost < best) {
+                best = cost;
                 A = a;
-                break;
             }
+        }
     } else {
         if (d <= 16 * 8) A = 8;
         else if (d <= 16 * 12) A = 12;
