@@ -197,6 +197,13 @@ int cqrrpt_gpu_comm_init(int32_t nranks, int32_t rank, const unsigned char id[12
 int cqrrpt_gpu_comm_allreduce(cqrrpt_gpu_comm *comm, double *buf, size_t count, void *stream);
 void cqrrpt_gpu_comm_destroy(cqrrpt_gpu_comm *comm);
 
+/* Helpers for caller-supplied collectives (cqrrpt_gpu_allreduce_fn):
+ * y += x on device (ordered on stream); synchronous copy of any direction;
+ * stream synchronisation. */
+int cqrrpt_gpu_add(double *y, const double *x, size_t n, void *stream);
+int cqrrpt_gpu_copy(void *dst, const void *src, size_t bytes, void *stream);
+int cqrrpt_gpu_stream_sync(void *stream);
+
 /* Free the library's cached device workspaces (calling thread). */
 void cqrrpt_gpu_release_workspace(void);
 

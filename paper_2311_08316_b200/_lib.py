@@ -59,6 +59,9 @@ SYMBOLS = {
     "cqrrpt_gpu_comm_allreduce": (ctypes.c_int, [_vp, _vp, _sz, _vp]),
     "cqrrpt_gpu_comm_destroy": (None, [_vp]),
     "cqrrpt_gpu_release_workspace": (None, []),
+    "cqrrpt_gpu_add": (ctypes.c_int, [_vp, _vp, _sz, _vp]),
+    "cqrrpt_gpu_copy": (ctypes.c_int, [_vp, _vp, _sz, _vp]),
+    "cqrrpt_gpu_stream_sync": (ctypes.c_int, [_vp]),
     "cqrrpt_gpu_last_error": (ctypes.c_char_p, []),
     "cqrrpt_gpu_launch_count": (_i64, [_i32]),
 }

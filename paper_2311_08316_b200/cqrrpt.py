@@ -229,10 +229,16 @@ class DeviceResult:
 def dgeqpt(a, d_factor: float = 1.25, nnz: int = 4, seed: int = 0, eps_tol: float = 1e-4,
            cond_method: int = CondMethod.identity_deviation, stage1: bool = True, exact_stage2: bool = False,
            diagnostics: bool = False, timings: bool = False, stream=None, comm: Optional[Comm] = None,
-           global_row_offset: int = 0, r_out=None, j_out=None) -> DeviceResult:
+           global_row_offset: int = 0, r_out=None, j_out=None, allreduce=None, nranks: int = 1,
+           rank: int = 0) -> DeviceResult:
     """The north-star entry point on a column-major CUDA tensor ``a``
     (m_local x n). Q overwrites ``a[:, :k]`` in place; R (k x n) and the
-    0-based pivots are returned as device tensors."""
+    0-based pivots are returned as device tensors.
+
+    Multi-rank: pass ``comm`` (NCCL, cqrrpt_gpu_comm_*) or ``allreduce`` — a
+    Python callable ``(ptr, count, stream_ptr) -> None`` that sum-allreduces
+    ``count`` doubles in place — together with ``nranks``/``rank`` and this
+    rank's ``global_row_offset``."""
     torch = _torch()
     L = _lib.load()
     m, n = a.shape
@@ -257,10 +263,23 @@ def dgeqpt(a, d_factor: float = 1.25, nnz: int = 4, seed: int = 0, eps_tol: floa
     if timings:
         flags |= _lib.F_TIMINGS
     ctx.flags = flags
+    cb = None
     if comm is not None:
         ctx.comm = comm.handle
         ctx.nranks = comm.nranks
         ctx.rank = comm.rank
+        ctx.global_row_offset = int(global_row_offset)
+    elif allreduce is not None:
+        def _ar(buf, count, st, user):
+            try:
+                allreduce(ctypes.cast(buf, ctypes.c_void_p).value, int(count), st)
+                return 0
+            except Exception:  # reported to the library as a failed collective
+                return 1
+        cb = _lib.ALLREDUCE_FN(_ar)  # kept alive for the duration of the call
+        ctx.allreduce = cb
+        ctx.nranks = int(nranks)
+        ctx.rank = int(rank)
         ctx.global_row_offset = int(global_row_offset)
     k, k0 = _lib._i64(), _lib._i64()
     rc = L.cqrrpt_gpu_dgeqpt(m, n, a.data_ptr() if a.numel() else None, lda, float(d_factor), int(nnz), int(seed),

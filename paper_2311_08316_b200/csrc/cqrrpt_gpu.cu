@@ -583,4 +583,30 @@ void cqrrpt_gpu_comm_destroy(cqrrpt_gpu_comm *comm) {
 
 void cqrrpt_gpu_release_workspace(void) { release_workspace(); }
 
+// ---- helpers for caller-supplied collectives -------------------------------
+namespace {
+__global__ void add_kernel(double *y, const double *x, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        y[i] += x[i];
+}
+}  // namespace
+
+int cqrrpt_gpu_add(double *y, const double *x, size_t n, void *stream) {
+    if (n == 0) return 0;
+    add_kernel<<<(unsigned)std::min<size_t>((n + 255) / 256, 4096), 256, 0, (cudaStream_t)stream>>>(y, x, n);
+    note_launch();
+    return check_launch("add_kernel");
+}
+
+int cqrrpt_gpu_copy(void *dst, const void *src, size_t bytes, void *stream) {
+    CQ_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream), "copy");
+    CQ_CUDA(cudaStreamSynchronize((cudaStream_t)stream), "copy sync");
+    return 0;
+}
+
+int cqrrpt_gpu_stream_sync(void *stream) {
+    CQ_CUDA(cudaStreamSynchronize((cudaStream_t)stream), "stream sync");
+    return 0;
+}
+
 }  // extern "C"

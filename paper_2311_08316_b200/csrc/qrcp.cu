@@ -29,6 +29,7 @@
 // counter.
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "common.cuh"
 #include "internal.hh"
@@ -565,6 +566,10 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
          int64_t *k_sk, Workspace &ws, cudaStream_t st) {
     if (d < 1) return fail_internal("qrcp: need at least one row");
     if (rank_tol < 0.0) rank_tol = (double)n * kUnitRoundoff;  // qrcp.cc:17,38
+    // One cooperative (grid-synchronising) QRCP per device at a time: host
+    // threads sharing a GPU never have two co-residency-dependent grids live.
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
     const int sms = num_sms();
     // shared memory: pivot buffer (d+2, even) + reflector (d) + 8 warp buffers
     const int64_t budget = (212 * 1024) / (int64_t)sizeof(double);

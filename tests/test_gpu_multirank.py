@@ -1,0 +1,84 @@
+"""The library's multi-rank path (row shards + two sum-allreduces) exercised on
+one GPU: two host threads act as two ranks, each with its own stream, row
+block and global row offset, joined by a caller-supplied allreduce (the
+cqrrpt_gpu_allreduce_fn hook) that sums the device buffers in rank order.
+No kernel waits on another: the ranks only meet in host code between phases.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+class ThreadAllreduce:
+    def __init__(self, nranks):
+        from paper_2311_08316_b200 import _lib
+        self.L = _lib.load()
+        self.n = nranks
+        self.bar = threading.Barrier(nranks)
+        self.bufs = [None] * nranks
+
+    def for_rank(self, rank):
+        L = self.L
+
+        def ar(ptr, count, stream):
+            L.cqrrpt_gpu_stream_sync(stream)
+            self.bufs[rank] = ptr
+            self.bar.wait()
+            if rank == 0:
+                for r in range(1, self.n):
+                    assert L.cqrrpt_gpu_add(ptr, self.bufs[r], count, stream) == 0
+                L.cqrrpt_gpu_stream_sync(stream)
+            self.bar.wait()
+            if rank != 0:
+                assert L.cqrrpt_gpu_copy(ptr, self.bufs[0], count * 8, stream) == 0
+            self.bar.wait()
+        return ar
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_threaded_ranks_match_single_gpu(cuda, oracle, nranks):
+    import torch
+    from paper_2311_08316_b200.distributed import shard_rows
+    m, n = 9000, 96
+    a = oracle.gen_gaussian(m, n, 17)
+    ref = oracle.cqrrpt(a, gamma=1.25, nnz=8, seed=0)
+    coll = ThreadAllreduce(nranks)
+    results = [None] * nranks
+    errors = []
+
+    def run(rank):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            off, cnt = shard_rows(m, nranks, rank)
+            with torch.cuda.stream(st):
+                A = cuda.to_device_colmajor(np.asfortranarray(a[off:off + cnt]))
+                st.synchronize()
+                res = cuda.dgeqpt(A, d_factor=1.25, nnz=8, seed=0, stream=st, allreduce=coll.for_rank(rank),
+                                  nranks=nranks, rank=rank, global_row_offset=off)
+                st.synchronize()
+                results[rank] = (off, A[:, : res.k].cpu().numpy(), res.r.cpu().numpy(),
+                                 res.pivots.cpu().numpy(), res.k, res.k0)
+        except Exception as exc:  # surfaced below
+            errors.append(repr(exc))
+            coll.bar.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errors, errors
+    _, _, r0, p0, k_0, k00 = results[0]
+    for (_, _, r, p, k, k0) in results:
+        assert np.array_equal(p, p0) and k == k_0 and k0 == k00
+        assert np.array_equal(r, r0)  # replicated phases are bit-identical across ranks
+    assert np.array_equal(p0, ref.pivots) and k_0 == ref.k and k00 == ref.k0
+    q = np.vstack([x[1] for x in sorted(results, key=lambda t: t[0])])
+    v = oracle.validate(a, np.asfortranarray(q), r0, p0)
+    vr = oracle.validate(a, ref.q, ref.r, ref.pivots)
+    assert v["orth_fro"] <= 10 * max(vr["orth_fro"], 1e-14)
+    assert v["recon_rel"] <= 10 * max(vr["recon_rel"], 1e-15)
