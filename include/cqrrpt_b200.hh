@@ -1,0 +1,216 @@
+// cqrrpt_b200.hh — C++ adapter with the reference's own signature.
+//
+//   namespace cqrrpt_b200 {
+//     CqrrptOutput cqrrpt(const DenseMatrix &m, const CqrrptConfig &cfg = {});
+//   }
+//
+// mirrors cqrrpt::cqrrpt (/root/reference/proj/include/cqrrpt/cqrrpt.hh:140)
+// and its types (dense_matrix.hh:15-89, qrcp.hh:19-60, cqrrpt.hh:61-129): same
+// member names, same meaning, same exceptions (std::invalid_argument for bad
+// configurations, std::domain_error for a singular preconditioner). A
+// reference caller switches with `namespace cqrrpt = cqrrpt_b200;`.
+//
+// Host data in, host data out (like the reference): the adapter copies M to
+// the device, runs cqrrpt_gpu_dgeqpt (include/cqrrpt_gpu.h) on sm_100a, and
+// copies Q (m x k), R (k x n) and the pivots back. Header-only; link
+// libcqrrpt_gpu.so and the CUDA runtime.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "cqrrpt_gpu.h"
+
+namespace cqrrpt_b200 {
+
+inline constexpr double unit_roundoff = 1.1102230246251565e-16;  // cqrrpt.hh:14
+
+// Column-major dense matrix (dense_matrix.hh:15-89, the subset callers use).
+class DenseMatrix {
+public:
+    DenseMatrix() : rows_(0), cols_(0) {}
+    DenseMatrix(int64_t rows, int64_t cols) : rows_(rows), cols_(cols), data_(size_t(rows * cols), 0.0) {
+        if (rows < 0 || cols < 0) throw std::invalid_argument("DenseMatrix: negative dimension");
+    }
+    static DenseMatrix identity(int64_t n) {
+        DenseMatrix m(n, n);
+        for (int64_t i = 0; i < n; ++i) m(i, i) = 1.0;
+        return m;
+    }
+    int64_t rows() const { return rows_; }
+    int64_t cols() const { return cols_; }
+    bool empty() const { return rows_ == 0 || cols_ == 0; }
+    double &operator()(int64_t i, int64_t j) { return data_[size_t(j * rows_ + i)]; }
+    double operator()(int64_t i, int64_t j) const { return data_[size_t(j * rows_ + i)]; }
+    std::span<double> col(int64_t j) { return {data_.data() + j * rows_, size_t(rows_)}; }
+    std::span<const double> col(int64_t j) const { return {data_.data() + j * rows_, size_t(rows_)}; }
+    double *data() { return data_.data(); }
+    const double *data() const { return data_.data(); }
+    size_t size() const { return data_.size(); }
+    bool operator==(const DenseMatrix &o) const { return rows_ == o.rows_ && cols_ == o.cols_ && data_ == o.data_; }
+
+private:
+    int64_t rows_, cols_;
+    std::vector<double> data_;
+};
+
+enum class SketchFamily { gaussian, saso, srft };                         // sketch.hh:24
+enum class CondMethod { diag_ratio, krylov_bounds, identity_deviation };  // cqrrpt.hh:61
+
+struct CqrrptConfig {  // cqrrpt.hh:92-102
+    double gamma = 1.25;
+    SketchFamily family = SketchFamily::saso;
+    int64_t nnz_per_col = 4;
+    double eps_tol = 1e-4;
+    CondMethod cond_method = CondMethod::identity_deviation;
+    bool stage1_enabled = true;
+    uint64_t seed = 0;
+    bool measure_distortion = false;
+    bool validate_output = true;
+};
+
+struct PhaseTimings {  // cqrrpt.hh:104-112 (seconds; CUDA events on the stream)
+    double sketch = 0.0, qrcp = 0.0, rank_select = 0.0, precondition = 0.0, cholesky_qr = 0.0, undo = 0.0,
+           total = 0.0;
+};
+
+struct ValidationReport {  // qrcp.hh:53-60 (+ Frobenius orthogonality)
+    double orth_loss = 0.0, orth_loss_fro = 0.0, recon_rel = 0.0, max_below_diag = 0.0;
+    bool pivots_valid = false, diag_nonincreasing = false, pass = false;
+};
+
+struct CqrrptDiagnostics {  // cqrrpt.hh:114-122
+    std::optional<double> distortion, effective_distortion;
+    double cond_m_pre = 1.0;
+    double truncation_ratio = 0.0;
+    double flop_estimate = 0.0;
+    PhaseTimings timings;
+    std::optional<ValidationReport> validation;
+};
+
+struct PivotedQR {  // qrcp.hh:19-24
+    DenseMatrix q, r;
+    std::vector<int64_t> pivots;
+    int64_t rank = 0;
+};
+
+struct CqrrptOutput {  // cqrrpt.hh:124-129
+    PivotedQR factorization;
+    int64_t k0 = 0;
+    int64_t k = 0;
+    CqrrptDiagnostics diagnostics;
+};
+
+inline int64_t sketch_rows_for(double gamma, int64_t n) { return cqrrpt_gpu_sketch_rows(gamma, n); }
+
+inline double flop_model(int64_t m, int64_t n, int64_t k, int64_t d, double c_sk) {
+    double v = cqrrpt_gpu_flop_model(m, n, k, d, c_sk);
+    if (v < 0) throw std::invalid_argument("flop_model: requires 0 <= k <= min(d, n)");
+    return v;
+}
+
+namespace detail {
+inline void throw_for(int rc, const char *what) {
+    std::string msg = std::string(what) + ": " + cqrrpt_gpu_last_error();
+    if (rc < 0) throw std::invalid_argument(msg);
+    if (rc == CQRRPT_GPU_ERR_SINGULAR) throw std::domain_error(msg);
+    throw std::runtime_error(msg);
+}
+struct DevBuf {
+    void *p = nullptr;
+    explicit DevBuf(size_t bytes) {
+        if (bytes && cudaMalloc(&p, bytes) != cudaSuccess) throw std::runtime_error("cudaMalloc failed");
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+}  // namespace detail
+
+// Drop-in for cqrrpt::cqrrpt (cqrrpt.cc:317-328). validate_output is evaluated
+// on the device (cqrrpt_gpu_validate) with the reference's tolerance.
+inline CqrrptOutput cqrrpt(const DenseMatrix &m, const CqrrptConfig &cfg = {}) {
+    if (cfg.gamma < 1.0) throw std::invalid_argument("cqrrpt: gamma must be >= 1");
+    if (!(cfg.eps_tol > unit_roundoff)) throw std::invalid_argument("cqrrpt: eps_tol must exceed the unit roundoff");
+    if (cfg.family != SketchFamily::saso) throw std::logic_error("cqrrpt_b200: only the SASO family runs on the GPU");
+    CqrrptOutput out;
+    const int64_t rows = m.rows(), n = m.cols();
+    if (n == 0) {
+        out.factorization.q = DenseMatrix(rows, 0);
+        out.factorization.r = DenseMatrix(0, 0);
+        return out;
+    }
+    const size_t abytes = sizeof(double) * size_t(rows * n);
+    detail::DevBuf a(abytes), a0(cfg.validate_output ? abytes : 0), r(sizeof(double) * size_t(n * n)),
+        j(sizeof(int64_t) * size_t(n));
+    if (cudaMemcpy(a.p, m.data(), abytes, cudaMemcpyHostToDevice) != cudaSuccess)
+        throw std::runtime_error("H2D copy failed");
+    if (cfg.validate_output) cudaMemcpy(a0.p, a.p, abytes, cudaMemcpyDeviceToDevice);
+    cqrrpt_gpu_ctx ctx;
+    cqrrpt_gpu_ctx_init(&ctx);
+    ctx.cond_method = int32_t(cfg.cond_method);
+    ctx.flags = CQRRPT_GPU_TIMINGS | CQRRPT_GPU_EXACT_STAGE2 | CQRRPT_GPU_DIAGNOSTICS |
+                (cfg.stage1_enabled ? 0 : CQRRPT_GPU_NO_STAGE1);
+    int64_t k = 0, k0 = 0;
+    int rc = cqrrpt_gpu_dgeqpt(rows, n, static_cast<double *>(a.p), rows, cfg.gamma, cfg.nnz_per_col, cfg.seed,
+                               cfg.eps_tol, static_cast<double *>(r.p), n, static_cast<int64_t *>(j.p), &k, &k0, &ctx);
+    if (rc) detail::throw_for(rc, "cqrrpt");
+    out.k = k;
+    out.k0 = k0;
+    out.factorization.rank = k;
+    out.factorization.q = DenseMatrix(rows, k);
+    out.factorization.r = DenseMatrix(k, n);
+    out.factorization.pivots.resize(size_t(n));
+    cudaMemcpy(out.factorization.q.data(), a.p, sizeof(double) * size_t(rows * k), cudaMemcpyDeviceToHost);
+    if (k > 0)
+        cudaMemcpy2D(out.factorization.r.data(), sizeof(double) * size_t(k), r.p, sizeof(double) * size_t(n),
+                     sizeof(double) * size_t(k), size_t(n), cudaMemcpyDeviceToHost);
+    cudaMemcpy(out.factorization.pivots.data(), j.p, sizeof(int64_t) * size_t(n), cudaMemcpyDeviceToHost);
+    auto &d = out.diagnostics;
+    d.cond_m_pre = ctx.cond_m_pre;
+    d.truncation_ratio = ctx.truncation_ratio;
+    d.flop_estimate = ctx.flop_estimate;
+    d.timings = PhaseTimings{ctx.timings_ms[0] * 1e-3, ctx.timings_ms[1] * 1e-3, ctx.timings_ms[2] * 1e-3,
+                             ctx.timings_ms[3] * 1e-3, ctx.timings_ms[4] * 1e-3, ctx.timings_ms[5] * 1e-3,
+                             ctx.timings_ms[6] * 1e-3};
+    if (cfg.validate_output) {  // qrcp.cc:150-196 with tol = max(100 n u, 10 eps_tol) (cqrrpt.cc:310)
+        ValidationReport v;
+        const double tol = std::max(100.0 * double(n) * unit_roundoff, 10.0 * cfg.eps_tol);
+        std::vector<char> seen(size_t(n), 0);
+        v.pivots_valid = true;
+        for (int64_t p : out.factorization.pivots) {
+            if (p < 0 || p >= n || seen[size_t(p)]) {
+                v.pivots_valid = false;
+                break;
+            }
+            seen[size_t(p)] = 1;
+        }
+        for (int64_t jj = 0; jj < n; ++jj)
+            for (int64_t ii = jj + 1; ii < k; ++ii)
+                v.max_below_diag = std::max(v.max_below_diag, std::abs(out.factorization.r(ii, jj)));
+        v.diag_nonincreasing = true;
+        for (int64_t ii = 1; ii < std::min(k, n); ++ii)
+            if (std::abs(out.factorization.r(ii, ii)) > std::abs(out.factorization.r(ii - 1, ii - 1)))
+                v.diag_nonincreasing = false;
+        if (v.pivots_valid) {
+            rc = cqrrpt_gpu_validate(rows, n, k, static_cast<double *>(a0.p), rows, static_cast<double *>(a.p), rows,
+                                     static_cast<double *>(r.p), n, static_cast<int64_t *>(j.p), &v.orth_loss_fro,
+                                     &v.orth_loss, &v.recon_rel, nullptr);
+            if (rc) detail::throw_for(rc, "validate");
+        }
+        v.pass = v.pivots_valid && v.max_below_diag == 0.0 && v.orth_loss <= tol && v.recon_rel <= tol;
+        d.validation = v;
+    }
+    return out;
+}
+
+}  // namespace cqrrpt_b200

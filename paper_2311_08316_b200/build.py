@@ -86,5 +86,26 @@ def build(verbose: bool = False, force: bool = False) -> str:
     return LIB
 
 
+def build_cxx_adapter_test() -> str:
+    """Compile tests/cxx/adapter_test.cc: the reference-signature C++ adapter
+    (include/cqrrpt_b200.hh) linked against libcqrrpt_gpu.so (+ the oracle
+    library for inputs/expected values; test infrastructure)."""
+    src = os.path.join(ROOT, "tests", "cxx", "adapter_test.cc")
+    out_dir = os.path.join(ROOT, "tests", "cxx", "_build")
+    os.makedirs(out_dir, exist_ok=True)
+    exe = os.path.join(out_dir, "adapter_test")
+    cuda = os.path.dirname(os.path.dirname(nvcc()))
+    gxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+    cmd = [gxx, "-std=c++20", "-O2", src, "-o", exe, "-I", os.path.join(ROOT, "include"),
+           "-I", os.path.join(cuda, "include"),
+           "-L", OUT_DIR, "-lcqrrpt_gpu", "-L", os.path.join(ROOT, "oracle", "_build"), "-loracle",
+           "-L", os.path.join(cuda, "lib64"), "-lcudart_static", "-ldl", "-lpthread", "-lrt",
+           "-Wl,-rpath,$ORIGIN/../../../paper_2311_08316_b200/_lib:$ORIGIN/../../../oracle/_build"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode:
+        raise RuntimeError("adapter test build failed:\n" + r.stderr)
+    return exe
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

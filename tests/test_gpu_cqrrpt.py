@@ -215,3 +215,17 @@ def test_c_abi_host_outputs_path(cuda, oracle):
     assert np.array_equal(out.factorization.pivots, ref.pivots)
     assert out.k == ref.k
     assert out.diagnostics.validation.passed
+
+
+def test_cxx_reference_signature_adapter(cuda):
+    """include/cqrrpt_b200.hh (cqrrpt_b200::cqrrpt(const DenseMatrix&, const CqrrptConfig&))
+    running the reference test-suite assertions from C++ (tests/cxx/adapter_test.cc)."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "cxx", "_build", "adapter_test")
+    if not os.path.exists(exe):
+        from paper_2311_08316_b200.build import build_cxx_adapter_test
+        exe = build_cxx_adapter_test()
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "OK" in r.stdout
