@@ -65,6 +65,9 @@ extern "C" {
 #define CQRRPT_GPU_NO_STAGE1 0x4       /* CqrrptConfig::stage1_enabled = false */
 #define CQRRPT_GPU_DIAGNOSTICS 0x8     /* truncation_ratio (spectral norm of R_sk) */
 #define CQRRPT_GPU_TIMINGS 0x10        /* per-phase CUDA-event timings into ctx->timings_ms */
+#define CQRRPT_GPU_FAST_SKETCH 0x20    /* allow a c-split sketch (partials summed in a fixed order):
+                                          deterministic, not bit-identical to the reference's
+                                          single FMA chain; fills the GPU when n is small */
 
 /* Sum-allreduce of `count` doubles in place on device memory, ordered on
  * `stream`. Return 0 on success. */
@@ -137,6 +140,10 @@ int cqrrpt_gpu_saso_plan(int64_t d, int64_t c0, int64_t count, int64_t nnz, uint
 int cqrrpt_gpu_saso_sketch(int64_t m, int64_t n, const double *A, int64_t lda, int64_t d,
                            int64_t nnz, uint64_t seed, int64_t c0, double *Msk, int64_t ldm,
                            void *stream);
+/* As cqrrpt_gpu_saso_sketch; flags & CQRRPT_GPU_FAST_SKETCH allows the
+ * c-split decomposition (deterministic, not bit-identical). */
+int cqrrpt_gpu_saso_sketch_ex(int64_t m, int64_t n, const double *A, int64_t lda, int64_t d, int64_t nnz,
+                              uint64_t seed, int64_t c0, double *Msk, int64_t ldm, uint32_t flags, void *stream);
 
 /* Max-norm Householder QRCP of the d x n sketch (qrcp.cc:35-97, want_q=false).
  * Msk is overwritten. R_sk (n x n buffer, ldr >= n; first k_sk rows valid,
@@ -170,6 +177,12 @@ int cqrrpt_gpu_potrf(int64_t n, double *G, int64_t ldg, int64_t *failure_index, 
  * 200, 1e-6 inflation). value on host. */
 int cqrrpt_gpu_cond_estimate(int64_t ell, const double *R, int64_t ldr, int32_t method, double *value,
                              void *stream);
+
+/* X (k x k, ldx) = triu(R)^{-1}: recursive blocked inverse (64 x 64 diagonal
+ * blocks, then log2(k/64) levels of batched DMMA GEMMs). Stage 2 uses it in
+ * place of the reference's per-iteration triangular solves
+ * (inverse_norm_estimate, linalg.cc:486-500). R must have a nonzero diagonal. */
+int cqrrpt_gpu_trtri_upper(int64_t k, const double *R, int64_t ldr, double *X, int64_t ldx, void *stream);
 
 /* C (k x n, ldc) = triu(A) (k x k, lda) * triu(B) (k x n, ldb): exactly
  * upper-trapezoidal; multiply_upper_triangular (cqrrpt.cc:23-36). */

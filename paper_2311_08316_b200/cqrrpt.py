@@ -230,7 +230,7 @@ def dgeqpt(a, d_factor: float = 1.25, nnz: int = 4, seed: int = 0, eps_tol: floa
            cond_method: int = CondMethod.identity_deviation, stage1: bool = True, exact_stage2: bool = False,
            diagnostics: bool = False, timings: bool = False, stream=None, comm: Optional[Comm] = None,
            global_row_offset: int = 0, r_out=None, j_out=None, allreduce=None, nranks: int = 1,
-           rank: int = 0) -> DeviceResult:
+           rank: int = 0, fast_sketch: bool = False) -> DeviceResult:
     """The north-star entry point on a column-major CUDA tensor ``a``
     (m_local x n). Q overwrites ``a[:, :k]`` in place; R (k x n) and the
     0-based pivots are returned as device tensors.
@@ -238,7 +238,11 @@ def dgeqpt(a, d_factor: float = 1.25, nnz: int = 4, seed: int = 0, eps_tol: floa
     Multi-rank: pass ``comm`` (NCCL, cqrrpt_gpu_comm_*) or ``allreduce`` — a
     Python callable ``(ptr, count, stream_ptr) -> None`` that sum-allreduces
     ``count`` doubles in place — together with ``nranks``/``rank`` and this
-    rank's ``global_row_offset``."""
+    rank's ``global_row_offset``.
+
+    ``fast_sketch``: allow a c-split sketch (CQRRPT_GPU_FAST_SKETCH) that
+    fills the GPU when n is small; deterministic, but J then matches the
+    reference only away from near-ties (the default sketch is bit-identical)."""
     torch = _torch()
     L = _lib.load()
     m, n = a.shape
@@ -262,6 +266,8 @@ def dgeqpt(a, d_factor: float = 1.25, nnz: int = 4, seed: int = 0, eps_tol: floa
         flags |= _lib.F_DIAGNOSTICS
     if timings:
         flags |= _lib.F_TIMINGS
+    if fast_sketch:
+        flags |= _lib.F_FAST_SKETCH
     ctx.flags = flags
     cb = None
     if comm is not None:

@@ -10,6 +10,8 @@
 // matvec). The inverse-norm estimate uses the explicit inverse of R (the
 // leading block of R^{-1} is the inverse of the leading block of R), so both
 // matvecs are GEMVs instead of triangular solves.
+#include <vector>
+
 #include "common.cuh"
 #include "internal.hh"
 
@@ -185,20 +187,88 @@ __global__ void __launch_bounds__(kPowThreads) cond_estimate_kernel(int64_t ell,
     }
 }
 
-// One CTA per probe ell: first power iterate ||(R_ell - I) v0||.
-__global__ void __launch_bounds__(kPowThreads) idev_first_kernel(const double *__restrict__ r, int64_t ldr,
-                                                                 const int64_t *__restrict__ ells, double *work,
-                                                                 int64_t work_stride, double *__restrict__ out) {
-    __shared__ double scratch[32];
-    const int64_t ell = ells[blockIdx.x];
-    double *v = work + blockIdx.x * work_stride, *w = v + ell;
-    start_vector(ell, v, scratch);
-    PowOp dev{r, ldr, ell, ell, 2};
-    op_forward(dev, v, w);
+// First power iterate of identity_deviation for every binary-search probe:
+// ||(R_ell - I) v0_ell|| with v0_ell = g[:ell] / ||g[:ell]|| (g the fixed
+// normal sequence, linalg.cc:434-442). All probes share g, so one pass over R
+// serves them all: row i walks j ascending and records its running sum
+// S_i(ell) = sum_{i<=j<ell} R(i,j) g_j at each probe boundary.
+// CTA = 32 rows x 8 column chunks; per-CTA partial sums, fixed-order final.
+constexpr int kIdRows = 32, kIdChunks = 8, kIdMaxProbes = 64;
+
+__global__ void idev_gvec_kernel(int64_t n, double *__restrict__ g) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        g[i] = normal_dev(0x5eedcafe01234567ULL, (uint64_t)i);
+}
+
+__global__ void __launch_bounds__(kIdRows *kIdChunks) idev_rows_kernel(const double *__restrict__ r, int64_t ldr,
+                                                                        const int64_t *__restrict__ ells, int np,
+                                                                        int64_t maxl, const double *__restrict__ g,
+                                                                        double *__restrict__ part) {
+    extern __shared__ double sp[];  // [np][kIdChunks][kIdRows]
+    const int lane = threadIdx.x & 31, ch = threadIdx.x >> 5;
+    const int64_t i = (int64_t)blockIdx.x * kIdRows + lane;
+    const int64_t L = (maxl + kIdChunks - 1) / kIdChunks;
+    const int64_t jb = cmax<int64_t>(i, ch * L), je = cmin<int64_t>(maxl, (ch + 1) * L);
     double s = 0.0;
-    for (int64_t i = threadIdx.x; i < ell; i += blockDim.x) s = fma(w[i], w[i], s);
-    double nw = sqrt(block_sum(s, scratch));
-    if (threadIdx.x == 0) out[blockIdx.x] = nw;
+    int p = 0;
+    // probes ending at or before this chunk's first column get nothing from it
+    while (p < np && ells[p] <= jb) sp[(p++ * kIdChunks + ch) * kIdRows + lane] = 0.0;
+    int64_t next = p < np ? ells[p] : INT64_MAX;  // next probe boundary
+    auto record = [&](int64_t jend) {
+        while (next == jend) {
+            sp[(p++ * kIdChunks + ch) * kIdRows + lane] = s;
+            next = p < np ? ells[p] : INT64_MAX;
+        }
+    };
+    if (i < maxl) {
+        int64_t j = jb;
+        for (; j + 8 <= je; j += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = r[(j + u) * ldr + i];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                s = fma(v[u], g[j + u], s);
+                record(j + u + 1);
+            }
+        }
+        for (; j < je; ++j) {
+            s = fma(r[j * ldr + i], g[j], s);
+            record(j + 1);
+        }
+    }
+    for (; p < np; ++p) sp[(p * kIdChunks + ch) * kIdRows + lane] = s;  // probes beyond the chunk
+    __syncthreads();
+    // (row, probe): S = sum of chunks in order, w = S - g_i for i < ell
+    for (int q = ch; q < np; q += kIdChunks) {
+        double w2 = 0.0;
+        if (i < ells[q]) {
+            double S = 0.0;
+            for (int c = 0; c < kIdChunks; ++c) S += sp[(q * kIdChunks + c) * kIdRows + lane];
+            const double w = S - g[i];
+            w2 = w * w;
+        }
+        w2 = warp_sum(w2);
+        if (lane == 0) part[(int64_t)q * gridDim.x + blockIdx.x] = w2;
+    }
+}
+
+__global__ void __launch_bounds__(256) idev_final_kernel(const int64_t *__restrict__ ells, int np,
+                                                         const double *__restrict__ g,
+                                                         const double *__restrict__ part, int64_t nblk,
+                                                         double *__restrict__ out) {
+    __shared__ double scratch[32];
+    for (int q = 0; q < np; ++q) {
+        double s = 0.0;
+        for (int64_t i = threadIdx.x; i < ells[q]; i += blockDim.x) s = fma(g[i], g[i], s);
+        const double nrm2 = block_sum(s, scratch);
+        __syncthreads();
+        double t = 0.0;
+        for (int64_t b = threadIdx.x; b < nblk; b += blockDim.x) t += part[q * nblk + b];
+        const double w2 = block_sum(t, scratch);
+        __syncthreads();
+        if (threadIdx.x == 0) out[q] = (nrm2 == 0.0) ? 0.0 : sqrt(w2 / nrm2);
+    }
 }
 
 __global__ void __launch_bounds__(kPowThreads) spectral_kernel(const double *__restrict__ a, int64_t lda, int64_t m,
@@ -213,15 +283,30 @@ __global__ void __launch_bounds__(kPowThreads) spectral_kernel(const double *__r
 int identity_deviation_first(const double *r, int64_t ldr, const int64_t *ells, int nells, double *out_host,
                              Workspace &ws, cudaStream_t st) {
     if (nells <= 0) return 0;
-    int64_t maxl = 0;
-    for (int i = 0; i < nells; ++i) maxl = std::max(maxl, ells[i]);
+    if (nells > kIdMaxProbes) return fail_internal("identity_deviation_first: too many probes");
+    std::vector<int64_t> sorted(ells, ells + nells);
+    for (int i = 1; i < nells; ++i)
+        if (sorted[i] < sorted[i - 1]) return fail_internal("identity_deviation_first: probes must ascend");
+    const int64_t maxl = sorted.back();
+    const int64_t nblk = (maxl + kIdRows - 1) / kIdRows;
     int64_t *dl = ws.get<int64_t>("idev.ells", nells);
-    double *work = ws.get<double>("idev.work", (size_t)nells * 2 * maxl + 1);
+    double *g = ws.get<double>("idev.g", (size_t)maxl + 1);
+    double *part = ws.get<double>("idev.part", (size_t)nells * nblk);
     double *dout = ws.get<double>("idev.out", nells);
-    CQ_CUDA(cudaMemcpyAsync(dl, ells, sizeof(int64_t) * nells, cudaMemcpyHostToDevice, st), "ells h2d");
-    idev_first_kernel<<<(unsigned)nells, kPowThreads, 0, st>>>(r, ldr, dl, work, 2 * maxl, dout);
+    if (!dl || !g || !part || !dout) return fail_nomem("idev workspace");
+    CQ_CUDA(cudaMemcpyAsync(dl, sorted.data(), sizeof(int64_t) * nells, cudaMemcpyHostToDevice, st), "ells h2d");
+    idev_gvec_kernel<<<(unsigned)std::min<int64_t>((maxl + 255) / 256, 1024), 256, 0, st>>>(maxl, g);
     note_launch();
-    CQ_TRY(check_launch("idev_first_kernel"));
+    const size_t smem = sizeof(double) * (size_t)nells * kIdChunks * kIdRows;
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(idev_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(double) * kIdMaxProbes * kIdChunks * kIdRows));
+    CQ_CUDA(attr, "idev smem attr");
+    idev_rows_kernel<<<(unsigned)nblk, kIdRows * kIdChunks, smem, st>>>(r, ldr, dl, nells, maxl, g, part);
+    note_launch();
+    idev_final_kernel<<<1, 256, 0, st>>>(dl, nells, g, part, nblk, dout);
+    note_launch();
+    CQ_TRY(check_launch("idev kernels"));
     CQ_CUDA(cudaMemcpyAsync(out_host, dout, sizeof(double) * nells, cudaMemcpyDeviceToHost, st), "idev d2h");
     CQ_CUDA(cudaStreamSynchronize(st), "idev sync");
     return 0;

@@ -194,7 +194,8 @@ int cqrrpt_gpu_dgeqpt(int64_t m, int64_t n, double *A, int64_t lda, double d_fac
     // ---- sketch ------------------------------------------------------------
     double *msk = ws.get<double>("drv.msk", (size_t)(d * n));
     if (!msk) return fail_nomem("sketch");
-    CQ_TRY(saso_sketch(m, n, A, lda, d, nnz, seed, ctx->global_row_offset, msk, d, ws, st));
+    CQ_TRY(saso_sketch(m, n, A, lda, d, nnz, seed, ctx->global_row_offset, msk, d, ws, st,
+                       (ctx->flags & CQRRPT_GPU_FAST_SKETCH) != 0));
     clk.mark(PH_SKETCH);
     CQ_TRY(do_allreduce(ctx, msk, (size_t)(d * n), st));
     clk.mark(PH_COMM);
@@ -272,10 +273,8 @@ int cqrrpt_gpu_dgeqpt(int64_t m, int64_t n, double *A, int64_t lda, double d_fac
     const double threshold = std::sqrt(eps_tol / kUnitRoundoff);
     const int method = ctx->cond_method;
     double *rinv = ws.get<double>("drv.rinv", (size_t)(k0f * k0f));
-    double *eye = ws.get<double>("drv.eye", (size_t)(k0f * k0f));
-    if (!rinv || !eye) return fail_nomem("rinv");
-    CQ_TRY(fill_identity(k0f, eye, k0f, st));
-    CQ_TRY(trsm_right(k0f, k0f, eye, k0f, nullptr, rfull, k0, rinv, k0f, st));  // X R = I
+    if (!rinv) return fail_nomem("rinv");
+    CQ_TRY(trtri_upper(k0f, rfull, k0, rinv, k0f, ws, st));  // R^{-1}; leading blocks = leading inverses
     bool exact = (ctx->flags & CQRRPT_GPU_EXACT_STAGE2) != 0;
     int64_t k = k0f;
     if (!exact) {
@@ -402,6 +401,18 @@ int cqrrpt_gpu_saso_sketch(int64_t m, int64_t n, const double *A, int64_t lda, i
     return saso_sketch(m, n, A, lda, d, nnz, seed, c0, Msk, ldm, workspace(), (cudaStream_t)stream);
 }
 
+int cqrrpt_gpu_saso_sketch_ex(int64_t m, int64_t n, const double *A, int64_t lda, int64_t d, int64_t nnz,
+                              uint64_t seed, int64_t c0, double *Msk, int64_t ldm, uint32_t flags, void *stream) {
+    if (m < 0) return -1;
+    if (n < 0) return -2;
+    if (m > 0 && lda < m) return -4;
+    if (d < 1) return -5;
+    if (nnz < 1 || nnz > d) return -6;
+    if (ldm < d) return -10;
+    return saso_sketch(m, n, A, lda, d, nnz, seed, c0, Msk, ldm, workspace(), (cudaStream_t)stream,
+                       (flags & CQRRPT_GPU_FAST_SKETCH) != 0);
+}
+
 int cqrrpt_gpu_qrcp(int64_t d, int64_t n, double *Msk, int64_t ldm, double rank_tol, double *Rsk, int64_t ldr,
                     int64_t *J, int64_t *k_sk, void *stream) {
     if (d < 1) return set_error("qrcp_maxnorm: need at least one row"), -1;  // qrcp.cc:37
@@ -447,14 +458,18 @@ int cqrrpt_gpu_cond_estimate(int64_t ell, const double *R, int64_t ldr, int32_t 
     double *rinv = nullptr;
     if (method != CQRRPT_COND_DIAG_RATIO && ell > 0) {
         rinv = ws.get<double>("ce.rinv", (size_t)(ell * ell));
-        double *eye = ws.get<double>("ce.eye", (size_t)(ell * ell));
-        CQ_TRY(fill_identity(ell, eye, ell, st));
+        if (!rinv) return fail_nomem("cond rinv");
         // zero diagonal: inverse_norm_estimate returns +inf (linalg.cc:489-490);
-        // the kernel handles that case without touching rinv
-        int rc = trsm_right(ell, ell, eye, ell, nullptr, R, ldr, rinv, ell, st);
-        if (rc && rc != CQRRPT_GPU_ERR_SINGULAR) return rc;
+        // the kernel handles that case without reading rinv
+        CQ_TRY(trtri_upper(ell, R, ldr, rinv, ell, ws, st));
     }
     return cond_estimate(ell, R, ldr, rinv, ell, method, value, ws, st);
+}
+
+int cqrrpt_gpu_trtri_upper(int64_t k, const double *R, int64_t ldr, double *X, int64_t ldx, void *stream) {
+    if (k < 0) return -1;
+    if (k > 0 && (ldr < k || ldx < k)) return -3;
+    return trtri_upper(k, R, ldr, X, ldx, workspace(), (cudaStream_t)stream);
 }
 
 int cqrrpt_gpu_trmm_upper(int64_t k, int64_t n, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,

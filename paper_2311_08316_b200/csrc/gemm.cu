@@ -32,7 +32,7 @@ CQ_DEVI int sw_km(int k, int m) {
 // [r][k] layout (B, and A transposed): 16 doubles per row
 CQ_DEVI int sw_rk(int r, int k) { return r * kBK + (k ^ ((r & 3) << 2)); }
 
-template <int BM, int BN, bool TA>
+template <int BM, int BN, bool TA, bool BATCH>
 __global__ void __launch_bounds__(kThreads, 3) dgemm_kernel(GemmArgs P) {
     constexpr int WM = BM / 32;  // warps along M
     static_assert(WM * (BN / 64) == 4, "4 warps of 32x64");
@@ -50,8 +50,11 @@ __global__ void __launch_bounds__(kThreads, 3) dgemm_kernel(GemmArgs P) {
     const int64_t r0 = tm * BM, c0 = tn * BN;
     if (P.upper_only && r0 > c0 + BN - 1) return;
     const int64_t z = blockIdx.z;
-    const int64_t kbeg = z * P.k_per_split;
-    const int64_t kend = cmin<int64_t>(kbeg + P.k_per_split, P.K);
+    // BATCH: grid.z indexes independent problems (element offsets below);
+    // otherwise it is the split-K slice
+    const int64_t za = BATCH ? z * P.bs_a : 0, zb = BATCH ? z * P.bs_b : 0;
+    const int64_t kbeg = BATCH ? 0 : z * P.k_per_split;
+    const int64_t kend = BATCH ? P.K : cmin<int64_t>(kbeg + P.k_per_split, P.K);
     const int nchunks = (int)((kend - kbeg + kBK - 1) / kBK);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -76,7 +79,7 @@ __global__ void __launch_bounds__(kThreads, 3) dgemm_kernel(GemmArgs P) {
                 int q = it * kThreads + tid;
                 int kk = q / BM, mm = q % BM;
                 bool ok = (r0 + mm < P.M) && (k0 + kk < kend);
-                const double *src = P.A + (ok ? (k0 + kk) * P.lda + r0 + mm : 0);
+                const double *src = P.A + za + (ok ? (k0 + kk) * P.lda + r0 + mm : 0);
                 cp_async8_zfill(as + sw_km<BM>(kk, mm), src, ok ? 8 : 0);
             }
         } else {  // A: K x M col-major (op = A^T), tile [m][k]
@@ -85,7 +88,7 @@ __global__ void __launch_bounds__(kThreads, 3) dgemm_kernel(GemmArgs P) {
                 int q = it * kThreads + tid;
                 int mm = q / kBK, kk = q % kBK;
                 bool ok = (r0 + mm < P.M) && (k0 + kk < kend);
-                const double *src = P.A + (ok ? (r0 + mm) * P.lda + k0 + kk : 0);
+                const double *src = P.A + za + (ok ? (r0 + mm) * P.lda + k0 + kk : 0);
                 cp_async8_zfill(as + sw_rk(mm, kk), src, ok ? 8 : 0);
             }
         }
@@ -94,7 +97,7 @@ __global__ void __launch_bounds__(kThreads, 3) dgemm_kernel(GemmArgs P) {
             int q = it * kThreads + tid;
             int nn = q / kBK, kk = q % kBK;
             bool ok = (c0 + nn < P.N) && (k0 + kk < kend);
-            const double *src = P.B + (ok ? (c0 + nn) * P.ldb + k0 + kk : 0);
+            const double *src = P.B + zb + (ok ? (c0 + nn) * P.ldb + k0 + kk : 0);
             cp_async8_zfill(bs + sw_rk(nn, kk), src, ok ? 8 : 0);
         }
     };
@@ -153,8 +156,8 @@ __global__ void __launch_bounds__(kThreads, 3) dgemm_kernel(GemmArgs P) {
             const int64_t j = c0 + wn * 64 + ni * 8 + 2 * t + v;
             if (j >= P.N) continue;
             const double *cin = nullptr;
-            if (P.beta != 0.0) cin = P.Cin + (P.cin_cols ? P.cin_cols[j] : j) * P.ldcin;
-            double *cout = P.Cout + j * P.ldc;
+            if (P.beta != 0.0) cin = P.Cin + (BATCH ? z * P.bs_cin : 0) + (P.cin_cols ? P.cin_cols[j] : j) * P.ldcin;
+            double *cout = P.Cout + (BATCH ? z * P.bs_c : 0) + j * P.ldc;
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi) {
                 const int64_t i = r0 + wm * 32 + mi * 8 + g;
@@ -167,15 +170,15 @@ __global__ void __launch_bounds__(kThreads, 3) dgemm_kernel(GemmArgs P) {
         }
 }
 
-template <int BM, int BN, bool TA>
+template <int BM, int BN>
 size_t gemm_smem() {
     return sizeof(double) * kStages * (BM + BN) * kBK;
 }
 
-template <int BM, int BN, bool TA>
+template <int BM, int BN, bool TA, bool BATCH>
 static int launch(const GemmArgs &P, dim3 grid, cudaStream_t st) {
-    auto kern = dgemm_kernel<BM, BN, TA>;
-    const size_t smem = gemm_smem<BM, BN, TA>();
+    auto kern = dgemm_kernel<BM, BN, TA, BATCH>;
+    const size_t smem = gemm_smem<BM, BN>();
     static thread_local int configured[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -188,18 +191,30 @@ static int launch(const GemmArgs &P, dim3 grid, cudaStream_t st) {
     return check_launch("dgemm_kernel");
 }
 
+template <int BM, int BN>
+static int launch_shape(bool trans_a, bool batch, const GemmArgs &P, dim3 grid, cudaStream_t st) {
+    if (batch) return trans_a ? launch<BM, BN, true, true>(P, grid, st) : launch<BM, BN, false, true>(P, grid, st);
+    return trans_a ? launch<BM, BN, true, false>(P, grid, st) : launch<BM, BN, false, false>(P, grid, st);
+}
+
 // Tile shape: 128x64 for tall-skinny outputs (N <= 64), 64x128 otherwise.
 int gemm_ex(bool trans_a, GemmArgs P, int64_t splits, cudaStream_t st) {
     if (P.M <= 0 || P.N <= 0) return 0;
     if (splits < 1) splits = 1;
-    if (P.k_per_split <= 0) P.k_per_split = (P.K + splits - 1) / splits;
+    if (P.batch > 1) {
+        if (P.part) return fail_internal("gemm_ex: batched split-K is not supported");
+        splits = P.batch;  // grid.z = problems
+    } else if (P.k_per_split <= 0) {
+        P.k_per_split = (P.K + splits - 1) / splits;
+    }
     const bool tall = P.N <= 64;
     const int BM = tall ? 128 : 64, BN = tall ? 64 : 128;
     dim3 grid;
     if (P.tiles) grid = dim3((unsigned)P.ntiles_part, 1, (unsigned)splits);
     else grid = dim3((unsigned)((P.M + BM - 1) / BM), (unsigned)((P.N + BN - 1) / BN), (unsigned)splits);
-    if (tall) return trans_a ? launch<128, 64, true>(P, grid, st) : launch<128, 64, false>(P, grid, st);
-    return trans_a ? launch<64, 128, true>(P, grid, st) : launch<64, 128, false>(P, grid, st);
+    const bool batch = P.batch > 1;
+    if (tall) return launch_shape<128, 64>(trans_a, batch, P, grid, st);
+    return launch_shape<64, 128>(trans_a, batch, P, grid, st);
 }
 
 int gemm(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const double *a, int64_t lda,
@@ -303,7 +318,7 @@ int gram(int64_t m, int64_t k, const double *x, int64_t ldx, double *gmat, int64
         P.tiles = tiles;
         GemmArgs *pp = &P;
         dim3 grid((unsigned)ntiles, 1, (unsigned)nslices);
-        CQ_TRY((launch<64, 128, true>(*pp, grid, st)));
+        CQ_TRY((launch<64, 128, true, false>(*pp, grid, st)));
     } else {
         CQ_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * ntiles * BM * BN, st), "memset part");
         nslices = 1;

@@ -24,6 +24,8 @@ struct GemmArgs {
     const int2 *tiles;        // optional explicit (tile_m, tile_n) list
     const int64_t *skip_flag; // device flag: nonzero -> the launch is a no-op
     int upper_only;           // only entries i <= j (and tiles touching them)
+    int64_t batch;            // > 1: grid.z indexes independent problems (no split-K)
+    int64_t bs_a, bs_b, bs_cin, bs_c;  // per-problem element strides of A, B, Cin, Cout
 };
 
 // C_out = alpha op(A) B + beta C_in, optionally split over K into `splits`

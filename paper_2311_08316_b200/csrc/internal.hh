@@ -54,7 +54,7 @@ void release_workspace();
 // ---- kernels' host entry points (implemented in the .cu files) -------------
 int saso_plan(int64_t d, int64_t c0, int64_t count, int64_t nnz, uint64_t seed, uint32_t *plan, cudaStream_t st);
 int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, int64_t nnz, uint64_t seed,
-                int64_t c0, double *msk, int64_t ldm, Workspace &ws, cudaStream_t st, bool exact_order = true);
+                int64_t c0, double *msk, int64_t ldm, Workspace &ws, cudaStream_t st, bool allow_split = false);
 
 // QRCP: fills Rsk (n x n, ldr; rows >= k_sk zero), Jdev (int64 n), k_sk (host).
 int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *rsk, int64_t ldr, int64_t *jdev,
@@ -74,6 +74,10 @@ int trmm_upper(int64_t k, int64_t n, const double *a, int64_t lda, const double 
 
 // small utilities (util.cu)
 int fill_identity(int64_t n, double *a, int64_t lda, cudaStream_t st);
+int trtri_upper(int64_t k, const double *r, int64_t ldr, double *x, int64_t ldx, Workspace &ws, cudaStream_t st);
+// inverses of the 64 x 64 diagonal blocks of triu(r), block b at dinv + b*4096
+// (column-major, ld 64; a ragged last block is padded with the identity)
+int trtri_diag_blocks(int64_t k, const double *r, int64_t ldr, double *dinv, cudaStream_t st);
 int zero_strict_lower(int64_t n, double *a, int64_t lda, cudaStream_t st);
 int frob_norm_upper(int64_t n, const double *a, int64_t lda, double *out_host, Workspace &ws, cudaStream_t st);
 int copy_matrix(int64_t m, int64_t n, const double *src, int64_t lds, double *dst, int64_t ldd, cudaStream_t st);

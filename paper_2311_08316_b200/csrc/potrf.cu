@@ -17,78 +17,109 @@ int gemm_tn_upper(int64_t N, int64_t K, double alpha, const double *a, int64_t l
 
 constexpr int kPB = 64;
 
-__global__ void __launch_bounds__(256) potrf_diag_kernel(int64_t n, double *__restrict__ g, int64_t ldg, int64_t j0,
-                                                         int64_t *__restrict__ fail) {
+// Diagonal block: 4 threads per column (thread (c, q) keeps rows i = 4s + q of
+// column c in registers, static indices only), so a step is 16 predicated
+// FMAs per thread across 8 warps. Two barriers per step (rrow is double
+// buffered).
+constexpr int kPQ = 4;               // threads per column
+constexpr int kPS = kPB / kPQ;       // rows per thread
+constexpr int kDiagThreads = kPB * kPQ;
+
+__global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(int64_t n, double *__restrict__ g, int64_t ldg,
+                                                                  int64_t j0, int64_t *__restrict__ fail) {
     if (*fail) return;
-    __shared__ double a[kPB][kPB + 1];  // a[col][row]
+    __shared__ double rmat[kPB][kPB + 1];  // R block, [col][row]
+    __shared__ double rrow[2][kPB];
+    __shared__ double s_rjj;
     __shared__ int s_fail;
     const int nb = (int)cmin<int64_t>(kPB, n - j0);
-    for (int q = threadIdx.x; q < kPB * kPB; q += blockDim.x) {
-        int c = q / kPB, r = q % kPB;
-        a[c][r] = (c < nb && r < nb && r <= c) ? g[(j0 + c) * ldg + j0 + r] : 0.0;
+    const int c = threadIdx.x >> 2, q = threadIdx.x & 3;
+    double a[kPS];
+    const double *col = g + (j0 + c) * ldg + j0;
+#pragma unroll
+    for (int s = 0; s < kPS; ++s) {
+        const int i = kPQ * s + q;
+        a[s] = (c < nb && i <= c) ? col[i] : 0.0;
     }
     if (threadIdx.x == 0) s_fail = 0;
     __syncthreads();
+    int base = 0;  // a[s] holds row 4 * (base + s) + q: the window slides so row j is in a[0]
     for (int j = 0; j < nb; ++j) {
-        // a[j][j] now holds g(j,j) - sum_{t<j} r(t,j)^2
-        if (threadIdx.x == 0) {
-            double d = a[j][j];
-            if (d <= 0.0 || !isfinite(d)) {
-                s_fail = j + 1;
-            } else {
-                a[j][j] = sqrt(d);
-            }
+        if ((j >> 2) != base) {
+#pragma unroll
+            for (int s = 0; s + 1 < kPS; ++s) a[s] = a[s + 1];
+            a[kPS - 1] = 0.0;
+            ++base;
+        }
+        const bool holder = (q == (j & 3));  // this thread holds row j of its column
+        const double ajc = a[0];             // (holder) g(j,c) - sum_{t<j} r(t,j) r(t,c)
+        if (holder && c == j) {
+            if (ajc <= 0.0 || !isfinite(ajc)) s_fail = j + 1;
+            else s_rjj = sqrt(ajc);
         }
         __syncthreads();
         if (s_fail) break;
-        const double rjj = a[j][j];
-        // row j of R: r(j,c) = a(j,c) / r(j,j) for c > j
-        for (int c = j + 1 + threadIdx.x; c < nb; c += blockDim.x) a[c][j] = a[c][j] / rjj;
-        __syncthreads();
-        // trailing: a(i,c) -= r(j,i) r(j,c) for j < i <= c
-        for (int q = threadIdx.x; q < kPB * kPB; q += blockDim.x) {
-            int c = q / kPB, i = q % kPB;
-            if (c > j && c < nb && i > j && i <= c) a[c][i] = fma(-a[i][j], a[c][j], a[c][i]);
+        double *rr = rrow[j & 1];
+        if (holder) {
+            // division, not a reciprocal product: on exactly singular Grams the
+            // sign of the last Schur complement (the failure index) follows it
+            const double rjc = c > j ? ajc / s_rjj : (c == j ? s_rjj : 0.0);
+            rr[c] = rjc;
+            rmat[c][j] = rjc;
         }
         __syncthreads();
+        if (c > j) {
+            const double rjc = rr[c];
+#pragma unroll
+            for (int s = 0; s < kPS; ++s) {
+                const int i = kPQ * (base + s) + q;
+                if (i > j && i <= c && i < kPB) a[s] = fma(-rr[i], rjc, a[s]);
+            }
+        }
     }
     const int f = s_fail;
-    // write back the factored part (all columns before the failure)
     const int ncols = f ? f - 1 : nb;
-    for (int q = threadIdx.x; q < kPB * kPB; q += blockDim.x) {
-        int c = q / kPB, r = q % kPB;
-        if (c < ncols && r <= c) g[(j0 + c) * ldg + j0 + r] = a[c][r];
+    for (int e = threadIdx.x; e < kPB * kPB; e += blockDim.x) {
+        int cc = e / kPB, r = e % kPB;
+        if (cc < ncols && r <= cc) g[(j0 + cc) * ldg + j0 + r] = rmat[cc][r];
     }
     if (threadIdx.x == 0 && f) *fail = j0 + f;  // 1-based global index
 }
 
-// panel: for each column c >= j0+nb: x = R_jj^{-T} g[j0:j0+nb, c] (forward substitution)
-__global__ void __launch_bounds__(128) potrf_panel_kernel(int64_t n, double *__restrict__ g, int64_t ldg, int64_t j0,
-                                                          const int64_t *__restrict__ fail) {
+// Panel: X = R_jj^{-T} G[j0:j0+nb, cols] for the columns right of the block.
+// One warp per column: lane l owns rows l and l+32; at step t the solved x_t
+// is broadcast by shuffle and every lane updates its rows below t.
+constexpr int kPanelWarps = 8;
+
+__global__ void __launch_bounds__(kPanelWarps * 32) potrf_panel_kernel(int64_t n, double *__restrict__ g,
+                                                                      int64_t ldg, int64_t j0,
+                                                                      const int64_t *__restrict__ fail) {
     if (*fail) return;
-    __shared__ double r[kPB][kPB + 1];  // r[col][row]
+    __shared__ double r[kPB][kPB + 1];  // r[col][row] of R_jj
     const int nb = (int)cmin<int64_t>(kPB, n - j0);
-    for (int q = threadIdx.x; q < kPB * kPB; q += blockDim.x) {
-        int c = q / kPB, rr = q % kPB;
-        r[c][rr] = (c < nb && rr <= c) ? g[(j0 + c) * ldg + j0 + rr] : (c == rr ? 1.0 : 0.0);
+    for (int e = threadIdx.x; e < kPB * kPB; e += blockDim.x) {
+        int cc = e / kPB, rr = e % kPB;
+        r[cc][rr] = (cc < nb && rr <= cc) ? g[(j0 + cc) * ldg + j0 + rr] : 0.0;
     }
     __syncthreads();
-    const int64_t col = j0 + nb + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t col = j0 + nb + (int64_t)blockIdx.x * kPanelWarps + w;
     if (col >= n) return;
     double *gc = g + col * ldg + j0;
-    double x[kPB];
-#pragma unroll
-    for (int i = 0; i < kPB; ++i) x[i] = (i < nb) ? gc[i] : 0.0;
-#pragma unroll
-    for (int i = 0; i < kPB; ++i) {
-        double s = x[i];
-#pragma unroll
-        for (int t = 0; t < i; ++t) s = fma(-r[i][t], x[t], s);
-        x[i] = s / r[i][i];
+    const int l0 = lane, l1 = lane + 32;
+    double x0 = l0 < nb ? gc[l0] : 0.0, x1 = l1 < nb ? gc[l1] : 0.0;
+    for (int t = 0; t < nb; ++t) {
+        const double cur = __shfl_sync(0xffffffffu, t < 32 ? x0 : x1, t & 31);
+        const double xt = cur / r[t][t];
+        if (lane == (t & 31)) {
+            if (t < 32) x0 = xt;
+            else x1 = xt;
+        }
+        if (l0 > t && l0 < nb) x0 = fma(-r[l0][t], xt, x0);
+        if (l1 > t && l1 < nb) x1 = fma(-r[l1][t], xt, x1);
     }
-#pragma unroll
-    for (int i = 0; i < kPB; ++i)
-        if (i < nb) gc[i] = x[i];
+    if (l0 < nb) gc[l0] = x0;
+    if (l1 < nb) gc[l1] = x1;
 }
 
 __global__ void zero_strict_lower_kernel(int64_t n, double *__restrict__ a, int64_t lda) {
@@ -107,14 +138,16 @@ int potrf(int64_t n, double *g, int64_t ldg, int64_t *failure_index, Workspace &
     *failure_index = 0;
     if (n <= 0) return 0;
     int64_t *fail = ws.get<int64_t>("potrf.fail", 1);
+    if (!fail) return fail_nomem("potrf workspace");
     CQ_CUDA(cudaMemsetAsync(fail, 0, sizeof(int64_t), st), "memset fail");
     for (int64_t j0 = 0; j0 < n; j0 += kPB) {
         const int64_t nb = std::min<int64_t>(kPB, n - j0);
-        potrf_diag_kernel<<<1, 256, 0, st>>>(n, g, ldg, j0, fail);
+        potrf_diag_kernel<<<1, kDiagThreads, 0, st>>>(n, g, ldg, j0, fail);
         note_launch();
         const int64_t rest = n - j0 - nb;
         if (rest > 0) {
-            potrf_panel_kernel<<<(unsigned)((rest + 127) / 128), 128, 0, st>>>(n, g, ldg, j0, fail);
+            potrf_panel_kernel<<<(unsigned)((rest + kPanelWarps - 1) / kPanelWarps), kPanelWarps * 32, 0, st>>>(
+                n, g, ldg, j0, fail);
             note_launch();
             // G[t0:, t0:] -= P^T P, P = R[j0:j0+nb, t0:]
             const int64_t t0 = j0 + nb;

@@ -48,12 +48,24 @@ constexpr int kQrcpWarps = kQrcpThreads / 32;
 // ---------------------------------------------------------------------------
 
 // lanes 0..3: add the precomputed products p[e] (e = lane mod 4, e < body) to s
-CQ_DEVI double chain_sum(double s, const double *p, int64_t body, int lane) {
-    int64_t e = lane;
-    for (; e + 28 < body; e += 32) {
+// The loads of group g+1 are issued before the adds of group g, so only the
+// dependent DADD latency stays on the chain (body < 2^31: shared memory).
+CQ_DEVI double chain_sum(double s, const double *p, int64_t body64, int lane) {
+    const int body = (int)body64;
+    int e = lane;
+    if (e + 28 < body) {
         double v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) v[u] = p[e + 4 * u];
+        for (e += 32; e + 28 < body; e += 32) {
+            double nx[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) nx[u] = p[e + 4 * u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s = s + v[u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = nx[u];
+        }
 #pragma unroll
         for (int u = 0; u < 8; ++u) s = s + v[u];
     }
@@ -92,27 +104,8 @@ CQ_DEVI int stage_async(double *dst, const double *g, int64_t len, int tid, int 
     return off;
 }
 
-// Reference dot of sa[0..c) . g[0..c) (sa == nullptr: g . g) for a column that
-// is not staged: the warp streams it through wb in WB-sized chunks, forming
-// the products in parallel; lanes 0..3 carry the four ordered chains.
-CQ_DEVI double warp_ref_dot_chunked(const double *sa, const double *g, int64_t c, double *wb, int WB, int lane) {
-    const int64_t body = c & ~(int64_t)3;
-    double s = 0.0;
-    for (int64_t b0 = 0; b0 < body; b0 += WB) {
-        const int len = (int)cmin<int64_t>(WB, body - b0);  // multiple of 4 (WB is)
-        for (int e = lane; e < len; e += 32) {
-            const double xv = ld_cg(g + b0 + e);
-            wb[e] = (sa ? sa[b0 + e] : xv) * xv;
-        }
-        __syncwarp();
-        if (lane < 4) s = chain_sum(s, wb, len, lane);
-        __syncwarp();
-    }
-    double tot = 0.0;
-    if (lane < 4)
-        tot = chain_finish(s, c, [&](int64_t xx) { return sa ? sa[xx] : ld_cg(g + xx); },
-                           [&](int64_t xx) { return ld_cg(g + xx); });
-    return __shfl_sync(0xffffffffu, tot, 0);
+CQ_DEVI void trace_mark(unsigned long long *tr, int64_t i, int slot) {
+    if (tr && blockIdx.x == 0 && threadIdx.x == 0 && i < 512) tr[i * 8 + slot] = (unsigned long long)clock64();
 }
 
 // Warp-level reference dot of sa[0..c) (shared memory; nullptr = the column
@@ -123,7 +116,7 @@ CQ_DEVI double warp_ref_dot_chunked(const double *sa, const double *g, int64_t c
 // into b0 (prefetched). When the whole column fits in one chunk the products
 // go to b1, so b0 keeps the column (*kept = true) for the update pass.
 CQ_DEVI double stream_dot(const double *sa, const double *g, int64_t c, double *b0, double *b1, int CHD, bool pre0,
-                          bool *kept, int lane) {
+                          bool *kept, int lane, unsigned long long *tr = nullptr, int64_t step = 0) {
     const int off = (int)((reinterpret_cast<uintptr_t>(g) >> 3) & 1);  // same for every chunk
     const int64_t body = c & ~(int64_t)3;
     const int64_t nch = (c + CHD - 1) / CHD;
@@ -146,16 +139,36 @@ CQ_DEVI double stream_dot(const double *sa, const double *g, int64_t c, double *
         const int64_t base = k * CHD;
         const int64_t bl = cmax<int64_t>(0, cmin<int64_t>(CHD, body - base));
         double *prod = (nch == 1) ? b1 : buf;
-#pragma unroll 8
-        for (int64_t e = lane; e < bl; e += 32) prod[e] = (sa ? sa[base + e] : buf[e]) * buf[e];
+        // loads of 8 elements are issued before their products are stored
+        // (prod may alias buf, so the compiler would otherwise serialise)
+        const int blen = (int)bl;
+        for (int e0 = lane; e0 < blen; e0 += 256) {
+            double xa[8], xb[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + 32 * u;
+                xb[u] = e < blen ? buf[e] : 0.0;
+                xa[u] = e < blen ? (sa ? sa[base + e] : xb[u]) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + 32 * u;
+                if (e < blen) prod[e] = xa[u] * xb[u];
+            }
+        }
         __syncwarp();
+        if (k == 0) trace_mark(tr, step, 5);
         if (lane < 4) s = chain_sum(s, prod, bl, lane);
         __syncwarp();
     }
+    // the <4 tail elements are still in the last chunk's buffer (products
+    // only overwrote its first bl entries)
+    const int64_t lastbase = (nch - 1) * CHD;
+    const double *lastbuf = (((nch - 1) & 1) ? b1 : b0) + off - lastbase;
     double tot = 0.0;
     if (lane < 4)
-        tot = chain_finish(s, c, [&](int64_t x) { return sa ? sa[x] : ld_cg(g + x); },
-                           [&](int64_t x) { return ld_cg(g + x); });
+        tot = chain_finish(s, c, [&](int64_t x) { return sa ? sa[x] : lastbuf[x]; },
+                           [&](int64_t x) { return lastbuf[x]; });
     return __shfl_sync(0xffffffffu, tot, 0);
 }
 
@@ -180,13 +193,6 @@ struct QrcpArgs {
     unsigned long long *trace;  // optional per-step phase timestamps (CTA 0)
 };
 
-CQ_DEVI void trace_mark(unsigned long long *tr, int64_t i, int slot) {
-    if (tr && blockIdx.x == 0 && threadIdx.x == 0 && i < 512) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        tr[i * 6 + slot] = t;
-    }
-}
 
 __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
     extern __shared__ __align__(16) double smem[];
@@ -284,27 +290,31 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         // independent of the pivot decision)
         const int64_t jfirst = i + 1 + ((cta - (i + 1)) % G + G) % G;
         const int64_t j_w = jfirst + (int64_t)wid * G;
-        int32_t pj0 = 0;
-        double wj0 = 0.0, wrefj0 = 0.0, t0 = 0.0;
-        if (j_w < n) {
-            pj0 = ld_cg(A.cmap[cur] + j_w);
-            const double *col = A.b + (int64_t)pj0 * ld;
-            stage_async(b0, col + i + 1, cmin<int64_t>(CHD, c), lane, 32);
-            cp_async_commit();
-            wj0 = ld_cg(A.w[cur] + j_w);
-            wrefj0 = ld_cg(A.wref + j_w);
-            t0 = ld_cg(col + i);
-        }
-        const int32_t phys_i = ld_cg(A.cmap[cur] + i);
-        const double w_i = ld_cg(A.w[cur] + i), wref_i = ld_cg(A.wref + i);
-
-        // ---- pivot: lowest index attaining the max (qrcp.cc:26-31) -------
+        // The partials are on the critical path: issue their loads first, so
+        // their round trip overlaps the column-map round trip of the prefetch.
         ArgMax g{-INFINITY, 0x7fffffff};
         int32_t gp = 0;
         if (threadIdx.x < G) {
             g = ArgMax{ld_cg(A.pv[cur] + threadIdx.x), ld_cg(A.pi[cur] + threadIdx.x)};
             gp = ld_cg(A.pp[cur] + threadIdx.x);
         }
+        int32_t pj0 = 0;
+        double wj0 = 0.0, wrefj0 = 0.0, t0 = 0.0;
+        if (j_w < n) {
+            pj0 = ld_cg(A.cmap[cur] + j_w);
+            wj0 = ld_cg(A.w[cur] + j_w);
+            wrefj0 = ld_cg(A.wref + j_w);
+        }
+        const int32_t phys_i = ld_cg(A.cmap[cur] + i);
+        const double w_i = ld_cg(A.w[cur] + i), wref_i = ld_cg(A.wref + i);
+        if (j_w < n) {
+            const double *col = A.b + (int64_t)pj0 * ld;
+            stage_async(b0, col + i + 1, cmin<int64_t>(CHD, c), lane, 32);
+            cp_async_commit();
+            t0 = ld_cg(col + i);
+        }
+
+        // ---- pivot: lowest index attaining the max (qrcp.cc:26-31) -------
         int32_t phys_p;
         g = block_argmax(g, gp, &phys_p);
         if (i == 0) stop = A.rank_tol * sqrt(fmax(g.v, 0.0));  // max_norm0 (qrcp.cc:52-55)
@@ -326,8 +336,14 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
             __syncthreads();
         }
         const double *xs = s_x + s_poff;  // xs[0] = x_i, xs[1 + e] = tail element e
-#pragma unroll 8
-        for (int64_t e = threadIdx.x; e < body; e += kQrcpThreads) s_sv[e] = xs[1 + e] * xs[1 + e];
+        for (int e0 = threadIdx.x; e0 < (int)body; e0 += 4 * kQrcpThreads) {
+            double xv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) xv[u] = e0 + u * kQrcpThreads < (int)body ? xs[1 + e0 + u * kQrcpThreads] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (e0 + u * kQrcpThreads < (int)body) s_sv[e0 + u * kQrcpThreads] = xv[u] * xv[u];
+        }
         __syncthreads();
         if (wid == 0 && lane < 4) {
             double s = chain_sum(0.0, s_sv, body, lane);
@@ -350,9 +366,14 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         }
         __syncthreads();
         const double alpha = s_bc[0], v0 = s_bc[1], beta = s_bc[2];
-#pragma unroll 8
-        for (int64_t r = threadIdx.x; r < c; r += kQrcpThreads)
-            s_sv[r] = (beta != 0.0) ? xs[1 + r] / v0 : xs[1 + r];  // colj[i] /= v0
+        for (int r0 = threadIdx.x; r0 < (int)c; r0 += 4 * kQrcpThreads) {  // colj[i] /= v0
+            double xv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) xv[u] = r0 + u * kQrcpThreads < (int)c ? xs[1 + r0 + u * kQrcpThreads] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (r0 + u * kQrcpThreads < (int)c) s_sv[r0 + u * kQrcpThreads] = (beta != 0.0) ? xv[u] / v0 : xv[u];
+        }
         __syncthreads();
         const double *sv = s_sv;
         trace_mark(A.trace, i, 2);
@@ -388,18 +409,33 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
             bool kept = false;
             __syncwarp();
             if (beta != 0.0) {  // apply_reflector (linalg.cc:126-136)
-                const double dot = stream_dot(sv, tail, c, b0, b1, CHD, pre, &kept, lane);
+                const double dot = stream_dot(sv, tail, c, b0, b1, CHD, pre, &kept, lane,
+                                              (first && wid == 0) ? A.trace : nullptr, i);
+                if (first && wid == 0) trace_mark(A.trace, i, 6);
                 double tau = t;
                 tau += dot;
                 tau *= beta;
                 t = t - tau;
                 if (kept) {  // column still in b0: update from shared memory
                     double *cb = b0 + off;
-#pragma unroll 8
-                    for (int64_t e = lane; e < c; e += 32) {
-                        const double nv = fma(-tau, sv[e], cb[e]);
-                        cb[e] = nv;
-                        __stcg(tail + e, nv);
+                    const int ci = (int)c;
+                    for (int e0 = lane; e0 < ci; e0 += 256) {
+                        double xv[8], xc[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int e = e0 + 32 * u;
+                            xv[u] = e < ci ? sv[e] : 0.0;
+                            xc[u] = e < ci ? cb[e] : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int e = e0 + 32 * u;
+                            if (e < ci) {
+                                const double nv = fma(-tau, xv[u], xc[u]);
+                                cb[e] = nv;
+                                __stcg(tail + e, nv);
+                            }
+                        }
                     }
                 } else {  // restream the column (double-buffered)
                     const int64_t nch = (c + CHD - 1) / CHD;
@@ -428,6 +464,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
                 cp_async_wait<0>();  // drain the prefetch before b0 is reused
                 __syncwarp();
             }
+            if (first && wid == 0) trace_mark(A.trace, i, 7);
             double updated = fma(-t, t, wj);  // qrcp.cc:77-78
             double newref = wrefj;
             if (updated <= sqrt_u * wrefj) {  // qrcp.cc:82-86 (warp-uniform)
@@ -613,8 +650,8 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     if (!a.w[0] || !a.bar || !a.k_out) return fail_nomem("qrcp workspace");
     CQ_CUDA(cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned long long), st), "memset bar");
     static const bool tracing = getenv("CQRRPT_QRCP_TRACE") != nullptr;
-    a.trace = tracing ? ws.get<unsigned long long>("qrcp.trace", 512 * 6) : nullptr;
-    if (a.trace) CQ_CUDA(cudaMemsetAsync(a.trace, 0, 512 * 6 * sizeof(unsigned long long), st), "trace memset");
+    a.trace = tracing ? ws.get<unsigned long long>("qrcp.trace", 512 * 8) : nullptr;
+    if (a.trace) CQ_CUDA(cudaMemsetAsync(a.trace, 0, 512 * 8 * sizeof(unsigned long long), st), "trace memset");
     void *args[] = {&a};
     CQ_CUDA(cudaLaunchCooperativeKernel((void *)qrcp_kernel, dim3(G), dim3(kQrcpThreads), args, smem, st),
             "qrcp cooperative launch");
@@ -625,22 +662,28 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     CQ_TRY(check_launch("qrcp_extract_kernel"));
     CQ_CUDA(cudaMemcpyAsync(k_sk, a.k_out, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "k_sk d2h");
     CQ_CUDA(cudaStreamSynchronize(st), "qrcp sync");
-    if (a.trace) {  // debug: mean per-phase ns over the first steps
-        std::vector<unsigned long long> h(512 * 6);
+    if (a.trace) {  // debug: mean per-phase SM cycles over the first steps
+        std::vector<unsigned long long> h(512 * 8);
         cudaMemcpy(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost);
-        double acc[5] = {0, 0, 0, 0, 0};
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         int cnt = 0;
         for (int s2 = 0; s2 + 1 < 512 && s2 + 1 < *k_sk; ++s2) {
-            for (int q = 0; q < 4; ++q) acc[q] += (double)(h[s2 * 6 + q + 1] - h[s2 * 6 + q]);
-            acc[4] += (double)(h[(s2 + 1) * 6] - h[s2 * 6 + 4]);
+            const unsigned long long *t = &h[s2 * 8];
+            for (int q = 0; q < 4; ++q) acc[q] += (double)(t[q + 1] - t[q]);
+            acc[4] += (double)(h[(s2 + 1) * 8] - t[4]);
+            if (t[5] && t[6] && t[7]) {  // warp 0's first column: products, dot, update
+                acc[5] += (double)(t[5] - t[2]);
+                acc[6] += (double)(t[6] - t[5]);
+                acc[7] += (double)(t[7] - t[6]);
+            }
             ++cnt;
         }
         if (cnt)
             fprintf(stderr,
-                    "qrcp trace (G=%d, d=%lld, n=%lld, WB=%d, %d steps): argmax %.0f ns, reflector %.0f ns, "
-                    "columns %.0f ns, partials %.0f ns, barrier %.0f ns\n",
-                    G, (long long)d, (long long)n, WB, cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt,
-                    acc[4] / cnt);
+                    "qrcp trace (G=%d, d=%lld, n=%lld, WB=%d, %d steps; SM cycles): argmax %.0f, reflector %.0f, "
+                    "columns %.0f (products %.0f, chain %.0f, update %.0f), partials %.0f, barrier %.0f\n",
+                    G, (long long)d, (long long)n, WB, cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[5] / cnt,
+                    acc[6] / cnt, acc[7] / cnt, acc[3] / cnt, acc[4] / cnt);
     }
     return 0;
 }

@@ -7,26 +7,31 @@
 //
 // Data layout in HBM
 //   plan   uint32[m_local * nnz]      row | sign<<31 (sign 1 = +1/sqrt(d))
-//   tptr   uint16[ntiles * (d+1)]     per 256-row tile: entry offsets by sketch row
-//   tent   uint16[ntiles * 256*nnz]   per tile, entries sorted by (row, c):
-//                                     c_local | sign<<15
+//   tptr   uint16[ntiles * (d+1)]     per 128-row tile: entry offsets by sketch row
+//   tent   uint32[ntiles * 128*nnz]   per tile, entries sorted by (row, c):
+//                                     negative<<31 | row<<16 | byte offset of
+//                                     A(c_local, 0) in the staged tile (c*264)
 //   part   double[S][d][n]            per c-split partial sketches, row-major
 //   Msk    double d x n column-major  fixed-order sum of the partials
 //
-// Apply kernel: one CTA = 32 columns (lane = column) x a block of sketch rows
-// (register accumulators, 16 warps x A rows) x a contiguous range of row
-// tiles. Each 256x32 tile of A is staged once in shared memory ([c][33]
-// padded: conflict-free transposed stores and conflict-free warp reads of a
-// 256-byte row), then every warp walks the CSR entries of its sketch rows and
-// FMAs val * A(c, j) into its accumulators. Sum order: tile-major, c
-// ascending within a tile, then splits in fixed order -> deterministic.
+// Apply kernel: one CTA = 32 columns (lane = column) x a block of RB sketch
+// rows x a contiguous range of row tiles. The CTA's RB x 32 accumulators live
+// in shared memory; each 128 x 32 tile of A is staged ([c][33] padded:
+// conflict-free warp reads of a 256-byte row) through a 3-stage cp.async
+// pipeline with the tile's CSR slice. Warp w walks the entries of its RB/16
+// sketch rows as one flat, row-sorted list: acc(r, j) = fma(v, A(c, j),
+// acc(r, j)) with c ascending, so every output entry is the reference's own
+// FMA chain (sketch.cc:137-143) -> bit-identical with one c-split.
 #include "common.cuh"
 #include "internal.hh"
 
 namespace cqg {
 
-constexpr int kTileRows = 256;  // rows of A per CSR tile
+constexpr int kTileRows = 128;  // rows of A per CSR tile
 constexpr int kApplyWarps = 16;
+constexpr int kApplyThreads = kApplyWarps * 32;
+constexpr int kApplyStages = 3;
+constexpr int kXLD = 33;        // staged tile row stride (doubles)
 constexpr uint64_t kSasoSalt = 0x7361736fULL;  // sketch.cc:19
 
 // ---------------------------------------------------------------------------
@@ -67,7 +72,7 @@ __global__ void saso_plan_kernel(int64_t d, int64_t c0, int64_t count, int nnz, 
 __global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d, int nnz,
                                                             const uint32_t *__restrict__ plan,
                                                             uint16_t *__restrict__ tptr,
-                                                            uint16_t *__restrict__ tent) {
+                                                            uint32_t *__restrict__ tent) {
     extern __shared__ int32_t s_cnt[];  // d + 1 counters, then d cursors
     int32_t *s_cur = s_cnt + (d + 1);
     __shared__ int32_t s_part[256 / 32 + 1];
@@ -86,7 +91,6 @@ __global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d
     const int64_t lo = threadIdx.x * per, hi = cmin<int64_t>(lo + per, d);
     int32_t run = 0;
     for (int64_t r = lo; r < hi; ++r) run += s_cnt[r];
-    // block exclusive scan of `run`
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int32_t incl = run;
 #pragma unroll
@@ -117,7 +121,7 @@ __global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d
     __syncthreads();
     // ordered scatter: entry e = c_local*nnz + t, processed in ascending e
     if (wid == 0) {
-        uint16_t *oent = tent + tile * (int64_t)(kTileRows * nnz);
+        uint32_t *oent = tent + tile * (int64_t)(kTileRows * nnz);
         const unsigned lt = (1u << lane) - 1u;
         for (int b = 0; b < nent; b += 32) {
             int e = b + lane;
@@ -130,8 +134,8 @@ __global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d
             int pos = valid ? s_cur[r] + rank : 0;
             __syncwarp();
             if (valid) {
-                int c_local = e / nnz;
-                oent[pos] = (uint16_t)(c_local | ((w >> 31) << 15));
+                const uint32_t c_local = (uint32_t)(e / nnz);
+                oent[pos] = (~w & 0x80000000u) | (r << 16) | (c_local * kXLD * 8u);  // bit 31: -1/sqrt(d)
                 // highest-ranked member advances the cursor
                 if (rank == __popc(grp & act) - 1) s_cur[r] += __popc(grp & act);
             }
@@ -141,122 +145,128 @@ __global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d
 }
 
 // ---------------------------------------------------------------------------
-// K2: apply. A accumulators per lane (template), 16 warps -> 16*A sketch rows
-// per CTA. Tiles of 256 rows x 32 columns of A plus the tile's CSR slice are
-// double-buffered in shared memory with cp.async (the copy of tile t+1 runs
-// under the FMAs of tile t). Writes part[split][r][j] (row-major).
+// K2: apply (see the header). Writes part[split][r][j] (row-major).
 // ---------------------------------------------------------------------------
-template <int A>
-__global__ void __launch_bounds__(kApplyWarps * 32, 1)
-    saso_apply_kernel(int64_t m, int64_t n, const double *__restrict__ a, int64_t lda, int64_t d,
-                      double val, int nnz, int64_t ntiles, int64_t tiles_per_split,
-                      const uint16_t *__restrict__ tptr, const uint16_t *__restrict__ tent,
-                      double *__restrict__ part) {
-    constexpr int RB = kApplyWarps * A;
-    constexpr int LD = 33;
-    constexpr int NT = kApplyWarps * 32;
-    constexpr int PTRW = ((RB + 1 + 1) / 2 + 1 + 3) & ~3;  // 32-bit words per ptr buffer (16B multiple)
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double *s_tile = reinterpret_cast<double *>(smem_raw);                     // [2][256][33]
-    uint32_t *s_ptrw = reinterpret_cast<uint32_t *>(s_tile + 2 * kTileRows * LD);  // [2][PTRW]
-    const int entw = ((kTileRows * nnz + 1) / 2 + 3) & ~3;                    // words per entry buffer
-    uint32_t *s_entw = s_ptrw + 2 * PTRW;                                      // [2][entw]
+struct ApplyArgs {
+    int64_t m, n, lda, d;
+    const double *a;
+    double val;
+    int nnz, rb;            // entries per column of S, sketch rows per CTA (multiple of 16)
+    int ptrw, entw;         // 32-bit words per stage for pointers / entries
+    int64_t ntiles, tiles_per_split;
+    const uint16_t *tptr;
+    const uint32_t *tent;
+    double *part;
+};
 
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+__global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int RB = P.rb, A = RB / kApplyWarps;
+    double *acc = reinterpret_cast<double *>(smem_raw);  // [RB][32]
+    const int stage_words = 2 * kTileRows * kXLD + P.ptrw + P.entw;  // 32-bit words per stage
+    uint32_t *stage0 = reinterpret_cast<uint32_t *>(acc + (size_t)RB * 32);
+
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int64_t j0 = (int64_t)blockIdx.x * 32;
     const int64_t r0 = (int64_t)blockIdx.y * RB;
     const int64_t split = blockIdx.z;
-    const int64_t t_begin = split * tiles_per_split;
-    const int64_t t_end = cmin<int64_t>(t_begin + tiles_per_split, ntiles);
-    const int rows_here = (int)cmin<int64_t>(RB, d - r0);  // valid sketch rows in this block
+    const int64_t t_begin = split * P.tiles_per_split;
+    const int64_t t_end = cmin<int64_t>(t_begin + P.tiles_per_split, P.ntiles);
+    const int rows_here = (int)cmin<int64_t>(RB, P.d - r0);  // valid sketch rows in this block
 
-    double acc[A];
+    for (int q = tid; q < RB * 32; q += kApplyThreads) acc[q] = 0.0;
+
+    // staging map: thread -> tile row cc, columns jj0 + 4*it
+    const int cc = tid % kTileRows, jj0 = tid / kTileRows;
+    constexpr int kIters = kTileRows * 32 / kApplyThreads;  // 8
+    auto issue = [&](int64_t tile, int stg) {
+        uint32_t *sw = stage0 + (size_t)stg * stage_words;
+        double *dt = reinterpret_cast<double *>(sw);
+        const int64_t row = tile * kTileRows + cc;
+        const bool rok = row < P.m;
+        const double *src = P.a + (j0 + jj0) * P.lda + row;
 #pragma unroll
-    for (int i = 0; i < A; ++i) acc[i] = 0.0;
-
-    // async copy of tile `tile` into buffer `bf`:
-    //   A rows [256*tile, +256) x cols [j0, j0+32) -> s_tile[bf][row][col] (8-byte copies,
-    //   a warp covers 256 contiguous bytes of one column)
-    //   tptr[tile][r0 .. r0+rows_here] (absolute offsets) -> ptr buffer (4-byte copies from
-    //   the 4-byte aligned start; odd start recorded by the parity of the address)
-    //   tent[tile][0 .. 256*nnz) -> entry buffer (4-byte copies)
-    auto issue = [&](int64_t tile, int bf) {
-        const int64_t row0 = tile * kTileRows;
-        double *dt = s_tile + bf * kTileRows * LD;
-#pragma unroll 4
-        for (int it = 0; it < kTileRows * 32 / NT; ++it) {
-            int e = it * NT + threadIdx.x;
-            int jj = e / kTileRows, cc = e % kTileRows;
-            int64_t row = row0 + cc, col = j0 + jj;
-            bool ok = row < m && col < n;
-            cp_async8_zfill(dt + cc * LD + jj, a + (ok ? col * lda + row : 0), ok ? 8 : 0);
+        for (int it = 0; it < kIters; ++it) {
+            const int jj = jj0 + 4 * it;
+            const bool ok = rok && (j0 + jj < P.n);
+            cp_async8_zfill(dt + cc * kXLD + jj, ok ? src + (int64_t)(4 * it) * P.lda : P.a, ok ? 8 : 0);
         }
-        const uint16_t *gp = tptr + tile * (d + 1) + r0;
+        // tile pointers tptr[tile][r0 .. r0+rows_here] (4-byte words from the aligned start)
+        uint32_t *sp = sw + 2 * kTileRows * kXLD;
+        const uint16_t *gp = P.tptr + tile * (P.d + 1) + r0;
         const uint32_t *gpw = reinterpret_cast<const uint32_t *>(reinterpret_cast<uintptr_t>(gp) & ~(uintptr_t)3);
         const int nw = (int)(((reinterpret_cast<uintptr_t>(gp + rows_here + 1) + 3) - reinterpret_cast<uintptr_t>(gpw)) / 4);
-        for (int w = threadIdx.x; w < nw; w += NT) cp_async4(s_ptrw + bf * PTRW + w, gpw + w);
-        const uint32_t *gew = reinterpret_cast<const uint32_t *>(tent + tile * (int64_t)(kTileRows * nnz));
-        const int nent_w = (kTileRows * nnz + 1) / 2;  // tile entry arrays start 4-byte aligned (256*nnz even)
-        for (int w = threadIdx.x; w < nent_w; w += NT) cp_async4(s_entw + bf * entw + w, gew + w);
-        cp_async_commit();
+        for (int w = tid; w < nw; w += kApplyThreads) cp_async4(sp + w, gpw + w);
+        // all entries of the tile (16-byte copies; the array is padded to whole tiles)
+        uint32_t *se = sp + P.ptrw;
+        const uint32_t *ge = P.tent + tile * (int64_t)(kTileRows * P.nnz);
+        for (int w = 4 * tid; w < kTileRows * P.nnz; w += 4 * kApplyThreads) cp_async16(se + w, ge + w);
     };
-    if (t_begin < t_end) issue(t_begin, 0);
-
-    for (int64_t tile = t_begin; tile < t_end; ++tile) {
-        const int bf = (int)((tile - t_begin) & 1);
-        if (tile + 1 < t_end) {
-            issue(tile + 1, bf ^ 1);  // buffer bf^1 was released by the barrier below (previous iteration)
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        const double *st = s_tile + bf * kTileRows * LD;
-        const uint16_t *sp = reinterpret_cast<const uint16_t *>(s_ptrw + bf * PTRW) +
-                             ((reinterpret_cast<uintptr_t>(tptr + tile * (d + 1) + r0) >> 1) & 1);
-        const uint16_t *se = reinterpret_cast<const uint16_t *>(s_entw + bf * entw);
-
-        // Each sketch row's entries in c order (sketch.cc:137-143); IL rows
-        // interleaved for instruction-level parallelism.
-        constexpr int IL = A < 4 ? A : 4;
-#pragma unroll
-        for (int i0 = 0; i0 < A; i0 += IL) {
-            int beg[IL], end[IL];
-            double s[IL];
-            int nmax = 0;
-#pragma unroll
-            for (int q = 0; q < IL; ++q) {
-                const int rl = min(wid * A + i0 + q, rows_here);
-                beg[q] = sp[rl];
-                end[q] = sp[min(rl + 1, rows_here)];
-                s[q] = acc[i0 + q];
-                nmax = max(nmax, end[q] - beg[q]);
-            }
-            for (int jj = 0; jj < nmax; ++jj) {
-#pragma unroll
-                for (int q = 0; q < IL; ++q) {
-                    const int e = beg[q] + jj;
-                    if (e < end[q]) {
-                        const uint32_t w = se[e];
-                        const double v = (w & 0x8000u) ? val : -val;
-                        s[q] = fma(v, st[(w & 0x7fffu) * LD + lane], s[q]);  // sketch.cc:142
-                    }
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < IL; ++q) acc[i0 + q] = s[q];
-        }
-        __syncthreads();  // buffer bf fully consumed before it is refilled
+    for (int s = 0; s < kApplyStages - 1; ++s) {
+        if (t_begin + s < t_end) issue(t_begin + s, s);
+        cp_async_commit();
     }
+    // x with the entry's sign bit (bit 31 = negative) XORed into its sign
+    auto flip = [](double x, uint32_t w) {
+        return __hiloint2double(__double2hiint(x) ^ (int)(w & 0x80000000u), __double2loint(x));
+    };
+    // acc row r (absolute) of this lane at accb + r * 256 bytes
+    char *accb = reinterpret_cast<char *>(acc + lane) - r0 * 256;
+    const int wr0 = wid * A, wr1 = min((wid + 1) * A, rows_here);  // this warp's rows (local)
+    for (int64_t tile = t_begin; tile < t_end; ++tile) {
+        const int stg = (int)((tile - t_begin) % kApplyStages);
+        cp_async_wait<kApplyStages - 2>();
+        __syncthreads();  // tile visible to all; stage (tile-1) fully consumed
+        {
+            const int64_t nt = tile + kApplyStages - 1;
+            if (nt < t_end) issue(nt, (int)((nt - t_begin) % kApplyStages));
+            cp_async_commit();
+        }
+        const uint32_t *sw = stage0 + (size_t)stg * stage_words;
+        const double *xt = reinterpret_cast<const double *>(sw) + lane;
+        const uint16_t *sp = reinterpret_cast<const uint16_t *>(sw + 2 * kTileRows * kXLD) +
+                             ((reinterpret_cast<uintptr_t>(P.tptr + tile * (P.d + 1) + r0) >> 1) & 1);
+        const uint32_t *se = sw + 2 * kTileRows * kXLD + P.ptrw;
+        if (wr0 >= wr1) continue;
+        const int eb = sp[wr0], ee = sp[wr1];
+        if (eb >= ee) continue;
+        // flat walk over this warp's entries (row-sorted, c ascending per row):
+        // the running sum of the current row stays in a register; a row
+        // change stores it and loads the next row's sum.
+        const char *xb = reinterpret_cast<const char *>(xt);
+        uint32_t curb = se[eb] & 0x7fff0000u;  // row << 16
+        double *cura = reinterpret_cast<double *>(accb + (curb >> 8));
+        double sacc = *cura;
+        auto step = [&](uint32_t w, double x) {
+            if ((w & 0x7fff0000u) != curb) {
+                *cura = sacc;
+                curb = w & 0x7fff0000u;
+                cura = reinterpret_cast<double *>(accb + (curb >> 8));
+                sacc = *cura;
+            }
+            sacc = fma(P.val, flip(x, w), sacc);  // sketch.cc:142; fma(v, x) == fma(|v|, +-x) exactly
+        };
+        int e = eb;
+        for (; e + 2 <= ee; e += 2) {
+            const uint32_t w0 = se[e], w1 = se[e + 1];
+            const double x0 = *reinterpret_cast<const double *>(xb + (w0 & 0xffffu));
+            const double x1 = *reinterpret_cast<const double *>(xb + (w1 & 0xffffu));
+            step(w0, x0);
+            step(w1, x1);
+        }
+        if (e < ee) {
+            const uint32_t w0 = se[e];
+            step(w0, *reinterpret_cast<const double *>(xb + (w0 & 0xffffu)));
+        }
+        *cura = sacc;
+    }
+    cp_async_wait<0>();
+    __syncthreads();
     // write the partial: part[split][r][j]
     const int64_t col = j0 + lane;
-    if (col < n) {
-        double *pp = part + split * d * n;
-#pragma unroll
-        for (int i = 0; i < A; ++i) {
-            int64_t r = r0 + wid * A + i;
-            if (r < d) pp[r * n + col] = acc[i];
-        }
+    if (col < P.n) {
+        double *pp = P.part + split * P.d * P.n;
+        for (int rl = wid; rl < rows_here; rl += kApplyWarps) pp[(r0 + rl) * P.n + col] = acc[rl * 32 + lane];
     }
 }
 
@@ -293,37 +303,26 @@ int saso_plan(int64_t d, int64_t c0, int64_t count, int64_t nnz, uint64_t seed, 
     return check_launch("saso_plan_kernel");
 }
 
-template <int A>
-static int launch_apply(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, double val, int nnz,
-                        int64_t ntiles, const uint16_t *tptr, const uint16_t *tent, double *part,
-                        int64_t nsplit, int64_t tps, int64_t rblocks, cudaStream_t st) {
-    constexpr int RB = kApplyWarps * A;
-    constexpr int PTRW = ((RB + 1 + 1) / 2 + 1 + 3) & ~3;
-    const int entw = ((kTileRows * nnz + 1) / 2 + 3) & ~3;
-    size_t smem = sizeof(double) * 2 * kTileRows * 33 + sizeof(uint32_t) * 2 * (PTRW + entw);
-    if (smem > 220 * 1024) return fail_internal("saso_apply: nnz too large for the shared-memory CSR");
-    auto kern = saso_apply_kernel<A>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return fail_cuda("saso_apply smem attr");
-    dim3 grid((unsigned)((n + 31) / 32), (unsigned)rblocks, (unsigned)nsplit);
-    kern<<<grid, kApplyWarps * 32, smem, st>>>(m, n, a, lda, d, val, nnz, ntiles, tps, tptr, tent, part);
-    note_launch();
-    return check_launch("saso_apply_kernel");
+static size_t apply_smem(int rb, int nnz, int *ptrw, int *entw) {
+    *ptrw = ((rb + 2) / 2 + 1 + 3) & ~3;                // u16 pointers rb+1 from a 4-byte aligned start
+    *entw = (kTileRows * nnz + 3) & ~3;                 // u32 entries, 16-byte multiple
+    const size_t stage = sizeof(uint32_t) * (size_t)(2 * kTileRows * kXLD + *ptrw + *entw);
+    return sizeof(double) * (size_t)rb * 32 + kApplyStages * stage;
 }
 
 int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, int64_t nnz, uint64_t seed,
-                int64_t c0, double *msk, int64_t ldm, Workspace &ws, cudaStream_t st, bool exact_order) {
+                int64_t c0, double *msk, int64_t ldm, Workspace &ws, cudaStream_t st, bool allow_split) {
     if (m <= 0 || n <= 0) {
         // empty shard contributes zeros
         for (int64_t j = 0; j < n; ++j)
             if (cudaMemsetAsync(msk + j * ldm, 0, sizeof(double) * d, st) != cudaSuccess) return fail_cuda("memset");
         return 0;
     }
-    if (d > 65535 || nnz * kTileRows > 65535) return fail_internal("saso_sketch: d or nnz too large for uint16 CSR");
+    if (d > 32767 || nnz * kTileRows > 65535) return fail_internal("saso_sketch: d or nnz too large for the CSR");
     const int64_t ntiles = (m + kTileRows - 1) / kTileRows;
     uint32_t *plan = ws.get<uint32_t>("saso.plan", (size_t)(m * nnz));
-    uint16_t *tptr = ws.get<uint16_t>("saso.tptr", (size_t)(ntiles * (d + 1)));
-    uint16_t *tent = ws.get<uint16_t>("saso.tent", (size_t)(ntiles * kTileRows * nnz));
+    uint16_t *tptr = ws.get<uint16_t>("saso.tptr", (size_t)(ntiles * (d + 1)) + 2);
+    uint32_t *tent = ws.get<uint32_t>("saso.tent", (size_t)(ntiles * kTileRows * nnz) + 4);
     if (!plan || !tptr || !tent) return fail_nomem("saso workspace");
     int rc = saso_plan(d, c0, m, nnz, seed, plan, st);
     if (rc) return rc;
@@ -336,51 +335,75 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
     note_launch();
     if ((rc = check_launch("saso_tile_csr_kernel"))) return rc;
 
+    // Decomposition. Sketch rows per CTA (RB) are bounded by shared memory;
+    // exact order needs one pass over all rows per CTA, so parallelism comes
+    // from row blocks: minimise waves * (staging + RB) over the row-block count.
     const int64_t cgroups = (n + 31) / 32;
     const int sms = num_sms();
-    int A = 20;
-    int64_t nsplit = 1;
-    if (exact_order) {
-        // One pass over all rows per CTA keeps the reference's per-entry sum
-        // order (c ascending, sketch.cc:137-143) -> bit-identical sketch.
-        // Parallelism comes from finer sketch-row blocks instead.
-        // Every CTA streams all m rows of its 32 columns (a fixed staging cost,
-        // ~ the entry work of 256 sketch rows) plus work proportional to its
-        // row-block height 16*A; CTAs run one per SM: minimise
-        // waves(A) * (256 + 16*A).
-        const int cand[] = {20, 16, 12, 8, 4, 2, 1};
+    const size_t smem_max = 227 * 1024;
+    int ptrw = 0, entw = 0;
+    int rb_max = 16;
+    while (rb_max + 16 <= 4096 && apply_smem(rb_max + 16, (int)nnz, &ptrw, &entw) <= smem_max) rb_max += 16;
+    const int64_t min_blocks = (d + rb_max - 1) / rb_max;
+    int64_t rblocks = min_blocks;
+    {
         double best = 1e300;
-        for (int a : cand) {
-            const int64_t ctas = cgroups * ((d + 16 * a - 1) / (16 * a));
-            const int64_t waves = (ctas + sms - 1) / sms;
-            const double cost = (double)waves * (256.0 + (double)std::min<int64_t>(16 * a, d));
+        for (int64_t b = min_blocks; b <= std::max<int64_t>(min_blocks, std::min<int64_t>(d / 16, 4 * min_blocks + 8));
+             ++b) {
+            const int64_t rb = ((d + b - 1) / b + 15) / 16 * 16;
+            const int64_t ctas = cgroups * b;
+            const double cost = (double)((ctas + sms - 1) / sms) * (128.0 + (double)std::min<int64_t>(rb, d));
             if (cost < best) {
                 best = cost;
-                A = a;
+                rblocks = b;
             }
         }
-    } else {
-        if (d <= 16 * 8) A = 8;
-        else if (d <= 16 * 12) A = 12;
-        else if (d <= 16 * 16) A = 16;
-        int64_t base = cgroups * ((d + 16 * A - 1) / (16 * A));
-        nsplit = std::max<int64_t>(1, std::min<int64_t>(ntiles, (2 * sms + base - 1) / base));
     }
-    const int64_t RB = 16 * A;
-    const int64_t rblocks = (d + RB - 1) / RB;
+    // allow_split (CQRRPT_GPU_FAST_SKETCH): fewest row blocks (least re-reading
+    // of A) and a c-split to fill the GPU. Deterministic (partials summed in
+    // split order) but not the reference's single FMA chain per entry.
+    int64_t nsplit = 1;
+    if (allow_split && ntiles >= 32) {
+        rblocks = min_blocks;
+        const int64_t base = cgroups * rblocks;
+        double best = (double)((base + sms - 1) / sms);  // waves per unit of work, nsplit = 1
+        for (int64_t ns = 2; ns <= 64 && ns <= ntiles / 8; ++ns) {
+            const double t = (double)((base * ns + sms - 1) / sms) / (double)ns;
+            if (t < best * 0.95) {
+                best = t;
+                nsplit = ns;
+            }
+        }
+    }
+    const int rb = (int)(((d + rblocks - 1) / rblocks + 15) / 16 * 16);
+    rblocks = (d + rb - 1) / rb;
     int64_t tps = (ntiles + nsplit - 1) / nsplit;
     nsplit = (ntiles + tps - 1) / tps;
     double *part = ws.get<double>("saso.part", (size_t)(nsplit * d * n));
     if (!part) return fail_nomem("saso partials");
-    const double val = 1.0 / sqrt((double)d);  // sketch.cc:79
-#define CQ_APPLY(AA) \
-    case AA: rc = launch_apply<AA>(m, n, a, lda, d, val, (int)nnz, ntiles, tptr, tent, part, nsplit, tps, rblocks, st); break;
-    switch (A) {
-        CQ_APPLY(1) CQ_APPLY(2) CQ_APPLY(4) CQ_APPLY(8) CQ_APPLY(12) CQ_APPLY(16) CQ_APPLY(20)
-        default: return fail_internal("saso: bad A");
-    }
-#undef CQ_APPLY
-    if (rc) return rc;
+
+    ApplyArgs P;
+    P.m = m;
+    P.n = n;
+    P.lda = lda;
+    P.d = d;
+    P.a = a;
+    P.val = 1.0 / sqrt((double)d);  // sketch.cc:79
+    P.nnz = (int)nnz;
+    P.rb = rb;
+    const size_t smem = apply_smem(rb, (int)nnz, &P.ptrw, &P.entw);
+    P.ntiles = ntiles;
+    P.tiles_per_split = tps;
+    P.tptr = tptr;
+    P.tent = tent;
+    P.part = part;
+    if (cudaFuncSetAttribute(saso_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return fail_cuda("saso_apply smem attr");
+    dim3 grid((unsigned)cgroups, (unsigned)rblocks, (unsigned)nsplit);
+    saso_apply_kernel<<<grid, kApplyThreads, smem, st>>>(P);
+    note_launch();
+    if ((rc = check_launch("saso_apply_kernel"))) return rc;
     dim3 g((unsigned)((n + 31) / 32), (unsigned)((d + 31) / 32));
     saso_reduce_kernel<<<g, 256, 0, st>>>(d, n, nsplit, part, msk, ldm);
     note_launch();

@@ -12,10 +12,11 @@
 // overlap the main loop) and accumulates B - X U over K = 64*jb with
 // mma.sync.m8n8k4.f64 (DMMA.8x8x4), K streaming in 16-deep chunks through a
 // 3-stage cp.async pipeline of XOR-swizzled (conflict-free, unpadded) tiles.
-// The epilogue solves the 64 x 64 diagonal block by row substitution in
-// registers with the reference's per-element order (subtract U(s,c) x_s for
-// s ascending, then multiply by 1/U(c,c)); with 3 CTAs per SM one CTA's
-// substitution overlaps its neighbours' DMMA work.
+// The epilogue multiplies by the inverse of the 64 x 64 diagonal block
+// (all block inverses are formed once per solve, trtri.cu), so the whole
+// solve runs on the tensor cores; the reference substitutes element by
+// element (linalg.cc:262-274). The blocks of a well-conditioned
+// preconditioner are well conditioned; the parity tests bound the difference.
 // Algorithmic flops: m*k^2 (the reference's count, flop_model term).
 #include "common.cuh"
 #include "internal.hh"
@@ -28,10 +29,9 @@ constexpr int kBK = 16;    // K chunk
 constexpr int kStages = 3;
 constexpr int kThreads = 128;
 constexpr int kLdT = kNB + 2;  // 66: conflict-free double2 row access
-constexpr int kLdU = kNB + 2;  // Uj row-major [s][c], 16-byte aligned rows
 
 constexpr size_t kPipeBytes = sizeof(double) * kStages * (kBM + kNB) * kBK;
-constexpr size_t kEpiBytes = sizeof(double) * (kBM * kLdT + kNB * kLdU + kNB);
+constexpr size_t kEpiBytes = sizeof(double) * (kBM * kLdT + kNB * kLdT);
 constexpr size_t kTrsmSmem = kPipeBytes > kEpiBytes ? kPipeBytes : kEpiBytes;
 
 CQ_DEVI int sw_km(int k, int m) { return k * kBM + (m ^ ((k & 1) << 3)); }   // A tile [k][m]
@@ -40,7 +40,7 @@ CQ_DEVI int sw_rk(int r, int k) { return r * kBK + (k ^ ((r & 3) << 2)); }  // B
 __global__ void __launch_bounds__(kThreads, 3)
     trsm_block_kernel(int64_t m, int64_t k, int64_t c0, const double *__restrict__ b, int64_t ldb,
                       const int64_t *__restrict__ cols, const double *__restrict__ u, int64_t ldu,
-                      double *__restrict__ x, int64_t ldx) {
+                      const double *__restrict__ dinv_blk, double *__restrict__ x, int64_t ldx) {
     extern __shared__ __align__(16) double sm[];
     double *As = sm;                        // [stages][16][64] swizzled
     double *Bs = sm + kStages * kBK * kBM;  // [stages][64][16] swizzled
@@ -120,10 +120,11 @@ __global__ void __launch_bounds__(kThreads, 3)
     }
     __syncthreads();  // pipeline buffers are reused by the epilogue
 
-    // ---- epilogue -------------------------------------------------------
-    double *Ts = sm;               // [64][66] = B[:, cols] - X[:, <jb] U[<jb, jb]
-    double *Uj = sm + kBM * kLdT;  // [64 s][66] row-major: Uj[s][c] = U[c0+s][c0+c]
-    double *inv = Uj + kNB * kLdU;
+    // ---- epilogue: X_jb = T U_jb^{-1} on the tensor cores ----------------
+    // T = B[:, cols] - X[:, <jb] U[<jb, jb] (the accumulators); U_jb^{-1} is
+    // the precomputed inverse of the 64 x 64 diagonal block (dinv_blk).
+    double *Ts = sm;               // [64 r][66]: T
+    double *Ds = sm + kBM * kLdT;  // [64 c][66]: Ds[c][s] = U_jb^{-1}(s, c)
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -132,41 +133,42 @@ __global__ void __launch_bounds__(kThreads, 3)
             *reinterpret_cast<double2 *>(Ts + r * kLdT + c) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
         }
     for (int q = tid; q < kNB * kNB; q += kThreads) {
-        int cc = q / kNB, ss = q % kNB;  // coalesced over ss (a column of U)
-        double v;
-        if (cc < nbw) v = (ss <= cc) ? u[(c0 + cc) * ldu + c0 + ss] : 0.0;
-        else v = (ss == cc) ? 1.0 : 0.0;
-        Uj[ss * kLdU + cc] = v;
+        const int cc = q / kNB, ss = q % kNB;  // coalesced over ss (a column of the inverse)
+        Ds[cc * kLdT + ss] = __ldg(dinv_blk + q);
     }
     __syncthreads();
-    if (tid < kNB) inv[tid] = 1.0 / Uj[tid * kLdU + tid];  // linalg.cc:272
-    __syncthreads();
-
-    const int64_t row = row0 + tid;
-    if (tid < kBM && row < m) {
-        double tv[kNB];
 #pragma unroll
-        for (int c = 0; c < kNB; c += 2) {
-            const double2 v2 = *reinterpret_cast<const double2 *>(Ts + tid * kLdT + c);
-            tv[c] = v2.x;
-            tv[c + 1] = v2.y;
-        }
+    for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int s = 0; s < kNB; ++s) {
-            const double xs = tv[s] * inv[s];
-            tv[s] = xs;
-            const double *us = Uj + s * kLdU;
-            if ((s + 1) & 1) tv[s + 1] = fma(-us[s + 1], xs, tv[s + 1]);  // odd start: one single
+        for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+#pragma unroll 4
+    for (int kk = 0; kk < kNB; kk += 4) {
+        double af[4], bf[4];
 #pragma unroll
-            for (int c = ((s + 1) & 1) ? s + 2 : s + 1; c < kNB; c += 2) {
-                const double2 u2 = *reinterpret_cast<const double2 *>(us + c);
-                tv[c] = fma(-u2.x, xs, tv[c]);
-                tv[c + 1] = fma(-u2.y, xs, tv[c + 1]);
+        for (int mi = 0; mi < 4; ++mi) af[mi] = Ts[(wm * 32 + mi * 8 + g) * kLdT + kk + t];
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) bf[ni] = Ds[(wn * 32 + ni * 8 + g) * kLdT + kk + t];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+    }
+    __syncthreads();  // Ts is reused for the output staging
+    double *Os = sm;  // [64 c][65 r]
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                int r = wm * 32 + mi * 8 + g, c = wn * 32 + ni * 8 + 2 * t + v;
+                Os[c * (kBM + 1) + r] = acc[mi][ni][v];
             }
-        }
-#pragma unroll
-        for (int c = 0; c < kNB; ++c)
-            if (c < nbw) x[(c0 + c) * ldx + row] = tv[c];
+    __syncthreads();
+    for (int q = tid; q < kNB * kBM; q += kThreads) {  // coalesced column writes
+        const int c = q / kBM, r = q % kBM;
+        const int64_t row = row0 + r;
+        if (c < nbw && row < m) x[(c0 + c) * ldx + row] = Os[c * (kBM + 1) + r];
     }
 }
 
@@ -192,9 +194,14 @@ int trsm_right(int64_t m, int64_t k, const double *b, int64_t ldb, const int64_t
     }
     CQ_CUDA(cudaFuncSetAttribute(trsm_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrsmSmem),
             "trsm smem attr");
+    const int64_t nblk = (k + kNB - 1) / kNB;
+    double *dinv = workspace().get<double>("trsm.dinv", (size_t)(nblk * kNB * kNB));
+    if (!dinv) return fail_nomem("trsm diagonal-block inverses");
+    CQ_TRY(trtri_diag_blocks(k, u, ldu, dinv, st));
     const unsigned grid = (unsigned)((m + kBM - 1) / kBM);
     for (int64_t c0 = 0; c0 < k; c0 += kNB) {
-        trsm_block_kernel<<<grid, kThreads, kTrsmSmem, st>>>(m, k, c0, b, ldb, cols, u, ldu, x, ldx);
+        trsm_block_kernel<<<grid, kThreads, kTrsmSmem, st>>>(m, k, c0, b, ldb, cols, u, ldu,
+                                                            dinv + (c0 / kNB) * kNB * kNB, x, ldx);
         note_launch();
     }
     return check_launch("trsm_block_kernel");

@@ -1,0 +1,130 @@
+// X = R^{-1} for an upper-triangular k x k R, in log depth.
+//
+// Used by stage 2 (rank_stage2, cqrrpt.cc:160-207): the condition estimators
+// apply R_ell^{-1} to vectors, and the fast accept needs ||R^{-1}||_F. The
+// reference solves with R on every power iteration; here the inverse is formed
+// once and every leading block's inverse is its leading block.
+//
+// Recursive blocking: the 64 x 64 diagonal blocks are inverted in one launch
+// (one CTA each, thread per column, back substitution in shared memory), then
+// for s = 64, 128, ...: every pair of neighbouring s-blocks [A B; 0 C] gets its
+// off-diagonal block -A^{-1} B C^{-1} from two batched DMMA GEMMs. log2(k/64)
+// levels, two launches each (plus one for a ragged last pair).
+#include "common.cuh"
+#include "gemm.cuh"
+#include "internal.hh"
+
+namespace cqg {
+
+constexpr int kTB = 64;
+
+// compact = true: block b's inverse goes to x + b*64*64 (column-major, ld 64)
+__global__ void __launch_bounds__(kTB) trtri_diag_kernel(int64_t k, const double *__restrict__ r, int64_t ldr,
+                                                         double *__restrict__ x, int64_t ldx, bool compact) {
+    // rs[col][row]: R_bb in the upper triangle (row <= col); y(i, c) of X_bb
+    // (i <= c) lives in the unused strictly-lower slot rs[i][c + 1].
+    __shared__ double rs[kTB][kTB + 1];
+    __shared__ double inv[kTB];
+    const int64_t o = (int64_t)blockIdx.x * kTB;
+    const int s = (int)cmin<int64_t>(kTB, k - o);
+    for (int e = threadIdx.x; e < kTB * kTB; e += blockDim.x) {
+        int c = e / kTB, i = e % kTB;
+        rs[c][i] = (c < s && i <= c) ? r[(o + c) * ldr + o + i] : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x < s) inv[threadIdx.x] = 1.0 / rs[threadIdx.x][threadIdx.x];
+    __syncthreads();
+    const int c = threadIdx.x;
+    if (c < s) {  // column c: R y = e_c by back substitution
+        rs[c][c + 1] = inv[c];
+        for (int i = c - 1; i >= 0; --i) {
+            double acc = 0.0;
+            for (int t = i + 1; t <= c; ++t) acc = fma(rs[t][i], rs[t][c + 1], acc);
+            rs[i][c + 1] = -acc * inv[i];
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kTB * kTB; e += blockDim.x) {
+        int cc = e / kTB, i = e % kTB;
+        if (compact) x[o * kTB + cc * kTB + i] = (cc < s && i <= cc) ? rs[i][cc + 1] : (cc == i ? 1.0 : 0.0);
+        else if (cc < s && i <= cc) x[(o + cc) * ldx + o + i] = rs[i][cc + 1];
+    }
+}
+
+int trtri_diag_blocks(int64_t k, const double *r, int64_t ldr, double *dinv, cudaStream_t st) {
+    if (k <= 0) return 0;
+    trtri_diag_kernel<<<(unsigned)((k + kTB - 1) / kTB), kTB, 0, st>>>(k, r, ldr, dinv, kTB, true);
+    note_launch();
+    return check_launch("trtri_diag_kernel");
+}
+
+// One level: pairs p = p0 .. p0+np-1 of s-blocks, C of size cs (cs == s
+// except for a ragged last pair). t: s x s scratch per pair.
+static int trtri_level(int64_t s, int64_t cs, int64_t p0, int64_t np, const double *r, int64_t ldr, double *x,
+                       int64_t ldx, double *t, cudaStream_t st) {
+    const int64_t o = 2 * s * p0;
+    GemmArgs P{};
+    // T_p = A_p^{-1} B_p  (s x cs, K = s)
+    P.M = s;
+    P.N = cs;
+    P.K = s;
+    P.A = x + o * ldx + o;
+    P.lda = ldx;
+    P.B = r + (o + s) * ldr + o;
+    P.ldb = ldr;
+    P.Cin = t;
+    P.ldcin = s;
+    P.Cout = t;
+    P.ldc = s;
+    P.alpha = 1.0;
+    P.beta = 0.0;
+    P.batch = np;
+    P.bs_a = 2 * s * (ldx + 1);
+    P.bs_b = 2 * s * (ldr + 1);
+    P.bs_cin = P.bs_c = s * s;
+    CQ_TRY(gemm_ex(false, P, 1, st));
+    // X[o:o+s, o+s:o+s+cs] = -T_p C_p^{-1}  (s x cs, K = cs)
+    GemmArgs Q{};
+    Q.M = s;
+    Q.N = cs;
+    Q.K = cs;
+    Q.A = t;
+    Q.lda = s;
+    Q.B = x + (o + s) * ldx + o + s;
+    Q.ldb = ldx;
+    Q.Cout = x + (o + s) * ldx + o;
+    Q.Cin = Q.Cout;
+    Q.ldcin = ldx;
+    Q.ldc = ldx;
+    Q.alpha = -1.0;
+    Q.beta = 0.0;
+    Q.batch = np;
+    Q.bs_a = s * s;
+    Q.bs_b = 2 * s * (ldx + 1);
+    Q.bs_cin = Q.bs_c = 2 * s * (ldx + 1);
+    return gemm_ex(false, Q, 1, st);
+}
+
+int trtri_upper(int64_t k, const double *r, int64_t ldr, double *x, int64_t ldx, Workspace &ws, cudaStream_t st) {
+    if (k <= 0) return 0;
+    CQ_CUDA(cudaMemset2DAsync(x, sizeof(double) * ldx, 0, sizeof(double) * k, k, st), "trtri zero");
+    const int64_t nblk = (k + kTB - 1) / kTB;
+    trtri_diag_kernel<<<(unsigned)nblk, kTB, 0, st>>>(k, r, ldr, x, ldx, false);
+    note_launch();
+    CQ_TRY(check_launch("trtri_diag_kernel"));
+    double *t = nullptr;
+    if (k > kTB) {
+        t = ws.get<double>("trtri.t", (size_t)k * (size_t)k);  // >= full*s*s + s*cs at every level
+        if (!t) return fail_nomem("trtri scratch");
+    }
+    for (int64_t s = kTB; s < k; s *= 2) {
+        const int64_t full = k / (2 * s);  // pairs with a full C block
+        if (full > 0) CQ_TRY(trtri_level(s, s, 0, full, r, ldr, x, ldx, t, st));
+        const int64_t o = 2 * s * full;
+        const int64_t cs = k - o - s;  // ragged last pair
+        if (cs > 0) CQ_TRY(trtri_level(s, cs, full, 1, r, ldr, x, ldx, t, st));
+    }
+    return 0;
+}
+
+}  // namespace cqg

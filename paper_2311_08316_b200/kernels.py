@@ -26,12 +26,14 @@ def saso_plan(d: int, m: int, nnz: int, seed: int, c0: int = 0, stream=None):
     return plan[:m]
 
 
-def saso_sketch(a, d: int, nnz: int, seed: int, c0: int = 0, stream=None):
-    """apply(S, M) for SASO (sketch.cc:131-146) -> d x n column-major."""
+def saso_sketch(a, d: int, nnz: int, seed: int, c0: int = 0, stream=None, fast: bool = False):
+    """apply(S, M) for SASO (sketch.cc:131-146) -> d x n column-major.
+    ``fast``: allow the c-split decomposition (not bit-identical)."""
     m, n = a.shape
     out = colmajor_empty(d, n)
-    _lib.check(_lib.load().cqrrpt_gpu_saso_sketch(m, n, _p(a), _ld(a) if m else 1, d, nnz, seed, c0, out.data_ptr(),
-                                                  _ld(out), _stream_ptr(stream)), "saso_sketch")
+    _lib.check(_lib.load().cqrrpt_gpu_saso_sketch_ex(m, n, _p(a), _ld(a) if m else 1, d, nnz, seed, c0,
+                                                     out.data_ptr(), _ld(out), _lib.F_FAST_SKETCH if fast else 0,
+                                                     _stream_ptr(stream)), "saso_sketch")
     return out
 
 
@@ -104,6 +106,16 @@ def trmm_upper(a, b, stream=None):
     _lib.check(_lib.load().cqrrpt_gpu_trmm_upper(k, n, _p(a), _ld(a) if k else 1, _p(b), _ld(b) if k else 1, _p(c),
                                                  _ld(c) if k else 1, _stream_ptr(stream)), "trmm_upper")
     return c
+
+
+def trtri_upper(r, stream=None):
+    """X = triu(R)^{-1} (k x k), the inverse stage 2 applies in place of the
+    reference's triangular solves (linalg.cc:486-500)."""
+    k = r.shape[0]
+    x = colmajor_empty(k, k)
+    _lib.check(_lib.load().cqrrpt_gpu_trtri_upper(k, _p(r), _ld(r) if k else 1, _p(x), _ld(x) if k else 1,
+                                                  _stream_ptr(stream)), "trtri_upper")
+    return x
 
 
 def launch_count(reset: bool = False) -> int:

@@ -87,3 +87,18 @@ def test_c1_golden_summary_on_gpu(cuda, oracle, meta):
     assert fnv_pivots(res.pivots.cpu().numpy()) == c1["jhash"]
     assert (res.k0, res.k) == (c1["k0"], c1["k"])
     assert abs(res.r[0, 0].item() - c1["r00"]) <= 1e-12 * abs(c1["r00"])
+
+
+def test_c1_fast_sketch_matches_reference_away_from_ties(cuda, oracle, meta):
+    """CQRRPT_GPU_FAST_SKETCH (c-split sketch): C1 has no near-tie pivot
+    decisions, so J and k still equal the reference's."""
+    from oracle.oracle import fnv_pivots
+    c1 = meta["C1"]
+    a = oracle.gen_gaussian(c1["m"], c1["n"], 0)
+    A = dev(cuda, a)
+    res = cuda.dgeqpt(A, d_factor=c1["gamma"], nnz=c1["nnz"], seed=c1["seed"], fast_sketch=True)
+    assert fnv_pivots(res.pivots.cpu().numpy()) == c1["jhash"]
+    assert (res.k0, res.k) == (c1["k0"], c1["k"])
+    q = A[:, :res.k].cpu().numpy()
+    v = oracle.validate(a, q, res.r.cpu().numpy(), res.pivots.cpu().numpy())
+    assert v["orth_fro"] <= 1e-12 and v["recon_rel"] <= 1e-14

@@ -45,6 +45,35 @@ def test_saso_sketch_matches_apply(cuda, oracle, m, n, d, nnz, seed):
     assert np.array_equal(got, ref)
 
 
+def test_saso_sketch_row_blocks_and_lda(cuda, oracle):
+    """Several sketch-row blocks per column group, ragged last column group and
+    tile, and a leading dimension larger than m: still bit-identical."""
+    import torch
+    from paper_2311_08316_b200 import kernels
+    m, n, d, nnz, seed = 20011, 70, 1500, 8, 3
+    a = oracle.gen_gaussian(m, n, 9)
+    big = torch.zeros((n, m + 5), dtype=torch.float64, device="cuda")
+    big[:, :m] = torch.from_numpy(np.ascontiguousarray(a.T)).cuda()
+    view = big.t()[:m, :]  # column-major, lda = m + 5
+    got = host(kernels.saso_sketch(view, d, nnz, seed))
+    assert np.array_equal(got, oracle.saso_apply(d, a, nnz, seed))
+
+
+@pytest.mark.parametrize("m,n,d", [(70000, 64, 80), (40000, 256, 320)])
+def test_saso_sketch_split_mode(cuda, oracle, m, n, d):
+    """CQRRPT_GPU_FAST_SKETCH: c-split partials summed in a fixed order ->
+    deterministic and within rounding of the reference's apply."""
+    from paper_2311_08316_b200 import kernels
+    a = oracle.gen_gaussian(m, n, 21)
+    A = dev(cuda, a)
+    x = host(kernels.saso_sketch(A, d, 8, 5, fast=True))
+    y = host(kernels.saso_sketch(A, d, 8, 5, fast=True))
+    assert np.array_equal(x, y)
+    ref = oracle.saso_apply(d, a, 8, 5)
+    scale = np.sqrt(m * 8.0 / d)  # |Msk(r,j)| ~ sqrt(entries per row) * |a|
+    assert np.max(np.abs(x - ref)) <= 1e-14 * scale * np.max(np.abs(a)) * 10
+
+
 def test_saso_sketch_row_offset_shards_sum(cuda, oracle):
     """Row-sharded sketch partials (global row offsets) sum to the full sketch."""
     from paper_2311_08316_b200 import kernels
@@ -232,6 +261,23 @@ def test_potrf_failure_inside_block(cuda, oracle):
     ref, fref = oracle.cholesky(g)
     assert fi == fref == 81
     assert np.allclose(host(r), ref, rtol=1e-10, atol=1e-10 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("k", [1, 37, 64, 65, 128, 200, 256, 1000, 1030])
+def test_trtri_upper_inverse(cuda, oracle, k):
+    # log-depth inverse (diagonal blocks + batched GEMM levels, ragged last pair)
+    from paper_2311_08316_b200 import kernels
+    a = oracle.gen_gaussian(3 * k + 10, k, 6)
+    r, fi = oracle.cholesky(oracle.gram(a))
+    assert fi == 0
+    x = host(kernels.trtri_upper(dev(cuda, r)))
+    assert np.all(np.tril(x, -1) == 0)
+    cond = np.linalg.cond(r)
+    assert np.linalg.norm(x @ r - np.eye(k)) <= 1e2 * k * U * cond
+    # leading blocks of the inverse are the inverses of the leading blocks
+    ell = max(1, k // 3)
+    xl = host(kernels.trtri_upper(dev(cuda, np.ascontiguousarray(r[:ell, :ell]))))
+    assert np.allclose(xl, x[:ell, :ell], rtol=0, atol=1e2 * ell * U * np.abs(x).max() * cond)
 
 
 # ---------------------------------------------------------------- K7 cond

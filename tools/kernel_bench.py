@@ -33,7 +33,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--m", type=int, default=131072)
     ap.add_argument("--n", type=int, default=1024)
-    ap.add_argument("--only", default="trsm,gram,sketch,qrcp,potrf")
+    ap.add_argument("--only", default="trsm,gram,sketch,qrcp,potrf,trtri")
     ap.add_argument("--reps", type=int, default=5)
     a = ap.parse_args()
     m, n = a.m, a.n
@@ -42,7 +42,7 @@ def main():
     out = {"m": m, "n": n}
     A = pkg.colmajor_empty(m, n)
     A.normal_()
-    if "trsm" in only or "gram" in only or "potrf" in only:
+    if "trsm" in only or "gram" in only or "potrf" in only or "trtri" in only:
         R = torch.linalg.qr(torch.randn((d, n), dtype=torch.float64, device="cuda"))[1]
         U = R.t().contiguous().t()  # column-major upper triangular
         cols = torch.randperm(n, device="cuda")
@@ -68,6 +68,11 @@ def main():
             kernels.potrf(G.clone())
         ms = timeit(potrf, a.reps)
         out["potrf_ms"] = ms
+    if "trtri" in only:
+        def tri():
+            kernels.trtri_upper(U)
+        ms = timeit(tri, a.reps)
+        out["trtri_ms"] = ms
     if "sketch" in only:
         def sk():
             kernels.saso_sketch(A, d, 8, 0)

@@ -1,6 +1,6 @@
 """Per-phase device timings of cqrrpt_gpu_dgeqpt on BASELINE-shaped inputs.
 
-usage: python tools/phase_timing.py [C1|C2|C3|C4|C5-256 ...] [--reps R]
+usage: python tools/phase_timing.py [C1|C2|C3|C4|C5-256 ...] [--reps R] [--fast-sketch]
 Inputs are generated on the GPU with torch (harness only).
 """
 import argparse
@@ -52,7 +52,7 @@ def make(cfg, seed=0):
     return a.t()
 
 
-def run(name, reps=3):
+def run(name, reps=3, fast_sketch=False):
     cfg = CONFIGS[name]
     a0 = make(cfg)
     m, n = a0.shape
@@ -63,7 +63,7 @@ def run(name, reps=3):
         work.copy_(a0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = pkg.dgeqpt(work, d_factor=1.25, nnz=8, seed=0, timings=True)
+        res = pkg.dgeqpt(work, d_factor=1.25, nnz=8, seed=0, timings=True, fast_sketch=fast_sketch)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         if it == 0:
@@ -73,7 +73,7 @@ def run(name, reps=3):
             best = (wall, tm, res.k, res.k0, res.ctx.k_sk)
     wall, tm, k, k0, ksk = best
     names = ["sketch", "qrcp", "rank_select", "precondition", "cholesky_qr", "undo", "total", "comm"]
-    out = dict(config=name, m=m, n=n, k=k, k0=k0, k_sk=ksk, wall_ms=wall * 1e3,
+    out = dict(config=name, fast_sketch=fast_sketch, m=m, n=n, k=k, k0=k0, k_sk=ksk, wall_ms=wall * 1e3,
                phases_ms=dict(zip(names, [round(x, 4) for x in tm])),
                canonical_gflops=canon / (tm[6] * 1e-3) / 1e9)
     print(json.dumps(out), flush=True)
@@ -84,7 +84,8 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="*", default=["C1", "C2"])
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--fast-sketch", action="store_true", help="CQRRPT_GPU_FAST_SKETCH (c-split sketch)")
     args = ap.parse_args()
     for c in args.configs:
-        run(c, args.reps)
+        run(c, args.reps, args.fast_sketch)
         torch.cuda.empty_cache()
