@@ -25,8 +25,8 @@
 // Columns are staged into shared memory with L2-coherent cp.async while the
 // pivot is decided; the products of each dot are formed by all 32 lanes in
 // parallel and only the ordered additions (lanes 0..3, one per reference
-// accumulator) stay serial. Grid barrier: one atomic per CTA on a monotonic
-// counter.
+// accumulator) stay serial. Grid barrier: the flagged argmax records
+// (rec_publish / rec_wait), one L2 round trip per step.
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -172,6 +172,35 @@ CQ_DEVI double stream_dot(const double *sa, const double *g, int64_t c, double *
     return __shfl_sync(0xffffffffu, tot, 0);
 }
 
+// Per-CTA argmax records double as the grid barrier. A record is four 8-byte
+// words, each carrying the step flag in its high half, so a reader that sees
+// the flag in all four words holds the whole record (8-byte accesses are
+// single-copy atomic) -- the LL-protocol idea. The writer fences after the
+// CTA barrier (its columns become visible first); readers fence after
+// polling. One L2 round trip per step replaces barrier + partials read.
+CQ_DEVI void rec_publish(unsigned long long *slot, uint32_t flag, double v, int32_t idx, int32_t phys) {
+    const unsigned long long f = (unsigned long long)flag << 32;
+    const unsigned long long w0 = f | (uint32_t)__double2hiint(v), w1 = f | (uint32_t)__double2loint(v);
+    const unsigned long long w2 = f | (uint32_t)idx, w3 = f | (uint32_t)phys;
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");  // release: the CTA's writes (ordered by bar.sync) first
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(slot), "l"(w0), "l"(w1) : "memory");
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(slot + 2), "l"(w2), "l"(w3) : "memory");
+}
+
+CQ_DEVI void rec_wait(const unsigned long long *slot, uint32_t flag, double *v, int32_t *idx, int32_t *phys) {
+    unsigned long long w0, w1, w2, w3;
+    for (;;) {
+        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(slot) : "memory");
+        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w2), "=l"(w3) : "l"(slot + 2) : "memory");
+        if ((uint32_t)(w0 >> 32) == flag && (uint32_t)(w1 >> 32) == flag && (uint32_t)(w2 >> 32) == flag &&
+            (uint32_t)(w3 >> 32) == flag)
+            break;
+    }
+    *v = __hiloint2double((int)(uint32_t)w0, (int)(uint32_t)w1);
+    *idx = (int32_t)(uint32_t)w2;
+    *phys = (int32_t)(uint32_t)w3;
+}
+
 struct QrcpArgs {
     int64_t d, n, ld;
     double *b;
@@ -180,10 +209,7 @@ struct QrcpArgs {
     int32_t *cmap[2];
     int32_t *piv;     // physical pivot chosen at each step
     double *alpha;    // R(i,i)
-    double *pv[2];    // per-CTA argmax partials: value, logical index, physical column
-    int32_t *pi[2];
-    int32_t *pp[2];
-    unsigned long long *bar;
+    unsigned long long *rec;  // [2][256][4] flagged argmax records (value hi/lo, index, physical column)
     int64_t *k_out;
     int32_t *final_buf;  // which cmap buffer holds positions >= k
     double rank_tol;
@@ -200,6 +226,8 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
     __shared__ int32_t s_ai[kQrcpWarps], s_ap[kQrcpWarps];
     __shared__ double s_bc[4];
     __shared__ int s_poff;
+    __shared__ double s_ct[kQrcpWarps], s_tau[kQrcpWarps];  // fast column phase: R(i,j), tau per warp
+    __shared__ int s_coff[kQrcpWarps];                        // column offset in its warp buffer (-1: none)
     const int G = gridDim.x, cta = blockIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t d = A.d, n = A.n, ld = A.ld;
@@ -210,7 +238,6 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
     double *s_x = smem + kQrcpWarps * WB;        // pivot column rows i..d-1 (+ alignment slack)
     double *s_sv = s_x + A.xlen;                 // products, then the scaled reflector (d doubles)
     const double sqrt_u = sqrt(kUnitRoundoff);
-    unsigned long long nbar = 0;
 
     // block argmax carrying the physical column of the winner
     auto block_argmax = [&](ArgMax a, int32_t phys, int32_t *phys_out) -> ArgMax {
@@ -269,13 +296,8 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
     {
         int32_t bp;
         loc = block_argmax(loc, locp, &bp);
-        if (threadIdx.x == 0) {
-            A.pv[0][cta] = loc.v;
-            A.pi[0][cta] = loc.i;
-            A.pp[0][cta] = bp;
-        }
+        if (threadIdx.x == 0) rec_publish(A.rec + (size_t)cta * 4, 1u, loc.v, loc.i, bp);  // consumed at step 0
     }
-    grid_barrier_mono(A.bar, (++nbar) * (unsigned long long)G);
 
     double stop = 0.0;
     int64_t k = 0;
@@ -290,29 +312,33 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         // independent of the pivot decision)
         const int64_t jfirst = i + 1 + ((cta - (i + 1)) % G + G) % G;
         const int64_t j_w = jfirst + (int64_t)wid * G;
-        // The partials are on the critical path: issue their loads first, so
-        // their round trip overlaps the column-map round trip of the prefetch.
-        ArgMax g{-INFINITY, 0x7fffffff};
-        int32_t gp = 0;
-        if (threadIdx.x < G) {
-            g = ArgMax{ld_cg(A.pv[cur] + threadIdx.x), ld_cg(A.pi[cur] + threadIdx.x)};
-            gp = ld_cg(A.pp[cur] + threadIdx.x);
-        }
+        // own columns were written by this CTA at the previous step: their
+        // prefetch does not wait for the other CTAs
         int32_t pj0 = 0;
         double wj0 = 0.0, wrefj0 = 0.0, t0 = 0.0;
         if (j_w < n) {
             pj0 = ld_cg(A.cmap[cur] + j_w);
             wj0 = ld_cg(A.w[cur] + j_w);
             wrefj0 = ld_cg(A.wref + j_w);
-        }
-        const int32_t phys_i = ld_cg(A.cmap[cur] + i);
-        const double w_i = ld_cg(A.w[cur] + i), wref_i = ld_cg(A.wref + i);
-        if (j_w < n) {
             const double *col = A.b + (int64_t)pj0 * ld;
             stage_async(b0, col + i + 1, cmin<int64_t>(CHD, c), lane, 32);
             cp_async_commit();
             t0 = ld_cg(col + i);
         }
+        // every CTA's record of the previous step (the grid barrier)
+        ArgMax g{-INFINITY, 0x7fffffff};
+        int32_t gp = 0;
+        if (threadIdx.x < G) {
+            double v;
+            int32_t ix;
+            rec_wait(A.rec + ((size_t)cur * 256 + threadIdx.x) * 4, (uint32_t)(i + 1), &v, &ix, &gp);
+            g = ArgMax{v, ix};
+        }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire: the records' writers' data
+        __syncthreads();
+        // position i belongs to CTA i % G: read after the barrier
+        const int32_t phys_i = ld_cg(A.cmap[cur] + i);
+        const double w_i = ld_cg(A.w[cur] + i), wref_i = ld_cg(A.wref + i);
 
         // ---- pivot: lowest index attaining the max (qrcp.cc:26-31) -------
         int32_t phys_p;
@@ -327,6 +353,20 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         const double *x = A.b + (int64_t)phys_p * ld;
         trace_mark(A.trace, i, 1);
 
+        // Fast column phase (<= one owned column per warp, each resident in its
+        // warp buffer): the warp whose position is the pivot's now holds the
+        // column from position i (the swap) -- restage it together with the
+        // pivot column so both round trips overlap.
+        const int64_t ncol_cta = (jfirst < n) ? (n - jfirst + G - 1) / G : 0;
+        const bool fast = ncol_cta <= kQrcpWarps && c <= CHD;
+        double t_sw = 0.0;
+        if (fast && j_w == p) {
+            cp_async_wait<0>();  // the prefetch of the old column is not needed
+            __syncwarp();
+            const double *colp = A.b + (int64_t)phys_i * ld;
+            stage_async(b0, colp + i + 1, c, lane, 32);
+            t_sw = ld_cg(colp + i);
+        }
         // ---- make_reflector (linalg.cc:110-124), redundantly per CTA ------
         {
             const int off = stage_async(s_x, x + i, d - i, threadIdx.x, kQrcpThreads);
@@ -378,11 +418,141 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         const double *sv = s_sv;
         trace_mark(A.trace, i, 2);
 
-        // ---- apply_reflector + norm downdate, one owned column per warp --
+        // ---- apply_reflector + norm downdate --------------------------------
         ArgMax mine{-INFINITY, 0x7fffffff};
         int32_t minep = 0;
+        if (fast) {
+            // Every warp's column is resident (the reflector's wait + barrier
+            // completed the copies). Warp 0 runs the CTA's <= 8 dots at once:
+            // lanes 4g..4g+3 are the reference's four accumulators for the
+            // column of warp g, products formed on the fly; warp buffers are
+            // 4 doubles apart modulo 16, so one load feeds all 8 columns in two
+            // wavefronts. Then each warp updates its own column.
+            const bool has = j_w < n;
+            const bool isp = has && j_w == p;
+            const int32_t pj = isp ? phys_i : pj0;
+            const double wj = isp ? w_i : wj0, wrefj = isp ? wref_i : wrefj0;
+            double t = isp ? t_sw : t0;
+            double *col = A.b + (int64_t)pj * ld;
+            double *tail = col + i + 1;
+            const int off = (int)((reinterpret_cast<uintptr_t>(tail) >> 3) & 1);
+            if (lane == 0) {
+                s_ct[wid] = t;
+                s_coff[wid] = has ? off : -1;
+            }
+            __syncthreads();
+            trace_mark(A.trace, i, 5);
+            if (wid == 0 && beta != 0.0) {  // apply_reflector's dot (linalg.cc:126-136)
+                const int gq = lane >> 2, q = lane & 3;
+                const int go = s_coff[gq];
+                const double *cg = smem + gq * WB + (go > 0 ? go : 0);
+                double sacc = 0.0;
+                if (go >= 0) {
+                    // the next group's loads are issued before this group's
+                    // adds: only the dependent DADDs remain on the chain
+                    const int bd = (int)body;
+                    int e = q;
+                    if (e + 28 < bd) {
+                        double xa[8], xb[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            xa[u] = sv[e + 4 * u];
+                            xb[u] = cg[e + 4 * u];
+                        }
+                        for (e += 32; e + 28 < bd; e += 32) {
+                            double na[8], nb[8];
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                na[u] = sv[e + 4 * u];
+                                nb[u] = cg[e + 4 * u];
+                            }
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) sacc = sacc + xa[u] * xb[u];
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                xa[u] = na[u];
+                                xb[u] = nb[u];
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) sacc = sacc + xa[u] * xb[u];
+                    }
+                    for (; e < bd; e += 4) sacc = sacc + sv[e] * cg[e];
+                }
+                const double pair = sacc + __shfl_xor_sync(0xffffffffu, sacc, 1);
+                double tot = pair + __shfl_xor_sync(0xffffffffu, pair, 2);
+                if (q == 0 && go >= 0) {
+                    int64_t e = body, rem = c - body;
+                    if (rem >= 2) {
+                        tot = tot + sv[e] * cg[e];
+                        tot = tot + sv[e + 1] * cg[e + 1];
+                        e += 2;
+                        rem -= 2;
+                    }
+                    if (rem == 1) tot = fma(sv[e], cg[e], tot);
+                    double tau = s_ct[gq];
+                    tau += tot;
+                    tau *= beta;
+                    s_tau[gq] = tau;
+                }
+            }
+            __syncthreads();
+            trace_mark(A.trace, i, 6);
+            if (has) {
+                const double tau = (beta != 0.0) ? s_tau[wid] : 0.0;
+                if (beta != 0.0) t = t - tau;
+                double updated = fma(-t, t, wj);  // qrcp.cc:77-78
+                double newref = wrefj;
+                const bool recompute = updated <= sqrt_u * wrefj;  // qrcp.cc:82-86 (warp-uniform)
+                double *cb = b0 + off;
+                if (beta != 0.0) {
+                    const int ci = (int)c;
+                    for (int e0 = lane; e0 < ci; e0 += 256) {
+                        double xv[8], xc[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int e = e0 + 32 * u;
+                            xv[u] = e < ci ? sv[e] : 0.0;
+                            xc[u] = e < ci ? cb[e] : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int e = e0 + 32 * u;
+                            if (e < ci) {
+                                const double nv = fma(-tau, xv[u], xc[u]);
+                                if (recompute) cb[e] = nv;
+                                __stcg(tail + e, nv);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
+                if (recompute) {
+                    for (int64_t e = lane; e < body; e += 32) b1[e] = cb[e] * cb[e];
+                    __syncwarp();
+                    double s2 = 0.0;
+                    if (lane < 4) {
+                        s2 = chain_sum(0.0, b1, body, lane);
+                        s2 = chain_finish(s2, c, [&](int64_t e) { return cb[e]; }, [&](int64_t e) { return cb[e]; });
+                    }
+                    updated = __shfl_sync(0xffffffffu, s2, 0);
+                    newref = updated;
+                    __syncwarp();
+                }
+                if (lane == 0) {
+                    __stcg(col + i, t);
+                    __stcg(A.w[nxt] + j_w, updated);
+                    __stcg(A.wref + j_w, newref);
+                    __stcg(A.cmap[nxt] + j_w, pj);
+                }
+                const ArgMax cnd = argmax_combine(mine, ArgMax{updated, (int32_t)j_w});
+                if (cnd.i != mine.i) minep = pj;
+                mine = cnd;
+            }
+            trace_mark(A.trace, i, 7);
+        }
         bool first = true;
-        for (int64_t j = j_w; j < n; j += (int64_t)kQrcpWarps * G, first = false) {
+        for (int64_t j = fast ? n : j_w; j < n; j += (int64_t)kQrcpWarps * G, first = false) {
             const bool isp = (j == p);
             int32_t pj;
             double wj, wrefj, t;
@@ -501,18 +671,15 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
             int32_t bp;
             mine = block_argmax(mine, minep, &bp);
             if (threadIdx.x == 0) {
-                __stcg(A.pv[nxt] + cta, mine.v);
-                __stcg(A.pi[nxt] + cta, mine.i);
-                __stcg(A.pp[nxt] + cta, bp);
                 if (cta == 0) {
                     __stcg(A.piv + i, phys_p);
                     __stcg(A.alpha + i, alpha);
                 }
+                rec_publish(A.rec + ((size_t)nxt * 256 + cta) * 4, (uint32_t)(i + 2), mine.v, mine.i, bp);
             }
         }
         k = i + 1;
         trace_mark(A.trace, i, 4);
-        grid_barrier_mono(A.bar, (++nbar) * (unsigned long long)G);
     }
     if (cta == 0 && threadIdx.x == 0) {
         *A.k_out = k;
@@ -614,7 +781,9 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     const int64_t room = budget - xlen - d;
     if (room < 8 * 128) return fail_internal("qrcp: d too large for the shared-memory reflector");
     // per warp: two halves; one half holds a whole column when it fits
-    const int WB = (int)std::min<int64_t>(2 * (((d + 2 + 31) / 32) * 32), (room / 8) & ~(int64_t)63);
+    // +4: warp buffers 4 doubles apart modulo 16 (bank-staggered for the
+    // fast path's 8-column chain loads); stays 16-byte aligned
+    const int WB = (int)std::min<int64_t>(2 * (((d + 2 + 31) / 32) * 32), (room / 8) & ~(int64_t)63) + 4;
     const size_t smem = sizeof(double) * (size_t)(8 * (int64_t)WB + xlen + d);
     CQ_CUDA(cudaFuncSetAttribute(qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "qrcp smem");
     // one owned column per warp per step at the start (8 warps per CTA)
@@ -634,21 +803,16 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     a.cmap[1] = ws.get<int32_t>("qrcp.c1", n);
     a.piv = ws.get<int32_t>("qrcp.piv", n);
     a.alpha = ws.get<double>("qrcp.alpha", n);
-    a.pv[0] = ws.get<double>("qrcp.pv0", 256);
-    a.pv[1] = ws.get<double>("qrcp.pv1", 256);
-    a.pi[0] = ws.get<int32_t>("qrcp.pi0", 256);
-    a.pi[1] = ws.get<int32_t>("qrcp.pi1", 256);
-    a.pp[0] = ws.get<int32_t>("qrcp.pp0", 256);
-    a.pp[1] = ws.get<int32_t>("qrcp.pp1", 256);
-    a.bar = ws.get<unsigned long long>("qrcp.bar", 2);
+    a.rec = ws.get<unsigned long long>("qrcp.rec", 2 * 256 * 4);
     a.k_out = ws.get<int64_t>("qrcp.k", 2);
     a.final_buf = ws.get<int32_t>("qrcp.fb", 2);
     a.rank_tol = rank_tol;
     a.steps = std::min(d, n);
     a.wb = WB;
     a.xlen = xlen;
-    if (!a.w[0] || !a.bar || !a.k_out) return fail_nomem("qrcp workspace");
-    CQ_CUDA(cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned long long), st), "memset bar");
+    if (!a.w[0] || !a.rec || !a.k_out) return fail_nomem("qrcp workspace");
+    // flags restart at 1 every call: clear the previous call's records
+    CQ_CUDA(cudaMemsetAsync(a.rec, 0, 2 * 256 * 4 * sizeof(unsigned long long), st), "memset records");
     static const bool tracing = getenv("CQRRPT_QRCP_TRACE") != nullptr;
     a.trace = tracing ? ws.get<unsigned long long>("qrcp.trace", 512 * 8) : nullptr;
     if (a.trace) CQ_CUDA(cudaMemsetAsync(a.trace, 0, 512 * 8 * sizeof(unsigned long long), st), "trace memset");

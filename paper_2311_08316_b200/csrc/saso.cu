@@ -9,28 +9,29 @@
 //   plan   uint32[m_local * nnz]      row | sign<<31 (sign 1 = +1/sqrt(d))
 //   tptr   uint16[ntiles * (d+1)]     per 128-row tile: entry offsets by sketch row
 //   tent   uint32[ntiles * 128*nnz]   per tile, entries sorted by (row, c):
-//                                     negative<<31 | row<<16 | byte offset of
-//                                     A(c_local, 0) in the staged tile (c*264)
+//                                     negative<<31 | (row % A)<<16 | byte offset
+//                                     of A(c_local, 0) in the staged tile (c*264)
 //   part   double[S][d][n]            per c-split partial sketches, row-major
 //   Msk    double d x n column-major  fixed-order sum of the partials
 //
-// Apply kernel: one CTA = 32 columns (lane = column) x a block of RB sketch
-// rows x a contiguous range of row tiles. The CTA's RB x 32 accumulators live
-// in shared memory; each 128 x 32 tile of A is staged ([c][33] padded:
-// conflict-free warp reads of a 256-byte row) through a 3-stage cp.async
-// pipeline with the tile's CSR slice. Warp w walks the entries of its RB/16
-// sketch rows as one flat, row-sorted list: acc(r, j) = fma(v, A(c, j),
-// acc(r, j)) with c ascending, so every output entry is the reference's own
-// FMA chain (sketch.cc:137-143) -> bit-identical with one c-split.
+// Apply kernel: one CTA = 32 columns (lane = column) x 32*A sketch rows (A
+// register accumulators per lane; warp w owns rows w*A .. w*A+A-1) x a
+// contiguous range of row tiles. Each 128 x 32 tile of A is staged ([c][33]
+// padded: conflict-free warp reads of a 256-byte row) through a 5-stage
+// cp.async pipeline with the tile's CSR slice. A warp walks its rows' entries
+// (contiguous, row-sorted, c ascending per row) once and sends each to its
+// row's accumulator through a jump table on the row % A stored in the entry:
+// acc = fma(v, A(c, j), acc) per entry in c order is the reference's own FMA
+// chain per output entry (sketch.cc:137-143), so one c-split is bit-identical.
 #include "common.cuh"
 #include "internal.hh"
 
 namespace cqg {
 
 constexpr int kTileRows = 128;  // rows of A per CSR tile
-constexpr int kApplyWarps = 16;
+constexpr int kApplyWarps = 32;  // 1024 threads: short per-warp entry chains, 8 warps per scheduler
 constexpr int kApplyThreads = kApplyWarps * 32;
-constexpr int kApplyStages = 3;
+constexpr int kApplyStages = 5;
 constexpr int kXLD = 33;        // staged tile row stride (doubles)
 constexpr uint64_t kSasoSalt = 0x7361736fULL;  // sketch.cc:19
 
@@ -69,7 +70,7 @@ __global__ void saso_plan_kernel(int64_t d, int64_t c0, int64_t count, int nnz, 
 // Per-tile CSR by sketch row (stable: c ascending within a row).
 // One CTA per tile; histogram + scan by the block, ordered scatter by warp 0.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d, int nnz,
+__global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d, int nnz, int A,
                                                             const uint32_t *__restrict__ plan,
                                                             uint16_t *__restrict__ tptr,
                                                             uint32_t *__restrict__ tent) {
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d
             __syncwarp();
             if (valid) {
                 const uint32_t c_local = (uint32_t)(e / nnz);
-                oent[pos] = (~w & 0x80000000u) | (r << 16) | (c_local * kXLD * 8u);  // bit 31: -1/sqrt(d)
+                oent[pos] = (~w & 0x80000000u) | ((r % (uint32_t)A) << 16) | (c_local * kXLD * 8u);  // bit 31: -1/sqrt(d)
                 // highest-ranked member advances the cursor
                 if (rank == __popc(grp & act) - 1) s_cur[r] += __popc(grp & act);
             }
@@ -151,7 +152,7 @@ struct ApplyArgs {
     int64_t m, n, lda, d;
     const double *a;
     double val;
-    int nnz, rb;            // entries per column of S, sketch rows per CTA (multiple of 16)
+    int nnz;
     int ptrw, entw;         // 32-bit words per stage for pointers / entries
     int64_t ntiles, tiles_per_split;
     const uint16_t *tptr;
@@ -159,12 +160,12 @@ struct ApplyArgs {
     double *part;
 };
 
+template <int A>
 __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs P) {
+    constexpr int RB = kApplyWarps * A;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int RB = P.rb, A = RB / kApplyWarps;
-    double *acc = reinterpret_cast<double *>(smem_raw);  // [RB][32]
     const int stage_words = 2 * kTileRows * kXLD + P.ptrw + P.entw;  // 32-bit words per stage
-    uint32_t *stage0 = reinterpret_cast<uint32_t *>(acc + (size_t)RB * 32);
+    uint32_t *stage0 = reinterpret_cast<uint32_t *>(smem_raw);
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int64_t j0 = (int64_t)blockIdx.x * 32;
@@ -174,99 +175,111 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
     const int64_t t_end = cmin<int64_t>(t_begin + P.tiles_per_split, P.ntiles);
     const int rows_here = (int)cmin<int64_t>(RB, P.d - r0);  // valid sketch rows in this block
 
-    for (int q = tid; q < RB * 32; q += kApplyThreads) acc[q] = 0.0;
+    double acc[A];
+#pragma unroll
+    for (int q = 0; q < A; ++q) acc[q] = 0.0;
 
-    // staging map: thread -> tile row cc, columns jj0 + 4*it
+    // staging map: thread -> tile row cc, columns jj0 + kCS*it. Addresses and
+    // column bounds are fixed per thread; a tile only moves the row.
+    constexpr int kCS = kApplyThreads / kTileRows;         // column stride (8)
+    constexpr int kIters = kTileRows * 32 / kApplyThreads;  // copies per thread (4)
+    static_assert(kCS * kIters == 32, "staging covers the 32 columns");
     const int cc = tid % kTileRows, jj0 = tid / kTileRows;
-    constexpr int kIters = kTileRows * 32 / kApplyThreads;  // 8
+    const int64_t ldas = kCS * P.lda;
+    unsigned colok = 0;
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) colok |= (j0 + jj0 + kCS * it < P.n) ? (1u << it) : 0u;
+    const double *src0 = P.a + (j0 + jj0) * P.lda + cc;  // column j0+jj0, row cc of tile 0
+    const uint32_t dst0 = (uint32_t)(cc * kXLD + jj0);
+    const int ent_words = kTileRows * P.nnz;
     auto issue = [&](int64_t tile, int stg) {
         uint32_t *sw = stage0 + (size_t)stg * stage_words;
-        double *dt = reinterpret_cast<double *>(sw);
-        const int64_t row = tile * kTileRows + cc;
-        const bool rok = row < P.m;
-        const double *src = P.a + (j0 + jj0) * P.lda + row;
+        double *dt = reinterpret_cast<double *>(sw) + dst0;
+        const int64_t row0 = tile * kTileRows;
+        const unsigned ok = (row0 + cc < P.m) ? colok : 0u;
+        const double *src = src0 + row0;
 #pragma unroll
         for (int it = 0; it < kIters; ++it) {
-            const int jj = jj0 + 4 * it;
-            const bool ok = rok && (j0 + jj < P.n);
-            cp_async8_zfill(dt + cc * kXLD + jj, ok ? src + (int64_t)(4 * it) * P.lda : P.a, ok ? 8 : 0);
+            cp_async8_zfill(dt + kCS * it, ((ok >> it) & 1u) ? src : P.a, ((ok >> it) & 1u) ? 8 : 0);
+            src += ldas;
         }
         // tile pointers tptr[tile][r0 .. r0+rows_here] (4-byte words from the aligned start)
         uint32_t *sp = sw + 2 * kTileRows * kXLD;
         const uint16_t *gp = P.tptr + tile * (P.d + 1) + r0;
         const uint32_t *gpw = reinterpret_cast<const uint32_t *>(reinterpret_cast<uintptr_t>(gp) & ~(uintptr_t)3);
         const int nw = (int)(((reinterpret_cast<uintptr_t>(gp + rows_here + 1) + 3) - reinterpret_cast<uintptr_t>(gpw)) / 4);
-        for (int w = tid; w < nw; w += kApplyThreads) cp_async4(sp + w, gpw + w);
+        if (tid < nw) cp_async4(sp + tid, gpw + tid);  // nw <= (RB + 4) / 2 < kApplyThreads
         // all entries of the tile (16-byte copies; the array is padded to whole tiles)
         uint32_t *se = sp + P.ptrw;
-        const uint32_t *ge = P.tent + tile * (int64_t)(kTileRows * P.nnz);
-        for (int w = 4 * tid; w < kTileRows * P.nnz; w += 4 * kApplyThreads) cp_async16(se + w, ge + w);
+        const uint32_t *ge = P.tent + tile * (int64_t)ent_words;
+        for (int w = 4 * tid; w < ent_words; w += 4 * kApplyThreads) cp_async16(se + w, ge + w);
     };
-    for (int s = 0; s < kApplyStages - 1; ++s) {
+    // Two tiles per CTA barrier (a warp's share of entries varies tile to
+    // tile; pairing halves the barriers and averages the imbalance), three
+    // more in flight: stages hold tiles modulo kApplyStages.
+    constexpr int kPair = 2, kAhead = kApplyStages - kPair;
+    for (int s = 0; s < kAhead; ++s) {
         if (t_begin + s < t_end) issue(t_begin + s, s);
         cp_async_commit();
     }
-    // x with the entry's sign bit (bit 31 = negative) XORed into its sign
+    int stg_next = kAhead % kApplyStages, stg_cur = 0;  // stage of the next tile to issue / to process
+    // x with the entry's sign bit (bit 31 = negative) XORed into its sign:
+    // fma(v, x, s) == fma(|v|, +-x, s) exactly
     auto flip = [](double x, uint32_t w) {
         return __hiloint2double(__double2hiint(x) ^ (int)(w & 0x80000000u), __double2loint(x));
     };
-    // acc row r (absolute) of this lane at accb + r * 256 bytes
-    char *accb = reinterpret_cast<char *>(acc + lane) - r0 * 256;
-    const int wr0 = wid * A, wr1 = min((wid + 1) * A, rows_here);  // this warp's rows (local)
-    for (int64_t tile = t_begin; tile < t_end; ++tile) {
-        const int stg = (int)((tile - t_begin) % kApplyStages);
-        cp_async_wait<kApplyStages - 2>();
-        __syncthreads();  // tile visible to all; stage (tile-1) fully consumed
-        {
-            const int64_t nt = tile + kApplyStages - 1;
-            if (nt < t_end) issue(nt, (int)((nt - t_begin) % kApplyStages));
+    const int wr0 = wid * A;  // this warp's first row (local)
+    for (int64_t t0 = t_begin; t0 < t_end; t0 += kPair) {
+        cp_async_wait<kAhead - kPair>();
+        __syncthreads();  // tiles t0, t0+1 visible; the previous pair's stages are free
+#pragma unroll
+        for (int u = 0; u < kPair; ++u) {
+            const int64_t nt = t0 + kAhead + u;
+            if (nt < t_end) issue(nt, stg_next);
             cp_async_commit();
+            stg_next = (stg_next + 1 == kApplyStages) ? 0 : stg_next + 1;
         }
-        const uint32_t *sw = stage0 + (size_t)stg * stage_words;
-        const double *xt = reinterpret_cast<const double *>(sw) + lane;
-        const uint16_t *sp = reinterpret_cast<const uint16_t *>(sw + 2 * kTileRows * kXLD) +
-                             ((reinterpret_cast<uintptr_t>(P.tptr + tile * (P.d + 1) + r0) >> 1) & 1);
-        const uint32_t *se = sw + 2 * kTileRows * kXLD + P.ptrw;
-        if (wr0 >= wr1) continue;
-        const int eb = sp[wr0], ee = sp[wr1];
-        if (eb >= ee) continue;
-        // flat walk over this warp's entries (row-sorted, c ascending per row):
-        // the running sum of the current row stays in a register; a row
-        // change stores it and loads the next row's sum.
-        const char *xb = reinterpret_cast<const char *>(xt);
-        uint32_t curb = se[eb] & 0x7fff0000u;  // row << 16
-        double *cura = reinterpret_cast<double *>(accb + (curb >> 8));
-        double sacc = *cura;
-        auto step = [&](uint32_t w, double x) {
-            if ((w & 0x7fff0000u) != curb) {
-                *cura = sacc;
-                curb = w & 0x7fff0000u;
-                cura = reinterpret_cast<double *>(accb + (curb >> 8));
-                sacc = *cura;
+        const int stg_pair = stg_cur;
+        stg_cur = (stg_cur + kPair) % kApplyStages;
+        if (wr0 >= rows_here) continue;
+#pragma unroll
+        for (int u = 0; u < kPair; ++u) {
+            const int64_t tile = t0 + u;
+            if (tile >= t_end) break;
+            const int stg = (stg_pair + u >= kApplyStages) ? stg_pair + u - kApplyStages : stg_pair + u;
+            const uint32_t *sw = stage0 + (size_t)stg * stage_words;
+            const char *xb = reinterpret_cast<const char *>(reinterpret_cast<const double *>(sw) + lane);
+            const uint16_t *sp = reinterpret_cast<const uint16_t *>(sw + 2 * kTileRows * kXLD) +
+                                 ((reinterpret_cast<uintptr_t>(P.tptr + tile * (P.d + 1) + r0) >> 1) & 1);
+            const uint32_t *se = sw + 2 * kTileRows * kXLD + P.ptrw;
+            // the warp's entries: contiguous, row-sorted (row % A in bits 16..20),
+            // c ascending within a row. The next entry's word is always in a
+            // register, so an empty row costs a compare.
+            const int ee = sp[min(wr0 + A, rows_here)];
+            int e = sp[wr0];
+            constexpr uint32_t kEnd = 31u << 16;  // sentinel: matches no row
+            uint32_t w = e < ee ? se[e] : kEnd;
+#pragma unroll
+            for (int q = 0; q < A; ++q) {  // row wr0+q: its entries in c order (sketch.cc:137-143)
+                double sq = acc[q];
+                while (((w >> 16) & 31u) == (uint32_t)q) {
+                    const double x = flip(*reinterpret_cast<const double *>(xb + (w & 0xffffu)), w);
+                    ++e;
+                    w = e < ee ? se[e] : kEnd;
+                    sq = fma(P.val, x, sq);  // sketch.cc:142
+                }
+                acc[q] = sq;
             }
-            sacc = fma(P.val, flip(x, w), sacc);  // sketch.cc:142; fma(v, x) == fma(|v|, +-x) exactly
-        };
-        int e = eb;
-        for (; e + 2 <= ee; e += 2) {
-            const uint32_t w0 = se[e], w1 = se[e + 1];
-            const double x0 = *reinterpret_cast<const double *>(xb + (w0 & 0xffffu));
-            const double x1 = *reinterpret_cast<const double *>(xb + (w1 & 0xffffu));
-            step(w0, x0);
-            step(w1, x1);
         }
-        if (e < ee) {
-            const uint32_t w0 = se[e];
-            step(w0, *reinterpret_cast<const double *>(xb + (w0 & 0xffffu)));
-        }
-        *cura = sacc;
     }
     cp_async_wait<0>();
-    __syncthreads();
     // write the partial: part[split][r][j]
     const int64_t col = j0 + lane;
     if (col < P.n) {
         double *pp = P.part + split * P.d * P.n;
-        for (int rl = wid; rl < rows_here; rl += kApplyWarps) pp[(r0 + rl) * P.n + col] = acc[rl * 32 + lane];
+#pragma unroll
+        for (int q = 0; q < A; ++q)
+            if (wr0 + q < rows_here) pp[(r0 + wr0 + q) * P.n + col] = acc[q];
     }
 }
 
@@ -306,8 +319,17 @@ int saso_plan(int64_t d, int64_t c0, int64_t count, int64_t nnz, uint64_t seed, 
 static size_t apply_smem(int rb, int nnz, int *ptrw, int *entw) {
     *ptrw = ((rb + 2) / 2 + 1 + 3) & ~3;                // u16 pointers rb+1 from a 4-byte aligned start
     *entw = (kTileRows * nnz + 3) & ~3;                 // u32 entries, 16-byte multiple
-    const size_t stage = sizeof(uint32_t) * (size_t)(2 * kTileRows * kXLD + *ptrw + *entw);
-    return sizeof(double) * (size_t)rb * 32 + kApplyStages * stage;
+    return sizeof(uint32_t) * (size_t)(2 * kTileRows * kXLD + *ptrw + *entw) * kApplyStages;
+}
+
+template <int A>
+static int launch_apply(ApplyArgs P, dim3 grid, size_t smem, cudaStream_t st) {
+    auto kern = saso_apply_kernel<A>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return fail_cuda("saso_apply smem attr");
+    kern<<<grid, kApplyThreads, smem, st>>>(P);
+    note_launch();
+    return check_launch("saso_apply_kernel");
 }
 
 int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, int64_t nnz, uint64_t seed,
@@ -326,45 +348,40 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
     if (!plan || !tptr || !tent) return fail_nomem("saso workspace");
     int rc = saso_plan(d, c0, m, nnz, seed, plan, st);
     if (rc) return rc;
+    // Decomposition: RB = 32*A sketch rows per CTA (A register accumulators
+    // per lane). Exact order needs one pass over all rows per CTA, so
+    // parallelism comes from row blocks: minimise waves * (staging + RB).
+    const int64_t cgroups = (n + 31) / 32;
+    const int sms = num_sms();
+    int A = 10;
+    if (!allow_split) {
+        const int cand[] = {10, 8, 6, 4, 2};
+        double best = 1e300;
+        for (int a : cand) {
+            const int64_t rb = (int64_t)kApplyWarps * a;
+            const int64_t ctas = cgroups * ((d + rb - 1) / rb);
+            const double cost = (double)((ctas + sms - 1) / sms) * (128.0 + (double)std::min<int64_t>(rb, d));
+            if (cost < best) {
+                best = cost;
+                A = a;
+            }
+        }
+    }
+    const int64_t rblocks = (d + (int64_t)kApplyWarps * A - 1) / ((int64_t)kApplyWarps * A);
     size_t csr_smem = sizeof(int32_t) * (size_t)(2 * d + 2);
     if (csr_smem > 48 * 1024 &&
         cudaFuncSetAttribute(saso_tile_csr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csr_smem) !=
             cudaSuccess)
         return fail_cuda("csr smem attr");
-    saso_tile_csr_kernel<<<(unsigned)ntiles, 256, csr_smem, st>>>(m, d, (int)nnz, plan, tptr, tent);
+    saso_tile_csr_kernel<<<(unsigned)ntiles, 256, csr_smem, st>>>(m, d, (int)nnz, A, plan, tptr, tent);
     note_launch();
     if ((rc = check_launch("saso_tile_csr_kernel"))) return rc;
 
-    // Decomposition. Sketch rows per CTA (RB) are bounded by shared memory;
-    // exact order needs one pass over all rows per CTA, so parallelism comes
-    // from row blocks: minimise waves * (staging + RB) over the row-block count.
-    const int64_t cgroups = (n + 31) / 32;
-    const int sms = num_sms();
-    const size_t smem_max = 227 * 1024;
-    int ptrw = 0, entw = 0;
-    int rb_max = 16;
-    while (rb_max + 16 <= 4096 && apply_smem(rb_max + 16, (int)nnz, &ptrw, &entw) <= smem_max) rb_max += 16;
-    const int64_t min_blocks = (d + rb_max - 1) / rb_max;
-    int64_t rblocks = min_blocks;
-    {
-        double best = 1e300;
-        for (int64_t b = min_blocks; b <= std::max<int64_t>(min_blocks, std::min<int64_t>(d / 16, 4 * min_blocks + 8));
-             ++b) {
-            const int64_t rb = ((d + b - 1) / b + 15) / 16 * 16;
-            const int64_t ctas = cgroups * b;
-            const double cost = (double)((ctas + sms - 1) / sms) * (128.0 + (double)std::min<int64_t>(rb, d));
-            if (cost < best) {
-                best = cost;
-                rblocks = b;
-            }
-        }
-    }
     // allow_split (CQRRPT_GPU_FAST_SKETCH): fewest row blocks (least re-reading
     // of A) and a c-split to fill the GPU. Deterministic (partials summed in
     // split order) but not the reference's single FMA chain per entry.
     int64_t nsplit = 1;
     if (allow_split && ntiles >= 32) {
-        rblocks = min_blocks;
         const int64_t base = cgroups * rblocks;
         double best = (double)((base + sms - 1) / sms);  // waves per unit of work, nsplit = 1
         for (int64_t ns = 2; ns <= 64 && ns <= ntiles / 8; ++ns) {
@@ -375,8 +392,6 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
             }
         }
     }
-    const int rb = (int)(((d + rblocks - 1) / rblocks + 15) / 16 * 16);
-    rblocks = (d + rb - 1) / rb;
     int64_t tps = (ntiles + nsplit - 1) / nsplit;
     nsplit = (ntiles + tps - 1) / tps;
     double *part = ws.get<double>("saso.part", (size_t)(nsplit * d * n));
@@ -390,20 +405,22 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
     P.a = a;
     P.val = 1.0 / sqrt((double)d);  // sketch.cc:79
     P.nnz = (int)nnz;
-    P.rb = rb;
-    const size_t smem = apply_smem(rb, (int)nnz, &P.ptrw, &P.entw);
+    const size_t smem = apply_smem(kApplyWarps * A, (int)nnz, &P.ptrw, &P.entw);
+    if (smem > 227 * 1024) return fail_internal("saso_apply: nnz too large for the staged CSR");
     P.ntiles = ntiles;
     P.tiles_per_split = tps;
     P.tptr = tptr;
     P.tent = tent;
     P.part = part;
-    if (cudaFuncSetAttribute(saso_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-        return fail_cuda("saso_apply smem attr");
     dim3 grid((unsigned)cgroups, (unsigned)rblocks, (unsigned)nsplit);
-    saso_apply_kernel<<<grid, kApplyThreads, smem, st>>>(P);
-    note_launch();
-    if ((rc = check_launch("saso_apply_kernel"))) return rc;
+    switch (A) {
+        case 2: rc = launch_apply<2>(P, grid, smem, st); break;
+        case 4: rc = launch_apply<4>(P, grid, smem, st); break;
+        case 6: rc = launch_apply<6>(P, grid, smem, st); break;
+        case 8: rc = launch_apply<8>(P, grid, smem, st); break;
+        default: rc = launch_apply<10>(P, grid, smem, st); break;
+    }
+    if (rc) return rc;
     dim3 g((unsigned)((n + 31) / 32), (unsigned)((d + 31) / 32));
     saso_reduce_kernel<<<g, 256, 0, st>>>(d, n, nsplit, part, msk, ldm);
     note_launch();

@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--n", type=int, default=1024)
     ap.add_argument("--only", default="trsm,gram,sketch,qrcp,potrf,trtri")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--fast-sketch", action="store_true")
     a = ap.parse_args()
     m, n = a.m, a.n
     d = int(1.25 * n)
@@ -75,7 +76,7 @@ def main():
         out["trtri_ms"] = ms
     if "sketch" in only:
         def sk():
-            kernels.saso_sketch(A, d, 8, 0)
+            kernels.saso_sketch(A, d, 8, 0, fast=a.fast_sketch)
         ms = timeit(sk, a.reps)
         out["sketch_ms"] = ms
         out["sketch_gbs"] = (8.0 * m * n + 8.0 * d * n) / (ms * 1e-3) / 1e9
