@@ -178,6 +178,15 @@ int cqrrpt_gpu_potrf(int64_t n, double *G, int64_t ldg, int64_t *failure_index, 
 int cqrrpt_gpu_cond_estimate(int64_t ell, const double *R, int64_t ldr, int32_t method, double *value,
                              void *stream);
 
+/* CholeskyQR (twice = 0) / CholeskyQR2 (twice = 1) of the m x n (m >= n)
+ * device matrix A: Q overwrites A, R (n x n, ldr) is upper triangular.
+ * cholesky_qr / cholesky_qr2 (cqrrpt.cc:75-90). A non-positive-definite Gram
+ * returns 0 with *failure_index = the 1-based first failing minor (A and R
+ * then hold partial results); m < n returns -2 (the reference throws
+ * std::invalid_argument). The comparator of the reference's stability check. */
+int cqrrpt_gpu_cholesky_qr(int64_t m, int64_t n, double *A, int64_t lda, double *R, int64_t ldr, int32_t twice,
+                           int64_t *failure_index, void *stream);
+
 /* X (k x k, ldx) = triu(R)^{-1}: recursive blocked inverse (64 x 64 diagonal
  * blocks, then log2(k/64) levels of batched DMMA GEMMs). Stage 2 uses it in
  * place of the reference's per-iteration triangular solves

@@ -250,6 +250,24 @@ class Oracle:
         self.lib.orc_multiply_upper_triangular(_i64(k), _i64(n), _p(a), _i64(k), _p(b), _i64(k), _p(c))
         return c
 
+    def cholesky_qr(self, a, twice=False):
+        """cholesky_qr / cholesky_qr2 (cqrrpt.cc:75-90) composed from the
+        restated gram, cholesky, trsm_right and multiply_upper_triangular.
+        Returns (q, r, failure_index); q, r are None on failure."""
+        a = _f(a)
+        if a.shape[0] < a.shape[1]:
+            raise ValueError("cholesky_qr: requires rows >= cols")
+        r1, fi = self.cholesky(self.gram(a))
+        if fi:
+            return None, None, fi
+        q1 = self.trsm_right(a, r1)
+        if not twice:
+            return q1, r1, 0
+        r2, fi = self.cholesky(self.gram(q1))
+        if fi:
+            return None, None, fi
+        return self.trsm_right(q1, r2), self.multiply_upper_triangular(r2, r1), 0
+
     def flop_model(self, m, n, k, d, c_sk=0.0):
         v = self.lib.orc_flop_model(m, n, k, d, c_sk)
         if v < 0:
@@ -425,6 +443,20 @@ class Reference:
         g = np.empty((a.shape[1], a.shape[1]), order="F")
         self.lib.ref_gram(_i64(a.shape[0]), _i64(a.shape[1]), _p(a), _p(g))
         return g
+
+    def cholesky_qr(self, a, twice=False):
+        a = _f(a)
+        m, n = a.shape
+        q = np.zeros((m, n), order="F")
+        r = np.zeros((n, n), order="F")
+        fi = _i64()
+        rc = self.lib.ref_cholesky_qr(_i64(m), _i64(n), _p(a), _i32(1 if twice else 0), _p(q), _p(r),
+                                      _c.byref(fi))
+        if rc == -1:
+            raise ValueError("cholesky_qr: requires rows >= cols")
+        if rc:
+            raise RuntimeError(f"ref_cholesky_qr failed ({rc})")
+        return (q, r, 0) if fi.value == 0 else (None, None, fi.value)
 
     def spectral_norm_estimate(self, a):
         a = _f(a)

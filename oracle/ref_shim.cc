@@ -182,6 +182,19 @@ int ref_gram(int64_t m, int64_t k, const double *a, double *g) {
     return guarded([&] { to_ptr(cq::gram(from_ptr(m, k, a)), g); });
 }
 
+// cholesky_qr / cholesky_qr2 (cqrrpt.cc:75-90): q (m x n), r (n x n) on success
+int ref_cholesky_qr(int64_t m, int64_t n, const double *a, int32_t twice, double *q_out, double *r_out,
+                    int64_t *failure_index) {
+    return guarded([&] {
+        cq::CholeskyQrResult res = twice ? cq::cholesky_qr2(from_ptr(m, n, a)) : cq::cholesky_qr(from_ptr(m, n, a));
+        *failure_index = res.failure_index;
+        if (res.ok()) {
+            to_ptr(res.q, q_out);
+            to_ptr(res.r, r_out);
+        }
+    });
+}
+
 int ref_spectral_norm_estimate(int64_t m, int64_t n, const double *a, double *value, int32_t *conv) {
     return guarded([&] {
         cq::NormEstimate e = cq::spectral_norm_estimate(from_ptr(m, n, a));

@@ -53,6 +53,8 @@ SYMBOLS = {
     "cqrrpt_gpu_gram": (ctypes.c_int, [_i64, _i64, _vp, _i64, _vp, _i64, _vp]),
     "cqrrpt_gpu_potrf": (ctypes.c_int, [_i64, _vp, _i64, ctypes.POINTER(_i64), _vp]),
     "cqrrpt_gpu_cond_estimate": (ctypes.c_int, [_i64, _vp, _i64, _i32, ctypes.POINTER(_f64), _vp]),
+    "cqrrpt_gpu_cholesky_qr": (ctypes.c_int, [_i64, _i64, _vp, _i64, _vp, _i64, ctypes.c_int32,
+                                              ctypes.POINTER(_i64), _vp]),
     "cqrrpt_gpu_trtri_upper": (ctypes.c_int, [_i64, _vp, _i64, _vp, _i64, _vp]),
     "cqrrpt_gpu_trmm_upper": (ctypes.c_int, [_i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp]),
     "cqrrpt_gpu_validate": (ctypes.c_int, [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp,

@@ -466,6 +466,40 @@ int cqrrpt_gpu_cond_estimate(int64_t ell, const double *R, int64_t ldr, int32_t 
     return cond_estimate(ell, R, ldr, rinv, ell, method, value, ws, st);
 }
 
+// ---- CholeskyQR / CholeskyQR2 (cqrrpt.cc:75-90) ------------------------------
+namespace {
+// one pass in place: G = A^T A (into r), r = chol(G), A <- A r^{-1}
+int cholqr_pass(int64_t m, int64_t n, double *A, int64_t lda, double *r, int64_t ldr, int64_t *failure_index,
+                Workspace &ws, cudaStream_t st) {
+    CQ_TRY(gram(m, n, A, lda, r, ldr, ws, st));
+    CQ_TRY(potrf(n, r, ldr, failure_index, ws, st));
+    if (*failure_index > 0) return 0;
+    return trsm_right(m, n, A, lda, nullptr, r, ldr, A, lda, st);  // in place: block jb reads B[:, jb] first
+}
+}  // namespace
+
+int cqrrpt_gpu_cholesky_qr(int64_t m, int64_t n, double *A, int64_t lda, double *R, int64_t ldr, int32_t twice,
+                           int64_t *failure_index, void *stream) {
+    if (m < 0) return -1;
+    if (n < 0 || m < n) return -2;  // cholesky_qr: requires rows >= cols (cqrrpt.cc:76-77)
+    if (n > 0 && lda < m) return -4;
+    if (n > 0 && ldr < n) return -6;
+    if (!failure_index) return -8;
+    *failure_index = 0;
+    if (n == 0) return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    Workspace &ws = workspace();
+    if (!twice) return cholqr_pass(m, n, A, lda, R, ldr, failure_index, ws, st);
+    double *r1 = ws.get<double>("cholqr2.r1", (size_t)(n * n));
+    double *r2 = ws.get<double>("cholqr2.r2", (size_t)(n * n));
+    if (!r1 || !r2) return fail_nomem("cholesky_qr2");
+    CQ_TRY(cholqr_pass(m, n, A, lda, r1, n, failure_index, ws, st));
+    if (*failure_index > 0) return 0;
+    CQ_TRY(cholqr_pass(m, n, A, lda, r2, n, failure_index, ws, st));
+    if (*failure_index > 0) return 0;
+    return gemm(false, n, n, n, 1.0, r2, n, r1, n, 0.0, R, ldr, st);  // R = R2 R1 (cqrrpt.cc:88)
+}
+
 int cqrrpt_gpu_trtri_upper(int64_t k, const double *R, int64_t ldr, double *X, int64_t ldx, void *stream) {
     if (k < 0) return -1;
     if (k > 0 && (ldr < k || ldx < k)) return -3;

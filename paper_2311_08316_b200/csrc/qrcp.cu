@@ -215,6 +215,7 @@ struct QrcpArgs {
     double rank_tol;
     int64_t steps;
     int wb;                     // per-warp buffer (doubles, multiple of 32)
+    int general;                // 1: never take the fast column phase (tests)
     int xlen;                   // pivot buffer length (doubles, >= d + 2, even)
     unsigned long long *trace;  // optional per-step phase timestamps (CTA 0)
 };
@@ -358,7 +359,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         // column from position i (the swap) -- restage it together with the
         // pivot column so both round trips overlap.
         const int64_t ncol_cta = (jfirst < n) ? (n - jfirst + G - 1) / G : 0;
-        const bool fast = ncol_cta <= kQrcpWarps && c <= CHD;
+        const bool fast = ncol_cta <= kQrcpWarps && c <= CHD && !A.general;
         double t_sw = 0.0;
         if (fast && j_w == p) {
             cp_async_wait<0>();  // the prefetch of the old column is not needed
@@ -810,6 +811,8 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     a.steps = std::min(d, n);
     a.wb = WB;
     a.xlen = xlen;
+    // CQRRPT_QRCP_GENERAL=1 forces the general column phase (tests cover both)
+    a.general = getenv("CQRRPT_QRCP_GENERAL") != nullptr ? 1 : 0;
     if (!a.w[0] || !a.rec || !a.k_out) return fail_nomem("qrcp workspace");
     // flags restart at 1 every call: clear the previous call's records
     CQ_CUDA(cudaMemsetAsync(a.rec, 0, 2 * 256 * 4 * sizeof(unsigned long long), st), "memset records");

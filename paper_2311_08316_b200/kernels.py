@@ -108,6 +108,19 @@ def trmm_upper(a, b, stream=None):
     return c
 
 
+def cholesky_qr(a, twice: bool = False, stream=None):
+    """cholesky_qr / cholesky_qr2 (cqrrpt.cc:75-90) on a column-major CUDA
+    tensor: Q overwrites ``a``; returns (R, failure_index) with R None on
+    failure."""
+    m, n = a.shape
+    r = colmajor_empty(n, n)
+    fi = _lib._i64(0)
+    _lib.check(_lib.load().cqrrpt_gpu_cholesky_qr(m, n, _p(a), _ld(a) if n else 1, _p(r), _ld(r) if n else 1,
+                                                  1 if twice else 0, ctypes.byref(fi), _stream_ptr(stream)),
+               "cholesky_qr")
+    return (r, 0) if fi.value == 0 else (None, fi.value)
+
+
 def trtri_upper(r, stream=None):
     """X = triu(R)^{-1} (k x k), the inverse stage 2 applies in place of the
     reference's triangular solves (linalg.cc:486-500)."""

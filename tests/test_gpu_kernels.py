@@ -116,6 +116,15 @@ def _qrcp_compare(cuda, oracle, a):
     return R, J, k
 
 
+@pytest.mark.parametrize("rows,n,seed", [(80, 64, 3), (320, 256, 1), (1000, 700, 2)])
+def test_qrcp_general_column_phase_bit_exact(cuda, oracle, monkeypatch, rows, n, seed):
+    """The general column phase (used when a CTA owns more than 8 columns in a
+    step or a column does not fit one warp buffer) against the reference,
+    forced by env var."""
+    monkeypatch.setenv("CQRRPT_QRCP_GENERAL", "1")
+    _qrcp_compare(cuda, oracle, oracle.gen_gaussian(rows, n, seed))
+
+
 def test_qrcp_known_answer_diag(cuda, oracle):
     # test_qrcp.cc:29-35: diag(1,5,3) -> pivots {1,2,0}, |R_ii| = (5,3,1)
     R, J, k = _qrcp_compare(cuda, oracle, np.diag([1.0, 5.0, 3.0]))

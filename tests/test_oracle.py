@@ -210,3 +210,16 @@ def test_flop_model_known_answers(oracle):
         assert oracle.flop_model(m, n, k, d, 5.0) == float(q6 + t6 + c6) / 6.0 + 5.0
     with pytest.raises(ValueError):
         oracle.flop_model(100, 10, 11, 20)
+
+
+@pytest.mark.parametrize("twice", [False, True])
+def test_cholesky_qr_composition_bit_exact(oracle, reference, twice):
+    """The oracle's cholesky_qr(2) (restated gram/cholesky/trsm/trmm) is
+    bit-identical to the reference's cqrrpt.cc:75-90, failure index included."""
+    a = oracle.gen_gaussian(300, 24, 2)
+    q1, r1, f1 = oracle.cholesky_qr(a, twice)
+    q2, r2, f2 = reference.cholesky_qr(a, twice)
+    assert f1 == f2 == 0 and np.array_equal(q1, q2) and np.array_equal(r1, r2)
+    b = oracle.gen_gaussian(30, 7, 13)
+    b[:, 5:7] = b[:, :2]
+    assert oracle.cholesky_qr(b, twice)[2] == reference.cholesky_qr(b, twice)[2] == 6
