@@ -307,13 +307,15 @@ def main():
     trsm_flops = float(m) * k0 * k0  # trsm_right flop count m k0^2 (flop_model term)
     trsm_ms = ph[3]
     achieved = trsm_flops / (trsm_ms * 1e-3) / 1e12
-    traffic = load_traffic().get("trsm_block_kernel_bytes_per_call")
+    # DRAM bytes of one TRSM pass (16 launches) from ncu, profiles/traffic.json
+    traffic = load_traffic().get("trsm_pass_dram_bytes")
     peaks, peak_src = measured_peaks()
     roofline = {"bound": "tensor", "kernel": "trsm_block_kernel (K5a gather+TRSM, DMMA.8x8x4)",
                 "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
                 "traffic": traffic,
                 "peak_source": "measured live in this run: cuBLAS DGEMM 8192^3 via torch.matmul(float64), best of 5",
-                "algorithmic": "m*k0^2 flops per TRSM pass (m=131072, k0=1024)"}
+                "algorithmic": "m*k0^2 flops per TRSM pass (m=131072, k0=1024)",
+                "traffic_unit": "DRAM bytes per TRSM pass (ncu dram__bytes_read+write, profiles/traffic.json)"}
     # secondary rooflines
     sketch_bytes = 8.0 * m * n + 8.0 * res.ctx.d * n
     sk = {"bound": "hbm", "achieved": sketch_bytes / (ph[0] * 1e-3) / 1e9, "peak": peaks.get("hbm_gbs"),

@@ -65,6 +65,10 @@ extern "C" {
 #define CQRRPT_GPU_NO_STAGE1 0x4       /* CqrrptConfig::stage1_enabled = false */
 #define CQRRPT_GPU_DIAGNOSTICS 0x8     /* truncation_ratio (spectral norm of R_sk) */
 #define CQRRPT_GPU_TIMINGS 0x10        /* per-phase CUDA-event timings into ctx->timings_ms */
+/* sketch families (SketchFamily, sketch.hh; SRFT is host-only in this build) */
+#define CQRRPT_SKETCH_SASO 0
+#define CQRRPT_SKETCH_GAUSSIAN 1
+
 #define CQRRPT_GPU_FAST_SKETCH 0x20    /* allow a c-split sketch (partials summed in a fixed order):
                                           deterministic, not bit-identical to the reference's
                                           single FMA chain; fills the GPU when n is small */
@@ -85,6 +89,8 @@ typedef struct cqrrpt_gpu_ctx {
     void *allreduce_user;
     int32_t cond_method;         /* CQRRPT_COND_* (default identity_deviation = 2) */
     int32_t flags;               /* CQRRPT_GPU_* */
+    int32_t sketch_family;       /* CQRRPT_SKETCH_SASO (default) or CQRRPT_SKETCH_GAUSSIAN */
+    int32_t reserved0;
     /* out: diagnostics (cqrrpt.hh:104-122) */
     int64_t d;                   /* sketch rows ceil(d_factor * n) */
     int64_t k_sk;                /* QRCP steps on the sketch */
@@ -140,6 +146,13 @@ int cqrrpt_gpu_saso_plan(int64_t d, int64_t c0, int64_t count, int64_t nnz, uint
 int cqrrpt_gpu_saso_sketch(int64_t m, int64_t n, const double *A, int64_t lda, int64_t d,
                            int64_t nnz, uint64_t seed, int64_t c0, double *Msk, int64_t ldm,
                            void *stream);
+/* Gaussian family (sketch.cc:62-72, apply = matmul): Msk (d x n, ldm) =
+ * S[:, c0:c0+m] A with S(i, c) = normal(c*d + i)/sqrt(d) from the reference's
+ * counter stream (c = global row), generated on device chunk by chunk and
+ * multiplied by a split-K DMMA GEMM (fixed-order slice sum). */
+int cqrrpt_gpu_gaussian_sketch(int64_t m, int64_t n, const double *A, int64_t lda, int64_t d, uint64_t seed,
+                               int64_t c0, double *Msk, int64_t ldm, void *stream);
+
 /* As cqrrpt_gpu_saso_sketch; flags & CQRRPT_GPU_FAST_SKETCH allows the
  * c-split decomposition (deterministic, not bit-identical). */
 int cqrrpt_gpu_saso_sketch_ex(int64_t m, int64_t n, const double *A, int64_t lda, int64_t d, int64_t nnz,

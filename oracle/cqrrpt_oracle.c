@@ -57,6 +57,18 @@ uint64_t orc_mix_seed(uint64_t seed, uint64_t salt) { /* rng.hh:50-53 */
     return orc_rng_bits(seed, 0x5eedULL + salt);
 }
 
+/* sketch.cc:62-72: Gaussian S columns c0 .. c0+m-1 (global rows of M), d x m
+   column-major: S(i, c) = normal(c * d + i) / sqrt(d) from mix_seed(seed, 0x6761757373). */
+int orc_gaussian_sample(int64_t d, int64_t m, uint64_t seed, int64_t c0, double *s) {
+    if (d < 1 || m < 0) return -1;
+    const uint64_t stream = orc_mix_seed(seed, 0x6761757373ULL);
+    const double scale = 1.0 / sqrt((double)d);
+    for (int64_t c = 0; c < m; ++c)
+        for (int64_t i = 0; i < d; ++i) s[c * d + i] = orc_rng_normal(stream, (uint64_t)((c0 + c) * d + i)) * scale;
+    return 0;
+}
+
+
 /* ------------------------------------------------------------------------ */
 /* dense kernels: linalg.cc                                                 */
 /* ------------------------------------------------------------------------ */

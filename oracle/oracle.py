@@ -146,6 +146,19 @@ class Oracle:
             raise ValueError("sample_sketch: SASO needs d >= 1 and 1 <= nnz <= d")
         return rows.reshape(m, nnz), vals.reshape(m, nnz)
 
+    def gaussian_sample(self, d, m, seed, c0=0):
+        """sketch.cc:62-72: the Gaussian operator's columns c0..c0+m-1 (d x m)."""
+        s = np.empty((d, m), order="F")
+        assert self.lib.orc_gaussian_sample(_i64(d), _i64(m), _u64(seed), _i64(c0), _p(s)) == 0
+        return s
+
+    def gaussian_apply(self, d, a, seed, c0=0):
+        """apply for the Gaussian family (sketch.cc:124-127: matmul(S, M)); the
+        product is formed by numpy (the reference's matmul order is not
+        restated: the device GEMM is compared with a rounding tolerance)."""
+        a = _f(a)
+        return np.asfortranarray(self.gaussian_sample(d, a.shape[0], seed, c0) @ a)
+
     def saso_apply(self, d, a, nnz, seed, c0=0, out=None):
         a = _f(a)
         m, n = a.shape

@@ -21,6 +21,7 @@ ERR = {1: "CUDA error", 2: "NCCL error", 3: "singular preconditioner (zero diago
 COND_DIAG_RATIO, COND_KRYLOV_BOUNDS, COND_IDENTITY_DEVIATION = 0, 1, 2
 F_OUTPUTS_ON_HOST, F_EXACT_STAGE2, F_NO_STAGE1, F_DIAGNOSTICS, F_TIMINGS = 0x1, 0x2, 0x4, 0x8, 0x10
 F_FAST_SKETCH = 0x20
+SKETCH_SASO, SKETCH_GAUSSIAN = 0, 1
 
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_size_t, ctypes.c_void_p,
                                 ctypes.c_void_p)
@@ -31,6 +32,7 @@ class Ctx(ctypes.Structure):
     _fields_ = [
         ("stream", _vp), ("rank", _i32), ("nranks", _i32), ("global_row_offset", _i64), ("comm", _vp),
         ("allreduce", ALLREDUCE_FN), ("allreduce_user", _vp), ("cond_method", _i32), ("flags", _i32),
+        ("sketch_family", _i32), ("reserved0", _i32),
         ("d", _i64), ("k_sk", _i64), ("k0_final", _i64), ("retries", _i32), ("stage2_exact", _i32),
         ("cond_m_pre", _f64), ("cond_upper_bound", _f64), ("truncation_ratio", _f64), ("flop_estimate", _f64),
         ("timings_ms", _f64 * 8),
@@ -45,6 +47,7 @@ SYMBOLS = {
     "cqrrpt_gpu_sketch_rows": (_i64, [_f64, _i64]),
     "cqrrpt_gpu_saso_plan": (ctypes.c_int, [_i64, _i64, _i64, _i64, _u64, _vp, _vp]),
     "cqrrpt_gpu_saso_sketch": (ctypes.c_int, [_i64, _i64, _vp, _i64, _i64, _i64, _u64, _i64, _vp, _i64, _vp]),
+    "cqrrpt_gpu_gaussian_sketch": (ctypes.c_int, [_i64, _i64, _vp, _i64, _i64, _u64, _i64, _vp, _i64, _vp]),
     "cqrrpt_gpu_saso_sketch_ex": (ctypes.c_int, [_i64, _i64, _vp, _i64, _i64, _i64, ctypes.c_uint64, _i64, _vp, _i64,
                                                    ctypes.c_uint32, _vp]),
     "cqrrpt_gpu_qrcp": (ctypes.c_int, [_i64, _i64, _vp, _i64, _f64, _vp, _i64, _vp, ctypes.POINTER(_i64), _vp]),

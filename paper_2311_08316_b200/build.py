@@ -83,6 +83,14 @@ def build(verbose: bool = False, force: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             raise RuntimeError("link failed:\n" + r.stdout + r.stderr)
+    # the C++ adapter test binary embeds the C ABI's struct layouts: keep it
+    # in step with the headers (it also needs the oracle library)
+    exe = os.path.join(ROOT, "tests", "cxx", "_build", "adapter_test")
+    if os.path.exists(os.path.join(ROOT, "oracle", "_build", "liboracle.so")) and _stale(
+            exe, [LIB, os.path.join(ROOT, "include", "cqrrpt_b200.hh"),
+                  os.path.join(ROOT, "include", "cqrrpt_gpu.h"),
+                  os.path.join(ROOT, "tests", "cxx", "adapter_test.cc")]):
+        build_cxx_adapter_test()
     return LIB
 
 

@@ -230,7 +230,7 @@ def dgeqpt(a, d_factor: float = 1.25, nnz: int = 4, seed: int = 0, eps_tol: floa
            cond_method: int = CondMethod.identity_deviation, stage1: bool = True, exact_stage2: bool = False,
            diagnostics: bool = False, timings: bool = False, stream=None, comm: Optional[Comm] = None,
            global_row_offset: int = 0, r_out=None, j_out=None, allreduce=None, nranks: int = 1,
-           rank: int = 0, fast_sketch: bool = False) -> DeviceResult:
+           rank: int = 0, fast_sketch: bool = False, sketch_family: str = "saso") -> DeviceResult:
     """The north-star entry point on a column-major CUDA tensor ``a``
     (m_local x n). Q overwrites ``a[:, :k]`` in place; R (k x n) and the
     0-based pivots are returned as device tensors.
@@ -239,6 +239,9 @@ def dgeqpt(a, d_factor: float = 1.25, nnz: int = 4, seed: int = 0, eps_tol: floa
     Python callable ``(ptr, count, stream_ptr) -> None`` that sum-allreduces
     ``count`` doubles in place — together with ``nranks``/``rank`` and this
     rank's ``global_row_offset``.
+
+    ``sketch_family``: "saso" (default, ``nnz`` nonzeros per column) or
+    "gaussian" (dense N(0, 1/d) operator, ``nnz`` ignored) -- SketchFamily.
 
     ``fast_sketch``: allow a c-split sketch (CQRRPT_GPU_FAST_SKETCH) that
     fills the GPU when n is small; deterministic, but J then matches the
@@ -269,6 +272,10 @@ def dgeqpt(a, d_factor: float = 1.25, nnz: int = 4, seed: int = 0, eps_tol: floa
     if fast_sketch:
         flags |= _lib.F_FAST_SKETCH
     ctx.flags = flags
+    families = {"saso": _lib.SKETCH_SASO, "gaussian": _lib.SKETCH_GAUSSIAN}
+    if sketch_family not in families:
+        raise InvalidArgument(f"sketch_family must be one of {sorted(families)} (SRFT is host-only)")
+    ctx.sketch_family = families[sketch_family]
     cb = None
     if comm is not None:
         ctx.comm = comm.handle
@@ -345,8 +352,8 @@ def cqrrpt(m, cfg: Optional[CqrrptConfig] = None) -> CqrrptOutput:
     (numpy, column-major); CUDA input -> CUDA outputs."""
     cfg = cfg or CqrrptConfig()
     check_config(cfg)
-    if cfg.family != SketchFamily.saso:
-        raise NotImplementedError("only the SASO sketch family runs on the GPU path (SURVEY §8(f) row 3)")
+    if cfg.family == SketchFamily.srft:
+        raise NotImplementedError("the SRFT sketch family is not on the GPU path (SURVEY §8(f) row 3)")
     if cfg.measure_distortion:
         raise NotImplementedError("measure_distortion is a desk-scale SVD diagnostic, out of scope")
     torch = _torch()
@@ -363,7 +370,8 @@ def cqrrpt(m, cfg: Optional[CqrrptConfig] = None) -> CqrrptOutput:
     src = A.clone() if cfg.validate_output else None
     res = dgeqpt(A, d_factor=cfg.gamma, nnz=cfg.nnz_per_col, seed=cfg.seed, eps_tol=cfg.eps_tol,
                  cond_method=int(cfg.cond_method), stage1=cfg.stage1_enabled, exact_stage2=True,
-                 diagnostics=True, timings=True)
+                 diagnostics=True, timings=True,
+                 sketch_family="gaussian" if cfg.family == SketchFamily.gaussian else "saso")
     k = res.k
     q_dev = A[:, :k]
     r_dev = res.r

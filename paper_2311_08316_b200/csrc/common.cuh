@@ -162,7 +162,7 @@ CQ_DEVI ArgMax warp_argmax(ArgMax a) {
 // ---------------------------------------------------------------------------
 // Counter RNG, bit-identical to the reference (rng.hh:18-53).
 // ---------------------------------------------------------------------------
-CQ_DEVI uint64_t rng_bits(uint64_t seed, uint64_t counter) {
+__host__ __device__ __forceinline__ uint64_t rng_bits(uint64_t seed, uint64_t counter) {
     uint64_t z = seed + (counter + 1) * 0x9e3779b97f4a7c15ULL;
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
     z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
@@ -171,6 +171,15 @@ CQ_DEVI uint64_t rng_bits(uint64_t seed, uint64_t counter) {
 CQ_DEVI uint64_t rng_below(uint64_t seed, uint64_t counter, uint64_t bound) {
     return __umul64hi(rng_bits(seed, counter), bound);
 }
-CQ_DEVI uint64_t mix_seed(uint64_t seed, uint64_t salt) { return rng_bits(seed, 0x5eedULL + salt); }
+__host__ __device__ __forceinline__ uint64_t mix_seed(uint64_t seed, uint64_t salt) {
+    return rng_bits(seed, 0x5eedULL + salt);
+}
+// CounterRng::normal (rng.hh:32-36): Box-Muller cosine branch, one value per
+// counter; device log/cos are within 1 ulp of the host libm's
+CQ_DEVI double normal_dev(uint64_t seed, uint64_t counter) {
+    const double u1 = (double)((rng_bits(seed, 2 * counter) >> 11) + 1) * 0x1.0p-53;
+    const double u2 = (double)(rng_bits(seed, 2 * counter + 1) >> 11) * 0x1.0p-53;
+    return sqrt(-2.0 * log(u1)) * cos(6.283185307179586476925287 * u2);
+}
 
 }  // namespace cqg

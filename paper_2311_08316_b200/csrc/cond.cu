@@ -31,13 +31,7 @@ CQ_DEVI double op_entry(const PowOp &op, int64_t i, int64_t j) {
     return v;
 }
 
-// deterministic_unit_vector(n) (linalg.cc:434-442), device libm
-__device__ double normal_dev(uint64_t seed, uint64_t counter) {
-    double u1 = (double)((rng_bits(seed, 2 * counter) >> 11) + 1) * 0x1.0p-53;
-    double u2 = (double)(rng_bits(seed, 2 * counter + 1) >> 11) * 0x1.0p-53;
-    return sqrt(-2.0 * log(u1)) * cos(6.283185307179586476925287 * u2);
-}
-
+// deterministic_unit_vector(n) (linalg.cc:434-442) uses normal_dev (common.cuh)
 __device__ void start_vector(int64_t n, double *v, double *scratch) {
     double s = 0.0;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
@@ -312,13 +306,226 @@ int identity_deviation_first(const double *r, int64_t ldr, const int64_t *ells, 
     return 0;
 }
 
+// ---------------------------------------------------------------------------
+// Grid-wide estimator (the exact stage-2 path): the same power iterations and
+// control flow as cond_estimate_kernel, with each matvec spread over the grid
+// (cooperative launch). y = op x: CTA rows in 32-row chunks (lane = row,
+// warp = column residue mod 8, coalesced column segments); z = op^T y: warp
+// per column. Vectors live in global memory and are staged in shared memory
+// per half-iteration; norms are per-CTA partials summed in CTA order by every
+// CTA, so all CTAs take the same branches and the result is deterministic.
+// Three grid barriers per iteration.
+// ---------------------------------------------------------------------------
+constexpr int kGridPowThreads = 256;
+
+struct GridPow {
+    double *v, *w, *z;   // global vectors (length >= max(rows, cols))
+    double *part;        // per-CTA partial sums [gridDim.x]
+    unsigned long long *bar;
+    unsigned long long nbar;
+    double *s_vec;       // shared staging (>= max(rows, cols))
+    double *s_red;       // shared [8][32] + 32
+};
+
+CQ_DEVI void gp_sync(GridPow &g) { grid_barrier_mono(g.bar, (++g.nbar) * (unsigned long long)gridDim.x); }
+
+// sum over CTAs of the partials, in CTA order (identical in every CTA)
+CQ_DEVI double gp_total(GridPow &g, double mine) {
+    double *sr = g.s_red + 256;
+    const double blk = block_sum(mine, sr);
+    if (threadIdx.x == 0) g.part[blockIdx.x] = blk;
+    gp_sync(g);
+    double t = 0.0;
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < (int)gridDim.x; ++b) t += ld_cg(g.part + b);
+        sr[0] = t;
+    }
+    __syncthreads();
+    t = sr[0];
+    __syncthreads();
+    return t;
+}
+
+// y[rows of this CTA] = op x (x = src, global), returns this thread's share of sum y^2
+CQ_DEVI double gp_forward(const PowOp &op, const double *src, double *dst, GridPow &g) {
+    for (int64_t j = threadIdx.x; j < op.cols; j += blockDim.x) g.s_vec[j] = ld_cg(src + j);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t chunks = (op.rows + 31) / 32;
+    double sq = 0.0;
+    for (int64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
+        const int64_t i = ch * 32 + lane;
+        const int64_t jb = (op.kind == 0) ? 0 : ch * 32;  // upper: columns before the chunk are zero
+        double acc = 0.0;
+        if (i < op.rows)
+            for (int64_t j = jb + wid; j < op.cols; j += 8)
+                if (op.kind == 0 || j >= i) acc = fma(g.s_vec[j], op_entry(op, i, j), acc);
+        g.s_red[wid * 32 + lane] = acc;
+        __syncthreads();
+        if (wid == 0) {
+            double y = 0.0;
+            for (int q = 0; q < 8; ++q) y += g.s_red[q * 32 + lane];
+            if (i < op.rows) {
+                dst[i] = y;
+                sq = fma(y, y, sq);
+            }
+        }
+        __syncthreads();
+    }
+    return sq;
+}
+
+// z[cols of this CTA] = op^T y (y = src, global), returns this thread's share of sum z^2
+CQ_DEVI double gp_adjoint(const PowOp &op, const double *src, double *dst, GridPow &g) {
+    for (int64_t i = threadIdx.x; i < op.rows; i += blockDim.x) g.s_vec[i] = ld_cg(src + i);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double sq = 0.0;
+    for (int64_t j = blockIdx.x * (int64_t)nw + wid; j < op.cols; j += (int64_t)gridDim.x * nw) {
+        const int64_t ie = (op.kind == 0) ? op.rows : j + 1;
+        double s = 0.0;
+        for (int64_t i = lane; i < ie; i += 32) s = fma(op_entry(op, i, j), g.s_vec[i], s);
+        s = warp_sum(s);
+        if (lane == 0) {
+            dst[j] = s;
+            sq = fma(s, s, sq);
+        }
+    }
+    return sq;
+}
+
+// power_iterate (linalg.cc:446-465) over the grid; same control flow as power_iterate_dev
+CQ_DEVI double gp_power(const PowOp &op, GridPow &g, int *conv) {
+    const int64_t n = op.cols;
+    // deterministic_unit_vector (linalg.cc:434-442)
+    double sq = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double x = normal_dev(0x5eedcafe01234567ULL, (uint64_t)i);
+        g.v[i] = x;
+        sq = fma(x, x, sq);
+    }
+    const double nrm = sqrt(gp_total(g, sq));
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        g.v[i] = (nrm == 0.0) ? (i == 0 ? 1.0 : 0.0) : g.v[i] / nrm;
+    gp_sync(g);
+    double est = 0.0, prev = -1.0;
+    for (int it = 0; it < 200; ++it) {
+        const double nw = sqrt(gp_total(g, gp_forward(op, g.v, g.w, g)));
+        if (nw == 0.0) {
+            *conv = 1;
+            return 0.0;
+        }
+        est = (est < nw) ? nw : est;
+        if (prev >= 0.0 && fabs(est - prev) <= 1e-10 * est) {
+            *conv = 1;
+            return est;
+        }
+        prev = est;
+        const double nz = sqrt(gp_total(g, gp_adjoint(op, g.w, g.z, g)));
+        if (nz == 0.0) {
+            *conv = 1;
+            return est;
+        }
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+             i += (int64_t)gridDim.x * blockDim.x)
+            g.v[i] = ld_cg(g.z + i) / nz;
+        gp_sync(g);
+    }
+    *conv = 0;
+    return est;
+}
+
+struct CondGridArgs {
+    int64_t ell, ldr, ldi;
+    const double *r, *rinv;
+    int method;
+    double *v, *w, *z, *part;
+    unsigned long long *bar;
+    double *out;
+};
+
+// methods 1..3 of cond_estimate_kernel, grid-wide (method 0 stays single-CTA)
+__global__ void __launch_bounds__(kGridPowThreads) cond_grid_kernel(CondGridArgs A) {
+    extern __shared__ double gsm[];
+    GridPow g{A.v, A.w, A.z, A.part, A.bar, 0, gsm + 8 * 32 + 64, gsm};
+    const int64_t ell = A.ell;
+    int conv = 1;
+    double value = 1.0;
+    bool need_krylov = (A.method == 1);
+    if (A.method == 2 || A.method == 3) {
+        PowOp dev{A.r, A.ldr, ell, ell, 2};
+        const double tau = gp_power(dev, g, &conv) * (1.0 + 1e-6);
+        if (tau >= 1.0) {
+            if (A.method == 3) need_krylov = true;  // NestedCondEstimator fallback (cqrrpt.cc:57-58)
+            else value = INFINITY;                  // cond_estimate returns +inf (cqrrpt.cc:141-142)
+        } else {
+            const double vv = (1.0 + tau) / (1.0 - tau);
+            value = vv < 1.0 ? 1.0 : vv;
+        }
+    }
+    if (need_krylov) {
+        int c1 = 1, c2 = 1;
+        PowOp fwd{A.r, A.ldr, ell, ell, 1};
+        const double hi = gp_power(fwd, g, &c1);
+        bool zero_diag = false;
+        for (int64_t i = 0; i < ell; ++i)
+            if (A.r[i * A.ldr + i] == 0.0) zero_diag = true;
+        double inv;
+        if (zero_diag) {
+            inv = INFINITY;  // linalg.cc:489-490
+        } else {
+            PowOp ri{A.rinv, A.ldi, ell, ell, 1};
+            inv = gp_power(ri, g, &c2);
+        }
+        const double vv = hi * (1.0 + 1e-6) * inv * (1.0 + 1e-6);
+        value = vv < 1.0 ? 1.0 : vv;
+        conv = c1 && c2;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        A.out[0] = value;
+        A.out[1] = conv;
+    }
+}
+
 int cond_estimate(int64_t ell, const double *r, int64_t ldr, const double *rinv, int64_t ldi, int method,
                   double *value_host, Workspace &ws, cudaStream_t st) {
-    double *work = ws.get<double>("cond.work", (size_t)(3 * std::max<int64_t>(ell, 1)));
     double *dout = ws.get<double>("cond.out", 2);
-    cond_estimate_kernel<<<1, kPowThreads, 0, st>>>(ell, r, ldr, rinv, ldi, method, work, dout);
-    note_launch();
-    CQ_TRY(check_launch("cond_estimate_kernel"));
+    if (method == 0 || ell < 256) {  // small blocks: one CTA runs every iteration
+        double *work = ws.get<double>("cond.work", (size_t)(3 * std::max<int64_t>(ell, 1)));
+        cond_estimate_kernel<<<1, kPowThreads, 0, st>>>(ell, r, ldr, rinv, ldi, method, work, dout);
+        note_launch();
+        CQ_TRY(check_launch("cond_estimate_kernel"));
+    } else {
+        const int sms = num_sms();
+        const int G = (int)std::max<int64_t>(1, std::min<int64_t>(sms, (ell + 31) / 32));
+        CondGridArgs a;
+        a.ell = ell;
+        a.ldr = ldr;
+        a.ldi = ldi;
+        a.r = r;
+        a.rinv = rinv;
+        a.method = method;
+        a.v = ws.get<double>("condg.v", (size_t)ell);
+        a.w = ws.get<double>("condg.w", (size_t)ell);
+        a.z = ws.get<double>("condg.z", (size_t)ell);
+        a.part = ws.get<double>("condg.part", (size_t)G);
+        a.bar = ws.get<unsigned long long>("condg.bar", 1);
+        a.out = dout;
+        if (!a.v || !a.w || !a.z || !a.part || !a.bar) return fail_nomem("cond estimator");
+        const size_t smem = sizeof(double) * (size_t)(8 * 32 + 64 + ell);
+        static thread_local bool attr = false;
+        if (!attr) {
+            CQ_CUDA(cudaFuncSetAttribute(cond_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+                    "cond grid smem");
+            attr = true;
+        }
+        if (smem > 200 * 1024) return fail_internal("cond estimator: block too large for shared memory");
+        CQ_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned long long), st), "cond bar");
+        void *args[] = {&a};
+        CQ_CUDA(cudaLaunchCooperativeKernel((void *)cond_grid_kernel, dim3(G), dim3(kGridPowThreads), args, smem, st),
+                "cond grid launch");
+        note_launch();
+    }
     CQ_CUDA(cudaMemcpyAsync(value_host, dout, sizeof(double), cudaMemcpyDeviceToHost, st), "cond d2h");
     CQ_CUDA(cudaStreamSynchronize(st), "cond sync");
     return 0;

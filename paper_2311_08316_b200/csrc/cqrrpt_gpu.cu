@@ -174,7 +174,10 @@ int cqrrpt_gpu_dgeqpt(int64_t m, int64_t n, double *A, int64_t lda, double d_fac
     if (m > 0 && !A) return -3;
     if (m > 0 && lda < m) return set_error("lda < m"), -4;
     const int64_t d = cqrrpt_gpu_sketch_rows(d_factor, n);
-    if (nnz < 1 || nnz > d) return set_error("SASO needs 1 <= nnz <= d"), -6;  // sketch.cc:74-75
+    if (ctx->sketch_family != CQRRPT_SKETCH_SASO && ctx->sketch_family != CQRRPT_SKETCH_GAUSSIAN)
+        return set_error("unknown sketch family"), -14;  // the reference throws std::logic_error
+    const bool gaussian = ctx->sketch_family == CQRRPT_SKETCH_GAUSSIAN;
+    if (!gaussian && (nnz < 1 || nnz > d)) return set_error("SASO needs 1 <= nnz <= d"), -6;  // sketch.cc:74-75
     if (!R) return -9;
     if (ldr < n) return set_error("ldr < n"), -10;
     if (!J) return -11;
@@ -194,8 +197,11 @@ int cqrrpt_gpu_dgeqpt(int64_t m, int64_t n, double *A, int64_t lda, double d_fac
     // ---- sketch ------------------------------------------------------------
     double *msk = ws.get<double>("drv.msk", (size_t)(d * n));
     if (!msk) return fail_nomem("sketch");
-    CQ_TRY(saso_sketch(m, n, A, lda, d, nnz, seed, ctx->global_row_offset, msk, d, ws, st,
-                       (ctx->flags & CQRRPT_GPU_FAST_SKETCH) != 0));
+    if (gaussian)
+        CQ_TRY(gaussian_sketch(m, n, A, lda, d, seed, ctx->global_row_offset, msk, d, ws, st));
+    else
+        CQ_TRY(saso_sketch(m, n, A, lda, d, nnz, seed, ctx->global_row_offset, msk, d, ws, st,
+                           (ctx->flags & CQRRPT_GPU_FAST_SKETCH) != 0));
     clk.mark(PH_SKETCH);
     CQ_TRY(do_allreduce(ctx, msk, (size_t)(d * n), st));
     clk.mark(PH_COMM);
@@ -225,8 +231,9 @@ int cqrrpt_gpu_dgeqpt(int64_t m, int64_t n, double *A, int64_t lda, double d_fac
         return 0;
     };
     auto finish_diag = [&](int64_t k) {
+        // sketch_flops (sketch.cc): SASO 2 nnz m n, Gaussian 2 d m n
         ctx->flop_estimate = cqrrpt_gpu_flop_model(m, n, k, d,
-                                                   2.0 * (double)nnz * (double)m * (double)n);
+                                                   2.0 * (double)(gaussian ? d : nnz) * (double)m * (double)n);
         clk.finish(ctx->timings_ms);
     };
     if (k0 == 0) {  // cqrrpt.cc:257-260
@@ -399,6 +406,16 @@ int cqrrpt_gpu_saso_sketch(int64_t m, int64_t n, const double *A, int64_t lda, i
     if (nnz < 1 || nnz > d) return -6;
     if (ldm < d) return -10;
     return saso_sketch(m, n, A, lda, d, nnz, seed, c0, Msk, ldm, workspace(), (cudaStream_t)stream);
+}
+
+int cqrrpt_gpu_gaussian_sketch(int64_t m, int64_t n, const double *A, int64_t lda, int64_t d, uint64_t seed,
+                               int64_t c0, double *Msk, int64_t ldm, void *stream) {
+    if (m < 0) return -1;
+    if (n < 0) return -2;
+    if (m > 0 && lda < m) return -4;
+    if (d < 1) return -5;
+    if (ldm < d) return -9;
+    return gaussian_sketch(m, n, A, lda, d, seed, c0, Msk, ldm, workspace(), (cudaStream_t)stream);
 }
 
 int cqrrpt_gpu_saso_sketch_ex(int64_t m, int64_t n, const double *A, int64_t lda, int64_t d, int64_t nnz,

@@ -217,6 +217,66 @@ int gemm_ex(bool trans_a, GemmArgs P, int64_t splits, cudaStream_t st) {
     return launch_shape<64, 128>(trans_a, batch, P, grid, st);
 }
 
+// Split-K reduction: C = alpha * sum_s part[s] (+ beta C), slices in order.
+template <int BM, int BN>
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(int64_t M, int64_t N, int64_t ntm, int64_t ntiles,
+                                                            int64_t splits, const double *__restrict__ part,
+                                                            double alpha, double beta, double *__restrict__ c,
+                                                            int64_t ldc) {
+    const int64_t tix = blockIdx.x;
+    const int64_t tm = tix % ntm, tn = tix / ntm;
+    for (int e = threadIdx.x; e < BM * BN; e += blockDim.x) {
+        const int r = e % BM, cc = e / BM;
+        const int64_t i = tm * BM + r, j = tn * BN + cc;
+        if (i >= M || j >= N) continue;
+        double s = 0.0;
+        for (int64_t k = 0; k < splits; ++k) s += part[(k * ntiles + tix) * (int64_t)(BM * BN) + e];
+        double v = alpha * s;
+        if (beta != 0.0) v = fma(beta, c[j * ldc + i], v);
+        c[j * ldc + i] = v;
+    }
+}
+
+int gemm_splitk(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const double *a, int64_t lda,
+                const double *b, int64_t ldb, double beta, double *c, int64_t ldc, int64_t splits, Workspace &ws,
+                cudaStream_t st) {
+    if (M <= 0 || N <= 0) return 0;
+    const bool tall = N <= 64;  // gemm_ex's tile choice
+    const int BM = tall ? 128 : 64, BN = tall ? 64 : 128;
+    const int64_t ntm = (M + BM - 1) / BM, ntn = (N + BN - 1) / BN, ntiles = ntm * ntn;
+    splits = std::max<int64_t>(1, std::min<int64_t>(splits, (K + kBK - 1) / kBK));
+    const int64_t kps = ((K + splits - 1) / splits + kBK - 1) / kBK * kBK;
+    splits = (K + kps - 1) / kps;
+    double *part = ws.get<double>("gemm.splitk", (size_t)(splits * ntiles * BM * BN));
+    if (!part) return fail_nomem("gemm split-K partials");
+    GemmArgs P{};
+    P.M = M;
+    P.N = N;
+    P.K = K;
+    P.A = a;
+    P.lda = lda;
+    P.B = b;
+    P.ldb = ldb;
+    P.Cin = c;
+    P.ldcin = ldc;
+    P.Cout = c;
+    P.ldc = ldc;
+    P.alpha = 1.0;
+    P.beta = 0.0;
+    P.k_per_split = kps;
+    P.part = part;
+    P.ntiles_part = ntiles;
+    CQ_TRY(gemm_ex(trans_a, P, splits, st));
+    if (tall)
+        splitk_reduce_kernel<128, 64><<<(unsigned)ntiles, 256, 0, st>>>(M, N, ntm, ntiles, splits, part, alpha, beta,
+                                                                        c, ldc);
+    else
+        splitk_reduce_kernel<64, 128><<<(unsigned)ntiles, 256, 0, st>>>(M, N, ntm, ntiles, splits, part, alpha, beta,
+                                                                        c, ldc);
+    note_launch();
+    return check_launch("splitk_reduce_kernel");
+}
+
 int gemm(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const double *a, int64_t lda,
          const double *b, int64_t ldb, double beta, double *c, int64_t ldc, cudaStream_t st) {
     GemmArgs P{};

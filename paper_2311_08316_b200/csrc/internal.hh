@@ -69,6 +69,13 @@ int gram(int64_t m, int64_t k, const double *x, int64_t ldx, double *g, int64_t 
 int gemm(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const double *a, int64_t lda,
          const double *b, int64_t ldb, double beta, double *c, int64_t ldc, cudaStream_t st);
 int potrf(int64_t n, double *g, int64_t ldg, int64_t *failure_index, Workspace &ws, cudaStream_t st);
+// C = alpha op(A) B + beta C with K split into `splits` slices summed in order
+int gemm_splitk(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const double *a, int64_t lda,
+                const double *b, int64_t ldb, double beta, double *c, int64_t ldc, int64_t splits, Workspace &ws,
+                cudaStream_t st);
+// Gaussian sketch (sketch.cc:62-72, apply = matmul): msk = S A, S generated on device
+int gaussian_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, uint64_t seed, int64_t c0,
+                    double *msk, int64_t ldm, Workspace &ws, cudaStream_t st);
 int trmm_upper(int64_t k, int64_t n, const double *a, int64_t lda, const double *b, int64_t ldb, double *c,
                int64_t ldc, Workspace &ws, cudaStream_t st);
 

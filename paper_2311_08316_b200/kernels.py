@@ -37,6 +37,15 @@ def saso_sketch(a, d: int, nnz: int, seed: int, c0: int = 0, stream=None, fast: 
     return out
 
 
+def gaussian_sketch(a, d: int, seed: int, c0: int = 0, stream=None):
+    """apply(S, M) for the Gaussian family (sketch.cc:62-72, 124-127) -> d x n."""
+    m, n = a.shape
+    out = colmajor_empty(d, n)
+    _lib.check(_lib.load().cqrrpt_gpu_gaussian_sketch(m, n, _p(a), _ld(a) if m else 1, d, seed, c0, out.data_ptr(),
+                                                      _ld(out), _stream_ptr(stream)), "gaussian_sketch")
+    return out
+
+
 def qrcp(msk, rank_tol: float = -1.0, stream=None):
     """qrcp_maxnorm(M_sk, rank_tol, want_q=false) (qrcp.cc:35-97) -> (R k x n, pivots, k).
     ``msk`` is overwritten."""

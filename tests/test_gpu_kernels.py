@@ -305,6 +305,23 @@ def test_cond_estimates_match_oracle(cuda, oracle):
         assert kernels.cond_estimate(dev(cuda, R), meth) == pytest.approx(oracle.cond_estimate(R, meth)[0], rel=1e-6)
 
 
+@pytest.mark.parametrize("n,meth", [(300, 1), (300, 2), (300, 3), (700, 1), (700, 2)])
+def test_cond_estimates_grid_path(cuda, oracle, n, meth):
+    """ell >= 256 runs the grid-wide power iterations (cond_grid_kernel):
+    same iterations and stopping rule as the reference, different summation
+    order -> converged estimates agree to ~1e-9."""
+    from paper_2311_08316_b200 import kernels
+    R, _, _ = oracle.qrcp(oracle.gen_gaussian(n + 40, n, 8))
+    if meth == 3:  # the nested estimator's identity-deviation leg on a near-orthogonal R (tau < 1)
+        q = np.linalg.qr(oracle.gen_gaussian(n, n, 3))[0]
+        R = np.triu(np.eye(n) + 1e-3 * np.triu(q))
+        ref = oracle.cond_estimate(R, 2)[0]
+    else:
+        ref = oracle.cond_estimate(R, meth)[0]
+    got = kernels.cond_estimate(dev(cuda, R), meth)
+    assert got == pytest.approx(ref, rel=1e-6)
+
+
 # ---------------------------------------------------------------- K9 TRMM
 @pytest.mark.parametrize("k,n", [(10, 13), (256, 256), (100, 300), (65, 65)])
 def test_trmm_upper(cuda, oracle, k, n):

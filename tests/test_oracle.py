@@ -223,3 +223,14 @@ def test_cholesky_qr_composition_bit_exact(oracle, reference, twice):
     b = oracle.gen_gaussian(30, 7, 13)
     b[:, 5:7] = b[:, :2]
     assert oracle.cholesky_qr(b, twice)[2] == reference.cholesky_qr(b, twice)[2] == 6
+
+
+def test_gaussian_operator_bit_exact_and_apply(oracle, reference):
+    """The oracle's Gaussian operator equals the reference's bit for bit
+    (apply on the identity returns S exactly); the product agrees to rounding."""
+    d, m, seed = 17, 64, 9
+    s_ref = reference.gaussian_sketch_apply(d, np.eye(m), seed)
+    assert np.array_equal(oracle.gaussian_sample(d, m, seed), s_ref)
+    a = oracle.gen_gaussian(2000, 40, 3)
+    x, y = oracle.gaussian_apply(50, a, 7), reference.gaussian_sketch_apply(50, a, 7)
+    assert np.max(np.abs(x - y)) <= 1e-13 * np.max(np.abs(y))
