@@ -712,41 +712,71 @@ __global__ void qrcp_extract_kernel(int64_t d, int64_t n, const double *__restri
 }
 
 // rank_stage1 (cqrrpt.cc:92-112) in the reference's arithmetic order.
-// Row masses: thread per row, acc = acc + R(i,j)^2 over j ascending (not
-// contracted as built); row max |R(i,:)| for max_abs (order-free).
-__global__ void row_stats_kernel(int64_t k, int64_t n, const double *__restrict__ r, int64_t ldr,
-                                 double *__restrict__ mass, double *__restrict__ rmax) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const bool act = i < k;
-    double acc = 0.0, mx = 0.0;
-    int64_t j = 0;
-    for (; j + 8 <= n; j += 8) {  // all lanes walk j together: coalesced over rows
-        double v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = act ? __ldg(r + (j + u) * ldr + i) : 0.0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            mx = fmax(mx, fabs(v[u]));
-            if (j + u >= i) acc = acc + v[u] * v[u];
+// Row masses: acc = acc + R(i,j)^2 over j ascending (not contracted as built);
+// row max |R(i,:)| for max_abs (order-free). CTA = 32 rows: all 8 warps stage
+// 32 x 64 column tiles (cp.async, coalesced, double-buffered, [c][33]) and
+// warp 0 (lane = row) runs the rows' ordered chains from shared memory.
+constexpr int kRsCols = 64, kRsLd = 33;
+
+__global__ void __launch_bounds__(256) row_stats_kernel(int64_t k, int64_t n, const double *__restrict__ r,
+                                                        int64_t ldr, double *__restrict__ mass,
+                                                        double *__restrict__ rmax) {
+    __shared__ __align__(16) double tile[2][kRsCols * kRsLd];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t i0 = (int64_t)blockIdx.x * 32;
+    const int64_t ntile = (n + kRsCols - 1) / kRsCols;
+    auto issue = [&](int64_t t, int buf) {
+        const int64_t row = i0 + lane;
+        for (int c = wid; c < kRsCols; c += 8) {
+            const int64_t col = t * kRsCols + c;
+            const bool ok = row < k && col < n;
+            cp_async8_zfill(&tile[buf][c * kRsLd + lane], r + (ok ? col * ldr + row : 0), ok ? 8 : 0);
         }
+        cp_async_commit();
+    };
+    issue(0, 0);
+    const int64_t i = i0 + lane;
+    double acc = 0.0, mx = 0.0;
+    for (int64_t t = 0; t < ntile; ++t) {
+        if (t + 1 < ntile) {
+            issue(t + 1, (int)((t + 1) & 1));
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        if (wid == 0) {
+            const double *tb = tile[t & 1];
+            const int64_t jb = t * kRsCols;
+            const int cols = (int)cmin<int64_t>(kRsCols, n - jb);
+            for (int c = 0; c < cols; ++c) {
+                const double v = tb[c * kRsLd + lane];
+                mx = fmax(mx, fabs(v));
+                if (jb + c >= i) acc = acc + v * v;
+            }
+        }
+        __syncthreads();  // the buffer is refilled next iteration
     }
-    for (; j < n; ++j) {
-        double v = act ? __ldg(r + j * ldr + i) : 0.0;
-        mx = fmax(mx, fabs(v));
-        if (j >= i) acc = acc + v * v;
-    }
-    if (act) {
+    if (wid == 0 && i < k) {
         mass[i] = acc;
         rmax[i] = mx;
     }
 }
 
-// Tail accumulation from the bottom, sequential as in the reference.
-__global__ void stage1_kernel(int64_t k, const double *__restrict__ mass, const double *__restrict__ rmax, double u,
-                              int64_t *__restrict__ k0_out) {
+// Tail accumulation from the bottom, sequential as in the reference; the
+// masses are staged in shared memory first (the scan is one thread).
+constexpr int kStage1Smem = 6016;
+
+__global__ void __launch_bounds__(1024) stage1_kernel(int64_t k, const double *__restrict__ mass,
+                                                      const double *__restrict__ rmax, double u,
+                                                      int64_t *__restrict__ k0_out) {
     __shared__ double s_red[32];
+    __shared__ double s_mass[kStage1Smem];
     double mx = 0.0;
-    for (int64_t i = threadIdx.x; i < k; i += blockDim.x) mx = fmax(mx, rmax[i]);
+    for (int64_t i = threadIdx.x; i < k; i += blockDim.x) {
+        mx = fmax(mx, rmax[i]);
+        if (i < kStage1Smem) s_mass[i] = mass[i];
+    }
     mx = warp_max(mx);
     if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mx;
     __syncthreads();
@@ -761,7 +791,7 @@ __global__ void stage1_kernel(int64_t k, const double *__restrict__ mass, const 
     double tail = 0.0;
     int64_t k0 = k;
     for (int64_t ell = k - 1; ell >= 0; --ell) {
-        tail += mass[ell];
+        tail += (ell < kStage1Smem) ? s_mass[ell] : mass[ell];
         if (tail <= target) k0 = ell;
     }
     *k0_out = k0;
@@ -863,7 +893,7 @@ int rank_stage1(int64_t k, int64_t n, const double *r, int64_t ldr, int64_t *k0,
     double *mass = ws.get<double>("s1.mass", k);
     double *rmax = ws.get<double>("s1.rmax", k);
     int64_t *kd = ws.get<int64_t>("s1.k0", 1);
-    row_stats_kernel<<<(unsigned)((k + 31) / 32), 32, 0, st>>>(k, n, r, ldr, mass, rmax);
+    row_stats_kernel<<<(unsigned)((k + 31) / 32), 256, 0, st>>>(k, n, r, ldr, mass, rmax);
     note_launch();
     stage1_kernel<<<1, 1024, 0, st>>>(k, mass, rmax, kUnitRoundoff, kd);
     note_launch();

@@ -37,10 +37,17 @@ __global__ void __launch_bounds__(kTB) trtri_diag_kernel(int64_t k, const double
     const int c = threadIdx.x;
     if (c < s) {  // column c: R y = e_c by back substitution
         rs[c][c + 1] = inv[c];
-        for (int i = c - 1; i >= 0; --i) {
-            double acc = 0.0;
-            for (int t = i + 1; t <= c; ++t) acc = fma(rs[t][i], rs[t][c + 1], acc);
-            rs[i][c + 1] = -acc * inv[i];
+        for (int i = c - 1; i >= 0; --i) {  // four partial sums: no dependent chain of length c
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            int t = i + 1;
+            for (; t + 3 <= c; t += 4) {
+                a0 = fma(rs[t][i], rs[t][c + 1], a0);
+                a1 = fma(rs[t + 1][i], rs[t + 1][c + 1], a1);
+                a2 = fma(rs[t + 2][i], rs[t + 2][c + 1], a2);
+                a3 = fma(rs[t + 3][i], rs[t + 3][c + 1], a3);
+            }
+            for (; t <= c; ++t) a0 = fma(rs[t][i], rs[t][c + 1], a0);
+            rs[i][c + 1] = -((a0 + a1) + (a2 + a3)) * inv[i];
         }
     }
     __syncthreads();
