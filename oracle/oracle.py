@@ -457,6 +457,22 @@ class Reference:
         self.lib.ref_gram(_i64(a.shape[0]), _i64(a.shape[1]), _p(a), _p(g))
         return g
 
+    def mm_write(self, path, a, coordinate=False):
+        a = _f(a)
+        rc = self.lib.ref_mm_write(path.encode(), _i64(a.shape[0]), _i64(a.shape[1]), _p(a),
+                                   _i32(1 if coordinate else 0))
+        if rc:
+            raise RuntimeError(f"ref_mm_write failed ({rc})")
+
+    def mm_read(self, path):
+        m, n = _i64(), _i64()
+        rc = self.lib.ref_mm_read(path.encode(), _c.byref(m), _c.byref(n), None)
+        if rc:
+            raise RuntimeError(f"ref_mm_read failed ({rc})")
+        out = np.zeros((m.value, n.value), order="F")
+        self.lib.ref_mm_read(path.encode(), _c.byref(m), _c.byref(n), _p(out))
+        return out
+
     def cholesky_qr(self, a, twice=False):
         a = _f(a)
         m, n = a.shape

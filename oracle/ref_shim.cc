@@ -20,6 +20,7 @@
 #endif
 
 #include "cqrrpt/cqrrpt.hh"
+#include "cqrrpt/matrix_market.hh"
 #include "cqrrpt/linalg.hh"
 #include "cqrrpt/qrcp.hh"
 #include "cqrrpt/rng.hh"
@@ -180,6 +181,24 @@ int ref_trsm_right(int64_t m, int64_t k, const double *b, const double *r, doubl
 
 int ref_gram(int64_t m, int64_t k, const double *a, double *g) {
     return guarded([&] { to_ptr(cq::gram(from_ptr(m, k, a)), g); });
+}
+
+// Matrix Market (matrix_market.cc:12-93)
+int ref_mm_write(const char *path, int64_t m, int64_t n, const double *a, int32_t coordinate) {
+    return guarded([&] {
+        cq::write_matrix_market(std::string(path), from_ptr(m, n, a),
+                                coordinate ? cq::MatrixMarketFormat::coordinate : cq::MatrixMarketFormat::array);
+    });
+}
+
+// out == NULL: only the shape
+int ref_mm_read(const char *path, int64_t *m, int64_t *n, double *out) {
+    return guarded([&] {
+        cq::DenseMatrix a = cq::read_matrix_market(std::string(path));
+        *m = a.rows();
+        *n = a.cols();
+        if (out) to_ptr(a, out);
+    });
 }
 
 // cholesky_qr / cholesky_qr2 (cqrrpt.cc:75-90): q (m x n), r (n x n) on success

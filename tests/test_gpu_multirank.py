@@ -82,3 +82,27 @@ def test_threaded_ranks_match_single_gpu(cuda, oracle, nranks):
     vr = oracle.validate(a, ref.q, ref.r, ref.pivots)
     assert v["orth_fro"] <= 10 * max(vr["orth_fro"], 1e-14)
     assert v["recon_rel"] <= 10 * max(vr["recon_rel"], 1e-15)
+
+
+def test_nccl_communicator_single_rank(cuda):
+    """The NCCL path of the library (libnccl dlopen'ed, cqrrpt_gpu_comm_*):
+    unique id -> init -> in-place sum-allreduce on device data -> destroy,
+    with one rank (one GPU per box); values must come back unchanged."""
+    import ctypes
+    import torch
+    from paper_2311_08316_b200 import _lib
+    L = _lib.load()
+    buf = ctypes.create_string_buffer(128)
+    if L.cqrrpt_gpu_comm_unique_id(buf) != 0:
+        pytest.skip("NCCL not loadable here: " + L.cqrrpt_gpu_last_error().decode())
+    h = _lib._vp()
+    _lib.check(L.cqrrpt_gpu_comm_init(1, 0, buf.raw, ctypes.byref(h)), "comm_init")
+    comm = cuda.Comm(h.value, 1, 0)
+    try:
+        x = torch.arange(1000, dtype=torch.float64, device="cuda") * 0.5
+        y = x.clone()
+        comm.allreduce(y)
+        torch.cuda.synchronize()
+        assert torch.equal(x, y)
+    finally:
+        comm.close()
