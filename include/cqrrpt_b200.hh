@@ -141,7 +141,6 @@ struct DevBuf {
 inline CqrrptOutput cqrrpt(const DenseMatrix &m, const CqrrptConfig &cfg = {}) {
     if (cfg.gamma < 1.0) throw std::invalid_argument("cqrrpt: gamma must be >= 1");
     if (!(cfg.eps_tol > unit_roundoff)) throw std::invalid_argument("cqrrpt: eps_tol must exceed the unit roundoff");
-    if (cfg.family == SketchFamily::srft) throw std::logic_error("cqrrpt_b200: the SRFT family is host-only");
     CqrrptOutput out;
     const int64_t rows = m.rows(), n = m.cols();
     if (n == 0) {
@@ -158,7 +157,9 @@ inline CqrrptOutput cqrrpt(const DenseMatrix &m, const CqrrptConfig &cfg = {}) {
     cqrrpt_gpu_ctx ctx;
     cqrrpt_gpu_ctx_init(&ctx);
     ctx.cond_method = int32_t(cfg.cond_method);
-    ctx.sketch_family = cfg.family == SketchFamily::gaussian ? CQRRPT_SKETCH_GAUSSIAN : CQRRPT_SKETCH_SASO;
+    ctx.sketch_family = cfg.family == SketchFamily::gaussian ? CQRRPT_SKETCH_GAUSSIAN
+                        : cfg.family == SketchFamily::srft  ? CQRRPT_SKETCH_SRFT
+                                                            : CQRRPT_SKETCH_SASO;
     ctx.flags = CQRRPT_GPU_TIMINGS | CQRRPT_GPU_EXACT_STAGE2 | CQRRPT_GPU_DIAGNOSTICS |
                 (cfg.stage1_enabled ? 0 : CQRRPT_GPU_NO_STAGE1);
     int64_t k = 0, k0 = 0;

@@ -65,9 +65,10 @@ extern "C" {
 #define CQRRPT_GPU_NO_STAGE1 0x4       /* CqrrptConfig::stage1_enabled = false */
 #define CQRRPT_GPU_DIAGNOSTICS 0x8     /* truncation_ratio (spectral norm of R_sk) */
 #define CQRRPT_GPU_TIMINGS 0x10        /* per-phase CUDA-event timings into ctx->timings_ms */
-/* sketch families (SketchFamily, sketch.hh; SRFT is host-only in this build) */
+/* sketch families (SketchFamily, sketch.hh) */
 #define CQRRPT_SKETCH_SASO 0
 #define CQRRPT_SKETCH_GAUSSIAN 1
+#define CQRRPT_SKETCH_SRFT 2     /* single rank: the transform mixes every row */
 
 #define CQRRPT_GPU_FAST_SKETCH 0x20    /* allow a c-split sketch (partials summed in a fixed order):
                                           deterministic, not bit-identical to the reference's
@@ -89,7 +90,7 @@ typedef struct cqrrpt_gpu_ctx {
     void *allreduce_user;
     int32_t cond_method;         /* CQRRPT_COND_* (default identity_deviation = 2) */
     int32_t flags;               /* CQRRPT_GPU_* */
-    int32_t sketch_family;       /* CQRRPT_SKETCH_SASO (default) or CQRRPT_SKETCH_GAUSSIAN */
+    int32_t sketch_family;       /* CQRRPT_SKETCH_SASO (default), _GAUSSIAN or _SRFT */
     int32_t reserved0;
     /* out: diagnostics (cqrrpt.hh:104-122) */
     int64_t d;                   /* sketch rows ceil(d_factor * n) */
@@ -152,6 +153,13 @@ int cqrrpt_gpu_saso_sketch(int64_t m, int64_t n, const double *A, int64_t lda, i
  * multiplied by a split-K DMMA GEMM (fixed-order slice sum). */
 int cqrrpt_gpu_gaussian_sketch(int64_t m, int64_t n, const double *A, int64_t lda, int64_t d, uint64_t seed,
                                int64_t c0, double *Msk, int64_t ldm, void *stream);
+
+/* SRFT family (sketch.cc:100-119 sample, 147-166 apply): Msk (d x n, ldm) =
+ * sqrt(P/d)/sqrt(P) * (FWHT(signs .* A zero-padded to P = next_pow2(m)))[rows],
+ * bit-identical to the reference (the butterflies run stage by stage in its
+ * order). Needs 1 <= d <= m and the whole matrix on one device. */
+int cqrrpt_gpu_srft_sketch(int64_t m, int64_t n, const double *A, int64_t lda, int64_t d, uint64_t seed,
+                           double *Msk, int64_t ldm, void *stream);
 
 /* As cqrrpt_gpu_saso_sketch; flags & CQRRPT_GPU_FAST_SKETCH allows the
  * c-split decomposition (deterministic, not bit-identical). */

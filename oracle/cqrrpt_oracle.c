@@ -57,6 +57,68 @@ uint64_t orc_mix_seed(uint64_t seed, uint64_t salt) { /* rng.hh:50-53 */
     return orc_rng_bits(seed, 0x5eedULL + salt);
 }
 
+/* sketch.cc:100-119: SRFT sample. signs (m), rows (d) in [0, padded). */
+int64_t orc_next_pow2(int64_t m) { /* sketch.cc:23-27 */
+    int64_t p = 1;
+    while (p < m) p <<= 1;
+    return p;
+}
+
+int orc_srft_sample(int64_t d, int64_t m, uint64_t seed, double *signs, int64_t *rows) {
+    if (d < 1 || m < 1 || d > m) return -1;
+    const int64_t padded = orc_next_pow2(m);
+    const uint64_t sign_seed = orc_mix_seed(seed, 0x7369676eULL), sel_seed = orc_mix_seed(seed, 0x73656c65ULL);
+    for (int64_t i = 0; i < m; ++i) signs[i] = (orc_rng_bits(sign_seed, (uint64_t)i) & 1) ? 1.0 : -1.0;
+    int64_t *perm = (int64_t *)malloc(sizeof(int64_t) * (size_t)padded);
+    if (!perm) return -2;
+    for (int64_t i = 0; i < padded; ++i) perm[i] = i;
+    for (int64_t i = 0; i < d; ++i) {
+        const int64_t j = i + (int64_t)orc_rng_below(sel_seed, (uint64_t)i, (uint64_t)(padded - i));
+        const int64_t t = perm[i];
+        perm[i] = perm[j];
+        perm[j] = t;
+    }
+    for (int64_t i = 0; i < d; ++i) rows[i] = perm[i];
+    free(perm);
+    return 0;
+}
+
+/* sketch.cc:31-39: unnormalised in-place Walsh-Hadamard butterflies */
+static void orc_fwht(double *x, int64_t len) {
+    for (int64_t half = 1; half < len; half <<= 1)
+        for (int64_t base = 0; base < len; base += 2 * half)
+            for (int64_t j = base; j < base + half; ++j) {
+                const double a = x[j], b = x[j + half];
+                x[j] = a + b;
+                x[j + half] = a - b;
+            }
+}
+
+/* sketch.cc:147-166: out (d x n, ld_out) = SRFT(A) for A (m x n, lda) */
+int orc_srft_apply(int64_t d, int64_t m, int64_t n, uint64_t seed, const double *a, int64_t lda, double *out,
+                   int64_t ld_out) {
+    if (d < 1 || m < 1 || d > m) return -1;
+    const int64_t padded = orc_next_pow2(m);
+    double *signs = (double *)malloc(sizeof(double) * (size_t)m);
+    int64_t *rows = (int64_t *)malloc(sizeof(int64_t) * (size_t)d);
+    double *buf = (double *)malloc(sizeof(double) * (size_t)padded);
+    if (!signs || !rows || !buf) return -2;
+    int rc = orc_srft_sample(d, m, seed, signs, rows);
+    if (rc) return rc;
+    const double scale = sqrt((double)padded / (double)d);
+    const double factor = scale / sqrt((double)padded);
+    for (int64_t j = 0; j < n; ++j) {
+        for (int64_t i = 0; i < padded; ++i) buf[i] = 0.0;
+        for (int64_t i = 0; i < m; ++i) buf[i] = signs[i] * a[j * lda + i];
+        orc_fwht(buf, padded);
+        for (int64_t r = 0; r < d; ++r) out[j * ld_out + r] = factor * buf[rows[r]];
+    }
+    free(signs);
+    free(rows);
+    free(buf);
+    return 0;
+}
+
 /* sketch.cc:62-72: Gaussian S columns c0 .. c0+m-1 (global rows of M), d x m
    column-major: S(i, c) = normal(c * d + i) / sqrt(d) from mix_seed(seed, 0x6761757373). */
 int orc_gaussian_sample(int64_t d, int64_t m, uint64_t seed, int64_t c0, double *s) {

@@ -44,6 +44,10 @@ int orc_c5_scale_columns(int64_t m, int64_t n, int64_t ld, double span_decades, 
  * rows/vals: count*nnz entries, column-major per S column. */
 int orc_saso_sample(int64_t d, int64_t c0, int64_t count, int64_t nnz, uint64_t seed,
                     int64_t *rows, double *vals);
+/* sketch.cc:100-119 / 147-166: SRFT sample and apply (out d x n, ld_out). */
+int orc_srft_sample(int64_t d, int64_t m, uint64_t seed, double *signs, int64_t *rows);
+int orc_srft_apply(int64_t d, int64_t m, int64_t n, uint64_t seed, const double *a, int64_t lda, double *out,
+                   int64_t ld_out);
 /* sketch.cc:62-72: Gaussian operator columns c0..c0+m-1 -> s (d x m, ld d). */
 int orc_gaussian_sample(int64_t d, int64_t m, uint64_t seed, int64_t c0, double *s);
 /* sketch.cc:131-146: out (d x n, ld_out) += S[:, c0:c0+m] * A (m x n, lda). */

@@ -159,6 +159,16 @@ class Oracle:
         a = _f(a)
         return np.asfortranarray(self.gaussian_sample(d, a.shape[0], seed, c0) @ a)
 
+    def srft_apply(self, d, a, seed):
+        """SRFT family apply (sketch.cc:100-119, 147-166), bit-exact."""
+        a = _f(a)
+        m, n = a.shape
+        out = np.zeros((d, n), order="F")
+        rc = self.lib.orc_srft_apply(_i64(d), _i64(m), _i64(n), _u64(seed), _p(a), _i64(m), _p(out), _i64(d))
+        if rc:
+            raise ValueError("srft: needs 1 <= d <= m")
+        return out
+
     def saso_apply(self, d, a, nnz, seed, c0=0, out=None):
         a = _f(a)
         m, n = a.shape
@@ -471,6 +481,15 @@ class Reference:
             raise RuntimeError(f"ref_mm_read failed ({rc})")
         out = np.zeros((m.value, n.value), order="F")
         self.lib.ref_mm_read(path.encode(), _c.byref(m), _c.byref(n), _p(out))
+        return out
+
+    def srft_sketch_apply(self, d, a, seed):
+        a = _f(a)
+        m, n = a.shape
+        out = np.zeros((d, n), order="F")
+        rc = self.lib.ref_srft_sketch_apply(_i64(d), _i64(m), _i64(n), _u64(seed), _p(a), _p(out))
+        if rc:
+            raise ValueError(f"ref_srft_sketch_apply failed ({rc})")
         return out
 
     def cholesky_qr(self, a, twice=False):

@@ -136,6 +136,14 @@ int ref_saso_apply(int64_t d, int64_t m, int64_t n, int64_t nnz, uint64_t seed, 
     });
 }
 
+// SRFT family (sketch.cc:100-119 sample, 147-166 apply): out (d x n)
+int ref_srft_sketch_apply(int64_t d, int64_t m, int64_t n, uint64_t seed, const double *a, double *out) {
+    return guarded([&] {
+        cq::SketchOperator s = cq::sample_sketch(cq::SketchFamily::srft, d, m, 0, seed);
+        to_ptr(cq::apply(s, from_ptr(m, n, a)), out);
+    });
+}
+
 int ref_gaussian_sketch_apply(int64_t d, int64_t m, int64_t n, uint64_t seed, const double *a,
                               double *out) {
     return guarded([&] {

@@ -142,7 +142,8 @@ def run_factor(args) -> int:
     from .cqrrpt import CqrrptConfig, SketchFamily, cqrrpt
     m = read_matrix_market(args.inp)
     cfg = CqrrptConfig(gamma=args.gamma, nnz_per_col=args.nnz, seed=args.seed,
-                       family=SketchFamily.gaussian if args.family == "gaussian" else SketchFamily.saso)
+                       family={"gaussian": SketchFamily.gaussian, "srft": SketchFamily.srft}.get(args.family,
+                                                                                                SketchFamily.saso))
     out = cqrrpt(m, cfg)
     write_matrix_market(args.out_prefix + "_Q.mtx", out.factorization.q)
     write_matrix_market(args.out_prefix + "_R.mtx", out.factorization.r)
@@ -181,7 +182,7 @@ def main(argv=None) -> int:
         p.add_argument("--theta", type=float, default=0.285)
 
     def sketch_opts(p):
-        p.add_argument("--family", default="saso", choices=("saso", "gaussian"))
+        p.add_argument("--family", default="saso", choices=("saso", "gaussian", "srft"))
         p.add_argument("--gamma", type=float, default=1.25)
         p.add_argument("--nnz", type=int, default=4)
 

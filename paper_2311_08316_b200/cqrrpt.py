@@ -240,8 +240,9 @@ def dgeqpt(a, d_factor: float = 1.25, nnz: int = 4, seed: int = 0, eps_tol: floa
     ``count`` doubles in place — together with ``nranks``/``rank`` and this
     rank's ``global_row_offset``.
 
-    ``sketch_family``: "saso" (default, ``nnz`` nonzeros per column) or
-    "gaussian" (dense N(0, 1/d) operator, ``nnz`` ignored) -- SketchFamily.
+    ``sketch_family``: "saso" (default, ``nnz`` nonzeros per column),
+    "gaussian" (dense N(0, 1/d) operator) or "srft" (subsampled randomized
+    Walsh-Hadamard, single rank) -- SketchFamily; ``nnz`` is SASO-only.
 
     ``fast_sketch``: allow a c-split sketch (CQRRPT_GPU_FAST_SKETCH) that
     fills the GPU when n is small; deterministic, but J then matches the
@@ -272,9 +273,9 @@ def dgeqpt(a, d_factor: float = 1.25, nnz: int = 4, seed: int = 0, eps_tol: floa
     if fast_sketch:
         flags |= _lib.F_FAST_SKETCH
     ctx.flags = flags
-    families = {"saso": _lib.SKETCH_SASO, "gaussian": _lib.SKETCH_GAUSSIAN}
+    families = {"saso": _lib.SKETCH_SASO, "gaussian": _lib.SKETCH_GAUSSIAN, "srft": _lib.SKETCH_SRFT}
     if sketch_family not in families:
-        raise InvalidArgument(f"sketch_family must be one of {sorted(families)} (SRFT is host-only)")
+        raise InvalidArgument(f"sketch_family must be one of {sorted(families)}")
     ctx.sketch_family = families[sketch_family]
     cb = None
     if comm is not None:
@@ -352,8 +353,6 @@ def cqrrpt(m, cfg: Optional[CqrrptConfig] = None) -> CqrrptOutput:
     (numpy, column-major); CUDA input -> CUDA outputs."""
     cfg = cfg or CqrrptConfig()
     check_config(cfg)
-    if cfg.family == SketchFamily.srft:
-        raise NotImplementedError("the SRFT sketch family is not on the GPU path (SURVEY §8(f) row 3)")
     if cfg.measure_distortion:
         raise NotImplementedError("measure_distortion is a desk-scale SVD diagnostic, out of scope")
     torch = _torch()
@@ -371,7 +370,7 @@ def cqrrpt(m, cfg: Optional[CqrrptConfig] = None) -> CqrrptOutput:
     res = dgeqpt(A, d_factor=cfg.gamma, nnz=cfg.nnz_per_col, seed=cfg.seed, eps_tol=cfg.eps_tol,
                  cond_method=int(cfg.cond_method), stage1=cfg.stage1_enabled, exact_stage2=True,
                  diagnostics=True, timings=True,
-                 sketch_family="gaussian" if cfg.family == SketchFamily.gaussian else "saso")
+                 sketch_family={SketchFamily.gaussian: "gaussian", SketchFamily.srft: "srft"}.get(cfg.family, "saso"))
     k = res.k
     q_dev = A[:, :k]
     r_dev = res.r

@@ -174,10 +174,15 @@ int cqrrpt_gpu_dgeqpt(int64_t m, int64_t n, double *A, int64_t lda, double d_fac
     if (m > 0 && !A) return -3;
     if (m > 0 && lda < m) return set_error("lda < m"), -4;
     const int64_t d = cqrrpt_gpu_sketch_rows(d_factor, n);
-    if (ctx->sketch_family != CQRRPT_SKETCH_SASO && ctx->sketch_family != CQRRPT_SKETCH_GAUSSIAN)
+    if (ctx->sketch_family != CQRRPT_SKETCH_SASO && ctx->sketch_family != CQRRPT_SKETCH_GAUSSIAN &&
+        ctx->sketch_family != CQRRPT_SKETCH_SRFT)
         return set_error("unknown sketch family"), -14;  // the reference throws std::logic_error
     const bool gaussian = ctx->sketch_family == CQRRPT_SKETCH_GAUSSIAN;
-    if (!gaussian && (nnz < 1 || nnz > d)) return set_error("SASO needs 1 <= nnz <= d"), -6;  // sketch.cc:74-75
+    const bool srft = ctx->sketch_family == CQRRPT_SKETCH_SRFT;
+    const bool saso = !gaussian && !srft;
+    if (saso && (nnz < 1 || nnz > d)) return set_error("SASO needs 1 <= nnz <= d"), -6;  // sketch.cc:74-75
+    if (srft && d > m) return set_error("sample_sketch: SRFT needs d <= m"), -6;         // sketch.cc:101
+    if (srft && multi) return set_error("the SRFT family needs the whole matrix on one rank"), -14;
     if (!R) return -9;
     if (ldr < n) return set_error("ldr < n"), -10;
     if (!J) return -11;
@@ -199,6 +204,8 @@ int cqrrpt_gpu_dgeqpt(int64_t m, int64_t n, double *A, int64_t lda, double d_fac
     if (!msk) return fail_nomem("sketch");
     if (gaussian)
         CQ_TRY(gaussian_sketch(m, n, A, lda, d, seed, ctx->global_row_offset, msk, d, ws, st));
+    else if (srft)
+        CQ_TRY(srft_sketch(m, n, A, lda, d, seed, msk, d, ws, st));
     else
         CQ_TRY(saso_sketch(m, n, A, lda, d, nnz, seed, ctx->global_row_offset, msk, d, ws, st,
                            (ctx->flags & CQRRPT_GPU_FAST_SKETCH) != 0));
@@ -231,9 +238,15 @@ int cqrrpt_gpu_dgeqpt(int64_t m, int64_t n, double *A, int64_t lda, double d_fac
         return 0;
     };
     auto finish_diag = [&](int64_t k) {
-        // sketch_flops (sketch.cc): SASO 2 nnz m n, Gaussian 2 d m n
-        ctx->flop_estimate = cqrrpt_gpu_flop_model(m, n, k, d,
-                                                   2.0 * (double)(gaussian ? d : nnz) * (double)m * (double)n);
+        // sketch_flops (sketch.cc:211-224): SASO 2 nnz m n, Gaussian 2 d m n,
+        // SRFT n (m + P log2 P + d)
+        double csk = 2.0 * (double)(gaussian ? d : nnz) * (double)m * (double)n;
+        if (srft) {
+            double P = 1.0;
+            while (P < (double)m) P *= 2.0;
+            csk = (double)n * ((double)m + P * std::log2(P) + (double)d);
+        }
+        ctx->flop_estimate = cqrrpt_gpu_flop_model(m, n, k, d, csk);
         clk.finish(ctx->timings_ms);
     };
     if (k0 == 0) {  // cqrrpt.cc:257-260
@@ -416,6 +429,16 @@ int cqrrpt_gpu_gaussian_sketch(int64_t m, int64_t n, const double *A, int64_t ld
     if (d < 1) return -5;
     if (ldm < d) return -9;
     return gaussian_sketch(m, n, A, lda, d, seed, c0, Msk, ldm, workspace(), (cudaStream_t)stream);
+}
+
+int cqrrpt_gpu_srft_sketch(int64_t m, int64_t n, const double *A, int64_t lda, int64_t d, uint64_t seed,
+                           double *Msk, int64_t ldm, void *stream) {
+    if (m < 1) return -1;
+    if (n < 0) return -2;
+    if (lda < m) return -4;
+    if (d < 1 || d > m) return -5;  // sample_sketch: SRFT needs d <= m (sketch.cc:101)
+    if (ldm < d) return -8;
+    return srft_sketch(m, n, A, lda, d, seed, Msk, ldm, workspace(), (cudaStream_t)stream);
 }
 
 int cqrrpt_gpu_saso_sketch_ex(int64_t m, int64_t n, const double *A, int64_t lda, int64_t d, int64_t nnz,

@@ -73,6 +73,9 @@ int potrf(int64_t n, double *g, int64_t ldg, int64_t *failure_index, Workspace &
 int gemm_splitk(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const double *a, int64_t lda,
                 const double *b, int64_t ldb, double beta, double *c, int64_t ldc, int64_t splits, Workspace &ws,
                 cudaStream_t st);
+// SRFT sketch (sketch.cc:100-119, 147-166), bit-identical, single rank
+int srft_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, uint64_t seed, double *msk,
+                int64_t ldm, Workspace &ws, cudaStream_t st);
 // Gaussian sketch (sketch.cc:62-72, apply = matmul): msk = S A, S generated on device
 int gaussian_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, uint64_t seed, int64_t c0,
                     double *msk, int64_t ldm, Workspace &ws, cudaStream_t st);

@@ -46,6 +46,15 @@ def gaussian_sketch(a, d: int, seed: int, c0: int = 0, stream=None):
     return out
 
 
+def srft_sketch(a, d: int, seed: int, stream=None):
+    """apply(S, M) for the SRFT family (sketch.cc:100-119, 147-166) -> d x n, bit-identical."""
+    m, n = a.shape
+    out = colmajor_empty(d, n)
+    _lib.check(_lib.load().cqrrpt_gpu_srft_sketch(m, n, _p(a), _ld(a) if m else 1, d, seed, out.data_ptr(),
+                                                  _ld(out), _stream_ptr(stream)), "srft_sketch")
+    return out
+
+
 def qrcp(msk, rank_tol: float = -1.0, stream=None):
     """qrcp_maxnorm(M_sk, rank_tol, want_q=false) (qrcp.cc:35-97) -> (R k x n, pivots, k).
     ``msk`` is overwritten."""

@@ -55,4 +55,30 @@ def test_dgeqpt_unknown_family_rejected(cuda, oracle):
     from paper_2311_08316_b200 import _lib
     A = dev(cuda, oracle.gen_gaussian(100, 10, 1))
     with pytest.raises(_lib.InvalidArgument):
-        cuda.dgeqpt(A, sketch_family="srft")
+        cuda.dgeqpt(A, sketch_family="bogus")
+
+
+# ---- SRFT family (sketch.cc:100-119, 147-166) --------------------------------
+@pytest.mark.parametrize("m,n,d,seed", [(100, 7, 20, 3), (1000, 30, 40, 7), (4096, 16, 100, 1),
+                                        (5000, 3, 5000, 2), (70000, 24, 300, 9), (131072, 5, 1280, 0)])
+def test_srft_sketch_bit_identical(cuda, oracle, m, n, d, seed):
+    """Stage-ordered butterflies (4096-blocks in shared memory, then the
+    strided residues) reproduce the reference's fwht bit for bit."""
+    from paper_2311_08316_b200 import kernels
+    a = oracle.gen_gaussian(m, n, seed + 1)
+    got = kernels.srft_sketch(dev(cuda, a), d, seed).cpu().numpy()
+    assert np.array_equal(got, oracle.srft_apply(d, a, seed))
+
+
+def test_dgeqpt_srft_family(cuda, oracle):
+    m, n, gamma, seed = 6000, 80, 1.25, 4
+    a = oracle.gen_gaussian(m, n, 2)
+    A = dev(cuda, a)
+    res = cuda.dgeqpt(A, d_factor=gamma, seed=seed, sketch_family="srft")
+    d = oracle.sketch_rows_for(gamma, n)
+    _, j_ref, k_ref = oracle.qrcp(oracle.srft_apply(d, a, seed))  # bit-identical sketch -> J exact
+    assert res.k0 == res.k == k_ref == n
+    assert np.array_equal(res.pivots.cpu().numpy(), j_ref)
+    q = A[:, :res.k].cpu().numpy()
+    v = oracle.validate(a, q, res.r.cpu().numpy(), res.pivots.cpu().numpy())
+    assert v["orth_fro"] <= 1e2 * n * U and v["recon_rel"] <= 1e2 * n * U

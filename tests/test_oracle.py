@@ -234,3 +234,10 @@ def test_gaussian_operator_bit_exact_and_apply(oracle, reference):
     a = oracle.gen_gaussian(2000, 40, 3)
     x, y = oracle.gaussian_apply(50, a, 7), reference.gaussian_sketch_apply(50, a, 7)
     assert np.max(np.abs(x - y)) <= 1e-13 * np.max(np.abs(y))
+
+
+@pytest.mark.parametrize("m,n,d,seed", [(100, 7, 20, 3), (1000, 30, 40, 7), (4096, 16, 100, 1), (5000, 3, 5000, 2)])
+def test_srft_restatement_bit_exact(oracle, reference, m, n, d, seed):
+    """sketch.cc:100-119 (sample) and 147-166 (apply, fwht 31-39) restated in C."""
+    a = oracle.gen_gaussian(m, n, seed)
+    assert np.array_equal(oracle.srft_apply(d, a, seed), reference.srft_sketch_apply(d, a, seed))
