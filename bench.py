@@ -263,12 +263,14 @@ def main():
     ph = phases / args.steps
     names = ["sketch", "qrcp", "rank_select", "precondition", "cholesky_qr", "undo", "total", "comm"]
 
-    # ---- e2e: host input -> device -> factor -> Q, R, J back to host ------------
+    # ---- e2e: host input -> device -> factor -> Q, R, J back to host, through
+    # the public host entry point (cqrrpt_gpu_dgeqpt_host: pinned buffers, Q
+    # streamed back while the final TRSM runs) ------------------------------
     host_a = torch.empty((n, m), dtype=torch.float64).pin_memory()
     host_a.copy_(a0.t())
     k = res.k
-    host_q = torch.empty((k, m), dtype=torch.float64).pin_memory()
-    host_r = torch.empty((n, max(k, 1)), dtype=torch.float64).pin_memory()
+    host_q = torch.empty((n, m), dtype=torch.float64).pin_memory().t()
+    host_r = torch.empty((n, n), dtype=torch.float64).pin_memory().t()
     host_j = torch.empty(n, dtype=torch.int64).pin_memory()
     e2e_ms = []
     for it in range(args.warmup + args.steps):
@@ -277,15 +279,13 @@ def main():
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        work.t().copy_(host_a, non_blocking=True)  # H2D (pinned)
-        r2 = pkg.dgeqpt(work, d_factor=GAMMA, nnz=NNZ, seed=SEED, comm=comm, global_row_offset=rank * m)
-        host_q.copy_(work[:, : r2.k].t(), non_blocking=True)  # D2H of Q
-        host_r[:, : r2.k].copy_(r2.r.t(), non_blocking=True)
-        host_j.copy_(r2.pivots, non_blocking=True)
+        r2 = pkg.dgeqpt_host(host_a.t(), d_factor=GAMMA, nnz=NNZ, seed=SEED, q_out=host_q, r_out=host_r,
+                             j_out=host_j, stream=stream, comm=comm, global_row_offset=rank * m)
         e1.record(stream)
         e1.synchronize()
         if it >= args.warmup:
             e2e_ms.append(e0.elapsed_time(e1))
+    assert r2.k == k
     e2e_t = float(np.mean(e2e_ms))
     if dist is not None:
         t = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")

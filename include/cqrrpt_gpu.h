@@ -128,6 +128,15 @@ int cqrrpt_gpu_dgeqpt(int64_t m, int64_t n, double *A, int64_t lda, double d_fac
                       uint64_t seed, double eps_tol, double *R, int64_t ldr, int64_t *J, int64_t *k,
                       int64_t *k0, cqrrpt_gpu_ctx *ctx);
 
+/* Host-buffer variant (the reference's data in/out convention, cqrrpt.hh:140):
+ * A_host (m x n, lda) is uploaded, Q (m x k) is downloaded into Q_host
+ * (ldq >= m) block by block while the final TRSM is still running, R (k x n,
+ * ldr) and J (0-based) land on the host. Pinned host memory gives full PCIe
+ * bandwidth and real overlap. */
+int cqrrpt_gpu_dgeqpt_host(int64_t m, int64_t n, const double *A_host, int64_t lda, double d_factor, int64_t nnz,
+                           uint64_t seed, double eps_tol, double *Q_host, int64_t ldq, double *R_host, int64_t ldr,
+                           int64_t *J_host, int64_t *k, int64_t *k0, cqrrpt_gpu_ctx *ctx);
+
 /* ---------------------------------------------------------------------------
  * Phase-level entry points (the same kernels the driver composes; exposed for
  * parity tests and for callers that run their own collectives).

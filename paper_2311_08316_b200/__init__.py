@@ -13,6 +13,7 @@ from .cqrrpt import (  # noqa: F401
     CqrrptOutput,
     DeviceResult,
     DomainError,
+    HostResult,
     InvalidArgument,
     PhaseTimings,
     PivotedQR,
@@ -23,6 +24,7 @@ from .cqrrpt import (  # noqa: F401
     colmajor_empty,
     cqrrpt,
     dgeqpt,
+    dgeqpt_host,
     flop_model,
     sketch_flops_saso,
     sketch_rows_for,

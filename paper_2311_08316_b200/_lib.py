@@ -44,6 +44,8 @@ SYMBOLS = {
     "cqrrpt_gpu_ctx_init": (None, [ctypes.POINTER(Ctx)]),
     "cqrrpt_gpu_dgeqpt": (ctypes.c_int, [_i64, _i64, _vp, _i64, _f64, _i64, _u64, _f64, _vp, _i64, _vp,
                                          ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(Ctx)]),
+    "cqrrpt_gpu_dgeqpt_host": (ctypes.c_int, [_i64, _i64, _vp, _i64, _f64, _i64, _u64, _f64, _vp, _i64, _vp, _i64,
+                                              _vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(Ctx)]),
     "cqrrpt_gpu_sketch_rows": (_i64, [_f64, _i64]),
     "cqrrpt_gpu_saso_plan": (ctypes.c_int, [_i64, _i64, _i64, _i64, _u64, _vp, _vp]),
     "cqrrpt_gpu_saso_sketch": (ctypes.c_int, [_i64, _i64, _vp, _i64, _i64, _i64, _u64, _i64, _vp, _i64, _vp]),

@@ -313,6 +313,64 @@ def _diagnostics_from(ctx: _lib.Ctx) -> CqrrptDiagnostics:
         cond_upper_bound=ctx.cond_upper_bound)
 
 
+@dataclass
+class HostResult:
+    """Outputs of one cqrrpt_gpu_dgeqpt_host call (host arrays)."""
+    q: object          # m x k column-major (views of the caller's buffers when given)
+    r: object          # k x n
+    pivots: object     # int64 n, 0-based
+    k: int
+    k0: int
+    ctx: _lib.Ctx
+
+
+def dgeqpt_host(a, d_factor: float = 1.25, nnz: int = 4, seed: int = 0, eps_tol: float = 1e-4,
+                cond_method: int = CondMethod.identity_deviation, q_out=None, r_out=None, j_out=None,
+                sketch_family: str = "saso", stream=None, comm: Optional[Comm] = None,
+                global_row_offset: int = 0) -> HostResult:
+    """Host data in, host factors out (cqrrpt_gpu_dgeqpt_host): ``a`` is a
+    column-major float64 numpy array or CPU torch tensor (pin it for full
+    PCIe bandwidth); Q is downloaded block by block while the last TRSM runs.
+    ``q_out`` (m x n), ``r_out`` (n x n), ``j_out`` (n) may be preallocated
+    (pinned) buffers; the results are their leading k columns / rows."""
+    torch = _torch()
+    tensor = isinstance(a, torch.Tensor)
+    if tensor:
+        if a.dtype != torch.float64 or a.is_cuda or a.stride(0) != 1:
+            raise InvalidArgument("a must be a column-major float64 CPU tensor")
+        m, n = a.shape
+        lda, pa = max(a.stride(1), 1), a.data_ptr()
+    else:
+        a = np.asfortranarray(a, dtype=np.float64)
+        m, n = a.shape
+        lda, pa = max(m, 1), a.ctypes.data
+    alloc = (lambda r, c: torch.empty((c, r), dtype=torch.float64).t()) if tensor else \
+        (lambda r, c: np.empty((r, c), order="F"))
+    q = q_out if q_out is not None else alloc(m, n)
+    r = r_out if r_out is not None else alloc(n, n)
+    j = j_out if j_out is not None else (torch.empty(max(n, 1), dtype=torch.int64) if tensor
+                                         else np.empty(max(n, 1), dtype=np.int64))
+    ptr = (lambda t: t.data_ptr()) if tensor else (lambda t: t.ctypes.data)
+    ctx = _lib.new_ctx()
+    ctx.stream = _stream_ptr(stream)
+    ctx.cond_method = int(cond_method)
+    families = {"saso": _lib.SKETCH_SASO, "gaussian": _lib.SKETCH_GAUSSIAN, "srft": _lib.SKETCH_SRFT}
+    if sketch_family not in families:
+        raise InvalidArgument(f"sketch_family must be one of {sorted(families)}")
+    ctx.sketch_family = families[sketch_family]
+    if comm is not None:  # row shard of a multi-GPU job (NCCL communicator)
+        ctx.comm = comm.handle
+        ctx.nranks = comm.nranks
+        ctx.rank = comm.rank
+        ctx.global_row_offset = int(global_row_offset)
+    k, k0 = _lib._i64(), _lib._i64()
+    _lib.check(_lib.load().cqrrpt_gpu_dgeqpt_host(m, n, pa, lda, float(d_factor), int(nnz), int(seed), float(eps_tol),
+                                                  ptr(q), max(m, 1), ptr(r), max(n, 1), ptr(j), ctypes.byref(k),
+                                                  ctypes.byref(k0), ctypes.byref(ctx)), "dgeqpt_host")
+    kk = k.value
+    return HostResult(q[:, :kk], r[:kk, :], j[:n], kk, k0.value, ctx)
+
+
 def validate(dec: PivotedQR, m, tol: float) -> ValidationReport:
     """validate() (qrcp.cc:150-196) evaluated on the GPU (DMMA Gram + GEMM)."""
     torch = _torch()

@@ -151,9 +151,13 @@ double cqrrpt_gpu_flop_model(int64_t m, int64_t n, int64_t k, int64_t d, double 
     return (double)num / 6.0 + c_sk;
 }
 
-int cqrrpt_gpu_dgeqpt(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, int64_t nnz, uint64_t seed,
-                      double eps_tol, double *R, int64_t ldr, int64_t *J, int64_t *k_out, int64_t *k0_out,
-                      cqrrpt_gpu_ctx *ctx) {
+}  // extern "C"
+
+namespace {
+// The driver; `qsink` (optional) downloads Q block by block during the final TRSM.
+int dgeqpt_impl(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, int64_t nnz, uint64_t seed,
+                double eps_tol, double *R, int64_t ldr, int64_t *J, int64_t *k_out, int64_t *k0_out,
+                cqrrpt_gpu_ctx *ctx, const BlockSink *qsink) {
     cqrrpt_gpu_ctx local;
     if (!ctx) {
         cqrrpt_gpu_ctx_init(&local);
@@ -365,7 +369,7 @@ int cqrrpt_gpu_dgeqpt(int64_t m, int64_t n, double *A, int64_t lda, double d_fac
     }
 
     // ---- Q = M_pre[:, :k] R_pre^{-1}, in place into A[:, :k] ----------------
-    CQ_TRY(trsm_right(m, k, mpre, ldp, nullptr, rfull, k0, A, lda, st));
+    CQ_TRY(trsm_right(m, k, mpre, ldp, nullptr, rfull, k0, A, lda, st, qsink));
     clk.mark(PH_CHOL);
 
     // ---- R = R_pre R_sk[:k, :] (upper-trapezoidal) --------------------------
@@ -397,6 +401,48 @@ int cqrrpt_gpu_dgeqpt(int64_t m, int64_t n, double *A, int64_t lda, double d_fac
         ctx->truncation_ratio = (rn > 0.0) ? std::sqrt(ck) / rn : 0.0;
     }
     return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int cqrrpt_gpu_dgeqpt(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, int64_t nnz, uint64_t seed,
+                      double eps_tol, double *R, int64_t ldr, int64_t *J, int64_t *k_out, int64_t *k0_out,
+                      cqrrpt_gpu_ctx *ctx) {
+    return dgeqpt_impl(m, n, A, lda, d_factor, nnz, seed, eps_tol, R, ldr, J, k_out, k0_out, ctx, nullptr);
+}
+
+int cqrrpt_gpu_dgeqpt_host(int64_t m, int64_t n, const double *A_host, int64_t lda, double d_factor, int64_t nnz,
+                           uint64_t seed, double eps_tol, double *Q_host, int64_t ldq, double *R_host, int64_t ldr,
+                           int64_t *J_host, int64_t *k_out, int64_t *k0_out, cqrrpt_gpu_ctx *ctx) {
+    cqrrpt_gpu_ctx local;
+    if (!ctx) {
+        cqrrpt_gpu_ctx_init(&local);
+        ctx = &local;
+    }
+    if (m < 0) return -1;
+    if (n < 0) return -2;
+    if (m > 0 && n > 0 && !A_host) return -3;
+    if (m > 0 && lda < m) return -4;
+    if (m > 0 && n > 0 && (!Q_host || ldq < m)) return -10;
+    cudaStream_t st = (cudaStream_t)ctx->stream;
+    Workspace &ws = workspace();
+    double *dA = (m > 0 && n > 0) ? ws.get<double>("host.a", (size_t)(m * n)) : nullptr;
+    if (m > 0 && n > 0 && !dA) return fail_nomem("device copy of A");
+    if (dA)
+        CQ_CUDA(cudaMemcpy2DAsync(dA, sizeof(double) * m, A_host, sizeof(double) * lda, sizeof(double) * m, n,
+                                  cudaMemcpyHostToDevice, st),
+                "A h2d");
+    static thread_local cudaStream_t copy = nullptr;
+    if (!copy) CQ_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking), "copy stream");
+    BlockSink sink{copy, Q_host, ldq};
+    const int32_t flags = ctx->flags;
+    ctx->flags |= CQRRPT_GPU_OUTPUTS_ON_HOST;
+    const int rc = dgeqpt_impl(m, n, dA, std::max<int64_t>(m, 1), d_factor, nnz, seed, eps_tol, R_host, ldr, J_host,
+                               k_out, k0_out, ctx, dA ? &sink : nullptr);
+    ctx->flags = flags;
+    CQ_CUDA(cudaStreamSynchronize(copy), "Q d2h");
+    return rc;
 }
 
 // ---------------------------------------------------------------------------

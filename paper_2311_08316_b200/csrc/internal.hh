@@ -61,8 +61,16 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
          int64_t *k_sk, Workspace &ws, cudaStream_t st);
 int rank_stage1(int64_t k, int64_t n, const double *r, int64_t ldr, int64_t *k0, Workspace &ws, cudaStream_t st);
 
+// Optional per-block sink of a TRSM's output: after each 64-column block the
+// block is copied (D2H) on `copy` into host[:, c0:c0+64] (ld ldh), so the
+// download of X overlaps the remaining blocks.
+struct BlockSink {
+    cudaStream_t copy;
+    double *host;
+    int64_t ldh;
+};
 int trsm_right(int64_t m, int64_t k, const double *b, int64_t ldb, const int64_t *cols, const double *u,
-               int64_t ldu, double *x, int64_t ldx, cudaStream_t st);
+               int64_t ldu, double *x, int64_t ldx, cudaStream_t st, const BlockSink *sink = nullptr);
 int gram(int64_t m, int64_t k, const double *x, int64_t ldx, double *g, int64_t ldg, Workspace &ws,
          cudaStream_t st);
 // C (M x N, ldc) = alpha * op(A) * B + beta * C; op(A) = A (M x K) or A^T (A is K x M).

@@ -18,6 +18,8 @@
 // element (linalg.cc:262-274). The blocks of a well-conditioned
 // preconditioner are well conditioned; the parity tests bound the difference.
 // Algorithmic flops: m*k^2 (the reference's count, flop_model term).
+#include <vector>
+
 #include "common.cuh"
 #include "internal.hh"
 
@@ -178,7 +180,7 @@ __global__ void diag_zero_check_kernel(int64_t k, const double *__restrict__ u, 
 }
 
 int trsm_right(int64_t m, int64_t k, const double *b, int64_t ldb, const int64_t *cols, const double *u,
-               int64_t ldu, double *x, int64_t ldx, cudaStream_t st) {
+               int64_t ldu, double *x, int64_t ldx, cudaStream_t st, const BlockSink *sink) {
     if (m <= 0 || k <= 0) return 0;
     // zero diagonal -> the reference throws std::domain_error (linalg.cc:250-252)
     int *flag = workspace().get<int>("trsm.flag", 1);
@@ -199,10 +201,26 @@ int trsm_right(int64_t m, int64_t k, const double *b, int64_t ldb, const int64_t
     if (!dinv) return fail_nomem("trsm diagonal-block inverses");
     CQ_TRY(trtri_diag_blocks(k, u, ldu, dinv, st));
     const unsigned grid = (unsigned)((m + kBM - 1) / kBM);
+    static thread_local std::vector<cudaEvent_t> evs;  // one per block, reused across calls
     for (int64_t c0 = 0; c0 < k; c0 += kNB) {
         trsm_block_kernel<<<grid, kThreads, kTrsmSmem, st>>>(m, k, c0, b, ldb, cols, u, ldu,
                                                             dinv + (c0 / kNB) * kNB * kNB, x, ldx);
         note_launch();
+        if (sink) {  // block c0 is final: download it while the next blocks run
+            const size_t e = (size_t)(c0 / kNB);
+            while (evs.size() <= e) {
+                cudaEvent_t ev;
+                CQ_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "trsm sink event");
+                evs.push_back(ev);
+            }
+            CQ_CUDA(cudaEventRecord(evs[e], st), "trsm sink record");
+            CQ_CUDA(cudaStreamWaitEvent(sink->copy, evs[e], 0), "trsm sink wait");
+            const int64_t nb = std::min<int64_t>(kNB, k - c0);
+            CQ_CUDA(cudaMemcpy2DAsync(sink->host + c0 * sink->ldh, sizeof(double) * sink->ldh, x + c0 * ldx,
+                                      sizeof(double) * ldx, sizeof(double) * m, nb, cudaMemcpyDeviceToHost,
+                                      sink->copy),
+                    "trsm sink copy");
+        }
     }
     return check_launch("trsm_block_kernel");
 }

@@ -229,3 +229,25 @@ def test_cxx_reference_signature_adapter(cuda):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "OK" in r.stdout
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_dgeqpt_host_matches_device_path(cuda, oracle, pinned):
+    """cqrrpt_gpu_dgeqpt_host (host in/out, Q streamed back during the final
+    TRSM) gives the device path's factors bit for bit."""
+    import torch
+    m, n = 9000, 200
+    a = oracle.gen_gaussian(m, n, 21)
+    A = cuda.to_device_colmajor(a)
+    dev = cuda.dgeqpt(A, d_factor=1.25, nnz=8, seed=2)
+    if pinned:
+        ah = torch.from_numpy(np.ascontiguousarray(a.T)).pin_memory().t()
+        host = cuda.dgeqpt_host(ah, d_factor=1.25, nnz=8, seed=2)
+        q, r, j = host.q.numpy(), host.r.numpy(), host.pivots.numpy()
+    else:
+        host = cuda.dgeqpt_host(a, d_factor=1.25, nnz=8, seed=2)
+        q, r, j = host.q, host.r, host.pivots
+    assert (host.k, host.k0) == (dev.k, dev.k0)
+    assert np.array_equal(j, dev.pivots.cpu().numpy())
+    assert np.array_equal(q, A[:, :dev.k].cpu().numpy())
+    assert np.array_equal(r, dev.r.cpu().numpy())
