@@ -352,10 +352,27 @@ int gram(int64_t m, int64_t k, const double *x, int64_t ldx, double *gmat, int64
         for (int64_t i = 0; i < tm; ++i)
             if (i * BM <= j * BN + BN - 1) h.push_back(make_int2((int)i, (int)j));
     const int64_t ntiles = (int64_t)h.size();
-    // split-K slices: fill >= 3 CTAs per SM for a couple of waves, >= 512 rows each
+    // split-K slices over m (>= 512 rows each): every CTA does the same work, so
+    // the time is waves(ns) * m / ns with waves = ceil(ntiles*ns / resident
+    // slots); pick the fewest slices within 2% of the best (no ragged last wave)
     const int sms = num_sms();
-    int64_t want = std::max<int64_t>(1, (6 * (int64_t)sms + ntiles - 1) / ntiles);
-    int64_t nslices = std::min<int64_t>(want, std::max<int64_t>(1, m / 512));
+    int per_sm = 0;
+    CQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dgemm_kernel<64, 128, true, false>, kThreads,
+                                                          gemm_smem<64, 128>()),
+            "gram occupancy");
+    const int64_t slots = (int64_t)std::max(1, per_sm) * sms;
+    const int64_t max_slices = std::max<int64_t>(1, std::min<int64_t>(64, m / 512));
+    int64_t nslices = 1;
+    {
+        double best = 1e300;
+        for (int64_t ns = 1; ns <= max_slices; ++ns) {
+            const double cost = (double)((ntiles * ns + slots - 1) / slots) / (double)ns;
+            if (cost < best * 0.98) {
+                best = cost;
+                nslices = ns;
+            }
+        }
+    }
     int64_t rps = ((m + nslices - 1) / nslices + kBK - 1) / kBK * kBK;
     nslices = std::max<int64_t>(1, (m + rps - 1) / rps);
     int2 *tiles = ws.get<int2>("gram.tiles", (size_t)ntiles);
