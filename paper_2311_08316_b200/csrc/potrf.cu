@@ -17,73 +17,96 @@ int gemm_tn_upper(int64_t N, int64_t K, double alpha, const double *a, int64_t l
 
 constexpr int kPB = 64;
 
-// Diagonal block: 4 threads per column (thread (c, q) keeps rows i = 4s + q of
-// column c in registers, static indices only), so a step is 16 predicated
-// FMAs per thread across 8 warps. Two barriers per step (rrow is double
-// buffered).
-constexpr int kPQ = 4;               // threads per column
-constexpr int kPS = kPB / kPQ;       // rows per thread
-constexpr int kDiagThreads = kPB * kPQ;
+// Diagonal block, one warp, in 32 x 32 sub-blocks: [A11 A12; . A22] ->
+// R11 = chol(A11) in registers (lane = column, row broadcasts by shuffle, no
+// barriers), R12 = R11^{-T} A12 (right-looking substitution, division),
+// A22 -= R12^T R12 (FMAs in k order), R22 = chol(A22). Every entry sees the
+// same FMAs in the same order as the unblocked right-looking factorization
+// (and the reference's failure rule), only without CTA barriers per column.
+constexpr int kWB = 32;
 
-__global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(int64_t n, double *__restrict__ g, int64_t ldg,
-                                                                  int64_t j0, int64_t *__restrict__ fail) {
+// In-place upper Cholesky of the 32 x 32 block whose column `lane` is a[0..31]
+// (rows). Returns the 1-based failing column or 0. Rows below the diagonal are
+// updated too (no predicates); they never feed an entry on or above it.
+CQ_DEVI int warp_potrf32(double (&a)[kWB]) {
+    const int c = threadIdx.x;
+#pragma unroll
+    for (int j = 0; j < kWB; ++j) {
+        const double d = __shfl_sync(0xffffffffu, a[j], j);  // g(j,j) - sum_{t<j} r(t,j)^2
+        if (d <= 0.0 || !isfinite(d)) return j + 1;          // warp-uniform
+        const double rjj = sqrt(d);
+        const double q = a[j] / rjj;
+        const double rjc = c == j ? rjj : q;
+        a[j] = rjc;
+#pragma unroll
+        for (int i = j + 1; i < kWB; ++i) a[i] = fma(-__shfl_sync(0xffffffffu, rjc, i), rjc, a[i]);
+    }
+    return 0;
+}
+
+// One warp. A ragged last block is padded with the identity (never fails, no
+// effect on the real columns).
+__global__ void __launch_bounds__(32) potrf_diag_kernel(int64_t n, double *__restrict__ g, int64_t ldg, int64_t j0,
+                                                       int64_t *__restrict__ fail) {
     if (*fail) return;
-    __shared__ double rmat[kPB][kPB + 1];  // R block, [col][row]
-    __shared__ double rrow[2][kPB];
-    __shared__ double s_rjj;
-    __shared__ int s_fail;
+    __shared__ double blk[kPB][kPB + 1];  // [col][row]
     const int nb = (int)cmin<int64_t>(kPB, n - j0);
-    const int c = threadIdx.x >> 2, q = threadIdx.x & 3;
-    double a[kPS];
-    const double *col = g + (j0 + c) * ldg + j0;
+    const int c = threadIdx.x;
+    for (int u0 = 0; u0 < kPB * kPB / 32; u0 += 16) {  // 16 loads in flight per lane
+        double v[16];
 #pragma unroll
-    for (int s = 0; s < kPS; ++s) {
-        const int i = kPQ * s + q;
-        a[s] = (c < nb && i <= c) ? col[i] : 0.0;
-    }
-    if (threadIdx.x == 0) s_fail = 0;
-    __syncthreads();
-    int base = 0;  // a[s] holds row 4 * (base + s) + q: the window slides so row j is in a[0]
-    for (int j = 0; j < nb; ++j) {
-        if ((j >> 2) != base) {
+        for (int u = 0; u < 16; ++u) {
+            const int q = c + 32 * (u0 + u), cc = q / kPB, r = q % kPB;
+            v[u] = (cc < nb && r <= cc) ? g[(j0 + cc) * ldg + j0 + r] : (cc == r ? 1.0 : 0.0);
+        }
 #pragma unroll
-            for (int s = 0; s + 1 < kPS; ++s) a[s] = a[s + 1];
-            a[kPS - 1] = 0.0;
-            ++base;
-        }
-        const bool holder = (q == (j & 3));  // this thread holds row j of its column
-        const double ajc = a[0];             // (holder) g(j,c) - sum_{t<j} r(t,j) r(t,c)
-        if (holder && c == j) {
-            if (ajc <= 0.0 || !isfinite(ajc)) s_fail = j + 1;
-            else s_rjj = sqrt(ajc);
-        }
-        __syncthreads();
-        if (s_fail) break;
-        double *rr = rrow[j & 1];
-        if (holder) {
-            // division, not a reciprocal product: on exactly singular Grams the
-            // sign of the last Schur complement (the failure index) follows it
-            const double rjc = c > j ? ajc / s_rjj : (c == j ? s_rjj : 0.0);
-            rr[c] = rjc;
-            rmat[c][j] = rjc;
-        }
-        __syncthreads();
-        if (c > j) {
-            const double rjc = rr[c];
-#pragma unroll
-            for (int s = 0; s < kPS; ++s) {
-                const int i = kPQ * (base + s) + q;
-                if (i > j && i <= c && i < kPB) a[s] = fma(-rr[i], rjc, a[s]);
-            }
+        for (int u = 0; u < 16; ++u) {
+            const int q = c + 32 * (u0 + u);
+            blk[q / kPB][q % kPB] = v[u];
         }
     }
-    const int f = s_fail;
+    __syncwarp();
+    double a[kWB];
+#pragma unroll
+    for (int i = 0; i < kWB; ++i) a[i] = blk[c][i];
+    int f = warp_potrf32(a);  // R11
+#pragma unroll
+    for (int i = 0; i < kWB; ++i) blk[c][i] = a[i];
+    __syncwarp();
+    if (!f) {
+        // R12 = R11^{-T} A12: column 32 + c, right-looking (division by r(t,t))
+#pragma unroll
+        for (int i = 0; i < kWB; ++i) a[i] = blk[kWB + c][i];
+#pragma unroll
+        for (int t = 0; t < kWB; ++t) {
+            a[t] = a[t] / blk[t][t];
+#pragma unroll
+            for (int i = t + 1; i < kWB; ++i) a[i] = fma(-blk[i][t], a[t], a[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < kWB; ++i) blk[kWB + c][i] = a[i];
+        __syncwarp();
+        // A22 -= R12^T R12, k ascending
+#pragma unroll
+        for (int i = 0; i < kWB; ++i) a[i] = blk[kWB + c][kWB + i];
+#pragma unroll
+        for (int k = 0; k < kWB; ++k) {
+            const double rkc = blk[kWB + c][k];
+#pragma unroll
+            for (int i = 0; i < kWB; ++i) a[i] = fma(-blk[kWB + i][k], rkc, a[i]);
+        }
+        const int f2 = warp_potrf32(a);  // R22
+#pragma unroll
+        for (int i = 0; i < kWB; ++i) blk[kWB + c][kWB + i] = a[i];
+        if (f2) f = kWB + f2;
+    }
+    __syncwarp();
     const int ncols = f ? f - 1 : nb;
-    for (int e = threadIdx.x; e < kPB * kPB; e += blockDim.x) {
-        int cc = e / kPB, r = e % kPB;
-        if (cc < ncols && r <= cc) g[(j0 + cc) * ldg + j0 + r] = rmat[cc][r];
+    for (int q = c; q < kPB * kPB; q += 32) {  // factored columns, rows <= col
+        const int cc = q / kPB, r = q % kPB;
+        if (cc < ncols && r <= cc) g[(j0 + cc) * ldg + j0 + r] = blk[cc][r];
     }
-    if (threadIdx.x == 0 && f) *fail = j0 + f;  // 1-based global index
+    if (c == 0 && f) *fail = j0 + f;  // 1-based global index
 }
 
 // Panel: X = R_jj^{-T} G[j0:j0+nb, cols] for the columns right of the block.
@@ -142,7 +165,7 @@ int potrf(int64_t n, double *g, int64_t ldg, int64_t *failure_index, Workspace &
     CQ_CUDA(cudaMemsetAsync(fail, 0, sizeof(int64_t), st), "memset fail");
     for (int64_t j0 = 0; j0 < n; j0 += kPB) {
         const int64_t nb = std::min<int64_t>(kPB, n - j0);
-        potrf_diag_kernel<<<1, kDiagThreads, 0, st>>>(n, g, ldg, j0, fail);
+        potrf_diag_kernel<<<1, 32, 0, st>>>(n, g, ldg, j0, fail);
         note_launch();
         const int64_t rest = n - j0 - nb;
         if (rest > 0) {
