@@ -105,7 +105,7 @@ CQ_DEVI int stage_async(double *dst, const double *g, int64_t len, int tid, int 
 }
 
 CQ_DEVI void trace_mark(unsigned long long *tr, int64_t i, int slot) {
-    if (tr && blockIdx.x == 0 && threadIdx.x == 0 && i < 512) tr[i * 8 + slot] = (unsigned long long)clock64();
+    if (tr && threadIdx.x == 0 && i < 4096) tr[((int64_t)blockIdx.x * 4096 + i) * 8 + slot] = (unsigned long long)clock64();
 }
 
 // Warp-level reference dot of sa[0..c) (shared memory; nullptr = the column
@@ -303,21 +303,37 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
     double stop = 0.0;
     int64_t k = 0;
     int64_t i = 0;
+    // Fast column phase (<= 8 remaining positions per CTA, tails fit a half
+    // buffer): warp w owns the CTA's position k = w (mod 8) for good and keeps
+    // its column resident in b0 across steps (rb[r] = row r), with its physical
+    // index and norms in registers; only the warp that receives the column
+    // swapped out of position i restages from global memory.
+    bool resident = false;
+    double *rb = b0;
+    int32_t r_pj = 0;
+    double r_w = 0.0, r_wref = 0.0;
     for (; i < A.steps; ++i) {
         const int cur = (int)(i & 1), nxt = cur ^ 1;
         const int64_t c = d - i - 1;  // rows below the diagonal
         const int64_t body = c & ~(int64_t)3;
         trace_mark(A.trace, i, 0);
 
-        // ---- prefetch chunk 0 of this warp's first owned column (async,
-        // independent of the pivot decision)
         const int64_t jfirst = i + 1 + ((cta - (i + 1)) % G + G) % G;
-        const int64_t j_w = jfirst + (int64_t)wid * G;
-        // own columns were written by this CTA at the previous step: their
-        // prefetch does not wait for the other CTAs
+        const int64_t ncol_cta = (jfirst < n) ? (n - jfirst + G - 1) / G : 0;
+        const bool fast = ncol_cta <= kQrcpWarps && c <= CHD && !A.general;
+        int64_t j_w;
+        if (fast) {
+            const int64_t kf = (jfirst - cta) / G;
+            j_w = cta + (kf + (((int64_t)wid - kf) % kQrcpWarps + kQrcpWarps) % kQrcpWarps) * G;
+        } else {
+            j_w = jfirst + (int64_t)wid * G;
+        }
+        // ---- general path: prefetch chunk 0 of this warp's first owned column
+        // (async, independent of the pivot decision; own columns were written
+        // by this CTA at the previous step)
         int32_t pj0 = 0;
         double wj0 = 0.0, wrefj0 = 0.0, t0 = 0.0;
-        if (j_w < n) {
+        if (!fast && j_w < n) {
             pj0 = ld_cg(A.cmap[cur] + j_w);
             wj0 = ld_cg(A.w[cur] + j_w);
             wrefj0 = ld_cg(A.wref + j_w);
@@ -354,26 +370,37 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         const double *x = A.b + (int64_t)phys_p * ld;
         trace_mark(A.trace, i, 1);
 
-        // Fast column phase (<= one owned column per warp, each resident in its
-        // warp buffer): the warp whose position is the pivot's now holds the
-        // column from position i (the swap) -- restage it together with the
-        // pivot column so both round trips overlap.
-        const int64_t ncol_cta = (jfirst < n) ? (n - jfirst + G - 1) / G : 0;
-        const bool fast = ncol_cta <= kQrcpWarps && c <= CHD && !A.general;
-        double t_sw = 0.0;
-        if (fast && j_w == p) {
-            cp_async_wait<0>();  // the prefetch of the old column is not needed
-            __syncwarp();
-            const double *colp = A.b + (int64_t)phys_i * ld;
-            stage_async(b0, colp + i + 1, c, lane, 32);
-            t_sw = ld_cg(colp + i);
-        }
         // ---- make_reflector (linalg.cc:110-124), redundantly per CTA ------
+        bool restage = false;
         {
             const int off = stage_async(s_x, x + i, d - i, threadIdx.x, kQrcpThreads);
             if (threadIdx.x == 0) s_poff = off;
             cp_async_commit();
-            cp_async_wait<0>();  // also completes this warp's column prefetch
+            // fast path: a warp whose column is not resident yet (first fast
+            // step), or that receives the column swapped out of position i,
+            // stages rows i..d-1 of it after its share of the pivot column; the
+            // reflector does not wait for that copy, the column phase does.
+            if (fast && j_w < n && (!resident || j_w == p)) {
+                if (j_w == p) {  // the column from position i (written last step)
+                    r_pj = ld_cg(A.cmap[cur] + i);
+                    r_w = ld_cg(A.w[cur] + i);
+                    r_wref = ld_cg(A.wref + i);
+                } else {
+                    r_pj = ld_cg(A.cmap[cur] + j_w);
+                    r_w = ld_cg(A.w[cur] + j_w);
+                    r_wref = ld_cg(A.wref + j_w);
+                }
+                const double *colr = A.b + (int64_t)r_pj * ld;
+                const int64_t base = (i - (d - CHD - 1)) & ~(int64_t)1;  // even slot for row i (>= 0)
+                const int offr = stage_async(b0 + base, colr + i, d - i, lane, 32);
+                rb = b0 + base + offr - i;
+                cp_async_commit();
+                restage = true;
+            }
+            if (restage)
+                cp_async_wait<1>();
+            else
+                cp_async_wait<0>();  // also completes the general path's column prefetch
             __syncthreads();
         }
         const double *xs = s_x + s_poff;  // xs[0] = x_i, xs[1 + e] = tail element e
@@ -423,30 +450,32 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         ArgMax mine{-INFINITY, 0x7fffffff};
         int32_t minep = 0;
         if (fast) {
-            // Every warp's column is resident (the reflector's wait + barrier
-            // completed the copies). Warp 0 runs the CTA's <= 8 dots at once:
-            // lanes 4g..4g+3 are the reference's four accumulators for the
-            // column of warp g, products formed on the fly; warp buffers are
-            // 4 doubles apart modulo 16, so one load feeds all 8 columns in two
+            // Every warp's column is resident in its b0 (rb[r] = row r). Warp 0
+            // runs the CTA's <= 8 dots at once: lanes 4g..4g+3 are the
+            // reference's four accumulators for the column of warp g, products
+            // formed on the fly; warp buffers are 4 doubles apart modulo 16
+            // (+-1 for alignment), so one load feeds all 8 columns in about two
             // wavefronts. Then each warp updates its own column.
+            if (restage) {
+                cp_async_wait<0>();
+                __syncwarp();
+            }
             const bool has = j_w < n;
-            const bool isp = has && j_w == p;
-            const int32_t pj = isp ? phys_i : pj0;
-            const double wj = isp ? w_i : wj0, wrefj = isp ? wref_i : wrefj0;
-            double t = isp ? t_sw : t0;
+            const int32_t pj = r_pj;
+            const double wj = r_w, wrefj = r_wref;
+            double t = has ? rb[i] : 0.0;
             double *col = A.b + (int64_t)pj * ld;
             double *tail = col + i + 1;
-            const int off = (int)((reinterpret_cast<uintptr_t>(tail) >> 3) & 1);
             if (lane == 0) {
                 s_ct[wid] = t;
-                s_coff[wid] = has ? off : -1;
+                s_coff[wid] = has ? (int)(rb + i + 1 - smem) : -1;
             }
             __syncthreads();
             trace_mark(A.trace, i, 5);
             if (wid == 0 && beta != 0.0) {  // apply_reflector's dot (linalg.cc:126-136)
                 const int gq = lane >> 2, q = lane & 3;
                 const int go = s_coff[gq];
-                const double *cg = smem + gq * WB + (go > 0 ? go : 0);
+                const double *cg = smem + (go > 0 ? go : 0);
                 double sacc = 0.0;
                 if (go >= 0) {
                     // the next group's loads are issued before this group's
@@ -505,7 +534,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
                 double updated = fma(-t, t, wj);  // qrcp.cc:77-78
                 double newref = wrefj;
                 const bool recompute = updated <= sqrt_u * wrefj;  // qrcp.cc:82-86 (warp-uniform)
-                double *cb = b0 + off;
+                double *cb = rb + i + 1;
                 if (beta != 0.0) {
                     const int ci = (int)c;
                     for (int e0 = lane; e0 < ci; e0 += 256) {
@@ -521,7 +550,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
                             const int e = e0 + 32 * u;
                             if (e < ci) {
                                 const double nv = fma(-tau, xv[u], xc[u]);
-                                if (recompute) cb[e] = nv;
+                                cb[e] = nv;  // stays resident for the next step
                                 __stcg(tail + e, nv);
                             }
                         }
@@ -546,10 +575,13 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
                     __stcg(A.wref + j_w, newref);
                     __stcg(A.cmap[nxt] + j_w, pj);
                 }
+                r_w = updated;
+                r_wref = newref;
                 const ArgMax cnd = argmax_combine(mine, ArgMax{updated, (int32_t)j_w});
                 if (cnd.i != mine.i) minep = pj;
                 mine = cnd;
             }
+            resident = true;
             trace_mark(A.trace, i, 7);
         }
         bool first = true;
@@ -847,8 +879,9 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     // flags restart at 1 every call: clear the previous call's records
     CQ_CUDA(cudaMemsetAsync(a.rec, 0, 2 * 256 * 4 * sizeof(unsigned long long), st), "memset records");
     static const bool tracing = getenv("CQRRPT_QRCP_TRACE") != nullptr;
-    a.trace = tracing ? ws.get<unsigned long long>("qrcp.trace", 512 * 8) : nullptr;
-    if (a.trace) CQ_CUDA(cudaMemsetAsync(a.trace, 0, 512 * 8 * sizeof(unsigned long long), st), "trace memset");
+    a.trace = tracing ? ws.get<unsigned long long>("qrcp.trace", 256 * 4096 * 8) : nullptr;
+    if (a.trace)
+        CQ_CUDA(cudaMemsetAsync(a.trace, 0, 256 * 4096 * 8 * sizeof(unsigned long long), st), "trace memset");
     void *args[] = {&a};
     CQ_CUDA(cudaLaunchCooperativeKernel((void *)qrcp_kernel, dim3(G), dim3(kQrcpThreads), args, smem, st),
             "qrcp cooperative launch");
@@ -859,28 +892,54 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     CQ_TRY(check_launch("qrcp_extract_kernel"));
     CQ_CUDA(cudaMemcpyAsync(k_sk, a.k_out, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "k_sk d2h");
     CQ_CUDA(cudaStreamSynchronize(st), "qrcp sync");
-    if (a.trace) {  // debug: mean per-phase SM cycles over the first steps
-        std::vector<unsigned long long> h(512 * 8);
+    if (a.trace) {  // debug: mean per-phase SM cycles per quarter of the steps
+        std::vector<unsigned long long> h((size_t)G * 4096 * 8);
         cudaMemcpy(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost);
-        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        int cnt = 0;
-        for (int s2 = 0; s2 + 1 < 512 && s2 + 1 < *k_sk; ++s2) {
-            const unsigned long long *t = &h[s2 * 8];
-            for (int q = 0; q < 4; ++q) acc[q] += (double)(t[q + 1] - t[q]);
-            acc[4] += (double)(h[(s2 + 1) * 8] - t[4]);
-            if (t[5] && t[6] && t[7]) {  // warp 0's first column: products, dot, update
-                acc[5] += (double)(t[5] - t[2]);
-                acc[6] += (double)(t[6] - t[5]);
-                acc[7] += (double)(t[7] - t[6]);
+        const int steps = (int)std::min<int64_t>(*k_sk, 4096) - 1;
+        for (int qt = 0; qt < 4 && steps > 4; ++qt) {
+            double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            int cnt = 0, cnt5 = 0;
+            for (int s2 = qt * steps / 4; s2 < (qt + 1) * steps / 4; ++s2) {
+                const unsigned long long *t = &h[s2 * 8];
+                for (int q = 0; q < 4; ++q) acc[q] += (double)(t[q + 1] - t[q]);
+                acc[4] += (double)(h[(s2 + 1) * 8] - t[4]);
+                if (t[5] && t[6] && t[7]) {  // warp 0's first column: products, dot, update
+                    acc[5] += (double)(t[5] - t[2]);
+                    acc[6] += (double)(t[6] - t[5]);
+                    acc[7] += (double)(t[7] - t[6]);
+                    ++cnt5;
+                }
+                ++cnt;
             }
-            ++cnt;
-        }
-        if (cnt)
+            cnt5 = cnt5 ? cnt5 : 1;
+            double wmax = 0, wmean = 0, rmax = 0, cmax = 0, pmax = 0;  // own work (slot 1 -> 4) over CTAs
+            int nst = 0;
+            for (int s2 = qt * steps / 4; s2 < (qt + 1) * steps / 4; ++s2) {
+                double mx = 0, mr = 0, mc = 0, mp = 0, sm = 0;
+                for (int q2 = 0; q2 < G; ++q2) {
+                    const unsigned long long *t = &h[((size_t)q2 * 4096 + s2) * 8];
+                    const double w = (double)(t[4] - t[1]);
+                    sm += w;
+                    mx = std::max(mx, w);
+                    mr = std::max(mr, (double)(t[2] - t[1]));
+                    mc = std::max(mc, (double)(t[3] - t[2]));
+                    mp = std::max(mp, (double)(t[4] - t[3]));
+                }
+                wmax += mx;
+                wmean += sm / G;
+                rmax += mr;
+                cmax += mc;
+                pmax += mp;
+                ++nst;
+            }
+            fprintf(stderr, "   own work over CTAs: mean %.0f, max %.0f (max reflector %.0f, columns %.0f, partials %.0f)\n",
+                    wmean / nst, wmax / nst, rmax / nst, cmax / nst, pmax / nst);
             fprintf(stderr,
-                    "qrcp trace (G=%d, d=%lld, n=%lld, WB=%d, %d steps; SM cycles): argmax %.0f, reflector %.0f, "
-                    "columns %.0f (products %.0f, chain %.0f, update %.0f), partials %.0f, barrier %.0f\n",
-                    G, (long long)d, (long long)n, WB, cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[5] / cnt,
-                    acc[6] / cnt, acc[7] / cnt, acc[3] / cnt, acc[4] / cnt);
+                    "qrcp trace q%d (G=%d, d=%lld, n=%lld, WB=%d, %d steps; SM cycles): argmax %.0f, reflector %.0f, "
+                    "columns %.0f (pre %.0f, chain %.0f, update %.0f), partials %.0f, barrier %.0f\n",
+                    qt, G, (long long)d, (long long)n, WB, cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt,
+                    acc[5] / cnt5, acc[6] / cnt5, acc[7] / cnt5, acc[3] / cnt, acc[4] / cnt);
+        }
     }
     return 0;
 }
