@@ -105,7 +105,7 @@ CQ_DEVI int stage_async(double *dst, const double *g, int64_t len, int tid, int 
 }
 
 CQ_DEVI void trace_mark(unsigned long long *tr, int64_t i, int slot) {
-    if (tr && threadIdx.x == 0 && i < 4096) tr[((int64_t)blockIdx.x * 4096 + i) * 8 + slot] = (unsigned long long)clock64();
+    if (tr && threadIdx.x == 0 && i < 4096) tr[((int64_t)blockIdx.x * 4096 + i) * 16 + slot] = (unsigned long long)clock64();
 }
 
 // Warp-level reference dot of sa[0..c) (shared memory; nullptr = the column
@@ -201,6 +201,53 @@ CQ_DEVI void rec_wait(const unsigned long long *slot, uint32_t flag, double *v, 
     *phys = (int32_t)(uint32_t)w3;
 }
 
+// argmax carrying the winner's physical column
+struct ArgMax3 {
+    double v;
+    int32_t i, p;
+};
+CQ_DEVI ArgMax3 argmax3_combine(ArgMax3 a, ArgMax3 b) {
+    if (b.v > a.v || (b.v == a.v && b.i < a.i)) return b;
+    return a;
+}
+CQ_DEVI ArgMax3 warp_argmax3(ArgMax3 a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ArgMax3 b;
+        b.v = __shfl_xor_sync(0xffffffffu, a.v, o);
+        b.i = __shfl_xor_sync(0xffffffffu, a.i, o);
+        b.p = __shfl_xor_sync(0xffffffffu, a.p, o);
+        a = argmax3_combine(a, b);
+    }
+    return a;
+}
+
+// One warp waits for the G records of a step (lane l: records l, l+32, ...,
+// all loads of a pass in flight together) and returns their argmax.
+CQ_DEVI ArgMax3 poll_records(const unsigned long long *recs, int G, uint32_t flag, int lane) {
+    ArgMax3 best{-INFINITY, 0x7fffffff, 0};
+    unsigned pending = 0;
+    for (int r = 0; r < 8; ++r)
+        if (lane + 32 * r < G) pending |= 1u << r;
+    while (pending) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            if (!(pending & (1u << r))) continue;
+            const unsigned long long *slot = recs + (size_t)(lane + 32 * r) * 4;
+            unsigned long long w0, w1, w2, w3;
+            asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(slot) : "memory");
+            asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w2), "=l"(w3) : "l"(slot + 2) : "memory");
+            if ((uint32_t)(w0 >> 32) == flag && (uint32_t)(w1 >> 32) == flag && (uint32_t)(w2 >> 32) == flag &&
+                (uint32_t)(w3 >> 32) == flag) {
+                pending &= ~(1u << r);
+                best = argmax3_combine(best, ArgMax3{__hiloint2double((int)(uint32_t)w0, (int)(uint32_t)w1),
+                                                     (int32_t)(uint32_t)w2, (int32_t)(uint32_t)w3});
+            }
+        }
+    }
+    return warp_argmax3(best);
+}
+
 struct QrcpArgs {
     int64_t d, n, ld;
     double *b;
@@ -229,6 +276,10 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
     __shared__ int s_poff;
     __shared__ double s_ct[kQrcpWarps], s_tau[kQrcpWarps];  // fast column phase: R(i,j), tau per warp
     __shared__ int s_coff[kQrcpWarps];                        // column offset in its warp buffer (-1: none)
+    __shared__ double s_pv;                                   // this step's pivot: value, position, column
+    __shared__ int32_t s_pi, s_pp;
+    __shared__ double s_cv[2][kQrcpWarps];                    // warp candidates, by step parity
+    __shared__ int32_t s_ci[2][kQrcpWarps], s_cp[2][kQrcpWarps];
     const int G = gridDim.x, cta = blockIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t d = A.d, n = A.n, ld = A.ld;
@@ -342,24 +393,24 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
             cp_async_commit();
             t0 = ld_cg(col + i);
         }
-        // every CTA's record of the previous step (the grid barrier)
-        ArgMax g{-INFINITY, 0x7fffffff};
-        int32_t gp = 0;
-        if (threadIdx.x < G) {
-            double v;
-            int32_t ix;
-            rec_wait(A.rec + ((size_t)cur * 256 + threadIdx.x) * 4, (uint32_t)(i + 1), &v, &ix, &gp);
-            g = ArgMax{v, ix};
+        // ---- grid barrier + pivot: warp 0 polls every CTA's record of the
+        // previous step (lane l: records l, l+32, ...) and reduces them --
+        // lowest index attaining the max (qrcp.cc:26-31; the rule is order
+        // independent); its acquire fence + one CTA barrier publish the pivot
+        if (wid == 0) {
+            const ArgMax3 gw = poll_records(A.rec + (size_t)cur * 256 * 4, G, (uint32_t)(i + 1), lane);
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire: the records' writers' data
+            if (lane == 0) {
+                s_pv = gw.v;
+                s_pi = gw.i;
+                s_pp = gw.p;
+            }
         }
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire: the records' writers' data
         __syncthreads();
-        // position i belongs to CTA i % G: read after the barrier
-        const int32_t phys_i = ld_cg(A.cmap[cur] + i);
-        const double w_i = ld_cg(A.w[cur] + i), wref_i = ld_cg(A.wref + i);
-
-        // ---- pivot: lowest index attaining the max (qrcp.cc:26-31) -------
-        int32_t phys_p;
-        g = block_argmax(g, gp, &phys_p);
+        trace_mark(A.trace, i, 11);
+        ArgMax g{s_pv, s_pi};
+        const int32_t phys_p = s_pp;
+        trace_mark(A.trace, i, 12);
         if (i == 0) stop = A.rank_tol * sqrt(fmax(g.v, 0.0));  // max_norm0 (qrcp.cc:52-55)
         const double wp = g.v;
         const int64_t p = g.i;
@@ -403,6 +454,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
                 cp_async_wait<0>();  // also completes the general path's column prefetch
             __syncthreads();
         }
+        trace_mark(A.trace, i, 8);
         const double *xs = s_x + s_poff;  // xs[0] = x_i, xs[1 + e] = tail element e
         for (int e0 = threadIdx.x; e0 < (int)body; e0 += 4 * kQrcpThreads) {
             double xv[4];
@@ -413,6 +465,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
                 if (e0 + u * kQrcpThreads < (int)body) s_sv[e0 + u * kQrcpThreads] = xv[u] * xv[u];
         }
         __syncthreads();
+        trace_mark(A.trace, i, 9);
         if (wid == 0 && lane < 4) {
             double s = chain_sum(0.0, s_sv, body, lane);
             double tail_sq = chain_finish(s, c, [&](int64_t e) { return xs[1 + e]; },
@@ -433,6 +486,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
             }
         }
         __syncthreads();
+        trace_mark(A.trace, i, 10);
         const double alpha = s_bc[0], v0 = s_bc[1], beta = s_bc[2];
         for (int r0 = threadIdx.x; r0 < (int)c; r0 += 4 * kQrcpThreads) {  // colj[i] /= v0
             double xv[4];
@@ -601,9 +655,12 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
                     cp_async_wait<0>();
                     __syncwarp();
                 }
-                pj = isp ? phys_i : ld_cg(A.cmap[cur] + j);
-                wj = isp ? w_i : ld_cg(A.w[cur] + j);
-                wrefj = isp ? wref_i : ld_cg(A.wref + j);
+                // the pivot's position receives the column from position i
+                // (written last step by CTA i % G, visible after the barrier)
+                const int64_t js = isp ? i : j;
+                pj = ld_cg(A.cmap[cur] + js);
+                wj = ld_cg(A.w[cur] + js);
+                wrefj = ld_cg(A.wref + js);
                 t = ld_cg(A.b + (int64_t)pj * ld + i);
             }
             double *col = A.b + (int64_t)pj * ld;
@@ -701,14 +758,26 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         }
         trace_mark(A.trace, i, 3);
         {
-            int32_t bp;
-            mine = block_argmax(mine, minep, &bp);
-            if (threadIdx.x == 0) {
-                if (cta == 0) {
-                    __stcg(A.piv + i, phys_p);
-                    __stcg(A.alpha + i, alpha);
+            // warp candidates (warp-uniform) -> slot [step parity][warp]; after
+            // one barrier warp 0 reduces them and publishes the CTA's record
+            if (lane == 0) {
+                s_cv[cur][wid] = mine.v;
+                s_ci[cur][wid] = mine.i;
+                s_cp[cur][wid] = minep;
+            }
+            __syncthreads();
+            if (wid == 0) {
+                ArgMax3 r{-INFINITY, 0x7fffffff, 0};
+                if (lane < kQrcpWarps) r = ArgMax3{s_cv[cur][lane], s_ci[cur][lane], s_cp[cur][lane]};
+                r = warp_argmax3(r);
+                trace_mark(A.trace, i, 13);
+                if (lane == 0) {
+                    if (cta == 0) {
+                        __stcg(A.piv + i, phys_p);
+                        __stcg(A.alpha + i, alpha);
+                    }
+                    rec_publish(A.rec + ((size_t)nxt * 256 + cta) * 4, (uint32_t)(i + 2), r.v, r.i, r.p);
                 }
-                rec_publish(A.rec + ((size_t)nxt * 256 + cta) * 4, (uint32_t)(i + 2), mine.v, mine.i, bp);
             }
         }
         k = i + 1;
@@ -879,9 +948,9 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     // flags restart at 1 every call: clear the previous call's records
     CQ_CUDA(cudaMemsetAsync(a.rec, 0, 2 * 256 * 4 * sizeof(unsigned long long), st), "memset records");
     static const bool tracing = getenv("CQRRPT_QRCP_TRACE") != nullptr;
-    a.trace = tracing ? ws.get<unsigned long long>("qrcp.trace", 256 * 4096 * 8) : nullptr;
+    a.trace = tracing ? ws.get<unsigned long long>("qrcp.trace", 256 * 4096 * 16) : nullptr;
     if (a.trace)
-        CQ_CUDA(cudaMemsetAsync(a.trace, 0, 256 * 4096 * 8 * sizeof(unsigned long long), st), "trace memset");
+        CQ_CUDA(cudaMemsetAsync(a.trace, 0, 256 * 4096 * 16 * sizeof(unsigned long long), st), "trace memset");
     void *args[] = {&a};
     CQ_CUDA(cudaLaunchCooperativeKernel((void *)qrcp_kernel, dim3(G), dim3(kQrcpThreads), args, smem, st),
             "qrcp cooperative launch");
@@ -893,16 +962,16 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     CQ_CUDA(cudaMemcpyAsync(k_sk, a.k_out, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "k_sk d2h");
     CQ_CUDA(cudaStreamSynchronize(st), "qrcp sync");
     if (a.trace) {  // debug: mean per-phase SM cycles per quarter of the steps
-        std::vector<unsigned long long> h((size_t)G * 4096 * 8);
+        std::vector<unsigned long long> h((size_t)G * 4096 * 16);
         cudaMemcpy(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost);
         const int steps = (int)std::min<int64_t>(*k_sk, 4096) - 1;
         for (int qt = 0; qt < 4 && steps > 4; ++qt) {
             double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             int cnt = 0, cnt5 = 0;
             for (int s2 = qt * steps / 4; s2 < (qt + 1) * steps / 4; ++s2) {
-                const unsigned long long *t = &h[s2 * 8];
+                const unsigned long long *t = &h[s2 * 16];
                 for (int q = 0; q < 4; ++q) acc[q] += (double)(t[q + 1] - t[q]);
-                acc[4] += (double)(h[(s2 + 1) * 8] - t[4]);
+                acc[4] += (double)(h[(s2 + 1) * 16] - t[4]);
                 if (t[5] && t[6] && t[7]) {  // warp 0's first column: products, dot, update
                     acc[5] += (double)(t[5] - t[2]);
                     acc[6] += (double)(t[6] - t[5]);
@@ -917,7 +986,7 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
             for (int s2 = qt * steps / 4; s2 < (qt + 1) * steps / 4; ++s2) {
                 double mx = 0, mr = 0, mc = 0, mp = 0, sm = 0;
                 for (int q2 = 0; q2 < G; ++q2) {
-                    const unsigned long long *t = &h[((size_t)q2 * 4096 + s2) * 8];
+                    const unsigned long long *t = &h[((size_t)q2 * 4096 + s2) * 16];
                     const double w = (double)(t[4] - t[1]);
                     sm += w;
                     mx = std::max(mx, w);
@@ -931,6 +1000,21 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
                 cmax += mc;
                 pmax += mp;
                 ++nst;
+            }
+            {
+                static const int seq[] = {0, 11, 12, 1, 8, 9, 10, 2, 3, 13, 4};
+                static const char *nm[] = {"pre+poll", "pivot-argmax", "stop", "x-fetch", "squares", "norm-chain",
+                                           "divide", "columns", "block-argmax", "publish"};
+                double seg[10] = {0};
+                long cntc = 0;
+                for (int s2 = qt * steps / 4; s2 < (qt + 1) * steps / 4; ++s2)
+                    for (int q2 = 0; q2 < G; ++q2, ++cntc) {
+                        const unsigned long long *t = &h[((size_t)q2 * 4096 + s2) * 16];
+                        for (int z = 0; z < 10; ++z) seg[z] += (double)(t[seq[z + 1]] - t[seq[z]]);
+                    }
+                fprintf(stderr, "   mean over CTAs:");
+                for (int z = 0; z < 10; ++z) fprintf(stderr, " %s %.0f", nm[z], seg[z] / cntc);
+                fprintf(stderr, "\n");
             }
             fprintf(stderr, "   own work over CTAs: mean %.0f, max %.0f (max reflector %.0f, columns %.0f, partials %.0f)\n",
                     wmean / nst, wmax / nst, rmax / nst, cmax / nst, pmax / nst);
