@@ -59,6 +59,16 @@ CQ_DEVI void cp_async8_zfill(void *smem, const void *gmem, int src_bytes) {
 CQ_DEVI void cp_async4(void *smem, const void *gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem)), "l"(gmem));
 }
+// the same copies addressed by a 32-bit shared-window address
+CQ_DEVI void cp_async16_s(uint32_t s, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+CQ_DEVI void cp_async8_zfill_s(uint32_t s, const void *gmem, int src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+CQ_DEVI void cp_async4_s(uint32_t s, const void *gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
 CQ_DEVI void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 CQ_DEVI void cp_async_wait() {

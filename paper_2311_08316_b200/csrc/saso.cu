@@ -7,7 +7,8 @@
 //
 // Data layout in HBM
 //   plan   uint32[m_local * nnz]      row | sign<<31 (sign 1 = +1/sqrt(d))
-//   tptr   uint16[ntiles * (d+1)]     per 128-row tile: entry offsets by sketch row
+//   tptr   uint16[ntiles * tstride]   per 128-row tile: entry offsets by sketch row
+//                                     (tstride = d+1 rounded up to even: 4-byte aligned slices)
 //   tent   uint32[ntiles * 128*nnz]   per tile, entries sorted by (row, c):
 //                                     negative<<31 | (row % A)<<16 | byte offset
 //                                     of A(c_local, 0) in the staged tile (c*264)
@@ -23,6 +24,8 @@
 // row's accumulator through a jump table on the row % A stored in the entry:
 // acc = fma(v, A(c, j), acc) per entry in c order is the reference's own FMA
 // chain per output entry (sketch.cc:137-143), so one c-split is bit-identical.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.hh"
 
@@ -70,7 +73,7 @@ __global__ void saso_plan_kernel(int64_t d, int64_t c0, int64_t count, int nnz, 
 // Per-tile CSR by sketch row (stable: c ascending within a row).
 // One CTA per tile; histogram + scan by the block, ordered scatter by warp 0.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d, int nnz, int A,
+__global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d, int64_t tstride, int nnz, int A,
                                                             const uint32_t *__restrict__ plan,
                                                             uint16_t *__restrict__ tptr,
                                                             uint32_t *__restrict__ tent) {
@@ -111,7 +114,7 @@ __global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d
     }
     __syncthreads();
     int32_t base = s_part[wid] + incl - run;
-    uint16_t *optr = tptr + tile * (d + 1);
+    uint16_t *optr = tptr + tile * tstride;
     for (int64_t r = lo; r < hi; ++r) {
         int32_t c = s_cnt[r];
         s_cur[r] = base;
@@ -154,6 +157,7 @@ struct ApplyArgs {
     double val;
     int nnz;
     int ptrw, entw;         // 32-bit words per stage for pointers / entries
+    int64_t tstride;        // tptr elements per tile (even)
     int64_t ntiles, tiles_per_split;
     const uint16_t *tptr;
     const uint32_t *tent;
@@ -190,29 +194,34 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
 #pragma unroll
     for (int it = 0; it < kIters; ++it) colok |= (j0 + jj0 + kCS * it < P.n) ? (1u << it) : 0u;
     const double *src0 = P.a + (j0 + jj0) * P.lda + cc;  // column j0+jj0, row cc of tile 0
-    const uint32_t dst0 = (uint32_t)(cc * kXLD + jj0);
     const int ent_words = kTileRows * P.nnz;
-    auto issue = [&](int64_t tile, int stg) {
-        uint32_t *sw = stage0 + (size_t)stg * stage_words;
-        double *dt = reinterpret_cast<double *>(sw) + dst0;
-        const int64_t row0 = tile * kTileRows;
-        const unsigned ok = (row0 + cc < P.m) ? colok : 0u;
-        const double *src = src0 + row0;
+    // shared byte addresses within a stage, fixed per thread
+    const uint32_t s_stage0 = smem_u32(stage0), stage_bytes = (uint32_t)stage_words * 4u;
+    const uint32_t a_off = (uint32_t)(cc * kXLD + jj0) * 8u;
+    const uint32_t ptr_off = (uint32_t)(2 * kTileRows * kXLD) * 4u, ent_off = ptr_off + (uint32_t)P.ptrw * 4u;
+    const int nwp = (rows_here + 2) / 2;  // words holding tptr[tile][r0 .. r0 + rows_here] (r0 even)
+    const uint32_t *tpw = reinterpret_cast<const uint32_t *>(P.tptr + r0);
+    const int64_t tsw = P.tstride / 2;
+    const int nent16 = ent_words / 4;     // 16-byte copies of the tile's entries
+    const double *srcA[kIters];  // row cc of tile 0 in this thread's columns (A itself if out of range)
 #pragma unroll
-        for (int it = 0; it < kIters; ++it) {
-            cp_async8_zfill(dt + kCS * it, ((ok >> it) & 1u) ? src : P.a, ((ok >> it) & 1u) ? 8 : 0);
-            src += ldas;
-        }
-        // tile pointers tptr[tile][r0 .. r0+rows_here] (4-byte words from the aligned start)
-        uint32_t *sp = sw + 2 * kTileRows * kXLD;
-        const uint16_t *gp = P.tptr + tile * (P.d + 1) + r0;
-        const uint32_t *gpw = reinterpret_cast<const uint32_t *>(reinterpret_cast<uintptr_t>(gp) & ~(uintptr_t)3);
-        const int nw = (int)(((reinterpret_cast<uintptr_t>(gp + rows_here + 1) + 3) - reinterpret_cast<uintptr_t>(gpw)) / 4);
-        if (tid < nw) cp_async4(sp + tid, gpw + tid);  // nw <= (RB + 4) / 2 < kApplyThreads
-        // all entries of the tile (16-byte copies; the array is padded to whole tiles)
-        uint32_t *se = sp + P.ptrw;
+    for (int it = 0; it < kIters; ++it) srcA[it] = ((colok >> it) & 1u) ? src0 + it * ldas : P.a;
+    auto issue = [&](int64_t tile, int stg) {
+        const uint32_t sb = s_stage0 + (uint32_t)stg * stage_bytes;
+        const int64_t row0 = tile * kTileRows;
+        const unsigned ok = (row0 + cc < P.m) ? colok : 0u;  // zero fill past m / n
+#pragma unroll
+        for (int it = 0; it < kIters; ++it)
+            cp_async8_zfill_s(sb + a_off + (uint32_t)(it * kCS * 8), srcA[it] + (ok ? row0 : 0),
+                              ((ok >> it) & 1u) ? 8 : 0);
+        if (tid < nwp) cp_async4_s(sb + ptr_off + 4u * (uint32_t)tid, tpw + tile * tsw + tid);
         const uint32_t *ge = P.tent + tile * (int64_t)ent_words;
-        for (int w = 4 * tid; w < ent_words; w += 4 * kApplyThreads) cp_async16(se + w, ge + w);
+        if (nent16 <= kApplyThreads) {  // nnz <= 32: one 16-byte copy per thread at most
+            if (tid < nent16) cp_async16_s(sb + ent_off + 16u * (uint32_t)tid, ge + 4 * tid);
+        } else {
+            for (int w = tid; w < nent16; w += kApplyThreads)
+                cp_async16_s(sb + ent_off + 16u * (uint32_t)w, ge + 4 * w);
+        }
     };
     // Two tiles per CTA barrier (a warp's share of entries varies tile to
     // tile; pairing halves the barriers and averages the imbalance), three
@@ -249,8 +258,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
             const int stg = (stg_pair + u >= kApplyStages) ? stg_pair + u - kApplyStages : stg_pair + u;
             const uint32_t *sw = stage0 + (size_t)stg * stage_words;
             const char *xb = reinterpret_cast<const char *>(reinterpret_cast<const double *>(sw) + lane);
-            const uint16_t *sp = reinterpret_cast<const uint16_t *>(sw + 2 * kTileRows * kXLD) +
-                                 ((reinterpret_cast<uintptr_t>(P.tptr + tile * (P.d + 1) + r0) >> 1) & 1);
+            const uint16_t *sp = reinterpret_cast<const uint16_t *>(sw + 2 * kTileRows * kXLD);
             const uint32_t *se = sw + 2 * kTileRows * kXLD + P.ptrw;
             // the warp's entries: contiguous, row-sorted (row % A in bits 16..20),
             // c ascending within a row. The next entry's word is always in a
@@ -343,7 +351,8 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
     if (d > 32767 || nnz * kTileRows > 65535) return fail_internal("saso_sketch: d or nnz too large for the CSR");
     const int64_t ntiles = (m + kTileRows - 1) / kTileRows;
     uint32_t *plan = ws.get<uint32_t>("saso.plan", (size_t)(m * nnz));
-    uint16_t *tptr = ws.get<uint16_t>("saso.tptr", (size_t)(ntiles * (d + 1)) + 2);
+    const int64_t tstride = (d + 2) & ~(int64_t)1;  // d + 1 rounded up to even
+    uint16_t *tptr = ws.get<uint16_t>("saso.tptr", (size_t)(ntiles * tstride) + 2);
     uint32_t *tent = ws.get<uint32_t>("saso.tent", (size_t)(ntiles * kTileRows * nnz) + 4);
     if (!plan || !tptr || !tent) return fail_nomem("saso workspace");
     int rc = saso_plan(d, c0, m, nnz, seed, plan, st);
@@ -355,7 +364,7 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
     const int sms = num_sms();
     int A = 10;
     if (!allow_split) {
-        const int cand[] = {10, 8, 6, 4, 2};
+        const int cand[] = {10, 8, 6, 4, 2, 1};
         double best = 1e300;
         for (int a : cand) {
             const int64_t rb = (int64_t)kApplyWarps * a;
@@ -367,13 +376,17 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
             }
         }
     }
+    if (const char *ev = getenv("CQRRPT_SASO_A")) {  // experiments: force the row-block width
+        const int fa = atoi(ev);
+        if (fa == 1 || fa == 2 || fa == 4 || fa == 6 || fa == 8 || fa == 10) A = fa;
+    }
     const int64_t rblocks = (d + (int64_t)kApplyWarps * A - 1) / ((int64_t)kApplyWarps * A);
     size_t csr_smem = sizeof(int32_t) * (size_t)(2 * d + 2);
     if (csr_smem > 48 * 1024 &&
         cudaFuncSetAttribute(saso_tile_csr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csr_smem) !=
             cudaSuccess)
         return fail_cuda("csr smem attr");
-    saso_tile_csr_kernel<<<(unsigned)ntiles, 256, csr_smem, st>>>(m, d, (int)nnz, A, plan, tptr, tent);
+    saso_tile_csr_kernel<<<(unsigned)ntiles, 256, csr_smem, st>>>(m, d, tstride, (int)nnz, A, plan, tptr, tent);
     note_launch();
     if ((rc = check_launch("saso_tile_csr_kernel"))) return rc;
 
@@ -410,10 +423,12 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
     P.ntiles = ntiles;
     P.tiles_per_split = tps;
     P.tptr = tptr;
+    P.tstride = tstride;
     P.tent = tent;
     P.part = part;
     dim3 grid((unsigned)cgroups, (unsigned)rblocks, (unsigned)nsplit);
     switch (A) {
+        case 1: rc = launch_apply<1>(P, grid, smem, st); break;
         case 2: rc = launch_apply<2>(P, grid, smem, st); break;
         case 4: rc = launch_apply<4>(P, grid, smem, st); break;
         case 6: rc = launch_apply<6>(P, grid, smem, st); break;
