@@ -376,13 +376,13 @@ int dgeqpt_impl(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, i
     if (host_out) {
         double *rk = ws.get<double>("drv.rout", (size_t)(k * n));
         if (!rk) return fail_nomem("rout");
-        CQ_TRY(gemm(false, k, n, k, 1.0, rfull, k0, rsk, ldk, 0.0, rk, k, st));
+        CQ_TRY(gemm_fill(false, k, n, k, 1.0, rfull, k0, rsk, ldk, 0.0, rk, k, ws, st));
         clk.mark(PH_UNDO);
         CQ_CUDA(cudaMemcpy2DAsync(R, sizeof(double) * ldr, rk, sizeof(double) * k, sizeof(double) * k, n,
                                   cudaMemcpyDeviceToHost, st),
                 "R d2h");
     } else {
-        CQ_TRY(gemm(false, k, n, k, 1.0, rfull, k0, rsk, ldk, 0.0, R, ldr, st));
+        CQ_TRY(gemm_fill(false, k, n, k, 1.0, rfull, k0, rsk, ldk, 0.0, R, ldr, ws, st));
         clk.mark(PH_UNDO);
     }
     CQ_TRY(emit_pivots());
@@ -583,7 +583,7 @@ int cqrrpt_gpu_cholesky_qr(int64_t m, int64_t n, double *A, int64_t lda, double 
     if (*failure_index > 0) return 0;
     CQ_TRY(cholqr_pass(m, n, A, lda, r2, n, failure_index, ws, st));
     if (*failure_index > 0) return 0;
-    return gemm(false, n, n, n, 1.0, r2, n, r1, n, 0.0, R, ldr, st);  // R = R2 R1 (cqrrpt.cc:88)
+    return gemm_fill(false, n, n, n, 1.0, r2, n, r1, n, 0.0, R, ldr, ws, st);  // R = R2 R1 (cqrrpt.cc:88)
 }
 
 int cqrrpt_gpu_trtri_upper(int64_t k, const double *R, int64_t ldr, double *X, int64_t ldx, void *stream) {
@@ -595,7 +595,7 @@ int cqrrpt_gpu_trtri_upper(int64_t k, const double *R, int64_t ldr, double *X, i
 int cqrrpt_gpu_trmm_upper(int64_t k, int64_t n, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
                           int64_t ldc, void *stream) {
     if (k < 0 || n < 0) return -1;
-    return gemm(false, k, n, k, 1.0, A, lda, B, ldb, 0.0, C, ldc, (cudaStream_t)stream);
+    return gemm_fill(false, k, n, k, 1.0, A, lda, B, ldb, 0.0, C, ldc, workspace(), (cudaStream_t)stream);
 }
 
 // ---- device validator ------------------------------------------------------

@@ -296,6 +296,20 @@ int gemm(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const doub
     return gemm_ex(trans_a, P, 1, st);
 }
 
+// Plain GEMM when its tiles fill the GPU, else split-K (fixed-order reduce)
+// to about three CTAs per SM, K slices of >= 128.
+int gemm_fill(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const double *a, int64_t lda,
+              const double *b, int64_t ldb, double beta, double *c, int64_t ldc, Workspace &ws, cudaStream_t st) {
+    if (M <= 0 || N <= 0) return 0;
+    const bool tall = N <= 64;
+    const int BM = tall ? 128 : 64, BN = tall ? 64 : 128;
+    const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+    const int64_t sms = num_sms();
+    const int64_t splits = std::min<int64_t>({(3 * sms + tiles - 1) / tiles, K / 128, 16});
+    if (tiles >= sms || splits < 2) return gemm(trans_a, M, N, K, alpha, a, lda, b, ldb, beta, c, ldc, st);
+    return gemm_splitk(trans_a, M, N, K, alpha, a, lda, b, ldb, beta, c, ldc, splits, ws, st);
+}
+
 int gemm_tn_upper(int64_t N, int64_t K, double alpha, const double *a, int64_t lda, const double *b, int64_t ldb,
                   double beta, double *c, int64_t ldc, const int64_t *skip_flag, cudaStream_t st) {
     GemmArgs P{};
@@ -326,19 +340,46 @@ int gemm_tn_upper(int64_t N, int64_t K, double alpha, const double *a, int64_t l
 // block of G equals gram(X[:, :j]) bitwise — the reference's Cholesky-retry
 // property (cqrrpt.cc:162-164) holds without recomputation.
 // ---------------------------------------------------------------------------
-__global__ void gram_reduce_kernel(int64_t k, int64_t nslices, const int2 *__restrict__ tiles, int64_t ntiles,
-                                   const double *__restrict__ part, double *__restrict__ gmat, int64_t ldg) {
+// Fixed-order sum of the split-K slices (slice 0 first, as before), one CTA per
+// (tile, 16-column strip): the slice loads are issued four at a time, and both
+// triangles are written coalesced through a shared 64 x 16 block.
+constexpr int kRedSW = 16;
+__global__ void __launch_bounds__(256) gram_reduce_kernel(int64_t k, int64_t nslices, const int2 *__restrict__ tiles,
+                                                          int64_t ntiles, const double *__restrict__ part,
+                                                          double *__restrict__ gmat, int64_t ldg) {
     constexpr int BM = 64, BN = 128;
+    __shared__ double sblk[kRedSW][BM + 1];
     const int64_t tile = blockIdx.x;
     const int2 tt = tiles[tile];
-    for (int q = threadIdx.x; q < BM * BN; q += blockDim.x) {
-        int c = q / BM, r = q % BM;
-        int64_t i = (int64_t)tt.x * BM + r, j = (int64_t)tt.y * BN + c;
-        if (i >= k || j >= k || i > j) continue;
-        double s = 0.0;
-        for (int64_t sl = 0; sl < nslices; ++sl) s += part[(sl * ntiles + tile) * (int64_t)(BM * BN) + q];
-        gmat[j * ldg + i] = s;
-        gmat[i * ldg + j] = s;
+    const int64_t i0 = (int64_t)tt.x * BM, j0 = (int64_t)tt.y * BN + (int64_t)blockIdx.y * kRedSW;
+    if (i0 >= k || j0 >= k || i0 > j0 + kRedSW - 1) return;  // strip entirely outside the upper triangle
+    const int64_t sstride = ntiles * (int64_t)(BM * BN);
+    for (int q = threadIdx.x; q < BM * kRedSW; q += blockDim.x) {
+        const int c = q / BM, r = q % BM;  // part element (r, c) of the tile at c * BM + r
+        const double *pp = part + tile * (int64_t)(BM * BN) + (int64_t)(blockIdx.y * kRedSW + c) * BM + r;
+        double sum = 0.0;
+        int64_t sl = 0;
+        for (; sl + 4 <= nslices; sl += 4) {
+            const double a0 = pp[sl * sstride], a1 = pp[(sl + 1) * sstride], a2 = pp[(sl + 2) * sstride],
+                         a3 = pp[(sl + 3) * sstride];
+            sum += a0;
+            sum += a1;
+            sum += a2;
+            sum += a3;
+        }
+        for (; sl < nslices; ++sl) sum += pp[sl * sstride];
+        sblk[c][r] = sum;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < BM * kRedSW; q += blockDim.x) {  // upper: column j, rows i0.. (coalesced)
+        const int c = q / BM, r = q % BM;
+        const int64_t i = i0 + r, j = j0 + c;
+        if (i < k && j < k && i <= j) gmat[j * ldg + i] = sblk[c][r];
+    }
+    for (int q = threadIdx.x; q < BM * kRedSW; q += blockDim.x) {  // mirror: column i, rows j0..j0+15
+        const int r = q / kRedSW, c = q % kRedSW;
+        const int64_t i = i0 + r, j = j0 + c;
+        if (i < k && j < k && i < j) gmat[i * ldg + j] = sblk[c][r];
     }
 }
 
@@ -347,7 +388,8 @@ int gram(int64_t m, int64_t k, const double *x, int64_t ldx, double *gmat, int64
     if (k <= 0) return 0;
     constexpr int BM = 64, BN = 128;
     const int64_t tm = (k + BM - 1) / BM, tn = (k + BN - 1) / BN;
-    std::vector<int2> h;
+    static thread_local std::vector<int2> h;  // outlives the async upload below
+    h.clear();
     for (int64_t j = 0; j < tn; ++j)
         for (int64_t i = 0; i < tm; ++i)
             if (i * BM <= j * BN + BN - 1) h.push_back(make_int2((int)i, (int)j));
@@ -400,9 +442,9 @@ int gram(int64_t m, int64_t k, const double *x, int64_t ldx, double *gmat, int64
         CQ_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * ntiles * BM * BN, st), "memset part");
         nslices = 1;
     }
-    gram_reduce_kernel<<<(unsigned)ntiles, 256, 0, st>>>(k, nslices, tiles, ntiles, part, gmat, ldg);
+    gram_reduce_kernel<<<dim3((unsigned)ntiles, (unsigned)(BN / kRedSW)), 256, 0, st>>>(k, nslices, tiles, ntiles,
+                                                                                       part, gmat, ldg);
     note_launch();
-    CQ_CUDA(cudaStreamSynchronize(st), "gram sync");  // h must outlive the async copy
     return check_launch("gram_reduce_kernel");
 }
 

@@ -78,6 +78,8 @@ int gemm(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const doub
          const double *b, int64_t ldb, double beta, double *c, int64_t ldc, cudaStream_t st);
 int potrf(int64_t n, double *g, int64_t ldg, int64_t *failure_index, Workspace &ws, cudaStream_t st);
 // C = alpha op(A) B + beta C with K split into `splits` slices summed in order
+int gemm_fill(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const double *a, int64_t lda,
+              const double *b, int64_t ldb, double beta, double *c, int64_t ldc, Workspace &ws, cudaStream_t st);
 int gemm_splitk(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const double *a, int64_t lda,
                 const double *b, int64_t ldb, double beta, double *c, int64_t ldc, int64_t splits, Workspace &ws,
                 cudaStream_t st);

@@ -65,10 +65,21 @@ int trtri_diag_blocks(int64_t k, const double *r, int64_t ldr, double *dinv, cud
     return check_launch("trtri_diag_kernel");
 }
 
+// A level's GEMM: batched over the pairs when that fills the GPU, else pair by
+// pair with split-K (the top levels have one or two large pairs).
+static int level_gemm(const GemmArgs &P, Workspace &ws, cudaStream_t st) {
+    const int64_t tiles = ((P.M + 63) / 64) * ((P.N + 127) / 128);
+    if (P.batch * tiles >= num_sms() || P.K < 256) return gemm_ex(false, P, 1, st);
+    for (int64_t p = 0; p < P.batch; ++p)
+        CQ_TRY(gemm_fill(false, P.M, P.N, P.K, P.alpha, P.A + p * P.bs_a, P.lda, P.B + p * P.bs_b, P.ldb, P.beta,
+                         P.Cout + p * P.bs_c, P.ldc, ws, st));
+    return 0;
+}
+
 // One level: pairs p = p0 .. p0+np-1 of s-blocks, C of size cs (cs == s
 // except for a ragged last pair). t: s x s scratch per pair.
 static int trtri_level(int64_t s, int64_t cs, int64_t p0, int64_t np, const double *r, int64_t ldr, double *x,
-                       int64_t ldx, double *t, cudaStream_t st) {
+                       int64_t ldx, double *t, Workspace &ws, cudaStream_t st) {
     const int64_t o = 2 * s * p0;
     GemmArgs P{};
     // T_p = A_p^{-1} B_p  (s x cs, K = s)
@@ -89,7 +100,7 @@ static int trtri_level(int64_t s, int64_t cs, int64_t p0, int64_t np, const doub
     P.bs_a = 2 * s * (ldx + 1);
     P.bs_b = 2 * s * (ldr + 1);
     P.bs_cin = P.bs_c = s * s;
-    CQ_TRY(gemm_ex(false, P, 1, st));
+    CQ_TRY(level_gemm(P, ws, st));
     // X[o:o+s, o+s:o+s+cs] = -T_p C_p^{-1}  (s x cs, K = cs)
     GemmArgs Q{};
     Q.M = s;
@@ -109,7 +120,7 @@ static int trtri_level(int64_t s, int64_t cs, int64_t p0, int64_t np, const doub
     Q.bs_a = s * s;
     Q.bs_b = 2 * s * (ldx + 1);
     Q.bs_cin = Q.bs_c = 2 * s * (ldx + 1);
-    return gemm_ex(false, Q, 1, st);
+    return level_gemm(Q, ws, st);
 }
 
 int trtri_upper(int64_t k, const double *r, int64_t ldr, double *x, int64_t ldx, Workspace &ws, cudaStream_t st) {
@@ -126,10 +137,10 @@ int trtri_upper(int64_t k, const double *r, int64_t ldr, double *x, int64_t ldx,
     }
     for (int64_t s = kTB; s < k; s *= 2) {
         const int64_t full = k / (2 * s);  // pairs with a full C block
-        if (full > 0) CQ_TRY(trtri_level(s, s, 0, full, r, ldr, x, ldx, t, st));
+        if (full > 0) CQ_TRY(trtri_level(s, s, 0, full, r, ldr, x, ldx, t, ws, st));
         const int64_t o = 2 * s * full;
         const int64_t cs = k - o - s;  // ragged last pair
-        if (cs > 0) CQ_TRY(trtri_level(s, cs, full, 1, r, ldr, x, ldx, t, st));
+        if (cs > 0) CQ_TRY(trtri_level(s, cs, full, 1, r, ldr, x, ldx, t, ws, st));
     }
     return 0;
 }
