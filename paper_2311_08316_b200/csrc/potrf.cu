@@ -8,6 +8,7 @@
 // of the upper triangle. After a failure, later launches see the device flag
 // and exit, so the leading block is exactly what was computed before it.
 #include "common.cuh"
+#include "gemm.cuh"
 #include "internal.hh"
 
 namespace cqg {
@@ -157,27 +158,67 @@ int zero_strict_lower(int64_t n, double *a, int64_t lda, cudaStream_t st) {
     return check_launch("zero_strict_lower");
 }
 
+// One-block lookahead on two streams. Step jb: diag(jb), panel(jb) and C1(jb)
+// = the update of row block jb+1 (G[t0:t1, t0:] -= P[:, :nb1]^T P) run on the
+// aux stream; C2(jb) = the rest of the trailing update (rows >= t1) runs on
+// the caller's stream, so diag(jb+1) and panel(jb+1) overlap it. C1(jb+1)
+// waits for C2(jb) (both touch row block jb+2). Every entry still receives
+// its updates in block order, so the factor is unchanged.
 int potrf(int64_t n, double *g, int64_t ldg, int64_t *failure_index, Workspace &ws, cudaStream_t st) {
     *failure_index = 0;
     if (n <= 0) return 0;
     int64_t *fail = ws.get<int64_t>("potrf.fail", 1);
     if (!fail) return fail_nomem("potrf workspace");
+    static thread_local cudaStream_t aux = nullptr;
+    static thread_local cudaEvent_t ev_in = nullptr, ev_c1 = nullptr, ev_c2 = nullptr;
+    if (!aux) {
+        CQ_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking), "potrf aux stream");
+        CQ_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming), "potrf event");
+        CQ_CUDA(cudaEventCreateWithFlags(&ev_c1, cudaEventDisableTiming), "potrf event");
+        CQ_CUDA(cudaEventCreateWithFlags(&ev_c2, cudaEventDisableTiming), "potrf event");
+    }
     CQ_CUDA(cudaMemsetAsync(fail, 0, sizeof(int64_t), st), "memset fail");
+    CQ_CUDA(cudaEventRecord(ev_in, st), "potrf record");
+    CQ_CUDA(cudaStreamWaitEvent(aux, ev_in, 0), "potrf wait");
     for (int64_t j0 = 0; j0 < n; j0 += kPB) {
         const int64_t nb = std::min<int64_t>(kPB, n - j0);
-        potrf_diag_kernel<<<1, 32, 0, st>>>(n, g, ldg, j0, fail);
+        potrf_diag_kernel<<<1, 32, 0, aux>>>(n, g, ldg, j0, fail);
         note_launch();
         const int64_t rest = n - j0 - nb;
-        if (rest > 0) {
-            potrf_panel_kernel<<<(unsigned)((rest + kPanelWarps - 1) / kPanelWarps), kPanelWarps * 32, 0, st>>>(
-                n, g, ldg, j0, fail);
-            note_launch();
-            // G[t0:, t0:] -= P^T P, P = R[j0:j0+nb, t0:]
-            const int64_t t0 = j0 + nb;
-            CQ_TRY(gemm_tn_upper(rest, nb, -1.0, g + t0 * ldg + j0, ldg, g + t0 * ldg + j0, ldg, 1.0,
-                                 g + t0 * ldg + t0, ldg, fail, st));
+        if (rest <= 0) break;
+        potrf_panel_kernel<<<(unsigned)((rest + kPanelWarps - 1) / kPanelWarps), kPanelWarps * 32, 0, aux>>>(
+            n, g, ldg, j0, fail);
+        note_launch();
+        const int64_t t0 = j0 + nb, nb1 = std::min<int64_t>(kPB, rest), t1 = t0 + nb1;
+        if (j0 > 0) CQ_CUDA(cudaStreamWaitEvent(aux, ev_c2, 0), "potrf wait c2");  // C2(jb-1) -> row block jb+1
+        {  // C1: G[t0:t1, t0:n] -= P[:, 0:nb1]^T P, P = R[j0:j0+nb, t0:n]
+            GemmArgs P{};
+            P.M = nb1;
+            P.N = rest;
+            P.K = nb;
+            P.A = g + t0 * ldg + j0;
+            P.lda = ldg;
+            P.B = g + t0 * ldg + j0;
+            P.ldb = ldg;
+            P.Cin = g + t0 * ldg + t0;
+            P.ldcin = ldg;
+            P.Cout = g + t0 * ldg + t0;
+            P.ldc = ldg;
+            P.alpha = -1.0;
+            P.beta = 1.0;
+            P.skip_flag = fail;
+            CQ_TRY(gemm_ex(true, P, 1, aux));
+        }
+        CQ_CUDA(cudaEventRecord(ev_c1, aux), "potrf record c1");
+        if (rest > nb1) {  // C2: G[t1:, t1:] -= P[:, nb1:]^T P[:, nb1:] (upper)
+            CQ_CUDA(cudaStreamWaitEvent(st, ev_c1, 0), "potrf wait c1");  // panel(jb) done
+            CQ_TRY(gemm_tn_upper(rest - nb1, nb, -1.0, g + t1 * ldg + j0, ldg, g + t1 * ldg + j0, ldg, 1.0,
+                                 g + t1 * ldg + t1, ldg, fail, st));
+            CQ_CUDA(cudaEventRecord(ev_c2, st), "potrf record c2");
         }
     }
+    CQ_CUDA(cudaEventRecord(ev_c1, aux), "potrf record end");
+    CQ_CUDA(cudaStreamWaitEvent(st, ev_c1, 0), "potrf join");
     CQ_TRY(check_launch("potrf kernels"));
     CQ_CUDA(cudaMemcpyAsync(failure_index, fail, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "fail d2h");
     CQ_CUDA(cudaStreamSynchronize(st), "potrf sync");
