@@ -73,6 +73,36 @@ __global__ void __launch_bounds__(kThreads, 3) dgemm_kernel(GemmArgs P) {
         const int64_t k0 = kbeg + (int64_t)kc * kBK;
         double *as = As0 + s * BM * kBK;
         double *bs = Bs0 + s * BN * kBK;
+        if (P.vec16) {  // element pairs (16-byte copies; the swizzles keep pairs adjacent)
+            if (!TA) {  // A tile [k][m]: pairs along m
+#pragma unroll
+                for (int it = 0; it < BM * kBK / 2 / kThreads; ++it) {
+                    const int q = it * kThreads + tid;
+                    const int kk = q / (BM / 2), mm = (q % (BM / 2)) * 2;
+                    const bool ok = (r0 + mm < P.M) && (k0 + kk < kend);
+                    const double *src = P.A + za + (ok ? (k0 + kk) * P.lda + r0 + mm : 0);
+                    cp_async16_zfill(as + sw_km<BM>(kk, mm), src, ok ? (r0 + mm + 1 < P.M ? 16 : 8) : 0);
+                }
+            } else {  // A^T tile [m][k]: pairs along k
+#pragma unroll
+                for (int it = 0; it < BM * kBK / 2 / kThreads; ++it) {
+                    const int q = it * kThreads + tid;
+                    const int mm = q / (kBK / 2), kk = (q % (kBK / 2)) * 2;
+                    const bool ok = (r0 + mm < P.M) && (k0 + kk < kend);
+                    const double *src = P.A + za + (ok ? (r0 + mm) * P.lda + k0 + kk : 0);
+                    cp_async16_zfill(as + sw_rk(mm, kk), src, ok ? (k0 + kk + 1 < kend ? 16 : 8) : 0);
+                }
+            }
+#pragma unroll
+            for (int it = 0; it < BN * kBK / 2 / kThreads; ++it) {  // B tile [n][k]: pairs along k
+                const int q = it * kThreads + tid;
+                const int nn = q / (kBK / 2), kk = (q % (kBK / 2)) * 2;
+                const bool ok = (c0 + nn < P.N) && (k0 + kk < kend);
+                const double *src = P.B + zb + (ok ? (c0 + nn) * P.ldb + k0 + kk : 0);
+                cp_async16_zfill(bs + sw_rk(nn, kk), src, ok ? (k0 + kk + 1 < kend ? 16 : 8) : 0);
+            }
+            return;
+        }
         if (!TA) {  // A: M x K col-major, tile [k][m]
 #pragma unroll
             for (int it = 0; it < BM * kBK / kThreads; ++it) {
@@ -209,6 +239,11 @@ int gemm_ex(bool trans_a, GemmArgs P, int64_t splits, cudaStream_t st) {
     }
     const bool tall = P.N <= 64;
     const int BM = tall ? 128 : 64, BN = tall ? 64 : 128;
+    {  // 16-byte staging: 16-byte aligned operands, even strides and split starts
+        auto al = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+        P.vec16 = al(P.A) && al(P.B) && P.lda % 2 == 0 && P.ldb % 2 == 0 &&
+                  (P.batch <= 1 || (P.bs_a % 2 == 0 && P.bs_b % 2 == 0)) && (splits <= 1 || P.k_per_split % 2 == 0);
+    }
     dim3 grid;
     if (P.tiles) grid = dim3((unsigned)P.ntiles_part, 1, (unsigned)splits);
     else grid = dim3((unsigned)((P.M + BM - 1) / BM), (unsigned)((P.N + BN - 1) / BN), (unsigned)splits);
