@@ -33,6 +33,9 @@ def main(path, start="saso_plan_kernel"):
     for n, (c, v) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         print(f"{n[:58]:58s} {c:4d} {v / 1e3:10.1f} us {100 * v / tot:5.1f}%")
     print(f"{'total':58s} {sum(c for c, _ in agg.values()):4d} {tot / 1e3:10.1f} us")
+    ours = [(c, v) for n, (c, v) in agg.items() if n.startswith("cqg::")]
+    print(f"{'ours (cqg::, excludes the harness setup kernels)':58s} {sum(c for c, _ in ours):4d} "
+          f"{sum(v for _, v in ours) / 1e3:10.1f} us")
 
 
 if __name__ == "__main__":

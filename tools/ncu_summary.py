@@ -29,6 +29,8 @@ KEYS = [
     "launch__grid_size",
     "launch__block_size",
     "launch__occupancy_limit_registers",
+    "smsp__inst_executed.sum",
+    "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
 ]
 
 
@@ -46,17 +48,18 @@ def rows(rep):
         for k in KEYS:
             if k in d and d[k] != "":
                 item[k] = f"{d[k]} {u.get(k, '')}".strip()
-        stalls = []
+        stalls = []  # warps stalled per issued instruction, by reason
         for k, v in d.items():
-            if "average_warp_latency_issue_stalled" in k or (
-                    "warps_issue_stalled" in k and k.endswith("per_warp_active.pct")):
+            if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
+                reason = k[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]
+                if reason in ("selected",):
+                    continue
                 try:
-                    stalls.append((float(v.replace(",", "")), k))
+                    stalls.append((float(v.replace(",", "")), reason))
                 except ValueError:
                     pass
         stalls.sort(reverse=True)
-        item["top_stalls"] = {k.split("stalled_")[-1].split(".")[0].replace("_per_warp_active", ""): round(v, 2)
-                              for v, k in stalls[:6]}
+        item["top_stalls_per_issue"] = {r: round(v, 3) for v, r in stalls[:6]}
         res.append(item)
     return res
 
