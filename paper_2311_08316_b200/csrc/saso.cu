@@ -7,35 +7,58 @@
 //
 // Data layout in HBM
 //   plan   uint32[m_local * nnz]      row | sign<<31 (sign 1 = +1/sqrt(d))
-//   tptr   uint16[ntiles * tstride]   per 128-row tile: entry offsets by sketch row
-//                                     (tstride = d+1 rounded up to even: 4-byte aligned slices)
-//   tent   uint32[ntiles * 128*nnz]   per tile, entries sorted by (row, c):
-//                                     negative<<31 | (row % A)<<16 | byte offset
-//                                     of A(c_local, 0) in the staged tile (c*264)
+//   tinfo  uint2[ntiles * nbs]        per 256-row tile, 32 slots per CTA row block
+//                                     (slot w < 28: consumer warp w's A rows):
+//                                     (first entry index, mask of its rows that
+//                                     have entries in the tile)
+//   tent   uint32[ntiles * entw]      per tile, entries sorted by (row, c):
+//                                     byte offset of A(c_local, 0) in the staged
+//                                     tile (c * 264) << 15 | last-of-row << 8 |
+//                                     negative (-1/sqrt(d)) << 0
 //   part   double[S][d][n]            per c-split partial sketches, row-major
 //   Msk    double d x n column-major  fixed-order sum of the partials
 //
-// Apply kernel: one CTA = 32 columns (lane = column) x 32*A sketch rows (A
-// register accumulators per lane; warp w owns rows w*A .. w*A+A-1) x a
-// contiguous range of row tiles. Each 128 x 32 tile of A is staged ([c][33]
-// padded: conflict-free warp reads of a 256-byte row) through a 5-stage
-// cp.async pipeline with the tile's CSR slice. A warp walks its rows' entries
-// (contiguous, row-sorted, c ascending per row) once and sends each to its
-// row's accumulator through a jump table on the row % A stored in the entry:
-// acc = fma(v, A(c, j), acc) per entry in c order is the reference's own FMA
-// chain per output entry (sketch.cc:137-143), so one c-split is bit-identical.
+// Apply kernel: one CTA = 32 columns (lane = column) x 28*A sketch rows x a
+// contiguous range of 256-row tiles. Warps 0..27 own A sketch rows each (A
+// register accumulators per lane); warps 28..31 (one per SM sub-partition)
+// only stage: each 256 x 32 tile of A ([c][33] padded: conflict-free 8-byte
+// cp.async writes of a 256-byte column run, conflict-free warp reads of a
+// 256-byte row), the tile's entry list and the CTA's 32 block words go through
+// a ring of up to 3 stages driven by mbarriers ("full": cp.async arrivals of
+// the producer lanes; "empty": one arrival per consumer warp). Consumers never
+// wait for each other, only for data, so the per-tile imbalance of their entry
+// counts (Poisson per warp and tile) averages out over the ring.
+//
+// Entry word: byte offset of A(c, 0) in the staged tile << 15 | last-of-row
+// << 8 | negative. Per entry a consumer issues LDS (next word, broadcast),
+// LEA.HI (x address), LDS.64 x, IMAD (adds sign * 2^31 to x's hi word: x -> -x
+// exactly), DFMA with the constant 1/sqrt(d), flag test + branch; the loop is
+// unrolled by two so no word rotates between registers. Rows with no entry in
+// the tile cost one test of a warp-uniform mask (REDUX). acc = fma(+-v, A(c,
+// j), acc) per entry in c order is the reference's own FMA chain per output
+// entry (sketch.cc:137-143), so one c-split is bit-identical.
+//
+// Bound: per entry two shared-memory wavefronts for x (256 B row read) and
+// one for the word; per tile 528 for the staging writes, repeated by every
+// row block. The x reads alone are 8 bytes of shared-memory traffic per FMA,
+// nnz = 8 times the HBM bytes of A, against ~5.5x more shared-memory than HBM
+// bandwidth: this kernel cannot reach the HBM roofline whatever its issue
+// efficiency.
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "internal.hh"
 
 namespace cqg {
 
-constexpr int kTileRows = 128;  // rows of A per CSR tile
-constexpr int kApplyWarps = 32;  // 1024 threads: short per-warp entry chains, 8 warps per scheduler
+constexpr int kTileRows = 256;  // rows of A per tile (one entry list per tile)
+constexpr int kApplyWarps = 32;  // 1024 threads: 8 warps per scheduler hide the shared-memory latency of each entry
 constexpr int kApplyThreads = kApplyWarps * 32;
-constexpr int kApplyStages = 5;
+constexpr int kProducers = 4;  // warps 28..31 (one per SM sub-partition) stage the tiles
+constexpr int kConsumers = kApplyWarps - kProducers;  // warps 0..27 own sketch rows
 constexpr int kXLD = 33;        // staged tile row stride (doubles)
+constexpr uint32_t kEntLast = 0x100u;  // entry flag: last entry of its row in the tile
 constexpr uint64_t kSasoSalt = 0x7361736fULL;  // sketch.cc:19
 
 // ---------------------------------------------------------------------------
@@ -70,15 +93,15 @@ __global__ void saso_plan_kernel(int64_t d, int64_t c0, int64_t count, int nnz, 
 }
 
 // ---------------------------------------------------------------------------
-// Per-tile CSR by sketch row (stable: c ascending within a row).
-// One CTA per tile; histogram + scan by the block, ordered scatter by warp 0.
+// Per-tile entry lists by sketch row (stable: c ascending within a row) and
+// the per-block words. One CTA per tile; histogram + scan by the block,
+// ordered scatter by warp 0.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d, int64_t tstride, int nnz, int A,
+__global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d, int nnz, int A, int nbs, int entw,
                                                             const uint32_t *__restrict__ plan,
-                                                            uint16_t *__restrict__ tptr,
-                                                            uint32_t *__restrict__ tent) {
-    extern __shared__ int32_t s_cnt[];  // d + 1 counters, then d cursors
-    int32_t *s_cur = s_cnt + (d + 1);
+                                                            uint2 *__restrict__ tinfo, uint32_t *__restrict__ tent) {
+    extern __shared__ int32_t s_beg[];  // d + 1 counters -> row begins (s_beg[d] = entries)
+    int32_t *s_cur = s_beg + (d + 1);   // d scatter cursors
     __shared__ int32_t s_part[256 / 32 + 1];
     const int64_t tile = blockIdx.x;
     const int64_t row0 = tile * kTileRows;
@@ -86,15 +109,15 @@ __global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d
     const int nent = rows * nnz;
     const uint32_t *tp = plan + row0 * nnz;
 
-    for (int64_t r = threadIdx.x; r <= d; r += blockDim.x) s_cnt[r] = 0;
+    for (int64_t r = threadIdx.x; r <= d; r += blockDim.x) s_beg[r] = 0;
     __syncthreads();
-    for (int e = threadIdx.x; e < nent; e += blockDim.x) atomicAdd(&s_cnt[tp[e] & 0x7fffffffu], 1);
+    for (int e = threadIdx.x; e < nent; e += blockDim.x) atomicAdd(&s_beg[tp[e] & 0x7fffffffu], 1);
     __syncthreads();
     // exclusive scan over d counters: each thread scans a contiguous chunk
     const int64_t per = (d + blockDim.x - 1) / blockDim.x;
     const int64_t lo = threadIdx.x * per, hi = cmin<int64_t>(lo + per, d);
     int32_t run = 0;
-    for (int64_t r = lo; r < hi; ++r) run += s_cnt[r];
+    for (int64_t r = lo; r < hi; ++r) run += s_beg[r];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int32_t incl = run;
 #pragma unroll
@@ -114,18 +137,32 @@ __global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d
     }
     __syncthreads();
     int32_t base = s_part[wid] + incl - run;
-    uint16_t *optr = tptr + tile * tstride;
     for (int64_t r = lo; r < hi; ++r) {
-        int32_t c = s_cnt[r];
+        const int32_t c = s_beg[r];
+        s_beg[r] = base;
         s_cur[r] = base;
-        optr[r] = (uint16_t)base;
         base += c;
     }
-    if (threadIdx.x == 0) optr[d] = (uint16_t)nent;
+    if (threadIdx.x == 0) s_beg[d] = nent;
     __syncthreads();
+    // block words: (first entry, rows of the block that have entries)
+    uint2 *oinfo = tinfo + tile * (int64_t)nbs;
+    for (int sl = threadIdx.x; sl < nbs; sl += blockDim.x) {  // slot = CTA row block * 32 + warp
+        const int w = sl % kApplyWarps;
+        const int64_t rb = ((int64_t)(sl / kApplyWarps) * kConsumers + w) * A;
+        uint2 word = make_uint2((uint32_t)nent, 0u);
+        if (w < kConsumers && rb < d) {
+            uint32_t mask = 0;
+            for (int q = 0; q < A && rb + q < d; ++q)
+                if (s_beg[rb + q + 1] > s_beg[rb + q]) mask |= 1u << q;
+            word = make_uint2((uint32_t)s_beg[rb], mask);
+        }
+        oinfo[sl] = word;
+    }
+    uint32_t *oent = tent + tile * (int64_t)entw;
+    for (int e = nent + threadIdx.x; e < entw; e += blockDim.x) oent[e] = 0;  // prefetch overrun pad
     // ordered scatter: entry e = c_local*nnz + t, processed in ascending e
     if (wid == 0) {
-        uint32_t *oent = tent + tile * (int64_t)(kTileRows * nnz);
         const unsigned lt = (1u << lane) - 1u;
         for (int b = 0; b < nent; b += 32) {
             int e = b + lane;
@@ -139,13 +176,60 @@ __global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d
             __syncwarp();
             if (valid) {
                 const uint32_t c_local = (uint32_t)(e / nnz);
-                oent[pos] = (~w & 0x80000000u) | ((r % (uint32_t)A) << 16) | (c_local * kXLD * 8u);  // bit 31: -1/sqrt(d)
+                const uint32_t neg = (~w >> 31) & 1u;  // plan bit 31 clear: -1/sqrt(d)
+                const uint32_t last = (pos == s_beg[r + 1] - 1) ? kEntLast : 0u;
+                oent[pos] = ((c_local * kXLD * 8u) << 15) | last | neg;
                 // highest-ranked member advances the cursor
                 if (rank == __popc(grp & act) - 1) s_cur[r] += __popc(grp & act);
             }
             __syncwarp();
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// mbarrier helpers (CTA scope)
+// ---------------------------------------------------------------------------
+CQ_DEVI void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+CQ_DEVI void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+// arrives when every cp.async this thread issued before it has landed
+CQ_DEVI void cp_async_mbar_arrive(uint32_t bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+// blocking wait: the suspend-time hint lets the thread sleep until the phase
+// completes instead of spinning on issue slots
+CQ_DEVI void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "MBAR_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
+        "@!p bra MBAR_WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+CQ_DEVI uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+CQ_DEVI uint2 lds_u32x2(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+    return v;
+}
+CQ_DEVI double lds_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a) : "memory");
+    return v;
+}
+CQ_DEVI void cp_async8_s(uint32_t s, const void *gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -156,21 +240,22 @@ struct ApplyArgs {
     const double *a;
     double val;
     int nnz;
-    int ptrw, entw;         // 32-bit words per stage for pointers / entries
-    int64_t tstride;        // tptr elements per tile (even)
+    int entw;    // 32-bit entry words per tile (16-byte multiple, >= kTileRows*nnz + 2)
+    int nbs;     // block words per tile (whole CTAs of kApplyWarps)
+    int stages;  // ring depth (2..4, as many as fit)
     int64_t ntiles, tiles_per_split;
-    const uint16_t *tptr;
+    const uint2 *tinfo;
     const uint32_t *tent;
     double *part;
 };
 
+constexpr uint32_t kTileBytes = kTileRows * kXLD * 8;  // 67584
+constexpr uint32_t kInfoBytes = kApplyWarps * 8;       // one (start, mask) word pair per warp
+
 template <int A>
 __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs P) {
-    constexpr int RB = kApplyWarps * A;
+    constexpr int RB = kConsumers * A;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int stage_words = 2 * kTileRows * kXLD + P.ptrw + P.entw;  // 32-bit words per stage
-    uint32_t *stage0 = reinterpret_cast<uint32_t *>(smem_raw);
-
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int64_t j0 = (int64_t)blockIdx.x * 32;
     const int64_t r0 = (int64_t)blockIdx.y * RB;
@@ -178,110 +263,126 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
     const int64_t t_begin = split * P.tiles_per_split;
     const int64_t t_end = cmin<int64_t>(t_begin + P.tiles_per_split, P.ntiles);
     const int rows_here = (int)cmin<int64_t>(RB, P.d - r0);  // valid sketch rows in this block
+    const int S = P.stages;
 
+    // shared layout: S tiles | S entry lists | S info blocks | S full + S empty mbarriers
+    const uint32_t s_tiles = smem_u32(smem_raw);
+    const uint32_t ent_bytes = (uint32_t)P.entw * 4u;
+    const uint32_t s_ents = s_tiles + (uint32_t)S * kTileBytes;
+    const uint32_t s_info = s_ents + (uint32_t)S * ent_bytes;
+    const uint32_t s_full = s_info + (uint32_t)S * kInfoBytes;
+    const uint32_t s_empty = s_full + (uint32_t)S * 8u;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(s_full + 8u * s, 32 * kProducers);  // the producer lanes (cp.async arrivals)
+            mbar_init(s_empty + 8u * s, kConsumers);  // one arrival per consumer warp
+        }
+    }
+    __syncthreads();
+    const int64_t ntl = t_end - t_begin;
+
+    if (wid >= kConsumers) {
+        // ---------------- producer warps: stage tile after tile, up to S ahead.
+        // Producer p copies columns p, p+4, ..., lane l rows l + 32k (k = 0..7):
+        // 256-byte coalesced runs, immediate offsets, one pointer step per column
+        const int pw = wid - kConsumers;
+        const int ncols = (int)cmin<int64_t>(32, P.n - j0);
+        const int64_t lda4 = kProducers * P.lda;
+        const int nent16 = P.entw / 4;
+        const double *a_tile = P.a + (j0 + pw) * P.lda + t_begin * kTileRows + lane;
+        const uint32_t *g_ent = P.tent + t_begin * (int64_t)P.entw;
+        const uint32_t *g_info =
+            reinterpret_cast<const uint32_t *>(P.tinfo + t_begin * P.nbs + (int64_t)blockIdx.y * kApplyWarps);
+        const int64_t full_tiles = P.m / kTileRows;  // tiles without rows past m
+        const int pl = pw * 32 + lane;                // producer lane 0..127
+        int stg = 0;
+        uint32_t use = 0;
+        for (int64_t i = 0; i < ntl; ++i) {
+            if (use) mbar_wait(s_empty + 8u * stg, (use - 1u) & 1u);  // consumers done with the stage's last tile
+            const uint32_t sb = s_tiles + (uint32_t)stg * kTileBytes + (uint32_t)lane * (kXLD * 8u);
+            const double *pa = a_tile;
+            if (t_begin + i < full_tiles) {
+                for (int j = pw; j < ncols; j += kProducers) {
+#pragma unroll
+                    for (int k = 0; k < kTileRows / 32; ++k)
+                        cp_async8_s(sb + 8u * (uint32_t)j + (uint32_t)(k * 32 * kXLD * 8), pa + 32 * k);
+                    pa += lda4;
+                }
+            } else {  // the ragged last tile
+                const int64_t rem = P.m - (t_begin + i) * kTileRows;
+                for (int j = pw; j < ncols; j += kProducers) {
+#pragma unroll
+                    for (int k = 0; k < kTileRows / 32; ++k)
+                        if (lane + 32 * k < rem)
+                            cp_async8_s(sb + 8u * (uint32_t)j + (uint32_t)(k * 32 * kXLD * 8), pa + 32 * k);
+                    pa += lda4;
+                }
+            }
+            if (pl < (int)(kInfoBytes / 16)) cp_async16_s(s_info + (uint32_t)stg * kInfoBytes + 16u * pl, g_info + 4 * pl);
+            const uint32_t se = s_ents + (uint32_t)stg * ent_bytes;
+            for (int w = pl; w < nent16; w += 32 * kProducers) cp_async16_s(se + 16u * (uint32_t)w, g_ent + 4 * w);
+            cp_async_mbar_arrive(s_full + 8u * stg);
+            a_tile += kTileRows;
+            g_ent += P.entw;
+            g_info += 2 * P.nbs;
+            if (++stg == S) stg = 0, ++use;
+        }
+        return;
+    }
+
+    // ---------------- consumer warps
     double acc[A];
 #pragma unroll
     for (int q = 0; q < A; ++q) acc[q] = 0.0;
-
-    // staging map: thread -> tile row cc, columns jj0 + kCS*it. Addresses and
-    // column bounds are fixed per thread; a tile only moves the row.
-    constexpr int kCS = kApplyThreads / kTileRows;         // column stride (8)
-    constexpr int kIters = kTileRows * 32 / kApplyThreads;  // copies per thread (4)
-    static_assert(kCS * kIters == 32, "staging covers the 32 columns");
-    const int cc = tid % kTileRows, jj0 = tid / kTileRows;
-    const int64_t ldas = kCS * P.lda;
-    unsigned colok = 0;
-#pragma unroll
-    for (int it = 0; it < kIters; ++it) colok |= (j0 + jj0 + kCS * it < P.n) ? (1u << it) : 0u;
-    const double *src0 = P.a + (j0 + jj0) * P.lda + cc;  // column j0+jj0, row cc of tile 0
-    const int ent_words = kTileRows * P.nnz;
-    // shared byte addresses within a stage, fixed per thread
-    const uint32_t s_stage0 = smem_u32(stage0), stage_bytes = (uint32_t)stage_words * 4u;
-    const uint32_t a_off = (uint32_t)(cc * kXLD + jj0) * 8u;
-    const uint32_t ptr_off = (uint32_t)(2 * kTileRows * kXLD) * 4u, ent_off = ptr_off + (uint32_t)P.ptrw * 4u;
-    const int nwp = (rows_here + 2) / 2;  // words holding tptr[tile][r0 .. r0 + rows_here] (r0 even)
-    const uint32_t *tpw = reinterpret_cast<const uint32_t *>(P.tptr + r0);
-    const int64_t tsw = P.tstride / 2;
-    const int nent16 = ent_words / 4;     // 16-byte copies of the tile's entries
-    const double *srcA[kIters];  // row cc of tile 0 in this thread's columns (A itself if out of range)
-#pragma unroll
-    for (int it = 0; it < kIters; ++it) srcA[it] = ((colok >> it) & 1u) ? src0 + it * ldas : P.a;
-    auto issue = [&](int64_t tile, int stg) {
-        const uint32_t sb = s_stage0 + (uint32_t)stg * stage_bytes;
-        const int64_t row0 = tile * kTileRows;
-        const unsigned ok = (row0 + cc < P.m) ? colok : 0u;  // zero fill past m / n
-#pragma unroll
-        for (int it = 0; it < kIters; ++it)
-            cp_async8_zfill_s(sb + a_off + (uint32_t)(it * kCS * 8), srcA[it] + (ok ? row0 : 0),
-                              ((ok >> it) & 1u) ? 8 : 0);
-        if (tid < nwp) cp_async4_s(sb + ptr_off + 4u * (uint32_t)tid, tpw + tile * tsw + tid);
-        const uint32_t *ge = P.tent + tile * (int64_t)ent_words;
-        if (nent16 <= kApplyThreads) {  // nnz <= 32: one 16-byte copy per thread at most
-            if (tid < nent16) cp_async16_s(sb + ent_off + 16u * (uint32_t)tid, ge + 4 * tid);
-        } else {
-            for (int w = tid; w < nent16; w += kApplyThreads)
-                cp_async16_s(sb + ent_off + 16u * (uint32_t)w, ge + 4 * w);
-        }
+    int stg = 0;
+    uint32_t use = 0;  // how many times this stage has been filled before the current tile
+    const double v = P.val;
+    const uint32_t lane_x = s_tiles + 8u * (uint32_t)lane;
+    // x with the entry's sign applied: bit 0 of the entry is 1 for -1/sqrt(d);
+    // adding cur * 2^31 flips bit 63 of x exactly when it is set, and
+    // fma(v, -x, s) == fma(-v, x, s) bit for bit
+    auto signed_x = [](double x, uint32_t cur) {
+        return __hiloint2double((int)((uint32_t)__double2hiint(x) + cur * 0x80000000u), __double2loint(x));
     };
-    // Two tiles per CTA barrier (a warp's share of entries varies tile to
-    // tile; pairing halves the barriers and averages the imbalance), three
-    // more in flight: stages hold tiles modulo kApplyStages.
-    constexpr int kPair = 2, kAhead = kApplyStages - kPair;
-    for (int s = 0; s < kAhead; ++s) {
-        if (t_begin + s < t_end) issue(t_begin + s, s);
-        cp_async_commit();
-    }
-    int stg_next = kAhead % kApplyStages, stg_cur = 0;  // stage of the next tile to issue / to process
-    // x with the entry's sign bit (bit 31 = negative) XORed into its sign:
-    // fma(v, x, s) == fma(|v|, +-x, s) exactly
-    auto flip = [](double x, uint32_t w) {
-        return __hiloint2double(__double2hiint(x) ^ (int)(w & 0x80000000u), __double2loint(x));
-    };
-    const int wr0 = wid * A;  // this warp's first row (local)
-    for (int64_t t0 = t_begin; t0 < t_end; t0 += kPair) {
-        cp_async_wait<kAhead - kPair>();
-        __syncthreads();  // tiles t0, t0+1 visible; the previous pair's stages are free
-#pragma unroll
-        for (int u = 0; u < kPair; ++u) {
-            const int64_t nt = t0 + kAhead + u;
-            if (nt < t_end) issue(nt, stg_next);
-            cp_async_commit();
-            stg_next = (stg_next + 1 == kApplyStages) ? 0 : stg_next + 1;
-        }
-        const int stg_pair = stg_cur;
-        stg_cur = (stg_cur + kPair) % kApplyStages;
-        if (wr0 >= rows_here) continue;
-#pragma unroll
-        for (int u = 0; u < kPair; ++u) {
-            const int64_t tile = t0 + u;
-            if (tile >= t_end) break;
-            const int stg = (stg_pair + u >= kApplyStages) ? stg_pair + u - kApplyStages : stg_pair + u;
-            const uint32_t *sw = stage0 + (size_t)stg * stage_words;
-            const char *xb = reinterpret_cast<const char *>(reinterpret_cast<const double *>(sw) + lane);
-            const uint16_t *sp = reinterpret_cast<const uint16_t *>(sw + 2 * kTileRows * kXLD);
-            const uint32_t *se = sw + 2 * kTileRows * kXLD + P.ptrw;
-            // the warp's entries: contiguous, row-sorted (row % A in bits 16..20),
-            // c ascending within a row. The next entry's word is always in a
-            // register, so an empty row costs a compare.
-            const int ee = sp[min(wr0 + A, rows_here)];
-            int e = sp[wr0];
-            constexpr uint32_t kEnd = 31u << 16;  // sentinel: matches no row
-            uint32_t w = e < ee ? se[e] : kEnd;
+    for (int64_t i = 0; i < ntl; ++i) {
+        mbar_wait(s_full + 8u * stg, use & 1u);
+        const uint2 info = lds_u32x2(s_info + (uint32_t)stg * kInfoBytes + 8u * (uint32_t)wid);
+        const uint32_t mask = __reduce_or_sync(0xffffffffu, info.y);  // warp-uniform
+        if (mask) {
+            // The warp's entries: rows ascending, c ascending within a row,
+            // the last entry of each row flagged. The loop is unrolled by two
+            // (cur / nxt swap roles) so no word rotates between registers.
+            uint32_t pe = s_ents + (uint32_t)stg * ent_bytes + 4u * info.x;
+            const uint32_t xb = lane_x + (uint32_t)stg * kTileBytes;
+            uint32_t cur = lds_u32(pe);
+            pe += 4u;
 #pragma unroll
             for (int q = 0; q < A; ++q) {  // row wr0+q: its entries in c order (sketch.cc:137-143)
-                double sq = acc[q];
-                while (((w >> 16) & 31u) == (uint32_t)q) {
-                    const double x = flip(*reinterpret_cast<const double *>(xb + (w & 0xffffu)), w);
-                    ++e;
-                    w = e < ee ? se[e] : kEnd;
-                    sq = fma(P.val, x, sq);  // sketch.cc:142
+                if (mask & (1u << q)) {
+                    double sq = acc[q];
+                    for (;;) {
+                        const uint32_t nxt = lds_u32(pe);  // may be past the list: zero pad, in bounds
+                        sq = fma(v, signed_x(lds_f64(xb + (cur >> 15)), cur), sq);  // sketch.cc:142
+                        if (cur & kEntLast) {
+                            cur = nxt;
+                            pe += 4u;
+                            break;
+                        }
+                        cur = lds_u32(pe + 4u);
+                        pe += 8u;
+                        sq = fma(v, signed_x(lds_f64(xb + (nxt >> 15)), nxt), sq);
+                        if (nxt & kEntLast) break;
+                    }
+                    acc[q] = sq;
                 }
-                acc[q] = sq;
             }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_empty + 8u * stg);
+        if (++stg == S) stg = 0, ++use;
     }
-    cp_async_wait<0>();
     // write the partial: part[split][r][j]
+    const int wr0 = wid * A;
     const int64_t col = j0 + lane;
     if (col < P.n) {
         double *pp = P.part + split * P.d * P.n;
@@ -324,10 +425,13 @@ int saso_plan(int64_t d, int64_t c0, int64_t count, int64_t nnz, uint64_t seed, 
     return check_launch("saso_plan_kernel");
 }
 
-static size_t apply_smem(int rb, int nnz, int *ptrw, int *entw) {
-    *ptrw = ((rb + 2) / 2 + 1 + 3) & ~3;                // u16 pointers rb+1 from a 4-byte aligned start
-    *entw = (kTileRows * nnz + 3) & ~3;                 // u32 entries, 16-byte multiple
-    return sizeof(uint32_t) * (size_t)(2 * kTileRows * kXLD + *ptrw + *entw) * kApplyStages;
+static size_t apply_smem(int nnz, int *entw, int *nbs, int *stages, int64_t d, int A) {
+    *entw = (kTileRows * nnz + 2 + 3) & ~3;  // u32 entries + two prefetch overrun words, 16-byte multiple
+    const int64_t nb = (d + A - 1) / A;      // blocks of A sketch rows, kConsumers per CTA
+    *nbs = (int)(((nb + kConsumers - 1) / kConsumers) * kApplyWarps);  // 32 slots per CTA row block
+    const size_t per = kTileBytes + 4 * (size_t)*entw + kInfoBytes + 16;
+    *stages = (int)std::min<size_t>(6, (227 * 1024) / per);
+    return per * (size_t)*stages;
 }
 
 template <int A>
@@ -351,26 +455,31 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
     if (d > 32767 || nnz * kTileRows > 65535) return fail_internal("saso_sketch: d or nnz too large for the CSR");
     const int64_t ntiles = (m + kTileRows - 1) / kTileRows;
     uint32_t *plan = ws.get<uint32_t>("saso.plan", (size_t)(m * nnz));
-    const int64_t tstride = (d + 2) & ~(int64_t)1;  // d + 1 rounded up to even
-    uint16_t *tptr = ws.get<uint16_t>("saso.tptr", (size_t)(ntiles * tstride) + 2);
-    uint32_t *tent = ws.get<uint32_t>("saso.tent", (size_t)(ntiles * kTileRows * nnz) + 4);
-    if (!plan || !tptr || !tent) return fail_nomem("saso workspace");
+    if (!plan) return fail_nomem("saso workspace");
     int rc = saso_plan(d, c0, m, nnz, seed, plan, st);
     if (rc) return rc;
-    // Decomposition: RB = 32*A sketch rows per CTA (A register accumulators
-    // per lane). Exact order needs one pass over all rows per CTA, so
-    // parallelism comes from row blocks: minimise waves * (staging + RB).
+    // Decomposition: RB = 28*A sketch rows per CTA (A register accumulators
+    // per lane of each of the 28 consumer warps). Exact order needs one pass over all
+    // tiles per CTA, so parallelism comes from row blocks. Cost per 256-row
+    // tile and CTA (cycles) is the larger of the shared-memory wavefronts (528
+    // for the tile writes, three per entry: word + x, the entry list) and the
+    // issue slots (per consumer warp ~30 per tile and ~5 per row, ~7.5 per
+    // entry, ~500 for the producer warps, over 4 schedulers); minimise
+    // waves * that.
     const int64_t cgroups = (n + 31) / 32;
     const int sms = num_sms();
-    int A = 10;
+    int A = 12;
     if (!allow_split) {
-        const int cand[] = {10, 8, 6, 4, 2, 1};
+        const int cand[] = {12, 8, 6, 4, 2, 1};
         double best = 1e300;
         for (int a : cand) {
-            const int64_t rb = (int64_t)kApplyWarps * a;
+            const int64_t rb = (int64_t)kConsumers * a;
             const int64_t ctas = cgroups * ((d + rb - 1) / rb);
-            const double cost = (double)((ctas + sms - 1) / sms) * (128.0 + (double)std::min<int64_t>(rb, d));
-            if (cost < best) {
+            const double ents = (double)kTileRows * (double)nnz * (double)std::min<int64_t>(rb, d) / (double)d;
+            const double smem_c = 528.0 + 3.0 * ents + (double)kTileRows * (double)nnz / 32.0;
+            const double issue_c = (kConsumers * (30.0 + 5.0 * a) + 7.5 * ents + 500.0) / 4.0;
+            const double cost = (double)((ctas + sms - 1) / sms) * std::max(smem_c, issue_c);
+            if (cost < best * 0.999) {
                 best = cost;
                 A = a;
             }
@@ -378,15 +487,21 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
     }
     if (const char *ev = getenv("CQRRPT_SASO_A")) {  // experiments: force the row-block width
         const int fa = atoi(ev);
-        if (fa == 1 || fa == 2 || fa == 4 || fa == 6 || fa == 8 || fa == 10) A = fa;
+        if (fa == 1 || fa == 2 || fa == 4 || fa == 6 || fa == 8 || fa == 12) A = fa;
     }
-    const int64_t rblocks = (d + (int64_t)kApplyWarps * A - 1) / ((int64_t)kApplyWarps * A);
+    const int64_t rblocks = (d + (int64_t)kConsumers * A - 1) / ((int64_t)kConsumers * A);
+    int entw = 0, nbs = 0, stages = 0;
+    const size_t smem = apply_smem((int)nnz, &entw, &nbs, &stages, d, A);
+    if (stages < 2) return fail_internal("saso_apply: nnz too large for the staged entry lists");
+    uint2 *tinfo = ws.get<uint2>("saso.tinfo", (size_t)(ntiles * nbs) + 32);
+    uint32_t *tent = ws.get<uint32_t>("saso.tent", (size_t)(ntiles * entw) + 4);
+    if (!tinfo || !tent) return fail_nomem("saso workspace");
     size_t csr_smem = sizeof(int32_t) * (size_t)(2 * d + 2);
     if (csr_smem > 48 * 1024 &&
         cudaFuncSetAttribute(saso_tile_csr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csr_smem) !=
             cudaSuccess)
         return fail_cuda("csr smem attr");
-    saso_tile_csr_kernel<<<(unsigned)ntiles, 256, csr_smem, st>>>(m, d, tstride, (int)nnz, A, plan, tptr, tent);
+    saso_tile_csr_kernel<<<(unsigned)ntiles, 256, csr_smem, st>>>(m, d, (int)nnz, A, nbs, entw, plan, tinfo, tent);
     note_launch();
     if ((rc = check_launch("saso_tile_csr_kernel"))) return rc;
 
@@ -418,12 +533,12 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
     P.a = a;
     P.val = 1.0 / sqrt((double)d);  // sketch.cc:79
     P.nnz = (int)nnz;
-    const size_t smem = apply_smem(kApplyWarps * A, (int)nnz, &P.ptrw, &P.entw);
-    if (smem > 227 * 1024) return fail_internal("saso_apply: nnz too large for the staged CSR");
+    P.entw = entw;
+    P.nbs = nbs;
+    P.stages = stages;
     P.ntiles = ntiles;
     P.tiles_per_split = tps;
-    P.tptr = tptr;
-    P.tstride = tstride;
+    P.tinfo = tinfo;
     P.tent = tent;
     P.part = part;
     dim3 grid((unsigned)cgroups, (unsigned)rblocks, (unsigned)nsplit);
@@ -433,7 +548,7 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
         case 4: rc = launch_apply<4>(P, grid, smem, st); break;
         case 6: rc = launch_apply<6>(P, grid, smem, st); break;
         case 8: rc = launch_apply<8>(P, grid, smem, st); break;
-        default: rc = launch_apply<10>(P, grid, smem, st); break;
+        default: rc = launch_apply<12>(P, grid, smem, st); break;
     }
     if (rc) return rc;
     dim3 g((unsigned)((n + 31) / 32), (unsigned)((d + 31) / 32));
