@@ -75,10 +75,10 @@ CQ_DEVI double chain_sum(double s, const double *p, int64_t body64, int lane) {
 
 // lanes 0..3: (s0+s1)+(s2+s3), then the tail elements body..c-1 of a.b
 template <class FA, class FB>
-CQ_DEVI double chain_finish(double s, int64_t c, FA fa, FB fb) {
+CQ_DEVI double chain_finish(double s, int64_t c, FA fa, FB fb, unsigned quad = 0xfu) {
     const int64_t body = c & ~(int64_t)3;
-    double pair = s + __shfl_xor_sync(0xfu, s, 1);
-    double tot = pair + __shfl_xor_sync(0xfu, pair, 2);
+    double pair = s + __shfl_xor_sync(quad, s, 1);
+    double tot = pair + __shfl_xor_sync(quad, pair, 2);
     int64_t e = body, rem = c - body;
     if (rem >= 2) {
         tot = tot + fa(e) * fb(e);
@@ -201,6 +201,21 @@ CQ_DEVI void rec_wait(const unsigned long long *slot, uint32_t flag, double *v, 
     *phys = (int32_t)(uint32_t)w3;
 }
 
+// A flagged double (two 8-byte words: flag | hi, flag | lo), same protocol.
+CQ_DEVI void dbl_publish(unsigned long long *slot, uint32_t flag, double v) {
+    const unsigned long long f = (unsigned long long)flag << 32;
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(slot),
+                 "l"(f | (uint32_t)__double2hiint(v)), "l"(f | (uint32_t)__double2loint(v))
+                 : "memory");
+}
+CQ_DEVI double dbl_wait(const unsigned long long *slot, uint32_t flag) {
+    unsigned long long w0, w1;
+    do {
+        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(slot) : "memory");
+    } while ((uint32_t)(w0 >> 32) != flag || (uint32_t)(w1 >> 32) != flag);
+    return __hiloint2double((int)(uint32_t)w0, (int)(uint32_t)w1);
+}
+
 // argmax carrying the winner's physical column
 struct ArgMax3 {
     double v;
@@ -257,6 +272,7 @@ struct QrcpArgs {
     int32_t *piv;     // physical pivot chosen at each step
     double *alpha;    // R(i,i)
     unsigned long long *rec;  // [2][256][4] flagged argmax records (value hi/lo, index, physical column)
+    unsigned long long *tsq;  // [n][2] flagged next-step reflector tails sum of squares, by physical column
     int64_t *k_out;
     int32_t *final_buf;  // which cmap buffer holds positions >= k
     double rank_tol;
@@ -276,6 +292,8 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
     __shared__ int s_poff;
     __shared__ double s_ct[kQrcpWarps], s_tau[kQrcpWarps];  // fast column phase: R(i,j), tau per warp
     __shared__ int s_coff[kQrcpWarps];                        // column offset in its warp buffer (-1: none)
+    __shared__ int32_t s_cpj[kQrcpWarps];                     // its physical column
+    __shared__ double s_tsq;                                  // the pivot's speculative tail_sq
     __shared__ double s_pv;                                   // this step's pivot: value, position, column
     __shared__ int32_t s_pi, s_pp;
     __shared__ double s_cv[2][kQrcpWarps];                    // warp candidates, by step parity
@@ -290,6 +308,15 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
     double *s_x = smem + kQrcpWarps * WB;        // pivot column rows i..d-1 (+ alignment slack)
     double *s_sv = s_x + A.xlen;                 // products, then the scaled reflector (d doubles)
     const double sqrt_u = sqrt(kUnitRoundoff);
+    // Speculative reflector tails: when every CTA is in the fast column phase
+    // at step i (all columns resident), each warp finishes step i by forming
+    // dot(col[i+2:], col[i+2:]) of its updated column in the reference order
+    // (the tail_sq of make_reflector, linalg.cc:113-114, should that column be
+    // the pivot of step i+1) while the grid barrier is in flight; step i+1
+    // then reads the pivot's value instead of running that ordered chain.
+    auto spec_at = [&](int64_t i) {
+        return !A.general && i >= 0 && (n - i - 1) <= (int64_t)kQrcpWarps * G && (d - i - 1) <= (int64_t)CHD;
+    };
 
     // block argmax carrying the physical column of the winner
     auto block_argmax = [&](ArgMax a, int32_t phys, int32_t *phys_out) -> ArgMax {
@@ -427,6 +454,8 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
             const int off = stage_async(s_x, x + i, d - i, threadIdx.x, kQrcpThreads);
             if (threadIdx.x == 0) s_poff = off;
             cp_async_commit();
+            // the pivot's speculative tail (another L2 round trip) overlaps the copy
+            if (threadIdx.x == 32 && spec_at(i - 1)) s_tsq = dbl_wait(A.tsq + 2 * (size_t)phys_p, (uint32_t)(i + 1));
             // fast path: a warp whose column is not resident yet (first fast
             // step), or that receives the column swapped out of position i,
             // stages rows i..d-1 of it after its share of the pivot column; the
@@ -456,33 +485,40 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         }
         trace_mark(A.trace, i, 8);
         const double *xs = s_x + s_poff;  // xs[0] = x_i, xs[1 + e] = tail element e
-        for (int e0 = threadIdx.x; e0 < (int)body; e0 += 4 * kQrcpThreads) {
-            double xv[4];
+        auto reflector_scalars = [&](double tail_sq) {
+            double x0 = xs[0];
+            double norm_x = sqrt(fma(x0, x0, tail_sq));
+            double alpha = x0, v0 = 1.0, beta = 0.0;
+            if (norm_x != 0.0) {
+                double sign = (x0 >= 0.0) ? 1.0 : -1.0;
+                alpha = -sign * norm_x;
+                v0 = x0 - alpha;
+                beta = (norm_x + fabs(x0)) / norm_x;
+            }
+            s_bc[0] = alpha;
+            s_bc[1] = v0;
+            s_bc[2] = beta;
+        };
+        if (spec_at(i - 1)) {  // the pivot's owner formed tail_sq at step i-1
+            if (threadIdx.x == 0) reflector_scalars(s_tsq);
+            trace_mark(A.trace, i, 9);
+        } else {
+            for (int e0 = threadIdx.x; e0 < (int)body; e0 += 4 * kQrcpThreads) {
+                double xv[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) xv[u] = e0 + u * kQrcpThreads < (int)body ? xs[1 + e0 + u * kQrcpThreads] : 0.0;
+                for (int u = 0; u < 4; ++u)
+                    xv[u] = e0 + u * kQrcpThreads < (int)body ? xs[1 + e0 + u * kQrcpThreads] : 0.0;
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (e0 + u * kQrcpThreads < (int)body) s_sv[e0 + u * kQrcpThreads] = xv[u] * xv[u];
-        }
-        __syncthreads();
-        trace_mark(A.trace, i, 9);
-        if (wid == 0 && lane < 4) {
-            double s = chain_sum(0.0, s_sv, body, lane);
-            double tail_sq = chain_finish(s, c, [&](int64_t e) { return xs[1 + e]; },
-                                          [&](int64_t e) { return xs[1 + e]; });
-            if (lane == 0) {
-                double x0 = xs[0];
-                double norm_x = sqrt(fma(x0, x0, tail_sq));
-                double alpha = x0, v0 = 1.0, beta = 0.0;
-                if (norm_x != 0.0) {
-                    double sign = (x0 >= 0.0) ? 1.0 : -1.0;
-                    alpha = -sign * norm_x;
-                    v0 = x0 - alpha;
-                    beta = (norm_x + fabs(x0)) / norm_x;
-                }
-                s_bc[0] = alpha;
-                s_bc[1] = v0;
-                s_bc[2] = beta;
+                for (int u = 0; u < 4; ++u)
+                    if (e0 + u * kQrcpThreads < (int)body) s_sv[e0 + u * kQrcpThreads] = xv[u] * xv[u];
+            }
+            __syncthreads();
+            trace_mark(A.trace, i, 9);
+            if (wid == 0 && lane < 4) {
+                double s = chain_sum(0.0, s_sv, body, lane);
+                double tail_sq = chain_finish(s, c, [&](int64_t e) { return xs[1 + e]; },
+                                              [&](int64_t e) { return xs[1 + e]; });
+                if (lane == 0) reflector_scalars(tail_sq);
             }
         }
         __syncthreads();
@@ -503,6 +539,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         // ---- apply_reflector + norm downdate --------------------------------
         ArgMax mine{-INFINITY, 0x7fffffff};
         int32_t minep = 0;
+        bool spec_has = false;  // this warp holds a resident column to form the next tail for
         if (fast) {
             // Every warp's column is resident in its b0 (rb[r] = row r). Warp 0
             // runs the CTA's <= 8 dots at once: lanes 4g..4g+3 are the
@@ -523,6 +560,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
             if (lane == 0) {
                 s_ct[wid] = t;
                 s_coff[wid] = has ? (int)(rb + i + 1 - smem) : -1;
+                s_cpj[wid] = pj;
             }
             __syncthreads();
             trace_mark(A.trace, i, 5);
@@ -636,6 +674,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
                 mine = cnd;
             }
             resident = true;
+            spec_has = has;
             trace_mark(A.trace, i, 7);
         }
         bool first = true;
@@ -782,6 +821,35 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         }
         k = i + 1;
         trace_mark(A.trace, i, 4);
+        if (spec_at(i) && i + 1 < A.steps && wid >= 1) {
+            // next step's tail of the resident columns: rows i+2..d-1, squares
+            // then the reference's ordered chain, as in make_reflector. Warp 0
+            // goes straight to the next grid poll; warp 1 runs warp 0's chain
+            // (lanes 4..7) next to its own (lanes 0..3), so the chains overlap
+            // the barrier instead of preceding it.
+            const int64_t c2 = d - i - 2, body2 = c2 & ~(int64_t)3;
+            const bool two = (wid == 1) && s_coff[0] >= 0;  // set this step, read after the barrier
+            const double *cbo = two ? smem + s_coff[0] + 1 : nullptr;  // warp 0's rows i+2..
+            double *b1o = smem + WB / 2;                               // warp 0's free half buffer
+            if (spec_has) {
+                const double *cb2 = rb + i + 2;
+                for (int64_t e = lane; e < body2; e += 32) b1[e] = cb2[e] * cb2[e];
+            }
+            if (two)
+                for (int64_t e = lane; e < body2; e += 32) b1o[e] = cbo[e] * cbo[e];
+            __syncwarp();
+            const bool mine_q = lane < 4 && spec_has, other_q = lane >= 4 && lane < 8 && two;
+            double s2 = 0.0;
+            if (mine_q || other_q) {
+                const double *cq = mine_q ? rb + i + 2 : cbo;
+                s2 = chain_sum(0.0, mine_q ? b1 : b1o, body2, lane & 3);
+                s2 = chain_finish(s2, c2, [&](int64_t e) { return cq[e]; }, [&](int64_t e) { return cq[e]; },
+                                  mine_q ? 0xfu : 0xf0u);
+            }
+            if (lane == 0 && spec_has) dbl_publish(A.tsq + 2 * (size_t)r_pj, (uint32_t)(i + 2), s2);
+            if (lane == 4 && two) dbl_publish(A.tsq + 2 * (size_t)s_cpj[0], (uint32_t)(i + 2), s2);
+            __syncwarp();
+        }
     }
     if (cta == 0 && threadIdx.x == 0) {
         *A.k_out = k;
@@ -936,6 +1004,7 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     a.piv = ws.get<int32_t>("qrcp.piv", n);
     a.alpha = ws.get<double>("qrcp.alpha", n);
     a.rec = ws.get<unsigned long long>("qrcp.rec", 2 * 256 * 4);
+    a.tsq = ws.get<unsigned long long>("qrcp.tsq", 2 * (size_t)n);
     a.k_out = ws.get<int64_t>("qrcp.k", 2);
     a.final_buf = ws.get<int32_t>("qrcp.fb", 2);
     a.rank_tol = rank_tol;
@@ -944,9 +1013,10 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     a.xlen = xlen;
     // CQRRPT_QRCP_GENERAL=1 forces the general column phase (tests cover both)
     a.general = getenv("CQRRPT_QRCP_GENERAL") != nullptr ? 1 : 0;
-    if (!a.w[0] || !a.rec || !a.k_out) return fail_nomem("qrcp workspace");
+    if (!a.w[0] || !a.rec || !a.tsq || !a.k_out) return fail_nomem("qrcp workspace");
     // flags restart at 1 every call: clear the previous call's records
     CQ_CUDA(cudaMemsetAsync(a.rec, 0, 2 * 256 * 4 * sizeof(unsigned long long), st), "memset records");
+    CQ_CUDA(cudaMemsetAsync(a.tsq, 0, 2 * (size_t)n * sizeof(unsigned long long), st), "memset tails");
     static const bool tracing = getenv("CQRRPT_QRCP_TRACE") != nullptr;
     a.trace = tracing ? ws.get<unsigned long long>("qrcp.trace", 256 * 4096 * 16) : nullptr;
     if (a.trace)
