@@ -626,6 +626,8 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
                 double updated = fma(-t, t, wj);  // qrcp.cc:77-78
                 double newref = wrefj;
                 const bool recompute = updated <= sqrt_u * wrefj;  // qrcp.cc:82-86 (warp-uniform)
+                if (recompute && A.trace && lane == 0 && i < 4096)
+                    atomicAdd(&A.trace[((int64_t)blockIdx.x * 4096 + i) * 16 + 14], 1ULL);  // recompute count
                 double *cb = rb + i + 1;
                 if (beta != 0.0) {
                     const int ci = (int)c;
@@ -799,12 +801,21 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         {
             // warp candidates (warp-uniform) -> slot [step parity][warp]; after
             // one barrier warp 0 reduces them and publishes the CTA's record
+            // named barrier 1: only warp 0 (the publisher) waits; warps 1..7
+            // arrive and go on to their speculative tails. Barrier 2 hands
+            // warp 0's updated column to warp 1, which forms its tail.
+            const bool spec_next = spec_at(i) && i + 1 < A.steps;
             if (lane == 0) {
                 s_cv[cur][wid] = mine.v;
                 s_ci[cur][wid] = mine.i;
                 s_cp[cur][wid] = minep;
             }
-            __syncthreads();
+            if (wid == 0) {
+                if (spec_next) asm volatile("bar.arrive 2, 64;" ::: "memory");
+                asm volatile("bar.sync 1, %0;" ::"r"(kQrcpThreads) : "memory");
+            } else {
+                asm volatile("bar.arrive 1, %0;" ::"r"(kQrcpThreads) : "memory");
+            }
             if (wid == 0) {
                 ArgMax3 r{-INFINITY, 0x7fffffff, 0};
                 if (lane < kQrcpWarps) r = ArgMax3{s_cv[cur][lane], s_ci[cur][lane], s_cp[cur][lane]};
@@ -828,7 +839,8 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
             // (lanes 4..7) next to its own (lanes 0..3), so the chains overlap
             // the barrier instead of preceding it.
             const int64_t c2 = d - i - 2, body2 = c2 & ~(int64_t)3;
-            const bool two = (wid == 1) && s_coff[0] >= 0;  // set this step, read after the barrier
+            if (wid == 1) asm volatile("bar.sync 2, 64;" ::: "memory");  // warp 0's column is updated
+            const bool two = (wid == 1) && s_coff[0] >= 0;  // set this step
             const double *cbo = two ? smem + s_coff[0] + 1 : nullptr;  // warp 0's rows i+2..
             double *b1o = smem + WB / 2;                               // warp 0's free half buffer
             if (spec_has) {
@@ -1088,6 +1100,16 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
             }
             fprintf(stderr, "   own work over CTAs: mean %.0f, max %.0f (max reflector %.0f, columns %.0f, partials %.0f)\n",
                     wmean / nst, wmax / nst, rmax / nst, cmax / nst, pmax / nst);
+            {
+                long nrec = 0, steps_with = 0;
+                for (int s2 = qt * steps / 4; s2 < (qt + 1) * steps / 4; ++s2) {
+                    long ns = 0;
+                    for (int q2 = 0; q2 < G; ++q2) ns += (long)h[((size_t)q2 * 4096 + s2) * 16 + 14];
+                    nrec += ns;
+                    steps_with += ns > 0;
+                }
+                fprintf(stderr, "   recomputes (fast phase): %ld, steps with >= 1: %ld of %d\n", nrec, steps_with, cnt);
+            }
             fprintf(stderr,
                     "qrcp trace q%d (G=%d, d=%lld, n=%lld, WB=%d, %d steps; SM cycles): argmax %.0f, reflector %.0f, "
                     "columns %.0f (pre %.0f, chain %.0f, update %.0f), partials %.0f, barrier %.0f\n",
