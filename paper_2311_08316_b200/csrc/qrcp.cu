@@ -277,6 +277,8 @@ struct QrcpArgs {
     int32_t *final_buf;  // which cmap buffer holds positions >= k
     double rank_tol;
     int64_t steps;
+    int64_t steps_grid;  // steps run by this kernel; the cluster kernel takes [steps_grid, steps)
+    double *stop_out;    // rank_tol * max_norm0, for the cluster kernel
     int wb;                     // per-warp buffer (doubles, multiple of 32)
     int general;                // 1: never take the fast column phase (tests)
     int xlen;                   // pivot buffer length (doubles, >= d + 2, even)
@@ -390,7 +392,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
     double *rb = b0;
     int32_t r_pj = 0;
     double r_w = 0.0, r_wref = 0.0;
-    for (; i < A.steps; ++i) {
+    for (; i < A.steps_grid; ++i) {
         const int cur = (int)(i & 1), nxt = cur ^ 1;
         const int64_t c = d - i - 1;  // rows below the diagonal
         const int64_t body = c & ~(int64_t)3;
@@ -438,7 +440,10 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         ArgMax g{s_pv, s_pi};
         const int32_t phys_p = s_pp;
         trace_mark(A.trace, i, 12);
-        if (i == 0) stop = A.rank_tol * sqrt(fmax(g.v, 0.0));  // max_norm0 (qrcp.cc:52-55)
+        if (i == 0) {
+            stop = A.rank_tol * sqrt(fmax(g.v, 0.0));  // max_norm0 (qrcp.cc:52-55)
+            if (cta == 0 && threadIdx.x == 0) *A.stop_out = stop;
+        }
         const double wp = g.v;
         const int64_t p = g.i;
         if (sqrt(wp > 0.0 ? wp : 0.0) <= stop) {
@@ -810,8 +815,13 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
                 s_ci[cur][wid] = mine.i;
                 s_cp[cur][wid] = minep;
             }
-            if (wid == 0) {
-                if (spec_next) asm volatile("bar.arrive 2, 64;" ::: "memory");
+            // (only in the all-resident phase: in the streaming phase the warp
+            // -> position map shifts every step, so every warp must see its
+            // siblings' map and tracker writes before the next step)
+            if (!spec_next) {
+                __syncthreads();
+            } else if (wid == 0) {
+                asm volatile("bar.arrive 2, 64;" ::: "memory");
                 asm volatile("bar.sync 1, %0;" ::"r"(kQrcpThreads) : "memory");
             } else {
                 asm volatile("bar.arrive 1, %0;" ::"r"(kQrcpThreads) : "memory");
@@ -867,6 +877,328 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         *A.k_out = k;
         *A.final_buf = (int32_t)(k & 1);
     }
+}
+
+// ---------------------------------------------------------------------------
+// K3b: the QRCP tail inside one thread-block cluster.
+//
+// Once the trailing matrix (rows i_s..d-1 of positions i_s..n-1) fits in the
+// shared memory of a cluster (one column per warp, 16 warps per CTA, up to 16
+// CTAs), the remaining steps run with every column resident: the per-CTA
+// argmax records are exchanged through distributed shared memory after a
+// hardware cluster barrier (instead of flagged records through L2 across the
+// whole GPU), and every CTA reads the pivot column straight out of its owner's
+// shared memory. Ownership follows the column, not the position: a swap only
+// exchanges the two columns' position labels, no data moves. Arithmetic is
+// the grid kernel's, operation for operation (make_reflector, apply_reflector,
+// the downdate and its recompute in the reference's order), so R, J and k stay
+// bit-identical.
+// ---------------------------------------------------------------------------
+constexpr int kClWarps = 16;
+constexpr int kClThreads = kClWarps * 32;
+
+struct QrcpClusterArgs {
+    int64_t d, n, ld;
+    double *b;
+    const double *w_in, *wref_in;  // trackers at step i_s (by position)
+    const int32_t *cmap_in;        // position -> column at step i_s (nullptr: identity)
+    int32_t *cmap_out;             // final map for positions >= k (the buffer *final_buf names)
+    int32_t *piv;
+    double *alpha;
+    int64_t *k_out;
+    int32_t *final_buf;
+    int fb_value;
+    double rank_tol;
+    const double *stop_in;  // nullptr: i_s == 0, computed here
+    int64_t i_s, steps;
+    int rows;  // buffer rows per warp (>= d - i_s)
+    unsigned long long *trace;  // optional per-step phase clocks (CTA 0, thread 0)
+};
+
+CQ_DEVI uint32_t cl_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+CQ_DEVI uint32_t cl_map(uint32_t laddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(laddr), "r"(rank));
+    return r;
+}
+CQ_DEVI double cl_ld_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+    return v;
+}
+CQ_DEVI int32_t cl_ld_s32(uint32_t a) {
+    int32_t v;
+    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+// cluster barrier with cluster-scope ordering only: the data exchanged inside
+// the cluster phase is shared memory (the R entries written to global are read
+// by the next kernel), so a .release arrive (a GPU-scope MEMBAR) is not needed
+CQ_DEVI void cl_sync() {
+    asm volatile(
+        "fence.acq_rel.cluster;\nbarrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+            : "memory");
+}
+
+// lanes 0..3: s += a[e] * b[e] (product rounded, then added) for e = q, q+4,
+// ... < body, in order -- the same bits as adding precomputed products
+// (chain_sum); the loads of group g+1 are issued before the adds of group g
+CQ_DEVI double chain_dot(double s, const double *a, const double *bb, int body, int q) {
+    int e = q;
+    if (e + 28 < body) {
+        double xa[8], xb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            xa[u] = a[e + 4 * u];
+            xb[u] = bb[e + 4 * u];
+        }
+        for (e += 32; e + 28 < body; e += 32) {
+            double na[8], nb[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                na[u] = a[e + 4 * u];
+                nb[u] = bb[e + 4 * u];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s = s + xa[u] * xb[u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                xa[u] = na[u];
+                xb[u] = nb[u];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s = s + xa[u] * xb[u];
+    }
+    for (; e < body; e += 4) s = s + a[e] * bb[e];
+    return s;
+}
+
+// the reference's dot (linalg.cc:36-50) of two shared arrays, one warp
+CQ_DEVI double warp_ref_dot(const double *a, const double *bb, int64_t c, int lane) {
+    double s = 0.0;
+    if (lane < 4) {
+        s = chain_dot(0.0, a, bb, (int)(c & ~(int64_t)3), lane);
+        s = chain_finish(s, c, [&](int64_t e) { return a[e]; }, [&](int64_t e) { return bb[e]; });
+    }
+    return __shfl_sync(0xffffffffu, s, 0);
+}
+
+__global__ void __launch_bounds__(kClThreads, 1) qrcp_cluster_kernel(QrcpClusterArgs A) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ double s_cv[kClWarps];
+    __shared__ int32_t s_cpos[kClWarps], s_cphys[kClWarps];
+    // every CTA's record of the step (by parity), pushed here by its owner:
+    // value, position, column, owner warp
+    __shared__ double s_rv[2][16];
+    __shared__ int32_t s_rpos[2][16], s_rphys[2][16], s_rown[2][16];
+    __shared__ double s_pv, s_bc[3];
+    __shared__ int32_t s_ppos, s_pphys, s_pown;
+    __shared__ int s_stop;
+    const int64_t d = A.d, n = A.n, ld = A.ld, i_s = A.i_s;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t rank = cl_rank(), CS = gridDim.x;  // one cluster
+    if (tid == 0) s_stop = 0;
+    if (A.stop_in && __ldcg(A.k_out) < i_s) return;  // the grid phase already stopped (rank < i_s)
+    const int R = A.rows;
+    double *colbuf = smem + (size_t)wid * R;     // rows i_s..d-1 of this warp's column
+    double *s_x = smem + (size_t)kClWarps * R;   // pivot rows i..d-1
+    double *s_sv = s_x + R;                      // scaled reflector
+    const double sqrt_u = sqrt(kUnitRoundoff);
+
+    // ---- this warp's column: the one at position i_s + rank + CS * wid ----
+    const int64_t pos0 = i_s + rank + (int64_t)CS * wid;
+    const bool active = pos0 < n;
+    int64_t pos = pos0;
+    int32_t phys = 0;
+    double w = 0.0, wref = 0.0;
+    if (active) {
+        phys = A.cmap_in ? __ldcg(A.cmap_in + pos0) : (int32_t)pos0;
+        const double *g = A.b + (int64_t)phys * ld + i_s;
+        // L2-only loads: nothing of this kernel lives in L1, so the L1
+        // invalidation of every cluster barrier's acquire has nothing to drop
+        for (int64_t r = lane; r < d - i_s; r += 32) colbuf[r] = __ldcg(g + r);
+        __syncwarp();
+        if (A.stop_in) {
+            w = __ldcg(A.w_in + pos0);
+            wref = __ldcg(A.wref_in + pos0);
+        } else {  // initial squared norms (qrcp.cc:48-51)
+            w = warp_ref_dot(colbuf, colbuf, d, lane);
+            wref = w;
+        }
+    }
+    double stop = A.stop_in ? __ldcg(A.stop_in) : 0.0;
+    int64_t k = i_s;
+    for (int64_t i = i_s; i < A.steps; ++i) {
+        const int par = (int)(i & 1);
+        if (A.trace && tid == 0 && rank == 0 && i - i_s < 4096) A.trace[(i - i_s) * 16 + 0] = clock64();
+        // ---- argmax over positions >= i (qrcp.cc:26-31) -------------------
+        if (lane == 0) {
+            const bool cand = active && pos >= i;
+            s_cv[wid] = cand ? w : -INFINITY;
+            s_cpos[wid] = cand ? (int32_t)pos : 0x7fffffff;
+            s_cphys[wid] = phys;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            ArgMax3 r{-INFINITY, 0x7fffffff, 0};
+            int32_t own = 0;
+            if (lane < kClWarps) {
+                r = ArgMax3{s_cv[lane], s_cpos[lane], s_cphys[lane]};
+                own = lane;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                ArgMax3 b2{__shfl_xor_sync(0xffffffffu, r.v, o), __shfl_xor_sync(0xffffffffu, r.i, o),
+                           __shfl_xor_sync(0xffffffffu, r.p, o)};
+                const int32_t ob = __shfl_xor_sync(0xffffffffu, own, o);
+                const ArgMax3 c2 = argmax3_combine(r, b2);
+                if (c2.i != r.i || c2.v != r.v) own = ob;
+                r = c2;
+            }
+            // lane q < CS pushes the record into CTA q's slot [par][rank]
+            r.v = __shfl_sync(0xffffffffu, r.v, 0);
+            r.i = __shfl_sync(0xffffffffu, r.i, 0);
+            r.p = __shfl_sync(0xffffffffu, r.p, 0);
+            own = __shfl_sync(0xffffffffu, own, 0);
+            if (lane < (int)CS) {
+                const int32_t ow2 = (int32_t)(rank * kClWarps) + own;
+                asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(cl_map(smem_u32(&s_rv[par][rank]), lane)), "d"(r.v)
+                             : "memory");
+                asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(cl_map(smem_u32(&s_rpos[par][rank]), lane)),
+                             "r"(r.i)
+                             : "memory");
+                asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(cl_map(smem_u32(&s_rphys[par][rank]), lane)),
+                             "r"(r.p)
+                             : "memory");
+                asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(cl_map(smem_u32(&s_rown[par][rank]), lane)),
+                             "r"(ow2)
+                             : "memory");
+            }
+        }
+        if (A.trace && tid == 0 && rank == 0 && i - i_s < 4096) A.trace[(i - i_s) * 16 + 1] = clock64();
+        cl_sync();  // every CTA's record of this step has landed in every CTA
+        if (A.trace && tid == 0 && rank == 0 && i - i_s < 4096) A.trace[(i - i_s) * 16 + 2] = clock64();
+        if (wid == 0) {
+            ArgMax3 r{-INFINITY, 0x7fffffff, 0};
+            int32_t own = 0;
+            if (lane < (int)CS) {
+                r.v = s_rv[par][lane];
+                r.i = s_rpos[par][lane];
+                r.p = s_rphys[par][lane];
+                own = s_rown[par][lane];
+            }
+            __syncwarp();
+            if (A.trace && lane == 0 && rank == 0 && i - i_s < 4096) A.trace[(i - i_s) * 16 + 9] = clock64() + (unsigned long long)(r.v > 1e300 ? 1 : 0);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                ArgMax3 b2{__shfl_xor_sync(0xffffffffu, r.v, o), __shfl_xor_sync(0xffffffffu, r.i, o),
+                           __shfl_xor_sync(0xffffffffu, r.p, o)};
+                const int32_t ob = __shfl_xor_sync(0xffffffffu, own, o);
+                const ArgMax3 c2 = argmax3_combine(r, b2);
+                if (c2.i != r.i || c2.v != r.v) own = ob;
+                r = c2;
+            }
+            if (A.trace && lane == 0 && rank == 0 && i - i_s < 4096) A.trace[(i - i_s) * 16 + 10] = clock64() + (unsigned long long)(r.v > 1e300 ? 1 : 0);
+            if (lane == 0) {
+                s_pv = r.v;
+                s_ppos = r.i;
+                s_pphys = r.p;
+                s_pown = own;
+                if (i == 0) stop = A.rank_tol * sqrt(fmax(r.v, 0.0));  // max_norm0 (qrcp.cc:52-55)
+                s_stop = sqrt(r.v > 0.0 ? r.v : 0.0) <= stop ? 1 : 0;  // qrcp.cc:62
+                if (A.trace && rank == 0 && i - i_s < 4096) A.trace[(i - i_s) * 16 + 8] = clock64();
+            }
+        }
+        __syncthreads();
+        if (A.trace && tid == 0 && rank == 0 && i - i_s < 4096) A.trace[(i - i_s) * 16 + 3] = clock64();
+        if (s_stop) break;
+        const int64_t p = s_ppos;
+        const int32_t phys_p = s_pphys;
+        const uint32_t oc = (uint32_t)s_pown / kClWarps, ow = (uint32_t)s_pown % kClWarps;
+        // ---- pivot rows i..d-1 from its owner's shared memory -------------
+        {
+            const uint32_t src = cl_map(smem_u32(smem + (size_t)ow * R + (i - i_s)), oc);
+            for (int64_t e = tid; e < d - i; e += kClThreads) s_x[e] = cl_ld_f64(src + 8u * (uint32_t)e);
+        }
+        __syncthreads();
+        if (A.trace && tid == 0 && rank == 0 && i - i_s < 4096) A.trace[(i - i_s) * 16 + 4] = clock64();
+
+        const int64_t c = d - i - 1;
+        // ---- make_reflector (linalg.cc:110-124) -----------------------------
+        const int64_t body = c & ~(int64_t)3;
+        for (int64_t e = tid; e < body; e += kClThreads) s_sv[e] = s_x[1 + e] * s_x[1 + e];
+        __syncthreads();
+        if (wid == 0 && lane < 4) {
+            double tail_sq = chain_sum(0.0, s_sv, body, lane);
+            tail_sq = chain_finish(tail_sq, c, [&](int64_t e) { return s_x[1 + e]; },
+                                   [&](int64_t e) { return s_x[1 + e]; });
+            if (lane == 0) {
+                const double x0 = s_x[0];
+                const double norm_x = sqrt(fma(x0, x0, tail_sq));
+                double alpha = x0, v0 = 1.0, beta = 0.0;
+                if (norm_x != 0.0) {
+                    const double sign = (x0 >= 0.0) ? 1.0 : -1.0;
+                    alpha = -sign * norm_x;
+                    v0 = x0 - alpha;
+                    beta = (norm_x + fabs(x0)) / norm_x;
+                }
+                s_bc[0] = alpha;
+                s_bc[1] = v0;
+                s_bc[2] = beta;
+                if (rank == 0) {
+                    A.piv[i] = phys_p;
+                    A.alpha[i] = alpha;
+                }
+            }
+        }
+        __syncthreads();
+        const double v0 = s_bc[1], beta = s_bc[2];
+        if (A.trace && tid == 0 && rank == 0 && i - i_s < 4096) A.trace[(i - i_s) * 16 + 5] = clock64();
+        for (int64_t e = tid; e < c; e += kClThreads) s_sv[e] = (beta != 0.0) ? s_x[1 + e] / v0 : s_x[1 + e];
+        __syncthreads();
+        if (A.trace && tid == 0 && rank == 0 && i - i_s < 4096) A.trace[(i - i_s) * 16 + 6] = clock64();
+
+        // ---- swap = relabel positions p <-> i ------------------------------
+        if (pos == p) pos = i;
+        else if (pos == i) pos = p;
+        // ---- apply_reflector + downdate (linalg.cc:126-136, qrcp.cc:72-88) --
+        if (active && pos > i) {
+            double *col = colbuf + (i - i_s);  // col[0] = row i
+            double t = col[0];
+            if (beta != 0.0) {
+                const double dot = warp_ref_dot(s_sv, col + 1, c, lane);
+                double tau = t;
+                tau += dot;
+                tau *= beta;
+                t = t - tau;
+                for (int64_t e = lane; e < c; e += 32) col[1 + e] = fma(-tau, s_sv[e], col[1 + e]);
+                __syncwarp();
+            }
+            double updated = fma(-t, t, w);  // qrcp.cc:77-78
+            double newref = wref;
+            if (updated <= sqrt_u * wref) {  // qrcp.cc:82-86
+                updated = warp_ref_dot(col + 1, col + 1, c, lane);
+                newref = updated;
+            }
+            w = updated;
+            wref = newref;
+            if (lane == 0) A.b[(int64_t)phys * ld + i] = t;  // R(i, j)
+        }
+        if (A.trace && tid == 0 && rank == 0 && i - i_s < 4096) A.trace[(i - i_s) * 16 + 7] = clock64();
+        k = i + 1;
+    }
+    // positions >= k keep their columns (J tail); rank 0 reports k
+    if (active && lane == 0 && pos >= k) A.cmap_out[pos] = phys;
+    if (rank == 0 && tid == 0) {
+        *A.k_out = k;
+        *A.final_buf = A.fb_value;
+    }
+    cl_sync();  // no CTA exits while another may still read its shared memory
 }
 
 // J[j] = pivot at step j (j < k) or the column map (j >= k);
@@ -1021,6 +1353,58 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     a.final_buf = ws.get<int32_t>("qrcp.fb", 2);
     a.rank_tol = rank_tol;
     a.steps = std::min(d, n);
+    a.stop_out = ws.get<double>("qrcp.stop", 1);
+    // ---- cluster QRCP: positions i_s..n-1 (one column per warp, 16 warps per
+    // CTA) with rows i_s..d-1 fit in one cluster's shared memory. 16 CTAs
+    // (non-portable) when the GPU can co-schedule them, else 8.
+    int cs = 0;
+    int64_t i_s = a.steps;
+    size_t cl_smem = 0;
+    const bool cluster_ok = getenv("CQRRPT_QRCP_GENERAL") == nullptr && getenv("CQRRPT_QRCP_NOCLUSTER") == nullptr;
+    if (cluster_ok) {
+        static int checked = 0, cs_ok16 = 0, cs_ok8 = 0;  // per process (one GPU type)
+        const int64_t rows_max = 1600;
+        if (!checked) {
+            checked = 1;
+            const size_t smem_max = sizeof(double) * (size_t)(kClWarps + 2) * rows_max;
+            cudaFuncSetAttribute(qrcp_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+            cudaFuncSetAttribute(qrcp_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            for (int c2 : {16, 8}) {
+                cudaLaunchConfig_t cfg = {};
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = c2;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                cfg.gridDim = dim3(c2);
+                cfg.blockDim = dim3(kClThreads);
+                cfg.dynamicSmemBytes = smem_max;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                int ncl = 0;
+                if (cudaOccupancyMaxActiveClusters(&ncl, qrcp_cluster_kernel, &cfg) == cudaSuccess && ncl >= 1)
+                    (c2 == 16 ? cs_ok16 : cs_ok8) = 1;
+            }
+            cudaGetLastError();
+        }
+        for (int c2 : {16, 8}) {
+            if (!(c2 == 16 ? cs_ok16 : cs_ok8)) continue;
+            const int64_t cand = std::max<int64_t>({0, n - (int64_t)c2 * kClWarps, d - rows_max});
+            // measured (B200): ~10% faster per step than the grid kernel when
+            // the whole factorization fits (C1, C5-256); for a tail after a
+            // grid phase (C2: last 256 steps) it is no faster, so only then
+            if (cand == 0 && a.steps >= 16) {
+                cs = c2;
+                i_s = cand;
+                break;
+            }
+        }
+        if (cs) {
+            const int64_t rows = ((d - i_s) + 1) & ~(int64_t)1;
+            cl_smem = sizeof(double) * (size_t)(kClWarps + 2) * (size_t)rows;
+        }
+    }
+    a.steps_grid = i_s;
     a.wb = WB;
     a.xlen = xlen;
     // CQRRPT_QRCP_GENERAL=1 forces the general column phase (tests cover both)
@@ -1033,10 +1417,70 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     a.trace = tracing ? ws.get<unsigned long long>("qrcp.trace", 256 * 4096 * 16) : nullptr;
     if (a.trace)
         CQ_CUDA(cudaMemsetAsync(a.trace, 0, 256 * 4096 * 16 * sizeof(unsigned long long), st), "trace memset");
-    void *args[] = {&a};
-    CQ_CUDA(cudaLaunchCooperativeKernel((void *)qrcp_kernel, dim3(G), dim3(kQrcpThreads), args, smem, st),
-            "qrcp cooperative launch");
-    note_launch();
+    if (i_s > 0) {
+        void *args[] = {&a};
+        CQ_CUDA(cudaLaunchCooperativeKernel((void *)qrcp_kernel, dim3(G), dim3(kQrcpThreads), args, smem, st),
+                "qrcp cooperative launch");
+        note_launch();
+    }
+    if (cs) {
+        QrcpClusterArgs c{};
+        c.d = d;
+        c.n = n;
+        c.ld = ldb;
+        c.b = b;
+        c.w_in = a.w[i_s & 1];
+        c.wref_in = a.wref;
+        c.cmap_in = i_s > 0 ? a.cmap[i_s & 1] : nullptr;
+        c.cmap_out = a.cmap[0];
+        c.piv = a.piv;
+        c.alpha = a.alpha;
+        c.k_out = a.k_out;
+        c.final_buf = a.final_buf;
+        c.fb_value = 0;
+        c.rank_tol = rank_tol;
+        c.stop_in = i_s > 0 ? a.stop_out : nullptr;
+        c.i_s = i_s;
+        c.steps = a.steps;
+        c.rows = (int)(((d - i_s) + 1) & ~(int64_t)1);
+        static const bool cl_tracing = getenv("CQRRPT_QRCP_TRACE") != nullptr;
+        c.trace = cl_tracing ? ws.get<unsigned long long>("qrcp.cltrace", 4096 * 16) : nullptr;
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(cs);
+        cfg.blockDim = dim3(kClThreads);
+        cfg.dynamicSmemBytes = cl_smem;
+        cfg.stream = st;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CQ_CUDA(cudaLaunchKernelEx(&cfg, qrcp_cluster_kernel, c), "qrcp cluster launch");
+        note_launch();
+        if (c.trace) {
+            std::vector<unsigned long long> h(4096 * 16);
+            cudaStreamSynchronize(st);
+            cudaMemcpy(h.data(), c.trace, h.size() * 8, cudaMemcpyDeviceToHost);
+            const int64_t ns = std::min<int64_t>(a.steps - i_s - 1, 4095);
+            double acc[8] = {0}, red = 0.0, ph[3] = {0, 0, 0};
+            for (int64_t s2 = 0; s2 < ns; ++s2) {
+                for (int q = 0; q < 7; ++q) acc[q] += (double)(h[s2 * 16 + q + 1] - h[s2 * 16 + q]);
+                acc[7] += (double)(h[(s2 + 1) * 16] - h[s2 * 16 + 7]);
+                red += (double)(h[s2 * 16 + 8] - h[s2 * 16 + 2]);
+                ph[0] += (double)(h[s2 * 16 + 9] - h[s2 * 16 + 2]);
+                ph[1] += (double)(h[s2 * 16 + 10] - h[s2 * 16 + 9]);
+                ph[2] += (double)(h[s2 * 16 + 8] - h[s2 * 16 + 10]);
+            }
+            fprintf(stderr,
+                    "qrcp cluster trace (CS=%d, i_s=%lld, %lld steps; SM cycles/step): cand %.0f, cl_sync %.0f, "
+                    "pivot %.0f (warp-0 reduce %.0f), xfetch %.0f, reflector %.0f, divide %.0f, columns %.0f, loop %.0f\n",
+                    cs, (long long)i_s, (long long)ns, acc[0] / ns, acc[1] / ns, acc[2] / ns, red / ns, acc[3] / ns,
+                    acc[4] / ns, acc[5] / ns, acc[6] / ns, acc[7] / ns);
+            fprintf(stderr, "   reduce split: loads %.0f, shuffles %.0f, stop test %.0f\n", ph[0] / ns, ph[1] / ns, ph[2] / ns);
+        }
+    }
     qrcp_extract_kernel<<<(unsigned)n, 128, 0, st>>>(d, n, b, ldb, a.k_out, a.piv, a.cmap[0], a.cmap[1],
                                                       a.final_buf, a.alpha, rsk, ldr, jdev);
     note_launch();
@@ -1046,7 +1490,7 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     if (a.trace) {  // debug: mean per-phase SM cycles per quarter of the steps
         std::vector<unsigned long long> h((size_t)G * 4096 * 16);
         cudaMemcpy(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost);
-        const int steps = (int)std::min<int64_t>(*k_sk, 4096) - 1;
+        const int steps = (int)std::min<int64_t>(std::min<int64_t>(*k_sk, i_s), 4096) - 1;  // grid-kernel steps
         for (int qt = 0; qt < 4 && steps > 4; ++qt) {
             double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             int cnt = 0, cnt5 = 0;
