@@ -96,6 +96,29 @@ def test_saso_sketch_deterministic(cuda, oracle):
     assert not np.array_equal(x, z)
 
 
+@pytest.mark.parametrize("A", [1, 2, 4, 6, 8, 12])
+def test_saso_sketch_every_row_block_width(cuda, oracle, monkeypatch, A):
+    """Every instantiation of the apply kernel (A accumulator rows per consumer
+    warp, forced by env var) against the reference's apply: several row
+    blocks, ragged last 256-row tile, ragged last column group."""
+    from paper_2311_08316_b200 import kernels
+    monkeypatch.setenv("CQRRPT_SASO_A", str(A))
+    m, n, d, nnz, seed = 5000, 45, 700, 8, 12
+    a = oracle.gen_gaussian(m, n, 31)
+    got = host(kernels.saso_sketch(dev(cuda, a), d, nnz, seed))
+    assert np.array_equal(got, oracle.saso_apply(d, a, nnz, seed))
+
+
+@pytest.mark.parametrize("nnz", [1, 2, 16])
+def test_saso_sketch_nnz(cuda, oracle, nnz):
+    """Other nonzeros per column (entry-list sizes per tile), bit-identical."""
+    from paper_2311_08316_b200 import kernels
+    m, n, d = 3000, 40, 120
+    a = oracle.gen_gaussian(m, n, 7)
+    got = host(kernels.saso_sketch(dev(cuda, a), d, nnz, 17))
+    assert np.array_equal(got, oracle.saso_apply(d, a, nnz, 17))
+
+
 def test_saso_sketch_zero(cuda, oracle):
     from paper_2311_08316_b200 import kernels
     got = host(kernels.saso_sketch(dev(cuda, np.zeros((20, 4))), 8, 2, 44))
@@ -123,6 +146,24 @@ def test_qrcp_general_column_phase_bit_exact(cuda, oracle, monkeypatch, rows, n,
     forced by env var."""
     monkeypatch.setenv("CQRRPT_QRCP_GENERAL", "1")
     _qrcp_compare(cuda, oracle, oracle.gen_gaussian(rows, n, seed))
+
+
+@pytest.mark.parametrize("rows,n,seed", [(320, 256, 5), (100, 90, 6), (300, 40, 7)])
+@pytest.mark.parametrize("cluster", [True, False])
+def test_qrcp_cluster_and_grid_paths(cuda, oracle, monkeypatch, rows, n, seed, cluster):
+    """n <= 256: the whole factorization runs in one thread-block cluster
+    (K3b); CQRRPT_QRCP_NOCLUSTER forces the grid kernel. Both bit-identical."""
+    if not cluster:
+        monkeypatch.setenv("CQRRPT_QRCP_NOCLUSTER", "1")
+    _qrcp_compare(cuda, oracle, oracle.gen_gaussian(rows, n, seed))
+
+
+def test_qrcp_cluster_rank_deficient_stop(cuda, oracle):
+    """Rank stop inside the cluster kernel: exact rank 9 of 64 columns."""
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((200, 9)) @ rng.standard_normal((9, 64))
+    R, J, k = _qrcp_compare(cuda, oracle, np.asfortranarray(a))
+    assert k < 64
 
 
 def test_qrcp_known_answer_diag(cuda, oracle):
