@@ -321,6 +321,21 @@ def main():
     sk = {"bound": "hbm", "achieved": sketch_bytes / (ph[0] * 1e-3) / 1e9, "peak": peaks.get("hbm_gbs"),
           "unit": "GB/s", "peak_source": peak_src}
     sk["frac"] = sk["achieved"] / sk["peak"] if sk["peak"] else None
+    # the sketch's binding resource: shared-memory wavefronts (128 B each) of
+    # the apply kernel, counted by ncu for this configuration
+    # (profiles/traffic.json), over the live sketch-phase time, against
+    # 128 B/clk/SM x SMs x the SM clock sampled under load
+    tr = load_traffic()
+    wf = tr.get("saso_apply_smem_wavefronts")
+    if wf:
+        props = torch.cuda.get_device_properties(local)
+        sm_ghz = (clk.summary().get("sm_mhz") or 1965.0) / 1e3
+        smem_peak = 128.0 * props.multi_processor_count * sm_ghz  # GB/s
+        sk["smem"] = {"bound": "shared memory", "achieved": wf * 128.0 / (ph[0] * 1e-3) / 1e9, "peak": smem_peak,
+                      "unit": "GB/s", "wavefronts_per_launch": wf,
+                      "peak_source": "128 B/clk/SM x SMs x sampled SM clock",
+                      "traffic": tr.get("saso_apply_dram_bytes")}
+        sk["smem"]["frac"] = sk["smem"]["achieved"] / smem_peak
     contraction_flops = float(m) * k0 * k0 + float(m) * k0 * (k0 + 1) + float(m) * k * k
     con = {"bound": "tensor", "achieved": contraction_flops / ((ph[3] + ph[4]) * 1e-3) / 1e12, "peak": fp64_peak,
            "unit": "TFLOP/s"}
