@@ -27,6 +27,7 @@ struct GemmArgs {
     int64_t batch;            // > 1: grid.z indexes independent problems (no split-K)
     int64_t bs_a, bs_b, bs_cin, bs_c;  // per-problem element strides of A, B, Cin, Cout
     int vec16;                // set by gemm_ex: A/B tiles staged with 16-byte copies
+    int tile_n64;             // tiles[]: column tile index in units of 64 columns (not BN)
 };
 
 // C_out = alpha op(A) B + beta C_in, optionally split over K into `splits`
