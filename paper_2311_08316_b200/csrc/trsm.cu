@@ -68,10 +68,32 @@ __global__ void __launch_bounds__(kThreads, 3)
         }
 
     const int nchunks = (int)(c0 / kBK);  // c0 is a multiple of 64
+    // 16-byte copies of element pairs when X and U are 16-byte aligned with
+    // even leading dimensions (the swizzles keep pairs adjacent)
+    const bool vec16 = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(u)) & 15) == 0 &&
+                       ((ldx | ldu) & 1) == 0;
     auto load_chunk = [&](int kc, int stage) {
         const int64_t kb = (int64_t)kc * kBK;
         double *as = As + stage * kBK * kBM;
         double *bs = Bs + stage * kNB * kBK;
+        if (vec16) {
+#pragma unroll
+            for (int it = 0; it < (kBK * kBM) / 2 / kThreads; ++it) {  // A: X[row0 + mm .. +1][kb + kk]
+                const int q = it * kThreads + tid;
+                const int kk = q / (kBM / 2), mm = (q % (kBM / 2)) * 2;
+                const int64_t row = row0 + mm;
+                cp_async16_zfill(as + sw_km(kk, mm), x + (kb + kk) * ldx + (row < m ? row : 0),
+                                 row < m ? (row + 1 < m ? 16 : 8) : 0);
+            }
+#pragma unroll
+            for (int it = 0; it < (kBK * kNB) / 2 / kThreads; ++it) {  // B: U[kb + kk .. +1][c0 + nn]
+                const int q = it * kThreads + tid;
+                const int nn = q / (kBK / 2), kk = (q % (kBK / 2)) * 2;
+                const bool ok = nn < nbw;
+                cp_async16_zfill(bs + sw_rk(nn, kk), u + (c0 + (ok ? nn : 0)) * ldu + kb + kk, ok ? 16 : 0);
+            }
+            return;
+        }
 #pragma unroll
         for (int it = 0; it < (kBK * kBM) / kThreads; ++it) {  // A: X[row0 + mm][kb + kk]
             int q = it * kThreads + tid;
