@@ -161,32 +161,41 @@ __global__ void __launch_bounds__(kThreads, 3)
         Ds[cc * kLdT + ss] = __ldg(dinv_blk + q);
     }
     __syncthreads();
+    // U_jb^{-1} is upper triangular: the 8-column block nb only takes the
+    // k-steps kk <= 8 nb + 4 (2 nb + 2 of 16). Warp w computes the column
+    // blocks w and 7 - w for all 64 rows, so every warp issues 144 DMMAs
+    // instead of 256 (the all-zero k-steps are skipped, balanced).
+    const int nbA = warp, nbB = 7 - warp;
+    double ep[8][2][2];
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+    for (int mi = 0; mi < 8; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-#pragma unroll 4
+        for (int b2 = 0; b2 < 2; ++b2) ep[mi][b2][0] = ep[mi][b2][1] = 0.0;
+#pragma unroll
     for (int kk = 0; kk < kNB; kk += 4) {
-        double af[4], bf[4];
+        if (kk > 8 * nbB + 4) break;  // nbB >= 4 > nbA: the longer of the two (warp-uniform)
+        double af[8];
 #pragma unroll
-        for (int mi = 0; mi < 4; ++mi) af[mi] = Ts[(wm * 32 + mi * 8 + g) * kLdT + kk + t];
+        for (int mi = 0; mi < 8; ++mi) af[mi] = Ts[(mi * 8 + g) * kLdT + kk + t];
+        const double bfB = Ds[(nbB * 8 + g) * kLdT + kk + t];
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) bf[ni] = Ds[(wn * 32 + ni * 8 + g) * kLdT + kk + t];
+        for (int mi = 0; mi < 8; ++mi) dmma884(ep[mi][1][0], ep[mi][1][1], af[mi], bfB);
+        if (kk <= 8 * nbA + 4) {
+            const double bfA = Ds[(nbA * 8 + g) * kLdT + kk + t];
 #pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < 4; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+            for (int mi = 0; mi < 8; ++mi) dmma884(ep[mi][0][0], ep[mi][0][1], af[mi], bfA);
+        }
     }
     __syncthreads();  // Ts is reused for the output staging
     double *Os = sm;  // [64 c][65 r]
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+    for (int mi = 0; mi < 8; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
+        for (int b2 = 0; b2 < 2; ++b2)
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
-                int r = wm * 32 + mi * 8 + g, c = wn * 32 + ni * 8 + 2 * t + v;
-                Os[c * (kBM + 1) + r] = acc[mi][ni][v];
+                const int r = mi * 8 + g, c = (b2 ? nbB : nbA) * 8 + 2 * t + v;
+                Os[c * (kBM + 1) + r] = ep[mi][b2][v];
             }
     __syncthreads();
     for (int q = tid; q < kNB * kBM; q += kThreads) {  // coalesced column writes
