@@ -26,21 +26,29 @@ constexpr int kPB = 64;
 // (and the reference's failure rule), only without CTA barriers per column.
 constexpr int kWB = 32;
 
-// In-place upper Cholesky of the 32 x 32 block whose column `lane` is a[0..31]
-// (rows). Returns the 1-based failing column or 0. Rows below the diagonal are
-// updated too (no predicates); they never feed an entry on or above it.
-CQ_DEVI int warp_potrf32(double (&a)[kWB]) {
+// Upper Cholesky of the 32 x 32 block whose column `lane` is b[0..31]
+// (rows). R(j, c) goes to out[j]. Returns the 1-based failing column or 0.
+// The column is shifted up one row per step, so the active row is always
+// b[0] and the loop body is static: a fully unrolled 32-step factor is ~60 KB
+// of straight-line code that runs once per launch with a cold instruction
+// cache (instruction-fetch bound); this body stays cached. Same operations in
+// the same order as the unrolled version (rows below the diagonal are updated
+// too, no predicates; they never feed an entry on or above it).
+CQ_DEVI int warp_potrf32(double (&b)[kWB], double *out) {
     const int c = threadIdx.x;
-#pragma unroll
+#pragma unroll 1
     for (int j = 0; j < kWB; ++j) {
-        const double d = __shfl_sync(0xffffffffu, a[j], j);  // g(j,j) - sum_{t<j} r(t,j)^2
+        const double d = __shfl_sync(0xffffffffu, b[0], j);  // g(j,j) - sum_{t<j} r(t,j)^2
         if (d <= 0.0 || !isfinite(d)) return j + 1;          // warp-uniform
         const double rjj = sqrt(d);
-        const double q = a[j] / rjj;
+        const double q = b[0] / rjj;
         const double rjc = c == j ? rjj : q;
-        a[j] = rjc;
+        out[j] = rjc;
 #pragma unroll
-        for (int i = j + 1; i < kWB; ++i) a[i] = fma(-__shfl_sync(0xffffffffu, rjc, i), rjc, a[i]);
+        for (int t = 1; t < kWB; ++t)  // row j + t (garbage past row 31, never used)
+            b[t] = fma(-__shfl_sync(0xffffffffu, rjc, (j + t) & 31), rjc, b[t]);
+#pragma unroll
+        for (int t = 0; t + 1 < kWB; ++t) b[t] = b[t + 1];
     }
     return 0;
 }
@@ -70,35 +78,34 @@ __global__ void __launch_bounds__(32) potrf_diag_kernel(int64_t n, double *__res
     double a[kWB];
 #pragma unroll
     for (int i = 0; i < kWB; ++i) a[i] = blk[c][i];
-    int f = warp_potrf32(a);  // R11
-#pragma unroll
-    for (int i = 0; i < kWB; ++i) blk[c][i] = a[i];
+    int f = warp_potrf32(a, blk[c]);  // R11 -> blk[c][0..31]
     __syncwarp();
     if (!f) {
-        // R12 = R11^{-T} A12: column 32 + c, right-looking (division by r(t,t))
+        // R12 = R11^{-T} A12: column 32 + c, right-looking (division by r(t,t)),
+        // shifted like warp_potrf32 (active row in a[0])
 #pragma unroll
         for (int i = 0; i < kWB; ++i) a[i] = blk[kWB + c][i];
-#pragma unroll
+#pragma unroll 1
         for (int t = 0; t < kWB; ++t) {
-            a[t] = a[t] / blk[t][t];
+            const double xt = a[0] / blk[t][t];
+            blk[kWB + c][t] = xt;
 #pragma unroll
-            for (int i = t + 1; i < kWB; ++i) a[i] = fma(-blk[i][t], a[t], a[i]);
+            for (int s2 = 1; s2 < kWB; ++s2) a[s2] = fma(-blk[t + s2][t], xt, a[s2]);  // rows past 31: unused
+#pragma unroll
+            for (int s2 = 0; s2 + 1 < kWB; ++s2) a[s2] = a[s2 + 1];
         }
-#pragma unroll
-        for (int i = 0; i < kWB; ++i) blk[kWB + c][i] = a[i];
         __syncwarp();
         // A22 -= R12^T R12, k ascending
 #pragma unroll
         for (int i = 0; i < kWB; ++i) a[i] = blk[kWB + c][kWB + i];
-#pragma unroll
+#pragma unroll 1
         for (int k = 0; k < kWB; ++k) {
             const double rkc = blk[kWB + c][k];
 #pragma unroll
             for (int i = 0; i < kWB; ++i) a[i] = fma(-blk[kWB + i][k], rkc, a[i]);
         }
-        const int f2 = warp_potrf32(a);  // R22
-#pragma unroll
-        for (int i = 0; i < kWB; ++i) blk[kWB + c][kWB + i] = a[i];
+        __syncwarp();
+        const int f2 = warp_potrf32(a, blk[kWB + c] + kWB);  // R22
         if (f2) f = kWB + f2;
     }
     __syncwarp();
