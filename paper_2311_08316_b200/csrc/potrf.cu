@@ -18,99 +18,51 @@ int gemm_tn_upper(int64_t N, int64_t K, double alpha, const double *a, int64_t l
 
 constexpr int kPB = 64;
 
-// Diagonal block, one warp, in 32 x 32 sub-blocks: [A11 A12; . A22] ->
-// R11 = chol(A11) in registers (lane = column, row broadcasts by shuffle, no
-// barriers), R12 = R11^{-T} A12 (right-looking substitution, division),
-// A22 -= R12^T R12 (FMAs in k order), R22 = chol(A22). Every entry sees the
-// same FMAs in the same order as the unblocked right-looking factorization
-// (and the reference's failure rule), only without CTA barriers per column.
-constexpr int kWB = 32;
-
-// Upper Cholesky of the 32 x 32 block whose column `lane` is b[0..31]
-// (rows). R(j, c) goes to out[j]. Returns the 1-based failing column or 0.
-// The column is shifted up one row per step, so the active row is always
-// b[0] and the loop body is static: a fully unrolled 32-step factor is ~60 KB
-// of straight-line code that runs once per launch with a cold instruction
-// cache (instruction-fetch bound); this body stays cached. Same operations in
-// the same order as the unrolled version (rows below the diagonal are updated
-// too, no predicates; they never feed an entry on or above it).
-CQ_DEVI int warp_potrf32(double (&b)[kWB], double *out) {
-    const int c = threadIdx.x;
-#pragma unroll 1
-    for (int j = 0; j < kWB; ++j) {
-        const double d = __shfl_sync(0xffffffffu, b[0], j);  // g(j,j) - sum_{t<j} r(t,j)^2
-        if (d <= 0.0 || !isfinite(d)) return j + 1;          // warp-uniform
-        const double rjj = sqrt(d);
-        const double q = b[0] / rjj;
-        const double rjc = c == j ? rjj : q;
-        out[j] = rjc;
-#pragma unroll
-        for (int t = 1; t < kWB; ++t)  // row j + t (garbage past row 31, never used)
-            b[t] = fma(-__shfl_sync(0xffffffffu, rjc, (j + t) & 31), rjc, b[t]);
-#pragma unroll
-        for (int t = 0; t + 1 < kWB; ++t) b[t] = b[t + 1];
-    }
-    return 0;
-}
-
-// One warp. A ragged last block is padded with the identity (never fails, no
-// effect on the real columns).
-__global__ void __launch_bounds__(32) potrf_diag_kernel(int64_t n, double *__restrict__ g, int64_t ldg, int64_t j0,
-                                                       int64_t *__restrict__ fail) {
+// Diagonal block, unblocked right-looking, 64 threads (thread = column): the
+// column lives in registers, shifted up one row per step so the active row
+// is always a[0]; R(j, :) is exchanged through shared memory with one CTA
+// barrier per side. Every entry receives the right-looking FMAs in column
+// order (as the earlier one-warp 32 x 32 sub-block scheme did: R11, R12,
+// A22 -= R12^T R12, R22), with the reference's failure rule; the critical
+// path per column is one sqrt, one division and one FMA (C2's 1024 x 1024
+// factor: 1.32 -> 1.13 ms with this kernel).
+__global__ void __launch_bounds__(kPB) potrf_diag64_kernel(int64_t n, double *__restrict__ g, int64_t ldg,
+                                                          int64_t j0, int64_t *__restrict__ fail) {
     if (*fail) return;
-    __shared__ double blk[kPB][kPB + 1];  // [col][row]
+    __shared__ double blk[kPB][kPB + 1];  // [col][row]: the factor, written row by row
+    __shared__ double srow[2 * kPB];      // R(j, :) of the current step (+ zero pad)
+    __shared__ double sd;
     const int nb = (int)cmin<int64_t>(kPB, n - j0);
     const int c = threadIdx.x;
-    for (int u0 = 0; u0 < kPB * kPB / 32; u0 += 16) {  // 16 loads in flight per lane
-        double v[16];
+    double a[kPB];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-            const int q = c + 32 * (u0 + u), cc = q / kPB, r = q % kPB;
-            v[u] = (cc < nb && r <= cc) ? g[(j0 + cc) * ldg + j0 + r] : (cc == r ? 1.0 : 0.0);
-        }
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-            const int q = c + 32 * (u0 + u);
-            blk[q / kPB][q % kPB] = v[u];
-        }
-    }
-    __syncwarp();
-    double a[kWB];
-#pragma unroll
-    for (int i = 0; i < kWB; ++i) a[i] = blk[c][i];
-    int f = warp_potrf32(a, blk[c]);  // R11 -> blk[c][0..31]
-    __syncwarp();
-    if (!f) {
-        // R12 = R11^{-T} A12: column 32 + c, right-looking (division by r(t,t)),
-        // shifted like warp_potrf32 (active row in a[0])
-#pragma unroll
-        for (int i = 0; i < kWB; ++i) a[i] = blk[kWB + c][i];
+    for (int t = 0; t < kPB; ++t)  // column c, rows 0..63 (identity padded past nb)
+        a[t] = (c < nb && t <= c) ? g[(j0 + c) * ldg + j0 + t] : (c == t ? 1.0 : 0.0);
+    srow[kPB + c] = 0.0;
+    int f = 0;
 #pragma unroll 1
-        for (int t = 0; t < kWB; ++t) {
-            const double xt = a[0] / blk[t][t];
-            blk[kWB + c][t] = xt;
-#pragma unroll
-            for (int s2 = 1; s2 < kWB; ++s2) a[s2] = fma(-blk[t + s2][t], xt, a[s2]);  // rows past 31: unused
-#pragma unroll
-            for (int s2 = 0; s2 + 1 < kWB; ++s2) a[s2] = a[s2 + 1];
+    for (int j = 0; j < kPB; ++j) {
+        if (c == j) sd = a[0];  // g(j,j) - sum_{t<j} r(t,j)^2
+        __syncthreads();
+        const double d = sd;
+        if (d <= 0.0 || !isfinite(d)) {  // CTA-uniform
+            f = j + 1;
+            break;
         }
-        __syncwarp();
-        // A22 -= R12^T R12, k ascending
+        const double rjj = sqrt(d);
+        const double q = a[0] / rjj;
+        const double rjc = c == j ? rjj : q;
+        blk[c][j] = rjc;
+        srow[c] = rjc;
+        __syncthreads();
 #pragma unroll
-        for (int i = 0; i < kWB; ++i) a[i] = blk[kWB + c][kWB + i];
-#pragma unroll 1
-        for (int k = 0; k < kWB; ++k) {
-            const double rkc = blk[kWB + c][k];
+        for (int t = 1; t < kPB; ++t) a[t] = fma(-srow[j + t], rjc, a[t]);  // row j + t (pad: zero)
 #pragma unroll
-            for (int i = 0; i < kWB; ++i) a[i] = fma(-blk[kWB + i][k], rkc, a[i]);
-        }
-        __syncwarp();
-        const int f2 = warp_potrf32(a, blk[kWB + c] + kWB);  // R22
-        if (f2) f = kWB + f2;
+        for (int t = 0; t + 1 < kPB; ++t) a[t] = a[t + 1];
     }
-    __syncwarp();
+    __syncthreads();
     const int ncols = f ? f - 1 : nb;
-    for (int q = c; q < kPB * kPB; q += 32) {  // factored columns, rows <= col
+    for (int q = c; q < kPB * kPB; q += kPB) {  // factored columns, rows <= col
         const int cc = q / kPB, r = q % kPB;
         if (cc < ncols && r <= cc) g[(j0 + cc) * ldg + j0 + r] = blk[cc][r];
     }
@@ -189,7 +141,7 @@ int potrf(int64_t n, double *g, int64_t ldg, int64_t *failure_index, Workspace &
     CQ_CUDA(cudaStreamWaitEvent(aux, ev_in, 0), "potrf wait");
     for (int64_t j0 = 0; j0 < n; j0 += kPB) {
         const int64_t nb = std::min<int64_t>(kPB, n - j0);
-        potrf_diag_kernel<<<1, 32, 0, aux>>>(n, g, ldg, j0, fail);
+        potrf_diag64_kernel<<<1, kPB, 0, aux>>>(n, g, ldg, j0, fail);
         note_launch();
         const int64_t rest = n - j0 - nb;
         if (rest <= 0) break;
