@@ -155,9 +155,11 @@ double cqrrpt_gpu_flop_model(int64_t m, int64_t n, int64_t k, int64_t d, double 
 
 namespace {
 // The driver; `qsink` (optional) downloads Q block by block during the final TRSM.
+constexpr int kInputChunks = 4;  // H2D row chunks of the host-buffer entry point
+
 int dgeqpt_impl(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, int64_t nnz, uint64_t seed,
                 double eps_tol, double *R, int64_t ldr, int64_t *J, int64_t *k_out, int64_t *k0_out,
-                cqrrpt_gpu_ctx *ctx, const BlockSink *qsink) {
+                cqrrpt_gpu_ctx *ctx, const BlockSink *qsink, const InputChunks *ichunks = nullptr) {
     cqrrpt_gpu_ctx local;
     if (!ctx) {
         cqrrpt_gpu_ctx_init(&local);
@@ -206,13 +208,15 @@ int dgeqpt_impl(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, i
     // ---- sketch ------------------------------------------------------------
     double *msk = ws.get<double>("drv.msk", (size_t)(d * n));
     if (!msk) return fail_nomem("sketch");
+    if (ichunks && !saso)  // A still arriving: only the exact SASO sketch follows the chunks
+        for (int c = 0; c < ichunks->count; ++c) CQ_CUDA(cudaStreamWaitEvent(st, ichunks->ev[c], 0), "wait input");
     if (gaussian)
         CQ_TRY(gaussian_sketch(m, n, A, lda, d, seed, ctx->global_row_offset, msk, d, ws, st));
     else if (srft)
         CQ_TRY(srft_sketch(m, n, A, lda, d, seed, msk, d, ws, st));
     else
         CQ_TRY(saso_sketch(m, n, A, lda, d, nnz, seed, ctx->global_row_offset, msk, d, ws, st,
-                           (ctx->flags & CQRRPT_GPU_FAST_SKETCH) != 0));
+                           (ctx->flags & CQRRPT_GPU_FAST_SKETCH) != 0, ichunks));
     clk.mark(PH_SKETCH);
     CQ_TRY(do_allreduce(ctx, msk, (size_t)(d * n), st));
     clk.mark(PH_COMM);
@@ -429,17 +433,42 @@ int cqrrpt_gpu_dgeqpt_host(int64_t m, int64_t n, const double *A_host, int64_t l
     Workspace &ws = workspace();
     double *dA = (m > 0 && n > 0) ? ws.get<double>("host.a", (size_t)(m * n)) : nullptr;
     if (m > 0 && n > 0 && !dA) return fail_nomem("device copy of A");
-    if (dA)
-        CQ_CUDA(cudaMemcpy2DAsync(dA, sizeof(double) * m, A_host, sizeof(double) * lda, sizeof(double) * m, n,
-                                  cudaMemcpyHostToDevice, st),
-                "A h2d");
     static thread_local cudaStream_t copy = nullptr;
     if (!copy) CQ_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking), "copy stream");
+    // H2D of A in row chunks on the copy stream; the exact sketch consumes
+    // each chunk as it lands (its FMA chains run in row order), so only the
+    // last chunk's share of the sketch remains after the transfer
+    static thread_local std::vector<cudaEvent_t> in_ev;
+    int64_t row_end[kInputChunks];
+    int nch = 0;
+    if (dA) {
+        const int64_t tiles = (m + 255) / 256;
+        nch = (int)std::max<int64_t>(1, std::min<int64_t>(kInputChunks, tiles / 64));
+        while ((int)in_ev.size() < nch) {
+            cudaEvent_t ev;
+            CQ_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "input event");
+            in_ev.push_back(ev);
+        }
+        CQ_CUDA(cudaEventRecord(in_ev[0], st), "input order");  // A's buffer is free once st reaches here
+        CQ_CUDA(cudaStreamWaitEvent(copy, in_ev[0], 0), "input order wait");
+        int64_t r0 = 0;
+        for (int c = 0; c < nch; ++c) {
+            const int64_t r1 = (c + 1 == nch) ? m : ((tiles * (c + 1) / nch) * 256);
+            CQ_CUDA(cudaMemcpy2DAsync(dA + r0, sizeof(double) * m, A_host + r0, sizeof(double) * lda,
+                                      sizeof(double) * (r1 - r0), n, cudaMemcpyHostToDevice, copy),
+                    "A h2d");
+            CQ_CUDA(cudaEventRecord(in_ev[c], copy), "input chunk event");
+            row_end[c] = r1;
+            r0 = r1;
+        }
+    }
+    const InputChunks chunks{nch, in_ev.data(), row_end};
     BlockSink sink{copy, Q_host, ldq};
     const int32_t flags = ctx->flags;
     ctx->flags |= CQRRPT_GPU_OUTPUTS_ON_HOST;
     const int rc = dgeqpt_impl(m, n, dA, std::max<int64_t>(m, 1), d_factor, nnz, seed, eps_tol, R_host, ldr, J_host,
-                               k_out, k0_out, ctx, dA ? &sink : nullptr);
+                               k_out, k0_out, ctx, dA ? &sink : nullptr, dA ? &chunks : nullptr);
+    if (dA) CQ_CUDA(cudaStreamWaitEvent(st, in_ev[nch - 1], 0), "input join");  // early returns
     ctx->flags = flags;
     CQ_CUDA(cudaStreamSynchronize(copy), "Q d2h");
     return rc;

@@ -53,8 +53,18 @@ void release_workspace();
 
 // ---- kernels' host entry points (implemented in the .cu files) -------------
 int saso_plan(int64_t d, int64_t c0, int64_t count, int64_t nnz, uint64_t seed, uint32_t *plan, cudaStream_t st);
+// Rows of A still arriving when the sketch is launched: chunk c (rows up to
+// row_end[c], multiples of 256 except the last) is on the device once ev[c]
+// has completed. The exact SASO sketch follows the chunks (its chains run in
+// row order and are carried across launches); other paths wait for all.
+struct InputChunks {
+    int count;
+    const cudaEvent_t *ev;
+    const int64_t *row_end;
+};
 int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, int64_t nnz, uint64_t seed,
-                int64_t c0, double *msk, int64_t ldm, Workspace &ws, cudaStream_t st, bool allow_split = false);
+                int64_t c0, double *msk, int64_t ldm, Workspace &ws, cudaStream_t st, bool allow_split = false,
+                const InputChunks *chunks = nullptr);
 
 // QRCP: fills Rsk (n x n, ldr; rows >= k_sk zero), Jdev (int64 n), k_sk (host).
 int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *rsk, int64_t ldr, int64_t *jdev,

@@ -244,6 +244,8 @@ struct ApplyArgs {
     int nbs;     // block words per tile (whole CTAs of kApplyWarps)
     int stages;  // ring depth (2..4, as many as fit)
     int64_t ntiles, tiles_per_split;
+    int64_t tile_lo, tile_hi;  // tile_hi > 0: this launch takes tiles [tile_lo, tile_hi) (one split)
+    int carry;                 // start the chains from part (a previous launch's tiles)
     const uint2 *tinfo;
     const uint32_t *tent;
     double *part;
@@ -260,8 +262,8 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
     const int64_t j0 = (int64_t)blockIdx.x * 32;
     const int64_t r0 = (int64_t)blockIdx.y * RB;
     const int64_t split = blockIdx.z;
-    const int64_t t_begin = split * P.tiles_per_split;
-    const int64_t t_end = cmin<int64_t>(t_begin + P.tiles_per_split, P.ntiles);
+    const int64_t t_begin = P.tile_hi ? P.tile_lo : split * P.tiles_per_split;
+    const int64_t t_end = P.tile_hi ? P.tile_hi : cmin<int64_t>(t_begin + P.tiles_per_split, P.ntiles);
     const int rows_here = (int)cmin<int64_t>(RB, P.d - r0);  // valid sketch rows in this block
     const int S = P.stages;
 
@@ -332,8 +334,14 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
 
     // ---------------- consumer warps
     double acc[A];
+    {
+        const int wr0c = wid * A;
+        const int64_t colc = j0 + lane;
+        const double *pp = P.part + split * P.d * P.n;
 #pragma unroll
-    for (int q = 0; q < A; ++q) acc[q] = 0.0;
+        for (int q = 0; q < A; ++q)  // carried chains continue bit for bit
+            acc[q] = (P.carry && colc < P.n && wr0c + q < rows_here) ? pp[(r0 + wr0c + q) * P.n + colc] : 0.0;
+    }
     int stg = 0;
     uint32_t use = 0;  // how many times this stage has been filled before the current tile
     const double v = P.val;
@@ -445,7 +453,12 @@ static int launch_apply(ApplyArgs P, dim3 grid, size_t smem, cudaStream_t st) {
 }
 
 int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, int64_t nnz, uint64_t seed,
-                int64_t c0, double *msk, int64_t ldm, Workspace &ws, cudaStream_t st, bool allow_split) {
+                int64_t c0, double *msk, int64_t ldm, Workspace &ws, cudaStream_t st, bool allow_split,
+                const InputChunks *chunks) {
+    const bool follow = chunks && chunks->count > 1 && !allow_split;
+    if (chunks && !follow)
+        for (int c = 0; c < chunks->count; ++c)
+            if (cudaStreamWaitEvent(st, chunks->ev[c], 0) != cudaSuccess) return fail_cuda("sketch wait input");
     if (m <= 0 || n <= 0) {
         // empty shard contributes zeros
         for (int64_t j = 0; j < n; ++j)
@@ -541,7 +554,36 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
     P.tinfo = tinfo;
     P.tent = tent;
     P.part = part;
+    P.tile_lo = 0;
+    P.tile_hi = 0;
+    P.carry = 0;
     dim3 grid((unsigned)cgroups, (unsigned)rblocks, (unsigned)nsplit);
+    auto launch_A = [&](dim3 gr) -> int {
+        switch (A) {
+            case 1: return launch_apply<1>(P, gr, smem, st);
+            case 2: return launch_apply<2>(P, gr, smem, st);
+            case 4: return launch_apply<4>(P, gr, smem, st);
+            case 6: return launch_apply<6>(P, gr, smem, st);
+            case 8: return launch_apply<8>(P, gr, smem, st);
+            default: return launch_apply<12>(P, gr, smem, st);
+        }
+    };
+    if (follow) {  // one launch per arrived chunk of rows, chains carried through `part`
+        int64_t lo = 0;
+        for (int c = 0; c < chunks->count; ++c) {
+            const int64_t hi = std::min<int64_t>(ntiles, (chunks->row_end[c] + kTileRows - 1) / kTileRows);
+            if (cudaStreamWaitEvent(st, chunks->ev[c], 0) != cudaSuccess) return fail_cuda("sketch wait chunk");
+            if (hi <= lo) continue;
+            P.tile_lo = lo;
+            P.tile_hi = hi;
+            if ((rc = launch_A(dim3((unsigned)cgroups, (unsigned)rblocks, 1)))) return rc;
+            P.carry = 1;
+            lo = hi;
+        }
+        P.tile_lo = P.tile_hi = 0;
+        P.carry = 0;
+        nsplit = 1;
+    } else
     switch (A) {
         case 1: rc = launch_apply<1>(P, grid, smem, st); break;
         case 2: rc = launch_apply<2>(P, grid, smem, st); break;

@@ -231,12 +231,14 @@ def test_cxx_reference_signature_adapter(cuda):
     assert "OK" in r.stdout
 
 
-@pytest.mark.parametrize("pinned", [False, True])
-def test_dgeqpt_host_matches_device_path(cuda, oracle, pinned):
+@pytest.mark.parametrize("pinned,m", [(False, 9000), (True, 9000), (True, 70001)])
+def test_dgeqpt_host_matches_device_path(cuda, oracle, pinned, m):
     """cqrrpt_gpu_dgeqpt_host (host in/out, Q streamed back during the final
-    TRSM) gives the device path's factors bit for bit."""
+    TRSM) gives the device path's factors bit for bit. m = 70001: A arrives in
+    4 row chunks and the exact sketch follows them with its chains carried
+    across launches (ragged last chunk)."""
     import torch
-    m, n = 9000, 200
+    n = 200
     a = oracle.gen_gaussian(m, n, 21)
     A = cuda.to_device_colmajor(a)
     dev = cuda.dgeqpt(A, d_factor=1.25, nnz=8, seed=2)
