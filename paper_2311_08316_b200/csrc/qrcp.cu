@@ -90,6 +90,40 @@ CQ_DEVI double chain_finish(double s, int64_t c, FA fa, FB fb, unsigned quad = 0
     return tot;
 }
 
+// lanes 0..3: s += a[e] * b[e] (product rounded, then added) for e = q, q+4,
+// ... < body, in order -- the same bits as adding precomputed products
+// (chain_sum); the loads of group g+1 are issued before the adds of group g
+CQ_DEVI double chain_dot(double s, const double *a, const double *bb, int body, int q) {
+    int e = q;
+    if (e + 28 < body) {
+        double xa[8], xb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            xa[u] = a[e + 4 * u];
+            xb[u] = bb[e + 4 * u];
+        }
+        for (e += 32; e + 28 < body; e += 32) {
+            double na[8], nb[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                na[u] = a[e + 4 * u];
+                nb[u] = bb[e + 4 * u];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s = s + xa[u] * xb[u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                xa[u] = na[u];
+                xb[u] = nb[u];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s = s + xa[u] * xb[u];
+    }
+    for (; e < body; e += 4) s = s + a[e] * bb[e];
+    return s;
+}
+
 // Async L2-coherent copy of g[0..len) into shared memory. The copy starts at
 // the 16-byte aligned address at or below g; returns the element offset of
 // g[0] inside dst (0 or 1). Only bytes inside [g-1, g+len) are read.
@@ -307,6 +341,9 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
     double *wb = smem + wid * WB;                // warp buffer: two halves b0/b1
     double *b0 = wb, *b1 = wb + WB / 2;
     const int CHD = ((WB / 2) - 2) & ~3;         // data doubles per chunk (alignment slack 2)
+    // all-resident phase: a column's rows i..d-1 may use the whole warp buffer
+    // (its norm recompute and next-step tail form their squares on the fly)
+    const int CAPF = (WB - 8) & ~3;
     double *s_x = smem + kQrcpWarps * WB;        // pivot column rows i..d-1 (+ alignment slack)
     double *s_sv = s_x + A.xlen;                 // products, then the scaled reflector (d doubles)
     const double sqrt_u = sqrt(kUnitRoundoff);
@@ -317,7 +354,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
     // the pivot of step i+1) while the grid barrier is in flight; step i+1
     // then reads the pivot's value instead of running that ordered chain.
     auto spec_at = [&](int64_t i) {
-        return !A.general && i >= 0 && (n - i - 1) <= (int64_t)kQrcpWarps * G && (d - i - 1) <= (int64_t)CHD;
+        return !A.general && i >= 0 && (n - i - 1) <= (int64_t)kQrcpWarps * G && (d - i - 1) <= (int64_t)CAPF;
     };
 
     // block argmax carrying the physical column of the winner
@@ -400,7 +437,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
 
         const int64_t jfirst = i + 1 + ((cta - (i + 1)) % G + G) % G;
         const int64_t ncol_cta = (jfirst < n) ? (n - jfirst + G - 1) / G : 0;
-        const bool fast = ncol_cta <= kQrcpWarps && c <= CHD && !A.general;
+        const bool fast = ncol_cta <= kQrcpWarps && c <= CAPF && !A.general;
         int64_t j_w;
         if (fast) {
             const int64_t kf = (jfirst - cta) / G;
@@ -476,7 +513,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
                     r_wref = ld_cg(A.wref + j_w);
                 }
                 const double *colr = A.b + (int64_t)r_pj * ld;
-                const int64_t base = (i - (d - CHD - 1)) & ~(int64_t)1;  // even slot for row i (>= 0)
+                const int64_t base = (i - (d - CAPF - 1)) & ~(int64_t)1;  // even slot for row i (>= 0)
                 const int offr = stage_async(b0 + base, colr + i, d - i, lane, 32);
                 rb = b0 + base + offr - i;
                 cp_async_commit();
@@ -656,12 +693,10 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
                     }
                     __syncwarp();
                 }
-                if (recompute) {
-                    for (int64_t e = lane; e < body; e += 32) b1[e] = cb[e] * cb[e];
-                    __syncwarp();
+                if (recompute) {  // squares formed on the fly (same rounded products)
                     double s2 = 0.0;
                     if (lane < 4) {
-                        s2 = chain_sum(0.0, b1, body, lane);
+                        s2 = chain_dot(0.0, cb, cb, (int)body, lane);
                         s2 = chain_finish(s2, c, [&](int64_t e) { return cb[e]; }, [&](int64_t e) { return cb[e]; });
                     }
                     updated = __shfl_sync(0xffffffffu, s2, 0);
@@ -852,19 +887,11 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
             if (wid == 1) asm volatile("bar.sync 2, 64;" ::: "memory");  // warp 0's column is updated
             const bool two = (wid == 1) && s_coff[0] >= 0;  // set this step
             const double *cbo = two ? smem + s_coff[0] + 1 : nullptr;  // warp 0's rows i+2..
-            double *b1o = smem + WB / 2;                               // warp 0's free half buffer
-            if (spec_has) {
-                const double *cb2 = rb + i + 2;
-                for (int64_t e = lane; e < body2; e += 32) b1[e] = cb2[e] * cb2[e];
-            }
-            if (two)
-                for (int64_t e = lane; e < body2; e += 32) b1o[e] = cbo[e] * cbo[e];
-            __syncwarp();
             const bool mine_q = lane < 4 && spec_has, other_q = lane >= 4 && lane < 8 && two;
             double s2 = 0.0;
-            if (mine_q || other_q) {
+            if (mine_q || other_q) {  // squares formed on the fly (same rounded products)
                 const double *cq = mine_q ? rb + i + 2 : cbo;
-                s2 = chain_sum(0.0, mine_q ? b1 : b1o, body2, lane & 3);
+                s2 = chain_dot(0.0, cq, cq, (int)body2, lane & 3);
                 s2 = chain_finish(s2, c2, [&](int64_t e) { return cq[e]; }, [&](int64_t e) { return cq[e]; },
                                   mine_q ? 0xfu : 0xf0u);
             }
@@ -942,40 +969,6 @@ CQ_DEVI void cl_sync() {
     asm volatile(
         "fence.acq_rel.cluster;\nbarrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
             : "memory");
-}
-
-// lanes 0..3: s += a[e] * b[e] (product rounded, then added) for e = q, q+4,
-// ... < body, in order -- the same bits as adding precomputed products
-// (chain_sum); the loads of group g+1 are issued before the adds of group g
-CQ_DEVI double chain_dot(double s, const double *a, const double *bb, int body, int q) {
-    int e = q;
-    if (e + 28 < body) {
-        double xa[8], xb[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            xa[u] = a[e + 4 * u];
-            xb[u] = bb[e + 4 * u];
-        }
-        for (e += 32; e + 28 < body; e += 32) {
-            double na[8], nb[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                na[u] = a[e + 4 * u];
-                nb[u] = bb[e + 4 * u];
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) s = s + xa[u] * xb[u];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                xa[u] = na[u];
-                xb[u] = nb[u];
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) s = s + xa[u] * xb[u];
-    }
-    for (; e < body; e += 4) s = s + a[e] * bb[e];
-    return s;
 }
 
 // the reference's dot (linalg.cc:36-50) of two shared arrays, one warp
