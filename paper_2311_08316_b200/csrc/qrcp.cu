@@ -124,6 +124,30 @@ CQ_DEVI double chain_dot(double s, const double *a, const double *bb, int body, 
     return s;
 }
 
+// lanes 0..3: s += a[e] * a[e] for e = q, q+4, ... < body, in order (the
+// squares of chain_dot(a, a) with one load per element)
+CQ_DEVI double chain_sq(double s, const double *a, int body, int q) {
+    int e = q;
+    if (e + 28 < body) {
+        double xa[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xa[u] = a[e + 4 * u];
+        for (e += 32; e + 28 < body; e += 32) {
+            double na[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) na[u] = a[e + 4 * u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s = s + xa[u] * xa[u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) xa[u] = na[u];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s = s + xa[u] * xa[u];
+    }
+    for (; e < body; e += 4) s = s + a[e] * a[e];
+    return s;
+}
+
 // Async L2-coherent copy of g[0..len) into shared memory. The copy starts at
 // the 16-byte aligned address at or below g; returns the element offset of
 // g[0] inside dst (0 or 1). Only bytes inside [g-1, g+len) are read.
@@ -696,7 +720,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
                 if (recompute) {  // squares formed on the fly (same rounded products)
                     double s2 = 0.0;
                     if (lane < 4) {
-                        s2 = chain_dot(0.0, cb, cb, (int)body, lane);
+                        s2 = chain_sq(0.0, cb, (int)body, lane);
                         s2 = chain_finish(s2, c, [&](int64_t e) { return cb[e]; }, [&](int64_t e) { return cb[e]; });
                     }
                     updated = __shfl_sync(0xffffffffu, s2, 0);
@@ -891,7 +915,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
             double s2 = 0.0;
             if (mine_q || other_q) {  // squares formed on the fly (same rounded products)
                 const double *cq = mine_q ? rb + i + 2 : cbo;
-                s2 = chain_dot(0.0, cq, cq, (int)body2, lane & 3);
+                s2 = chain_sq(0.0, cq, (int)body2, lane & 3);
                 s2 = chain_finish(s2, c2, [&](int64_t e) { return cq[e]; }, [&](int64_t e) { return cq[e]; },
                                   mine_q ? 0xfu : 0xf0u);
             }
