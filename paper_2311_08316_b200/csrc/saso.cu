@@ -334,13 +334,13 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
 
     // ---------------- consumer warps
     double acc[A];
-    {
-        const int wr0c = wid * A;
-        const int64_t colc = j0 + lane;
-        const double *pp = P.part + split * P.d * P.n;
 #pragma unroll
-        for (int q = 0; q < A; ++q)  // carried chains continue bit for bit
-            acc[q] = (P.carry && colc < P.n && wr0c + q < rows_here) ? pp[(r0 + wr0c + q) * P.n + colc] : 0.0;
+    for (int q = 0; q < A; ++q) acc[q] = 0.0;
+    if (P.carry && j0 + lane < P.n) {  // carried chains continue bit for bit (one split)
+        const double *pp = P.part + (r0 + wid * A) * P.n + j0 + lane;
+#pragma unroll
+        for (int q = 0; q < A; ++q)
+            if (wid * A + q < rows_here) acc[q] = pp[(int64_t)q * P.n];
     }
     int stg = 0;
     uint32_t use = 0;  // how many times this stage has been filled before the current tile
