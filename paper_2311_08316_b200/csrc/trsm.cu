@@ -67,6 +67,12 @@ __global__ void __launch_bounds__(kThreads, 3)
             }
         }
 
+    // Programmatic dependent launch: the next block's grid may start as soon
+    // as every CTA of this one has started; its CTAs gather their source
+    // columns (independent of earlier blocks) and then wait for this grid's
+    // completion before reading X[:, <c0]. No-ops without the launch attribute.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int nchunks = (int)(c0 / kBK);  // c0 is a multiple of 64
     // 16-byte copies of element pairs when X and U are 16-byte aligned with
     // even leading dimensions (the swizzles keep pairs adjacent)
@@ -234,8 +240,21 @@ int trsm_right(int64_t m, int64_t k, const double *b, int64_t ldb, const int64_t
     const unsigned grid = (unsigned)((m + kBM - 1) / kBM);
     static thread_local std::vector<cudaEvent_t> evs;  // one per block, reused across calls
     for (int64_t c0 = 0; c0 < k; c0 += kNB) {
-        trsm_block_kernel<<<grid, kThreads, kTrsmSmem, st>>>(m, k, c0, b, ldb, cols, u, ldu,
-                                                            dinv + (c0 / kNB) * kNB * kNB, x, ldx);
+        {
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.gridDim = dim3(grid);
+            cfg.blockDim = dim3(kThreads);
+            cfg.dynamicSmemBytes = kTrsmSmem;
+            cfg.stream = st;
+            cfg.attrs = at;
+            cfg.numAttrs = c0 > 0 ? 1 : 0;  // the first block follows trtri_diag normally
+            CQ_CUDA(cudaLaunchKernelEx(&cfg, trsm_block_kernel, m, k, c0, b, ldb, cols, u, ldu,
+                                       (const double *)(dinv + (c0 / kNB) * kNB * kNB), x, ldx),
+                    "trsm launch");
+        }
         note_launch();
         if (sink) {  // block c0 is final: download it while the next blocks run
             const size_t e = (size_t)(c0 / kNB);
