@@ -373,7 +373,7 @@ int dgeqpt_impl(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, i
     }
 
     // ---- Q = M_pre[:, :k] R_pre^{-1}, in place into A[:, :k] ----------------
-    CQ_TRY(trsm_right(m, k, mpre, ldp, nullptr, rfull, k0, A, lda, st, qsink));
+    CQ_TRY(trsm_right(m, k, mpre, ldp, nullptr, rfull, k0, A, lda, st, qsink, /*check_diag=*/false));
     clk.mark(PH_CHOL);
 
     // ---- R = R_pre R_sk[:k, :] (upper-trapezoidal) --------------------------
@@ -589,7 +589,8 @@ int cholqr_pass(int64_t m, int64_t n, double *A, int64_t lda, double *r, int64_t
     CQ_TRY(gram(m, n, A, lda, r, ldr, ws, st));
     CQ_TRY(potrf(n, r, ldr, failure_index, ws, st));
     if (*failure_index > 0) return 0;
-    return trsm_right(m, n, A, lda, nullptr, r, ldr, A, lda, st);  // in place: block jb reads B[:, jb] first
+    // in place (block jb reads B[:, jb] first); r is potrf's factor: no zero diagonal
+    return trsm_right(m, n, A, lda, nullptr, r, ldr, A, lda, st, nullptr, /*check_diag=*/false);
 }
 }  // namespace
 

@@ -79,8 +79,11 @@ struct BlockSink {
     double *host;
     int64_t ldh;
 };
+// check_diag = false: U is a Cholesky factor from potrf (diagonal sqrt(d),
+// d > 0), so the zero-diagonal check (a host synchronisation) is skipped
 int trsm_right(int64_t m, int64_t k, const double *b, int64_t ldb, const int64_t *cols, const double *u,
-               int64_t ldu, double *x, int64_t ldx, cudaStream_t st, const BlockSink *sink = nullptr);
+               int64_t ldu, double *x, int64_t ldx, cudaStream_t st, const BlockSink *sink = nullptr,
+               bool check_diag = true);
 int gram(int64_t m, int64_t k, const double *x, int64_t ldx, double *g, int64_t ldg, Workspace &ws,
          cudaStream_t st);
 // C (M x N, ldc) = alpha * op(A) * B + beta * C; op(A) = A (M x K) or A^T (A is K x M).

@@ -217,19 +217,21 @@ __global__ void diag_zero_check_kernel(int64_t k, const double *__restrict__ u, 
 }
 
 int trsm_right(int64_t m, int64_t k, const double *b, int64_t ldb, const int64_t *cols, const double *u,
-               int64_t ldu, double *x, int64_t ldx, cudaStream_t st, const BlockSink *sink) {
+               int64_t ldu, double *x, int64_t ldx, cudaStream_t st, const BlockSink *sink, bool check_diag) {
     if (m <= 0 || k <= 0) return 0;
-    // zero diagonal -> the reference throws std::domain_error (linalg.cc:250-252)
-    int *flag = workspace().get<int>("trsm.flag", 1);
-    CQ_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st), "memset flag");
-    diag_zero_check_kernel<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(k, u, ldu, flag);
-    note_launch();
-    int hflag = 0;
-    CQ_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "flag d2h");
-    CQ_CUDA(cudaStreamSynchronize(st), "trsm sync");
-    if (hflag) {
-        set_error("trsm_right: singular preconditioner (zero diagonal)");
-        return CQRRPT_GPU_ERR_SINGULAR;
+    if (check_diag) {
+        // zero diagonal -> the reference throws std::domain_error (linalg.cc:250-252)
+        int *flag = workspace().get<int>("trsm.flag", 1);
+        CQ_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st), "memset flag");
+        diag_zero_check_kernel<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(k, u, ldu, flag);
+        note_launch();
+        int hflag = 0;
+        CQ_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "flag d2h");
+        CQ_CUDA(cudaStreamSynchronize(st), "trsm sync");
+        if (hflag) {
+            set_error("trsm_right: singular preconditioner (zero diagonal)");
+            return CQRRPT_GPU_ERR_SINGULAR;
+        }
     }
     CQ_CUDA(cudaFuncSetAttribute(trsm_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrsmSmem),
             "trsm smem attr");
