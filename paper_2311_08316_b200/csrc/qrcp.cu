@@ -230,6 +230,81 @@ CQ_DEVI double stream_dot(const double *sa, const double *g, int64_t c, double *
     return __shfl_sync(0xffffffffu, tot, 0);
 }
 
+// Two reference dots at once, sa.ga[0..c) and sa.gb[0..c): both columns
+// stream through quarter buffers (chunk CQ, double-buffered: even chunks in
+// b0, odd ones in b1, A in the first half of each, B in the second), all
+// lanes form the products in place, lanes 0..3 run A's ordered chain and
+// lanes 4..7 B's in the same instructions. With one chunk the products go to
+// the other half-buffer so the columns stay staged (*kept) for the update.
+// Returns the dots in lanes 0 (A) and 4 (B), broadcast.
+CQ_DEVI void stream_dot2(const double *sa, const double *ga, const double *gb, int64_t c, double *b0, double *b1,
+                         int CQ, bool *kept, int lane, double *dota, double *dotb) {
+    const int QS = CQ + 4;  // quarter stride (alignment slack)
+    const int offa = (int)((reinterpret_cast<uintptr_t>(ga) >> 3) & 1);
+    const int offb = (int)((reinterpret_cast<uintptr_t>(gb) >> 3) & 1);
+    const int64_t body = c & ~(int64_t)3;
+    const int64_t nch = (c + CQ - 1) / CQ;
+    *kept = (nch == 1);
+    auto qa = [&](int64_t k) { return ((k & 1) ? b1 : b0); };
+    auto qb = [&](int64_t k) { return ((k & 1) ? b1 : b0) + QS; };
+    if (nch > 0) {
+        stage_async(qa(0), ga, cmin<int64_t>(CQ, c), lane, 32);
+        stage_async(qb(0), gb, cmin<int64_t>(CQ, c), lane, 32);
+        cp_async_commit();
+    }
+    const bool mine = lane < 8;
+    const int q = lane & 3;
+    double s = 0.0;
+    for (int64_t k = 0; k < nch; ++k) {
+        if (k + 1 < nch) {
+            const int64_t nb = (k + 1) * CQ, nl = cmin<int64_t>(CQ, c - nb);
+            stage_async(qa(k + 1), ga + nb, nl, lane, 32);
+            stage_async(qb(k + 1), gb + nb, nl, lane, 32);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncwarp();
+        double *bufa = qa(k) + offa, *bufb = qb(k) + offb;
+        const int64_t base = k * CQ;
+        const int bl = (int)cmax<int64_t>(0, cmin<int64_t>(CQ, body - base));
+        double *pa = (nch == 1) ? b1 + 2 : bufa;  // products (past the data when kept)
+        double *pb = (nch == 1) ? b1 + 2 + QS : bufb;
+        for (int e0 = lane; e0 < bl; e0 += 128) {
+            double xa[4], xb[4], xs[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + 32 * u;
+                xs[u] = e < bl ? sa[base + e] : 0.0;
+                xa[u] = e < bl ? bufa[e] : 0.0;
+                xb[u] = e < bl ? bufb[e] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + 32 * u;
+                if (e < bl) {
+                    pa[e] = xs[u] * xa[u];
+                    pb[e] = xs[u] * xb[u];
+                }
+            }
+        }
+        __syncwarp();
+        if (mine) s = chain_sum(s, lane < 4 ? pa : pb, bl, q);
+        __syncwarp();
+    }
+    // the <4 tail elements are still in the last chunk's buffers
+    const int64_t lastbase = (nch - 1) * CQ;
+    const double *la = qa(nch - 1) + offa - lastbase, *lb = qb(nch - 1) + offb - lastbase;
+    double tot = 0.0;
+    if (lane < 4)
+        tot = chain_finish(s, c, [&](int64_t x) { return sa[x]; }, [&](int64_t x) { return la[x]; }, 0xfu);
+    else if (lane < 8)
+        tot = chain_finish(s, c, [&](int64_t x) { return sa[x]; }, [&](int64_t x) { return lb[x]; }, 0xf0u);
+    *dota = __shfl_sync(0xffffffffu, tot, 0);
+    *dotb = __shfl_sync(0xffffffffu, tot, 4);
+}
+
 // Per-CTA argmax records double as the grid barrier. A record is four 8-byte
 // words, each carrying the step flag in its high half, so a reader that sees
 // the flag in all four words holds the whole record (8-byte accesses are
@@ -368,6 +443,8 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
     // all-resident phase: a column's rows i..d-1 may use the whole warp buffer
     // (its norm recompute and next-step tail form their squares on the fly)
     const int CAPF = (WB - 8) & ~3;
+    // general phase, two columns per warp at once: quarter-buffer chunks
+    const int CQ = ((WB / 2 - 12) / 2) & ~3;
     double *s_x = smem + kQrcpWarps * WB;        // pivot column rows i..d-1 (+ alignment slack)
     double *s_sv = s_x + A.xlen;                 // products, then the scaled reflector (d doubles)
     const double sqrt_u = sqrt(kUnitRoundoff);
@@ -474,7 +551,8 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         // by this CTA at the previous step)
         int32_t pj0 = 0;
         double wj0 = 0.0, wrefj0 = 0.0, t0 = 0.0;
-        if (!fast && j_w < n) {
+        const bool pair_first = !fast && j_w + (int64_t)kQrcpWarps * G < n;  // first iteration takes two columns
+        if (!fast && j_w < n && !pair_first) {
             pj0 = ld_cg(A.cmap[cur] + j_w);
             wj0 = ld_cg(A.w[cur] + j_w);
             wrefj0 = ld_cg(A.wref + j_w);
@@ -745,6 +823,110 @@ __global__ void __launch_bounds__(kQrcpThreads, 1) qrcp_kernel(QrcpArgs A) {
         }
         bool first = true;
         for (int64_t j = fast ? n : j_w; j < n; j += (int64_t)kQrcpWarps * G, first = false) {
+            if (j + (int64_t)kQrcpWarps * G < n) {
+                // ---- two columns at once (the second is this warp's next) ----
+                const int64_t jB = j + (int64_t)kQrcpWarps * G;
+                int32_t pjA, pjB;
+                double wA, wB, wrA, wrB, tA, tB;
+                {
+                    const int64_t jsA = (j == p) ? i : j, jsB = (jB == p) ? i : jB;
+                    pjA = ld_cg(A.cmap[cur] + jsA);
+                    pjB = ld_cg(A.cmap[cur] + jsB);
+                    wA = ld_cg(A.w[cur] + jsA);
+                    wB = ld_cg(A.w[cur] + jsB);
+                    wrA = ld_cg(A.wref + jsA);
+                    wrB = ld_cg(A.wref + jsB);
+                    tA = ld_cg(A.b + (int64_t)pjA * ld + i);
+                    tB = ld_cg(A.b + (int64_t)pjB * ld + i);
+                }
+                double *colA = A.b + (int64_t)pjA * ld, *colB = A.b + (int64_t)pjB * ld;
+                double *tailA = colA + i + 1, *tailB = colB + i + 1;
+                const int QS = CQ + 4;
+                const int offA = (int)((reinterpret_cast<uintptr_t>(tailA) >> 3) & 1);
+                const int offB = (int)((reinterpret_cast<uintptr_t>(tailB) >> 3) & 1);
+                __syncwarp();
+                if (beta != 0.0) {  // apply_reflector (linalg.cc:126-136) to both
+                    bool kept2 = false;
+                    double dA, dB;
+                    stream_dot2(sv, tailA, tailB, c, b0, b1, CQ, &kept2, lane, &dA, &dB);
+                    double tauA = tA, tauB = tB;
+                    tauA += dA;
+                    tauB += dB;
+                    tauA *= beta;
+                    tauB *= beta;
+                    tA = tA - tauA;
+                    tB = tB - tauB;
+                    if (kept2) {  // both columns still staged in b0
+                        const double *cbA = b0 + offA, *cbB = b0 + QS + offB;
+                        for (int64_t e = lane; e < c; e += 32) {
+                            const double sve = sv[e];
+                            __stcg(tailA + e, fma(-tauA, sve, cbA[e]));
+                            __stcg(tailB + e, fma(-tauB, sve, cbB[e]));
+                        }
+                    } else {  // restream both (double-buffered quarter chunks)
+                        const int64_t nch = (c + CQ - 1) / CQ;
+                        stage_async(b0, tailA, cmin<int64_t>(CQ, c), lane, 32);
+                        stage_async(b0 + QS, tailB, cmin<int64_t>(CQ, c), lane, 32);
+                        cp_async_commit();
+                        for (int64_t kk = 0; kk < nch; ++kk) {
+                            if (kk + 1 < nch) {
+                                const int64_t nb = (kk + 1) * CQ, nl = cmin<int64_t>(CQ, c - nb);
+                                double *h = ((kk + 1) & 1) ? b1 : b0;
+                                stage_async(h, tailA + nb, nl, lane, 32);
+                                stage_async(h + QS, tailB + nb, nl, lane, 32);
+                                cp_async_commit();
+                                cp_async_wait<1>();
+                            } else {
+                                cp_async_wait<0>();
+                            }
+                            __syncwarp();
+                            const double *h = (kk & 1) ? b1 : b0;
+                            const double *bufA = h + offA, *bufB = h + QS + offB;
+                            const int64_t base = kk * CQ, len = cmin<int64_t>(CQ, c - base);
+#pragma unroll 4
+                            for (int64_t e = lane; e < len; e += 32) {
+                                const double sve = sv[base + e];
+                                __stcg(tailA + base + e, fma(-tauA, sve, bufA[e]));
+                                __stcg(tailB + base + e, fma(-tauB, sve, bufB[e]));
+                            }
+                            __syncwarp();
+                        }
+                    }
+                    __syncwarp();
+                }
+                // downdates (qrcp.cc:77-88); a recompute re-reads the updated column
+                double updA = fma(-tA, tA, wA), updB = fma(-tB, tB, wB);
+                double refA = wrA, refB = wrB;
+                if (updA <= sqrt_u * wrA) {
+                    bool k2;
+                    updA = stream_dot(nullptr, tailA, c, b0, b1, CHD, false, &k2, lane);
+                    refA = updA;
+                }
+                if (updB <= sqrt_u * wrB) {
+                    bool k2;
+                    updB = stream_dot(nullptr, tailB, c, b0, b1, CHD, false, &k2, lane);
+                    refB = updB;
+                }
+                if (lane == 0) {
+                    __stcg(colA + i, tA);
+                    __stcg(A.w[nxt] + j, updA);
+                    __stcg(A.wref + j, refA);
+                    __stcg(A.cmap[nxt] + j, pjA);
+                    __stcg(colB + i, tB);
+                    __stcg(A.w[nxt] + jB, updB);
+                    __stcg(A.wref + jB, refB);
+                    __stcg(A.cmap[nxt] + jB, pjB);
+                }
+                ArgMax cnd = argmax_combine(mine, ArgMax{updA, (int32_t)j});
+                if (cnd.i != mine.i) minep = pjA;
+                mine = cnd;
+                cnd = argmax_combine(mine, ArgMax{updB, (int32_t)jB});
+                if (cnd.i != mine.i) minep = pjB;
+                mine = cnd;
+                __syncwarp();
+                j = jB;  // the loop step moves past the pair
+                continue;
+            }
             const bool isp = (j == p);
             int32_t pj;
             double wj, wrefj, t;
