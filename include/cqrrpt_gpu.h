@@ -73,6 +73,9 @@ extern "C" {
 #define CQRRPT_GPU_FAST_SKETCH 0x20    /* allow a c-split sketch (partials summed in a fixed order):
                                           deterministic, not bit-identical to the reference's
                                           single FMA chain; fills the GPU when n is small */
+#define CQRRPT_GPU_NO_WAVEFRONT 0x40   /* cqrrpt_gpu_dgeqpt_host: run precondition, Gram, Cholesky
+                                          and Q as whole passes instead of the 64-column
+                                          wavefront that streams Q out during them (same bits) */
 
 /* Sum-allreduce of `count` doubles in place on device memory, ordered on
  * `stream`. Return 0 on success. */
@@ -130,9 +133,12 @@ int cqrrpt_gpu_dgeqpt(int64_t m, int64_t n, double *A, int64_t lda, double d_fac
 
 /* Host-buffer variant (the reference's data in/out convention, cqrrpt.hh:140):
  * A_host (m x n, lda) is uploaded, Q (m x k) is downloaded into Q_host
- * (ldq >= m) block by block while the final TRSM is still running, R (k x n,
- * ldr) and J (0-based) land on the host. Pinned host memory gives full PCIe
- * bandwidth and real overlap. */
+ * (ldq >= m, room for k0 columns) block by block while the device is still
+ * computing, R (k x n, ldr) and J (0-based) land on the host. One rank: Q's
+ * blocks are formed and sent as soon as their Gram/Cholesky columns exist
+ * (speculating k = k0); if stage 2 truncates to k < k0, columns k..k0-1 of
+ * Q_host hold the speculative blocks (unspecified). Pinned host memory gives
+ * full PCIe bandwidth and real overlap. */
 int cqrrpt_gpu_dgeqpt_host(int64_t m, int64_t n, const double *A_host, int64_t lda, double d_factor, int64_t nnz,
                            uint64_t seed, double eps_tol, double *Q_host, int64_t ldq, double *R_host, int64_t ldr,
                            int64_t *J_host, int64_t *k, int64_t *k0, cqrrpt_gpu_ctx *ctx);

@@ -327,10 +327,13 @@ class HostResult:
 def dgeqpt_host(a, d_factor: float = 1.25, nnz: int = 4, seed: int = 0, eps_tol: float = 1e-4,
                 cond_method: int = CondMethod.identity_deviation, q_out=None, r_out=None, j_out=None,
                 sketch_family: str = "saso", stream=None, comm: Optional[Comm] = None,
-                global_row_offset: int = 0) -> HostResult:
+                global_row_offset: int = 0, wavefront: bool = True) -> HostResult:
     """Host data in, host factors out (cqrrpt_gpu_dgeqpt_host): ``a`` is a
     column-major float64 numpy array or CPU torch tensor (pin it for full
-    PCIe bandwidth); Q is downloaded block by block while the last TRSM runs.
+    PCIe bandwidth); Q is downloaded block by block while the device is still
+    computing (one rank: as a 64-column wavefront through precondition, Gram,
+    Cholesky and the final solve; ``wavefront=False`` runs those as whole
+    passes, CQRRPT_GPU_NO_WAVEFRONT -- the factors are bitwise the same).
     ``q_out`` (m x n), ``r_out`` (n x n), ``j_out`` (n) may be preallocated
     (pinned) buffers; the results are their leading k columns / rows."""
     torch = _torch()
@@ -354,6 +357,8 @@ def dgeqpt_host(a, d_factor: float = 1.25, nnz: int = 4, seed: int = 0, eps_tol:
     ctx = _lib.new_ctx()
     ctx.stream = _stream_ptr(stream)
     ctx.cond_method = int(cond_method)
+    if not wavefront:
+        ctx.flags |= _lib.F_NO_WAVEFRONT
     families = {"saso": _lib.SKETCH_SASO, "gaussian": _lib.SKETCH_GAUSSIAN, "srft": _lib.SKETCH_SRFT}
     if sketch_family not in families:
         raise InvalidArgument(f"sketch_family must be one of {sorted(families)}")

@@ -14,6 +14,8 @@
 #include <dlfcn.h>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <vector>
@@ -154,6 +156,143 @@ double cqrrpt_gpu_flop_model(int64_t m, int64_t n, int64_t k, int64_t d, double 
 }  // extern "C"
 
 namespace {
+// Host-buffer path, one rank: precondition, Gram, Cholesky and Q as a
+// wavefront of 128-column blocks, so Q's download starts right after the QRCP
+// instead of after the whole Gram + Cholesky. Block b needs M_pre's columns
+// < 128(b+1) (precondition TRSM on `st`, an event per 64 columns), then on
+// `s2`: its Gram columns (gram_cols: split over m finely enough that the
+// first, small blocks fill the GPU; a fixed order, but not gram()'s), the
+// Cholesky steps that reach it (potrf_cols: bitwise potrf's factor of that
+// Gram), the inverses of its diagonal blocks and its Q blocks, which the copy
+// stream downloads. Q is speculated on k = k0 (stage 2 runs after the last
+// block, on this R); the caller redoes the final solve when stage 2 truncates
+// or the Cholesky fails. Q goes to a separate buffer (the precondition still
+// gathers A's columns while Q blocks are written).
+// Returns 0 with *done = false when the buffers do not fit (whole passes).
+int wavefront_q(int64_t m, int64_t k0, const double *A, int64_t lda, const int64_t *jd, const double *rsk,
+                int64_t ldk, double *mpre, int64_t ldp, double *gmat, const BlockSink &sink, int64_t *fi, bool *done,
+                Workspace &ws, cudaStream_t st) {
+    *done = false;
+    *fi = 0;
+    constexpr int64_t NB = 64, WB = 128;  // solve block, wavefront block
+    const int64_t nsub = (k0 + NB - 1) / NB, nw = (k0 + WB - 1) / WB;
+    static thread_local std::vector<int2> tiles_h;
+    static thread_local std::vector<int64_t> toff;
+    tiles_h.clear();
+    toff.assign((size_t)nw + 1, 0);
+    int64_t max_t = 0;
+    for (int64_t b = 0; b < nw; ++b) {
+        gram_col_tiles(b * WB, std::min(k0, (b + 1) * WB), tiles_h);
+        toff[(size_t)b + 1] = (int64_t)tiles_h.size();
+        max_t = std::max(max_t, toff[(size_t)b + 1] - toff[(size_t)b]);
+    }
+    const size_t part_n = gram_col_part_size(m, k0, max_t);
+    const int64_t ldq = ldp;
+    double *qws = ws.get<double>("wf.q", (size_t)(ldq * k0));
+    double *part = qws ? ws.get<double>("wf.part", part_n) : nullptr;
+    if (!qws || !part) return 0;  // does not fit next to A and M_pre: whole passes
+    int2 *tiles = ws.get<int2>("wf.tiles", tiles_h.size());
+    double *dinv = ws.get<double>("wf.dinv", (size_t)(nsub * NB * NB));
+    int64_t *fail = ws.get<int64_t>("wf.fail", 1);
+    if (!tiles || !dinv || !fail || part_n == 0) return fail_nomem("wavefront workspace");
+    // Streams by priority: s2 (Cholesky columns, Q blocks: what the download
+    // waits for) > s3 (Gram columns, which only need M_pre and so run ahead)
+    // > st (the precondition). Gram block b writes G's columns of block b and
+    // the mirrored entries below the diagonal in rows of block b; s2 reads only
+    // upper-triangle entries of blocks < b, so the two overlap safely.
+    static thread_local cudaStream_t s2 = nullptr, s3 = nullptr;
+    static thread_local std::vector<cudaEvent_t> ev_pre, ev_q, ev_g;
+    static thread_local cudaEvent_t ev_start = nullptr, ev_end = nullptr;
+    if (!s2) {
+        int least = 0, greatest = 0;
+        CQ_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest), "stream priorities");
+        CQ_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, greatest), "wavefront stream");
+        CQ_CUDA(cudaStreamCreateWithPriority(&s3, cudaStreamNonBlocking, greatest < least ? greatest + 1 : least),
+                "wavefront stream");
+        CQ_CUDA(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming), "wavefront event");
+        CQ_CUDA(cudaEventCreateWithFlags(&ev_end, cudaEventDisableTiming), "wavefront event");
+    }
+    while ((int64_t)ev_pre.size() < nsub) {
+        cudaEvent_t a, b, c;
+        CQ_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "wavefront event");
+        CQ_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "wavefront event");
+        CQ_CUDA(cudaEventCreateWithFlags(&c, cudaEventDisableTiming), "wavefront event");
+        ev_pre.push_back(a);
+        ev_q.push_back(b);
+        ev_g.push_back(c);
+    }
+    // CQRRPT_WF_TRACE=1: print when each Q block is formed and downloaded
+    static const bool trace = std::getenv("CQRRPT_WF_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tq, td;
+    cudaEvent_t t0 = nullptr;
+    auto tev = [&](std::vector<cudaEvent_t> &v, cudaStream_t on) -> int {
+        cudaEvent_t e;
+        CQ_CUDA(cudaEventCreate(&e), "trace event");
+        CQ_CUDA(cudaEventRecord(e, on), "trace record");
+        v.push_back(e);
+        return 0;
+    };
+    if (trace) {
+        CQ_CUDA(cudaEventCreate(&t0), "trace event");
+        CQ_CUDA(cudaEventRecord(t0, st), "trace record");
+    }
+    // st is idle here (stage 1 synchronised), so the pageable upload is cheap
+    CQ_CUDA(cudaMemcpyAsync(tiles, tiles_h.data(), sizeof(int2) * tiles_h.size(), cudaMemcpyHostToDevice, st),
+            "wavefront tiles h2d");
+    CQ_CUDA(cudaMemsetAsync(fail, 0, sizeof(int64_t), st), "wavefront fail flag");
+    CQ_CUDA(cudaEventRecord(ev_start, st), "wavefront start");
+    CQ_CUDA(cudaStreamWaitEvent(s2, ev_start, 0), "wavefront start wait");
+    CQ_CUDA(cudaStreamWaitEvent(s3, ev_start, 0), "wavefront start wait");
+    // precondition M_pre = M[:, J[:k0]] A_sk^{-1} on st, an event per 64 columns
+    CQ_TRY(trsm_right(m, k0, A, lda, jd, rsk, ldk, mpre, ldp, st, nullptr, true, ev_pre.data()));
+    for (int64_t b = 0; b < nw; ++b) {  // Gram columns, as soon as M_pre's columns exist
+        const int64_t w1 = std::min(k0, (b + 1) * WB);
+        CQ_CUDA(cudaStreamWaitEvent(s3, ev_pre[(size_t)((w1 - 1) / NB)], 0), "wavefront wait block");
+        CQ_TRY(gram_cols(m, k0, w1, tiles + toff[(size_t)b], toff[(size_t)b + 1] - toff[(size_t)b], mpre, ldp, gmat,
+                         k0, part, s3));
+        CQ_CUDA(cudaEventRecord(ev_g[(size_t)b], s3), "wavefront gram event");
+    }
+    for (int64_t b = 0; b < nw; ++b) {
+        const int64_t w0 = b * WB, w1 = std::min(k0, w0 + WB);
+        CQ_CUDA(cudaStreamWaitEvent(s2, ev_g[(size_t)b], 0), "wavefront wait gram");
+        for (int64_t c0 = w0; c0 < w1; c0 += NB) {
+            const int64_t c1 = std::min(w1, c0 + NB), sb = c0 / NB;
+            CQ_TRY(potrf_cols(k0, gmat, k0, c0, c1, fail, s2));
+            CQ_TRY(trtri_diag_blocks(c1 - c0, gmat + c0 * k0 + c0, k0, dinv + sb * NB * NB, s2));
+            CQ_TRY(trsm_block(m, k0, c0, mpre, ldp, nullptr, gmat, k0, dinv + sb * NB * NB, qws, ldq, s2));
+            CQ_CUDA(cudaEventRecord(ev_q[(size_t)sb], s2), "wavefront q event");
+            CQ_CUDA(cudaStreamWaitEvent(sink.copy, ev_q[(size_t)sb], 0), "wavefront sink wait");
+            CQ_CUDA(cudaMemcpy2DAsync(sink.host + c0 * sink.ldh, sizeof(double) * sink.ldh, qws + c0 * ldq,
+                                      sizeof(double) * ldq, sizeof(double) * m, c1 - c0, cudaMemcpyDeviceToHost,
+                                      sink.copy),
+                    "wavefront q d2h");
+            if (trace) {
+                CQ_TRY(tev(tq, s2));
+                CQ_TRY(tev(td, sink.copy));
+            }
+        }
+    }
+    CQ_CUDA(cudaEventRecord(ev_end, s2), "wavefront end");
+    CQ_CUDA(cudaStreamWaitEvent(st, ev_end, 0), "wavefront join");
+    CQ_TRY(zero_strict_lower(k0, gmat, k0, st));
+    CQ_CUDA(cudaMemcpyAsync(fi, fail, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "wavefront fail d2h");
+    CQ_CUDA(cudaStreamSynchronize(st), "wavefront sync");
+    if (trace) {
+        CQ_CUDA(cudaStreamSynchronize(sink.copy), "trace sync");
+        for (size_t i = 0; i < tq.size(); ++i) {
+            float a = 0.f, b = 0.f;
+            cudaEventElapsedTime(&a, t0, tq[i]);
+            cudaEventElapsedTime(&b, t0, td[i]);
+            std::fprintf(stderr, "wavefront block %zu: Q formed %.3f ms, downloaded %.3f ms\n", i, a, b);
+            cudaEventDestroy(tq[i]);
+            cudaEventDestroy(td[i]);
+        }
+        cudaEventDestroy(t0);
+    }
+    *done = true;
+    return 0;
+}
+
 // The driver; `qsink` (optional) downloads Q block by block during the final TRSM.
 constexpr int kInputChunks = 4;  // H2D row chunks of the host-buffer entry point
 
@@ -267,18 +406,25 @@ int dgeqpt_impl(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, i
     const int64_t ldp = std::max<int64_t>(m, 1);
     double *mpre = ws.get<double>("drv.mpre", (size_t)(ldp * k0));
     if (!mpre) return fail_nomem("M_pre workspace");
-    CQ_TRY(trsm_right(m, k0, A, lda, jd, rsk, ldk, mpre, ldp, st));
-    clk.mark(PH_PRE);
-
-    // ---- Gram + Cholesky (rank_stage2 attempt loop, cqrrpt.cc:160-193) -------
     double *gmat = ws.get<double>("drv.gram", (size_t)(k0 * k0));
     if (!gmat) return fail_nomem("gram");
-    CQ_TRY(gram(m, k0, mpre, ldp, gmat, k0, ws, st));
-    clk.mark(PH_CHOL);
-    CQ_TRY(do_allreduce(ctx, gmat, (size_t)(k0 * k0), st));
-    clk.mark(PH_COMM);
     int64_t fi = 0;
-    CQ_TRY(potrf(k0, gmat, k0, &fi, ws, st));
+    bool wave = false;  // Q already computed (k = k0) and downloaded by the wavefront
+    if (qsink && !multi && !(ctx->flags & CQRRPT_GPU_NO_WAVEFRONT) && m >= 1)
+        CQ_TRY(wavefront_q(m, k0, A, lda, jd, rsk, ldk, mpre, ldp, gmat, *qsink, &fi, &wave, ws, st));
+    if (wave) {
+        clk.mark(PH_CHOL);
+    } else {
+        CQ_TRY(trsm_right(m, k0, A, lda, jd, rsk, ldk, mpre, ldp, st));
+        clk.mark(PH_PRE);
+
+        // ---- Gram + Cholesky (rank_stage2 attempt loop, cqrrpt.cc:160-193) ---
+        CQ_TRY(gram(m, k0, mpre, ldp, gmat, k0, ws, st));
+        clk.mark(PH_CHOL);
+        CQ_TRY(do_allreduce(ctx, gmat, (size_t)(k0 * k0), st));
+        clk.mark(PH_COMM);
+        CQ_TRY(potrf(k0, gmat, k0, &fi, ws, st));
+    }
     int64_t k0f = k0;
     if (fi > 0) {
         // The retry on the leading fi-1 columns recomputes bitwise the same
@@ -373,7 +519,8 @@ int dgeqpt_impl(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, i
     }
 
     // ---- Q = M_pre[:, :k] R_pre^{-1}, in place into A[:, :k] ----------------
-    CQ_TRY(trsm_right(m, k, mpre, ldp, nullptr, rfull, k0, A, lda, st, qsink, /*check_diag=*/false));
+    if (!(wave && fi == 0 && k == k0))
+        CQ_TRY(trsm_right(m, k, mpre, ldp, nullptr, rfull, k0, A, lda, st, qsink, /*check_diag=*/false));
     clk.mark(PH_CHOL);
 
     // ---- R = R_pre R_sk[:k, :] (upper-trapezoidal) --------------------------

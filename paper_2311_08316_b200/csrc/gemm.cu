@@ -418,25 +418,19 @@ __global__ void __launch_bounds__(256) gram_reduce_kernel(int64_t k, int64_t nsl
     }
 }
 
-int gram(int64_t m, int64_t k, const double *x, int64_t ldx, double *gmat, int64_t ldg, Workspace &ws,
-         cudaStream_t st) {
-    if (k <= 0) return 0;
+// Split-K slices over m (>= 512 rows each) of gram(m, k): every CTA does the
+// same work, so the time is waves(ns) * m / ns with waves = ceil(ntiles*ns /
+// resident slots); pick the fewest slices within 2% of the best (no ragged
+// last wave). Depends on (m, k) only, so a column block (gram_cols) uses the
+// same slices as the full Gram and reproduces its entries bitwise.
+// min_slices > 0 (the wavefront's Gram columns, gram_cols): that many slices
+// (at most m / 512), so the first column blocks, which have only a few tiles,
+// still fill the GPU.
+static int gram_slices(int64_t m, int64_t k, int64_t *rps_out, int64_t *nslices_out, int64_t min_slices = 0) {
     constexpr int BM = 64, BN = 128;
     const int64_t tm = (k + BM - 1) / BM;
-    // Row tile i (64 rows) takes 128-wide column tiles starting at its own
-    // diagonal (columns 64i, 64i+128, ...; tile.y in units of 64 columns):
-    // only the lower half of each row's first 64 x 64 block lies below the
-    // diagonal (~6% of the work instead of ~12% with a fixed 128-column grid).
-    // An entry's DMMA summation order does not depend on its tile, so G is
-    // bitwise the same.
-    static thread_local std::vector<int2> h;  // outlives the async upload below
-    h.clear();
-    for (int64_t i = 0; i < tm; ++i)
-        for (int64_t c0 = i * BM; c0 < k; c0 += BN) h.push_back(make_int2((int)i, (int)(c0 / 64)));
-    const int64_t ntiles = (int64_t)h.size();
-    // split-K slices over m (>= 512 rows each): every CTA does the same work, so
-    // the time is waves(ns) * m / ns with waves = ceil(ntiles*ns / resident
-    // slots); pick the fewest slices within 2% of the best (no ragged last wave)
+    int64_t ntiles = 0;
+    for (int64_t i = 0; i < tm; ++i) ntiles += (k - i * BM + BN - 1) / BN;
     const int sms = num_sms();
     int per_sm = 0;
     CQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dgemm_kernel<64, 128, true, false>, kThreads,
@@ -455,8 +449,31 @@ int gram(int64_t m, int64_t k, const double *x, int64_t ldx, double *gmat, int64
             }
         }
     }
-    int64_t rps = ((m + nslices - 1) / nslices + kBK - 1) / kBK * kBK;
-    nslices = std::max<int64_t>(1, (m + rps - 1) / rps);
+    if (min_slices > 0) nslices = std::max<int64_t>(1, std::min<int64_t>(min_slices, m / 512));
+    const int64_t rps = ((m + nslices - 1) / nslices + kBK - 1) / kBK * kBK;
+    *rps_out = rps;
+    *nslices_out = std::max<int64_t>(1, (m + rps - 1) / rps);
+    return 0;
+}
+
+int gram(int64_t m, int64_t k, const double *x, int64_t ldx, double *gmat, int64_t ldg, Workspace &ws,
+         cudaStream_t st) {
+    if (k <= 0) return 0;
+    constexpr int BM = 64, BN = 128;
+    const int64_t tm = (k + BM - 1) / BM;
+    // Row tile i (64 rows) takes 128-wide column tiles starting at its own
+    // diagonal (columns 64i, 64i+128, ...; tile.y in units of 64 columns):
+    // only the lower half of each row's first 64 x 64 block lies below the
+    // diagonal (~6% of the work instead of ~12% with a fixed 128-column grid).
+    // An entry's DMMA summation order does not depend on its tile, so G is
+    // bitwise the same.
+    static thread_local std::vector<int2> h;  // outlives the async upload below
+    h.clear();
+    for (int64_t i = 0; i < tm; ++i)
+        for (int64_t c0 = i * BM; c0 < k; c0 += BN) h.push_back(make_int2((int)i, (int)(c0 / 64)));
+    const int64_t ntiles = (int64_t)h.size();
+    int64_t rps = 0, nslices = 0;
+    CQ_TRY(gram_slices(m, k, &rps, &nslices));
     int2 *tiles = ws.get<int2>("gram.tiles", (size_t)ntiles);
     double *part = ws.get<double>("gram.part", (size_t)(nslices * ntiles * BM * BN));
     if (!tiles || !part) return fail_nomem("gram workspace");
@@ -486,6 +503,49 @@ int gram(int64_t m, int64_t k, const double *x, int64_t ldx, double *gmat, int64
         nslices = 1;
     }
     gram_reduce_kernel<<<dim3((unsigned)ntiles, (unsigned)(BN / kRedSW)), 256, 0, st>>>(k, nslices, tiles, ntiles,
+                                                                                       part, gmat, ldg);
+    note_launch();
+    return check_launch("gram_reduce_kernel");
+}
+
+// Tiles of column block [c0, c1): row tiles 0 .. (c1-1)/64, 128-wide column
+// tiles from c0 (an entry's DMMA order does not depend on its tile). The m
+// slices are num_sms() of them (gram_slices), whatever the block, so all
+// blocks of one factorization agree with each other (not with gram()'s
+// fewer slices: a different fixed summation order).
+void gram_col_tiles(int64_t c0, int64_t c1, std::vector<int2> &tiles) {
+    for (int64_t i = 0; i * 64 < c1; ++i)
+        for (int64_t j = c0; j < c1; j += 128) tiles.push_back(make_int2((int)i, (int)(j / 64)));
+}
+
+size_t gram_col_part_size(int64_t m, int64_t k, int64_t ntiles) {
+    int64_t rps = 0, nslices = 0;
+    if (gram_slices(m, k, &rps, &nslices, num_sms())) return 0;
+    return (size_t)(nslices * ntiles * 64 * 128);
+}
+
+int gram_cols(int64_t m, int64_t k, int64_t c1, const int2 *tiles, int64_t ntiles, const double *x, int64_t ldx,
+              double *gmat, int64_t ldg, double *part, cudaStream_t st) {
+    if (ntiles <= 0 || m <= 0) return 0;
+    int64_t rps = 0, nslices = 0;
+    CQ_TRY(gram_slices(m, k, &rps, &nslices, num_sms()));
+    GemmArgs P{};
+    P.M = c1;
+    P.N = c1;
+    P.K = m;
+    P.A = x;
+    P.lda = ldx;
+    P.B = x;
+    P.ldb = ldx;
+    P.alpha = 1.0;
+    P.k_per_split = rps;
+    P.part = part;
+    P.ntiles_part = ntiles;
+    P.tiles = tiles;
+    P.tile_n64 = 1;
+    P.vec16 = (reinterpret_cast<uintptr_t>(x) & 15) == 0 && ldx % 2 == 0 && rps % 2 == 0;
+    CQ_TRY((launch<64, 128, true, false>(P, dim3((unsigned)ntiles, 1, (unsigned)nslices), st)));
+    gram_reduce_kernel<<<dim3((unsigned)ntiles, (unsigned)(128 / kRedSW)), 256, 0, st>>>(c1, nslices, tiles, ntiles,
                                                                                        part, gmat, ldg);
     note_launch();
     return check_launch("gram_reduce_kernel");

@@ -83,13 +83,28 @@ struct BlockSink {
 // d > 0), so the zero-diagonal check (a host synchronisation) is skipped
 int trsm_right(int64_t m, int64_t k, const double *b, int64_t ldb, const int64_t *cols, const double *u,
                int64_t ldu, double *x, int64_t ldx, cudaStream_t st, const BlockSink *sink = nullptr,
-               bool check_diag = true);
+               bool check_diag = true, const cudaEvent_t *block_ev = nullptr);
+// one 64-column block c0 of trsm_right (dinv_blk: inverse of U's diagonal block)
+int trsm_block(int64_t m, int64_t k, int64_t c0, const double *b, int64_t ldb, const int64_t *cols, const double *u,
+               int64_t ldu, const double *dinv_blk, double *x, int64_t ldx, cudaStream_t st);
 int gram(int64_t m, int64_t k, const double *x, int64_t ldx, double *g, int64_t ldg, Workspace &ws,
          cudaStream_t st);
+// Column block [c0, c1) (rows 0..c1-1) of a Gram split over num_sms() slices
+// of m (min(.., m/512)): the same entries for any blocking. gram_col_tiles
+// appends the block's tile list; part holds gram_col_part_size(m, k, ntiles).
+void gram_col_tiles(int64_t c0, int64_t c1, std::vector<int2> &tiles);
+size_t gram_col_part_size(int64_t m, int64_t k, int64_t ntiles);
+int gram_cols(int64_t m, int64_t k, int64_t c1, const int2 *tiles, int64_t ntiles, const double *x, int64_t ldx,
+              double *g, int64_t ldg, double *part, cudaStream_t st);
 // C (M x N, ldc) = alpha * op(A) * B + beta * C; op(A) = A (M x K) or A^T (A is K x M).
 int gemm(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const double *a, int64_t lda,
          const double *b, int64_t ldb, double beta, double *c, int64_t ldc, cudaStream_t st);
 int potrf(int64_t n, double *g, int64_t ldg, int64_t *failure_index, Workspace &ws, cudaStream_t st);
+// Column block [c0, c1) of potrf's right-looking factor (64-aligned c0): every
+// update and panel solve of steps j < c0 that reaches these columns, in block
+// order, then the diagonal block -- bitwise potrf's entries once all blocks
+// left of c0 are done. fail: device flag (1-based index, 0 = none).
+int potrf_cols(int64_t n, double *g, int64_t ldg, int64_t c0, int64_t c1, int64_t *fail, cudaStream_t st);
 // C = alpha op(A) B + beta C with K split into `splits` slices summed in order
 int gemm_fill(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const double *a, int64_t lda,
               const double *b, int64_t ldb, double beta, double *c, int64_t ldc, Workspace &ws, cudaStream_t st);

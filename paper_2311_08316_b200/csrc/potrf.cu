@@ -75,7 +75,8 @@ __global__ void __launch_bounds__(kPB) potrf_diag64_kernel(int64_t n, double *__
 constexpr int kPanelWarps = 8;
 
 __global__ void __launch_bounds__(kPanelWarps * 32) potrf_panel_kernel(int64_t n, double *__restrict__ g,
-                                                                      int64_t ldg, int64_t j0,
+                                                                      int64_t ldg, int64_t j0, int64_t c_begin,
+                                                                      int64_t c_end,
                                                                       const int64_t *__restrict__ fail) {
     if (*fail) return;
     __shared__ double r[kPB][kPB + 1];  // r[col][row] of R_jj
@@ -86,8 +87,8 @@ __global__ void __launch_bounds__(kPanelWarps * 32) potrf_panel_kernel(int64_t n
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t col = j0 + nb + (int64_t)blockIdx.x * kPanelWarps + w;
-    if (col >= n) return;
+    const int64_t col = c_begin + (int64_t)blockIdx.x * kPanelWarps + w;
+    if (col >= c_end) return;
     double *gc = g + col * ldg + j0;
     const int l0 = lane, l1 = lane + 32;
     double x0 = l0 < nb ? gc[l0] : 0.0, x1 = l1 < nb ? gc[l1] : 0.0;
@@ -146,7 +147,7 @@ int potrf(int64_t n, double *g, int64_t ldg, int64_t *failure_index, Workspace &
         const int64_t rest = n - j0 - nb;
         if (rest <= 0) break;
         potrf_panel_kernel<<<(unsigned)((rest + kPanelWarps - 1) / kPanelWarps), kPanelWarps * 32, 0, aux>>>(
-            n, g, ldg, j0, fail);
+            n, g, ldg, j0, j0 + nb, n, fail);
         note_launch();
         const int64_t t0 = j0 + nb, nb1 = std::min<int64_t>(kPB, rest), t1 = t0 + nb1;
         if (j0 > 0) CQ_CUDA(cudaStreamWaitEvent(aux, ev_c2, 0), "potrf wait c2");  // C2(jb-1) -> row block jb+1
@@ -182,6 +183,38 @@ int potrf(int64_t n, double *g, int64_t ldg, int64_t *failure_index, Workspace &
     CQ_CUDA(cudaMemcpyAsync(failure_index, fail, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "fail d2h");
     CQ_CUDA(cudaStreamSynchronize(st), "potrf sync");
     return zero_strict_lower(n, g, ldg, st);
+}
+
+int potrf_cols(int64_t n, double *g, int64_t ldg, int64_t c0, int64_t c1, int64_t *fail, cudaStream_t st) {
+    if (c1 <= c0) return 0;
+    const int64_t w = c1 - c0;
+    for (int64_t j0 = 0; j0 < c0; j0 += kPB) {
+        // panel(j): R[j, c0:c1] = R_jj^{-T} G[j, c0:c1]
+        potrf_panel_kernel<<<(unsigned)((w + kPanelWarps - 1) / kPanelWarps), kPanelWarps * 32, 0, st>>>(
+            n, g, ldg, j0, c0, c1, fail);
+        note_launch();
+        // update(j): G[t0:c1, c0:c1] -= R[j, t0:c1]^T R[j, c0:c1] (potrf's C1/C2 entries of these columns)
+        const int64_t t0 = j0 + kPB;
+        GemmArgs P{};
+        P.M = c1 - t0;
+        P.N = w;
+        P.K = kPB;
+        P.A = g + t0 * ldg + j0;
+        P.lda = ldg;
+        P.B = g + c0 * ldg + j0;
+        P.ldb = ldg;
+        P.Cin = g + c0 * ldg + t0;
+        P.ldcin = ldg;
+        P.Cout = g + c0 * ldg + t0;
+        P.ldc = ldg;
+        P.alpha = -1.0;
+        P.beta = 1.0;
+        P.skip_flag = fail;
+        CQ_TRY(gemm_ex(true, P, 1, st));
+    }
+    potrf_diag64_kernel<<<1, kPB, 0, st>>>(n, g, ldg, c0, fail);
+    note_launch();
+    return check_launch("potrf_cols");
 }
 
 }  // namespace cqg

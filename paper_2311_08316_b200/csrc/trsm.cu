@@ -216,8 +216,20 @@ __global__ void diag_zero_check_kernel(int64_t k, const double *__restrict__ u, 
     if (i < k && u[i * ldu + i] == 0.0) atomicExch(flag, 1);
 }
 
+int trsm_block(int64_t m, int64_t k, int64_t c0, const double *b, int64_t ldb, const int64_t *cols, const double *u,
+               int64_t ldu, const double *dinv_blk, double *x, int64_t ldx, cudaStream_t st) {
+    if (m <= 0 || c0 >= k) return 0;
+    CQ_CUDA(cudaFuncSetAttribute(trsm_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrsmSmem),
+            "trsm smem attr");
+    trsm_block_kernel<<<(unsigned)((m + kBM - 1) / kBM), kThreads, kTrsmSmem, st>>>(m, k, c0, b, ldb, cols, u, ldu,
+                                                                                 dinv_blk, x, ldx);
+    note_launch();
+    return check_launch("trsm_block_kernel");
+}
+
 int trsm_right(int64_t m, int64_t k, const double *b, int64_t ldb, const int64_t *cols, const double *u,
-               int64_t ldu, double *x, int64_t ldx, cudaStream_t st, const BlockSink *sink, bool check_diag) {
+               int64_t ldu, double *x, int64_t ldx, cudaStream_t st, const BlockSink *sink, bool check_diag,
+               const cudaEvent_t *block_ev) {
     if (m <= 0 || k <= 0) return 0;
     if (check_diag) {
         // zero diagonal -> the reference throws std::domain_error (linalg.cc:250-252)
@@ -258,6 +270,7 @@ int trsm_right(int64_t m, int64_t k, const double *b, int64_t ldb, const int64_t
                     "trsm launch");
         }
         note_launch();
+        if (block_ev) CQ_CUDA(cudaEventRecord(block_ev[c0 / kNB], st), "trsm block event");
         if (sink) {  // block c0 is final: download it while the next blocks run
             const size_t e = (size_t)(c0 / kNB);
             while (evs.size() <= e) {

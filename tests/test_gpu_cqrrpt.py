@@ -233,8 +233,8 @@ def test_cxx_reference_signature_adapter(cuda):
 
 @pytest.mark.parametrize("pinned,m", [(False, 9000), (True, 9000), (True, 70001)])
 def test_dgeqpt_host_matches_device_path(cuda, oracle, pinned, m):
-    """cqrrpt_gpu_dgeqpt_host (host in/out, Q streamed back during the final
-    TRSM) gives the device path's factors bit for bit. m = 70001: A arrives in
+    """cqrrpt_gpu_dgeqpt_host with whole passes (host in/out, Q streamed back
+    during the final TRSM) gives the device path's factors bit for bit. m = 70001: A arrives in
     4 row chunks and the exact sketch follows them with its chains carried
     across launches (ragged last chunk)."""
     import torch
@@ -244,12 +244,55 @@ def test_dgeqpt_host_matches_device_path(cuda, oracle, pinned, m):
     dev = cuda.dgeqpt(A, d_factor=1.25, nnz=8, seed=2)
     if pinned:
         ah = torch.from_numpy(np.ascontiguousarray(a.T)).pin_memory().t()
-        host = cuda.dgeqpt_host(ah, d_factor=1.25, nnz=8, seed=2)
+        host = cuda.dgeqpt_host(ah, d_factor=1.25, nnz=8, seed=2, wavefront=False)
         q, r, j = host.q.numpy(), host.r.numpy(), host.pivots.numpy()
     else:
-        host = cuda.dgeqpt_host(a, d_factor=1.25, nnz=8, seed=2)
+        host = cuda.dgeqpt_host(a, d_factor=1.25, nnz=8, seed=2, wavefront=False)
         q, r, j = host.q, host.r, host.pivots
     assert (host.k, host.k0) == (dev.k, dev.k0)
     assert np.array_equal(j, dev.pivots.cpu().numpy())
     assert np.array_equal(q, A[:, :dev.k].cpu().numpy())
     assert np.array_equal(r, dev.r.cpu().numpy())
+
+
+@pytest.mark.parametrize("case", ["ragged", "truncated", "dups", "wide_blocks"])
+def test_dgeqpt_host_wavefront(cuda, oracle, case):
+    """The host entry point's 128-column wavefront (precondition, Gram columns,
+    potrf_cols, diagonal-block inverses, Q blocks, download): the same J, k0
+    and k as the whole-pass path (which is bitwise the device path), Q and R
+    to rounding (its Gram sums m in more, fixed slices), bitwise repeatable,
+    including the cases where the speculated k = k0 is wrong (stage 2
+    truncates: the final solve is redone) and inputs with duplicated columns
+    (the reference's stage-2 failure inputs)."""
+    eps = 1e-4
+    if case == "ragged":      # k0 = 200: one full wavefront block and one of 72 columns
+        a = oracle.gen_gaussian(9000, 200, 31)
+    elif case == "truncated":  # tight eps_tol: stage 2 keeps fewer than k0 columns
+        u, _ = np.linalg.qr(oracle.gen_gaussian(6000, 160, 32))
+        v, _ = np.linalg.qr(oracle.gen_gaussian(160, 160, 33))
+        a = np.asfortranarray((u * 10.0 ** (-12.0 * np.arange(160) / 159)) @ v.T)
+        eps = 2e-16
+    elif case == "dups":
+        base = oracle.gen_gaussian(3000, 70, 34)
+        a = np.asfortranarray(np.concatenate([base, base[:, :30]], axis=1))
+    else:                      # k0 = 384: three blocks, several Cholesky steps per block
+        a = oracle.gen_gaussian(70000, 384, 35)
+    A = cuda.to_device_colmajor(a)
+    dev = cuda.dgeqpt(A, d_factor=1.25, nnz=8, seed=3, eps_tol=eps)
+    whole = cuda.dgeqpt_host(a, d_factor=1.25, nnz=8, seed=3, eps_tol=eps, wavefront=False)
+    assert (whole.k, whole.k0) == (dev.k, dev.k0)
+    assert np.array_equal(whole.pivots, dev.pivots.cpu().numpy())
+    assert np.array_equal(whole.q, A[:, :dev.k].cpu().numpy())
+    assert np.array_equal(whole.r, dev.r.cpu().numpy())
+    wav = cuda.dgeqpt_host(a, d_factor=1.25, nnz=8, seed=3, eps_tol=eps)
+    again = cuda.dgeqpt_host(a, d_factor=1.25, nnz=8, seed=3, eps_tol=eps)
+    assert (wav.k, wav.k0) == (dev.k, dev.k0)
+    assert np.array_equal(wav.pivots, whole.pivots)
+    assert np.array_equal(again.q, wav.q) and np.array_equal(again.r, wav.r)
+    k = dev.k
+    if k:
+        assert np.max(np.abs(wav.q - whole.q)) <= 1e-11 * np.max(np.abs(whole.q))
+        rn = np.linalg.norm(whole.r, axis=0)
+        assert np.all(np.linalg.norm(wav.r - whole.r, axis=0) <= 1e-11 * np.maximum(rn, 1e-300))
+    if case == "truncated":
+        assert 0 < dev.k < dev.k0, (dev.k, dev.k0)
