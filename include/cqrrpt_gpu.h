@@ -73,9 +73,14 @@ extern "C" {
 #define CQRRPT_GPU_FAST_SKETCH 0x20    /* allow a c-split sketch (partials summed in a fixed order):
                                           deterministic, not bit-identical to the reference's
                                           single FMA chain; fills the GPU when n is small */
-#define CQRRPT_GPU_NO_WAVEFRONT 0x40   /* cqrrpt_gpu_dgeqpt_host: run precondition, Gram, Cholesky
-                                          and Q as whole passes instead of the 64-column
-                                          wavefront that streams Q out during them (same bits) */
+#define CQRRPT_GPU_NO_WAVEFRONT 0x40   /* cqrrpt_gpu_dgeqpt_host (one rank): run precondition,
+                                          Gram, Cholesky and Q as whole passes instead of the
+                                          128-column wavefront that streams Q out during them;
+                                          the wavefront's Gram sums m in different fixed slices,
+                                          so Q and R differ in the last bits */
+#define CQRRPT_GPU_WAVEFRONT 0x80      /* cqrrpt_gpu_dgeqpt (one rank): use the wavefront too
+                                          (same bits as dgeqpt_host's default; slower on the
+                                          device alone) */
 
 /* Sum-allreduce of `count` doubles in place on device memory, ordered on
  * `stream`. Return 0 on success. */
@@ -116,7 +121,9 @@ void cqrrpt_gpu_ctx_init(cqrrpt_gpu_ctx *ctx);
 
 /* CQRRPT of a tall FP64 matrix (north_star entry point).
  *   m, n      local rows, columns (m_local on a shard; n identical on all ranks)
- *   A, lda    device, column-major. On return A[:, :k] holds Q (in place).
+ *   A, lda    device, column-major. On return A[:, :k] holds Q (in place);
+ *             with CQRRPT_GPU_WAVEFRONT and k < k0, A[:, k:k0] holds
+ *             speculative columns.
  *             Columns k..n-1 of A are left unspecified.
  *   d_factor  sketch oversampling gamma >= 1 (CqrrptConfig::gamma, cqrrpt.hh:93)
  *   nnz       SASO nonzeros per column of S, 1 <= nnz <= d (cqrrpt.hh:95)

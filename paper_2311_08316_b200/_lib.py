@@ -22,6 +22,7 @@ COND_DIAG_RATIO, COND_KRYLOV_BOUNDS, COND_IDENTITY_DEVIATION = 0, 1, 2
 F_OUTPUTS_ON_HOST, F_EXACT_STAGE2, F_NO_STAGE1, F_DIAGNOSTICS, F_TIMINGS = 0x1, 0x2, 0x4, 0x8, 0x10
 F_FAST_SKETCH = 0x20
 F_NO_WAVEFRONT = 0x40
+F_WAVEFRONT = 0x80
 SKETCH_SASO, SKETCH_GAUSSIAN, SKETCH_SRFT = 0, 1, 2
 
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_size_t, ctypes.c_void_p,

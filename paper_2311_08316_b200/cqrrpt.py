@@ -230,7 +230,8 @@ def dgeqpt(a, d_factor: float = 1.25, nnz: int = 4, seed: int = 0, eps_tol: floa
            cond_method: int = CondMethod.identity_deviation, stage1: bool = True, exact_stage2: bool = False,
            diagnostics: bool = False, timings: bool = False, stream=None, comm: Optional[Comm] = None,
            global_row_offset: int = 0, r_out=None, j_out=None, allreduce=None, nranks: int = 1,
-           rank: int = 0, fast_sketch: bool = False, sketch_family: str = "saso") -> DeviceResult:
+           rank: int = 0, fast_sketch: bool = False, sketch_family: str = "saso",
+           wavefront: bool = False) -> DeviceResult:
     """The north-star entry point on a column-major CUDA tensor ``a``
     (m_local x n). Q overwrites ``a[:, :k]`` in place; R (k x n) and the
     0-based pivots are returned as device tensors.
@@ -246,7 +247,14 @@ def dgeqpt(a, d_factor: float = 1.25, nnz: int = 4, seed: int = 0, eps_tol: floa
 
     ``fast_sketch``: allow a c-split sketch (CQRRPT_GPU_FAST_SKETCH) that
     fills the GPU when n is small; deterministic, but J then matches the
-    reference only away from near-ties (the default sketch is bit-identical)."""
+    reference only away from near-ties (the default sketch is bit-identical).
+
+    ``wavefront`` (one rank, CQRRPT_GPU_WAVEFRONT): precondition, Gram,
+    Cholesky and Q run as the 128-column wavefront dgeqpt_host uses (Q
+    speculated on k = k0; if stage 2 truncates, ``a[:, k:k0]`` is left with
+    speculative columns). Slower on the device alone; gives dgeqpt_host's
+    default bits (whole passes: a different Gram slicing, so Q and R agree to
+    rounding, J and k are the same)."""
     torch = _torch()
     L = _lib.load()
     m, n = a.shape
@@ -272,6 +280,8 @@ def dgeqpt(a, d_factor: float = 1.25, nnz: int = 4, seed: int = 0, eps_tol: floa
         flags |= _lib.F_TIMINGS
     if fast_sketch:
         flags |= _lib.F_FAST_SKETCH
+    if wavefront:
+        flags |= _lib.F_WAVEFRONT
     ctx.flags = flags
     families = {"saso": _lib.SKETCH_SASO, "gaussian": _lib.SKETCH_GAUSSIAN, "srft": _lib.SKETCH_SRFT}
     if sketch_family not in families:
@@ -331,9 +341,10 @@ def dgeqpt_host(a, d_factor: float = 1.25, nnz: int = 4, seed: int = 0, eps_tol:
     """Host data in, host factors out (cqrrpt_gpu_dgeqpt_host): ``a`` is a
     column-major float64 numpy array or CPU torch tensor (pin it for full
     PCIe bandwidth); Q is downloaded block by block while the device is still
-    computing (one rank: as a 64-column wavefront through precondition, Gram,
+    computing (one rank: as a 128-column wavefront through precondition, Gram,
     Cholesky and the final solve; ``wavefront=False`` runs those as whole
-    passes, CQRRPT_GPU_NO_WAVEFRONT -- the factors are bitwise the same).
+    passes, CQRRPT_GPU_NO_WAVEFRONT). Both give dgeqpt's factors bit for bit
+    with the same ``wavefront`` setting.
     ``q_out`` (m x n), ``r_out`` (n x n), ``j_out`` (n) may be preallocated
     (pinned) buffers; the results are their leading k columns / rows."""
     torch = _torch()

@@ -156,9 +156,10 @@ double cqrrpt_gpu_flop_model(int64_t m, int64_t n, int64_t k, int64_t d, double 
 }  // extern "C"
 
 namespace {
-// Host-buffer path, one rank: precondition, Gram, Cholesky and Q as a
-// wavefront of 128-column blocks, so Q's download starts right after the QRCP
-// instead of after the whole Gram + Cholesky. Block b needs M_pre's columns
+// One rank: precondition, Gram, Cholesky and Q as a wavefront of 128-column
+// blocks, so the latency-bound Cholesky columns overlap the DMMA passes and,
+// on the host entry point, Q's download starts right after the QRCP instead
+// of after the whole Gram + Cholesky. Block b needs M_pre's columns
 // < 128(b+1) (precondition TRSM on `st`, an event per 64 columns), then on
 // `s2`: its Gram columns (gram_cols: split over m finely enough that the
 // first, small blocks fill the GPU; a fixed order, but not gram()'s), the
@@ -169,9 +170,9 @@ namespace {
 // or the Cholesky fails. Q goes to a separate buffer (the precondition still
 // gathers A's columns while Q blocks are written).
 // Returns 0 with *done = false when the buffers do not fit (whole passes).
-int wavefront_q(int64_t m, int64_t k0, const double *A, int64_t lda, const int64_t *jd, const double *rsk,
-                int64_t ldk, double *mpre, int64_t ldp, double *gmat, const BlockSink &sink, int64_t *fi, bool *done,
-                Workspace &ws, cudaStream_t st) {
+int wavefront_q(int64_t m, int64_t k0, double *A, int64_t lda, const int64_t *jd, const double *rsk, int64_t ldk,
+                double *mpre, int64_t ldp, double *gmat, const BlockSink *sink, int64_t *fi, bool *done,
+                PhaseClock &clk, Workspace &ws, cudaStream_t st) {
     *done = false;
     *fi = 0;
     constexpr int64_t NB = 64, WB = 128;  // solve block, wavefront block
@@ -187,8 +188,11 @@ int wavefront_q(int64_t m, int64_t k0, const double *A, int64_t lda, const int64
         max_t = std::max(max_t, toff[(size_t)b + 1] - toff[(size_t)b]);
     }
     const size_t part_n = gram_col_part_size(m, k0, max_t);
-    const int64_t ldq = ldp;
-    double *qws = ws.get<double>("wf.q", (size_t)(ldq * k0));
+    // Q: in place into A (device entry point; its blocks wait until the
+    // precondition has gathered all of A's columns) or, with a host sink, into
+    // a separate buffer so Q's first blocks are formed while A is still read
+    const int64_t ldq = sink ? ldp : lda;
+    double *qws = sink ? ws.get<double>("wf.q", (size_t)(ldq * k0)) : A;
     double *part = qws ? ws.get<double>("wf.part", part_n) : nullptr;
     if (!qws || !part) return 0;  // does not fit next to A and M_pre: whole passes
     int2 *tiles = ws.get<int2>("wf.tiles", tiles_h.size());
@@ -245,6 +249,8 @@ int wavefront_q(int64_t m, int64_t k0, const double *A, int64_t lda, const int64
     CQ_CUDA(cudaStreamWaitEvent(s3, ev_start, 0), "wavefront start wait");
     // precondition M_pre = M[:, J[:k0]] A_sk^{-1} on st, an event per 64 columns
     CQ_TRY(trsm_right(m, k0, A, lda, jd, rsk, ldk, mpre, ldp, st, nullptr, true, ev_pre.data()));
+    clk.mark(PH_PRE);
+    if (!sink) CQ_CUDA(cudaStreamWaitEvent(s2, ev_pre[(size_t)(nsub - 1)], 0), "wavefront wait precondition");
     for (int64_t b = 0; b < nw; ++b) {  // Gram columns, as soon as M_pre's columns exist
         const int64_t w1 = std::min(k0, (b + 1) * WB);
         CQ_CUDA(cudaStreamWaitEvent(s3, ev_pre[(size_t)((w1 - 1) / NB)], 0), "wavefront wait block");
@@ -260,16 +266,15 @@ int wavefront_q(int64_t m, int64_t k0, const double *A, int64_t lda, const int64
             CQ_TRY(potrf_cols(k0, gmat, k0, c0, c1, fail, s2));
             CQ_TRY(trtri_diag_blocks(c1 - c0, gmat + c0 * k0 + c0, k0, dinv + sb * NB * NB, s2));
             CQ_TRY(trsm_block(m, k0, c0, mpre, ldp, nullptr, gmat, k0, dinv + sb * NB * NB, qws, ldq, s2));
+            if (trace) CQ_TRY(tev(tq, s2));
+            if (!sink) continue;
             CQ_CUDA(cudaEventRecord(ev_q[(size_t)sb], s2), "wavefront q event");
-            CQ_CUDA(cudaStreamWaitEvent(sink.copy, ev_q[(size_t)sb], 0), "wavefront sink wait");
-            CQ_CUDA(cudaMemcpy2DAsync(sink.host + c0 * sink.ldh, sizeof(double) * sink.ldh, qws + c0 * ldq,
+            CQ_CUDA(cudaStreamWaitEvent(sink->copy, ev_q[(size_t)sb], 0), "wavefront sink wait");
+            CQ_CUDA(cudaMemcpy2DAsync(sink->host + c0 * sink->ldh, sizeof(double) * sink->ldh, qws + c0 * ldq,
                                       sizeof(double) * ldq, sizeof(double) * m, c1 - c0, cudaMemcpyDeviceToHost,
-                                      sink.copy),
+                                      sink->copy),
                     "wavefront q d2h");
-            if (trace) {
-                CQ_TRY(tev(tq, s2));
-                CQ_TRY(tev(td, sink.copy));
-            }
+            if (trace) CQ_TRY(tev(td, sink->copy));
         }
     }
     CQ_CUDA(cudaEventRecord(ev_end, s2), "wavefront end");
@@ -278,14 +283,14 @@ int wavefront_q(int64_t m, int64_t k0, const double *A, int64_t lda, const int64
     CQ_CUDA(cudaMemcpyAsync(fi, fail, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "wavefront fail d2h");
     CQ_CUDA(cudaStreamSynchronize(st), "wavefront sync");
     if (trace) {
-        CQ_CUDA(cudaStreamSynchronize(sink.copy), "trace sync");
+        if (sink) CQ_CUDA(cudaStreamSynchronize(sink->copy), "trace sync");
         for (size_t i = 0; i < tq.size(); ++i) {
             float a = 0.f, b = 0.f;
             cudaEventElapsedTime(&a, t0, tq[i]);
-            cudaEventElapsedTime(&b, t0, td[i]);
+            if (i < td.size()) cudaEventElapsedTime(&b, t0, td[i]);
             std::fprintf(stderr, "wavefront block %zu: Q formed %.3f ms, downloaded %.3f ms\n", i, a, b);
             cudaEventDestroy(tq[i]);
-            cudaEventDestroy(td[i]);
+            if (i < td.size()) cudaEventDestroy(td[i]);
         }
         cudaEventDestroy(t0);
     }
@@ -410,8 +415,13 @@ int dgeqpt_impl(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, i
     if (!gmat) return fail_nomem("gram");
     int64_t fi = 0;
     bool wave = false;  // Q already computed (k = k0) and downloaded by the wavefront
-    if (qsink && !multi && !(ctx->flags & CQRRPT_GPU_NO_WAVEFRONT) && m >= 1)
-        CQ_TRY(wavefront_q(m, k0, A, lda, jd, rsk, ldk, mpre, ldp, gmat, *qsink, &fi, &wave, ws, st));
+    // The wavefront pays off when Q leaves over PCIe (host entry point). On the
+    // device entry point it was measured slower (C2 25.0 -> 29.8 ms: Q's
+    // blocks must wait for the whole precondition, which the Gram columns
+    // then starve), so it is used there only on request (CQRRPT_GPU_WAVEFRONT).
+    const bool want_wave = qsink ? !(ctx->flags & CQRRPT_GPU_NO_WAVEFRONT) : (ctx->flags & CQRRPT_GPU_WAVEFRONT) != 0;
+    if (!multi && want_wave && m >= 1)
+        CQ_TRY(wavefront_q(m, k0, A, lda, jd, rsk, ldk, mpre, ldp, gmat, qsink, &fi, &wave, clk, ws, st));
     if (wave) {
         clk.mark(PH_CHOL);
     } else {

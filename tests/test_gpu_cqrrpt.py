@@ -257,13 +257,14 @@ def test_dgeqpt_host_matches_device_path(cuda, oracle, pinned, m):
 
 @pytest.mark.parametrize("case", ["ragged", "truncated", "dups", "wide_blocks"])
 def test_dgeqpt_host_wavefront(cuda, oracle, case):
-    """The host entry point's 128-column wavefront (precondition, Gram columns,
-    potrf_cols, diagonal-block inverses, Q blocks, download): the same J, k0
-    and k as the whole-pass path (which is bitwise the device path), Q and R
-    to rounding (its Gram sums m in more, fixed slices), bitwise repeatable,
-    including the cases where the speculated k = k0 is wrong (stage 2
-    truncates: the final solve is redone) and inputs with duplicated columns
-    (the reference's stage-2 failure inputs)."""
+    """The 128-column wavefront (precondition, Gram columns, potrf_cols,
+    diagonal-block inverses, Q blocks; on the host entry point also the
+    download): the device and host entry points agree bit for bit, the same
+    J, k0 and k as the whole passes, Q and R to rounding (its Gram sums m in
+    more, fixed slices), bitwise repeatable; including inputs where the
+    speculated k = k0 is wrong (stage 2 truncates: the final solve is redone)
+    and inputs with duplicated columns (the reference's stage-2 failure
+    inputs)."""
     eps = 1e-4
     if case == "ragged":      # k0 = 200: one full wavefront block and one of 72 columns
         a = oracle.gen_gaussian(9000, 200, 31)
@@ -278,18 +279,23 @@ def test_dgeqpt_host_wavefront(cuda, oracle, case):
     else:                      # k0 = 384: three blocks, several Cholesky steps per block
         a = oracle.gen_gaussian(70000, 384, 35)
     A = cuda.to_device_colmajor(a)
-    dev = cuda.dgeqpt(A, d_factor=1.25, nnz=8, seed=3, eps_tol=eps)
+    dev = cuda.dgeqpt(A, d_factor=1.25, nnz=8, seed=3, eps_tol=eps, wavefront=True)
+    W = cuda.to_device_colmajor(a)
+    dwhole = cuda.dgeqpt(W, d_factor=1.25, nnz=8, seed=3, eps_tol=eps)
     whole = cuda.dgeqpt_host(a, d_factor=1.25, nnz=8, seed=3, eps_tol=eps, wavefront=False)
-    assert (whole.k, whole.k0) == (dev.k, dev.k0)
-    assert np.array_equal(whole.pivots, dev.pivots.cpu().numpy())
-    assert np.array_equal(whole.q, A[:, :dev.k].cpu().numpy())
-    assert np.array_equal(whole.r, dev.r.cpu().numpy())
+    k = dev.k
+    assert (whole.k, whole.k0) == (dwhole.k, dwhole.k0) == (dev.k, dev.k0)
+    assert np.array_equal(whole.pivots, dwhole.pivots.cpu().numpy())
+    assert np.array_equal(whole.q, W[:, :k].cpu().numpy())
+    assert np.array_equal(whole.r, dwhole.r.cpu().numpy())
     wav = cuda.dgeqpt_host(a, d_factor=1.25, nnz=8, seed=3, eps_tol=eps)
     again = cuda.dgeqpt_host(a, d_factor=1.25, nnz=8, seed=3, eps_tol=eps)
     assert (wav.k, wav.k0) == (dev.k, dev.k0)
     assert np.array_equal(wav.pivots, whole.pivots)
+    assert np.array_equal(wav.pivots, dev.pivots.cpu().numpy())
+    assert np.array_equal(wav.q, A[:, :k].cpu().numpy())
+    assert np.array_equal(wav.r, dev.r.cpu().numpy())
     assert np.array_equal(again.q, wav.q) and np.array_equal(again.r, wav.r)
-    k = dev.k
     if k:
         assert np.max(np.abs(wav.q - whole.q)) <= 1e-11 * np.max(np.abs(whole.q))
         rn = np.linalg.norm(whole.r, axis=0)
