@@ -453,12 +453,53 @@ int dgeqpt_impl(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, i
     const double *rfull = gmat;  // upper triangle, ld k0
     clk.mark(PH_CHOL);
 
+    // Device entry point: the final solve Q = M_pre R_pre^{-1} is speculated
+    // on k = k0_final and runs on a side stream while stage 2 (R^{-1}, the
+    // condition bounds, their host round trips) decides k on st; it is redone
+    // for k columns in the rare case stage 2 truncates (A[:, k:k0] then holds
+    // speculative columns). The side stream touches only M_pre, R_pre, A and
+    // the TRSM's own block inverses, none of which stage 2 writes.
+    static thread_local cudaStream_t sq = nullptr;
+    static thread_local cudaEvent_t ev_sq0 = nullptr, ev_sq1 = nullptr;
+    const bool spec_q = !wave && !qsink && !(ctx->flags & CQRRPT_GPU_NO_WAVEFRONT);
+    if (spec_q) {
+        if (!sq) {
+            CQ_CUDA(cudaStreamCreateWithFlags(&sq, cudaStreamNonBlocking), "final solve stream");
+            CQ_CUDA(cudaEventCreateWithFlags(&ev_sq0, cudaEventDisableTiming), "final solve event");
+            CQ_CUDA(cudaEventCreateWithFlags(&ev_sq1, cudaEventDisableTiming), "final solve event");
+        }
+        CQ_CUDA(cudaEventRecord(ev_sq0, st), "final solve fork");
+        CQ_CUDA(cudaStreamWaitEvent(sq, ev_sq0, 0), "final solve fork wait");
+        CQ_TRY(trsm_right(m, k0f, mpre, ldp, nullptr, rfull, k0, A, lda, sq, nullptr, /*check_diag=*/false));
+        CQ_CUDA(cudaEventRecord(ev_sq1, sq), "final solve join");
+    }
+    auto join_spec = [&]() -> int {
+        if (spec_q) CQ_CUDA(cudaStreamWaitEvent(st, ev_sq1, 0), "final solve join wait");
+        return 0;
+    };
+
     // ---- stage 2: largest leading block with cond <= sqrt(eps_tol/u) -------
+    // with the speculative final solve in flight, stage 2 runs on a
+    // high-priority stream so its small kernels are not queued behind the
+    // solve's CTAs
+    static thread_local cudaStream_t shi = nullptr;
+    static thread_local cudaEvent_t ev_hi = nullptr;
+    cudaStream_t s2st = st;
+    if (spec_q) {
+        if (!shi) {
+            int least = 0, greatest = 0;
+            CQ_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest), "stream priorities");
+            CQ_CUDA(cudaStreamCreateWithPriority(&shi, cudaStreamNonBlocking, greatest), "stage-2 stream");
+            CQ_CUDA(cudaEventCreateWithFlags(&ev_hi, cudaEventDisableTiming), "stage-2 event");
+        }
+        CQ_CUDA(cudaStreamWaitEvent(shi, ev_sq0, 0), "stage-2 fork");
+        s2st = shi;
+    }
     const double threshold = std::sqrt(eps_tol / kUnitRoundoff);
     const int method = ctx->cond_method;
     double *rinv = ws.get<double>("drv.rinv", (size_t)(k0f * k0f));
     if (!rinv) return fail_nomem("rinv");
-    CQ_TRY(trtri_upper(k0f, rfull, k0, rinv, k0f, ws, st));  // R^{-1}; leading blocks = leading inverses
+    CQ_TRY(trtri_upper(k0f, rfull, k0, rinv, k0f, ws, s2st));  // R^{-1}; leading blocks = leading inverses
     bool exact = (ctx->flags & CQRRPT_GPU_EXACT_STAGE2) != 0;
     int64_t k = k0f;
     if (!exact) {
@@ -474,13 +515,13 @@ int dgeqpt_impl(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, i
             // first iterate already gives tau >= 1 the reference returns +inf
             // and falls back to krylov_bounds, whatever the later iterates.
             std::vector<double> first(ells.size());
-            CQ_TRY(identity_deviation_first(rfull, k0, ells.data(), (int)ells.size(), first.data(), ws, st));
+            CQ_TRY(identity_deviation_first(rfull, k0, ells.data(), (int)ells.size(), first.data(), ws, s2st));
             for (double v : first)
                 if (!(v * (1.0 + 1e-6) >= 1.0)) exact = true;
         }
         double fr = 0.0, fi_ = 0.0;
-        CQ_TRY(frob_norm_upper(k0f, rfull, k0, &fr, ws, st));
-        CQ_TRY(frob_norm_upper(k0f, rinv, k0f, &fi_, ws, st));
+        CQ_TRY(frob_norm_upper(k0f, rfull, k0, &fr, ws, s2st));
+        CQ_TRY(frob_norm_upper(k0f, rinv, k0f, &fi_, ws, s2st));
         const double bound = fr * fi_;  // >= cond_2(R_ell) for every leading block
         ctx->cond_upper_bound = bound;
         if (!(bound * (1.0 + 1e-5) <= threshold)) exact = true;
@@ -497,7 +538,7 @@ int dgeqpt_impl(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, i
                 double v = 1.0;
                 // method 3 = identity_deviation with the nested krylov fallback
                 const int m_nested = (method == CQRRPT_COND_IDENTITY_DEVIATION) ? 3 : method;
-                CQ_TRY(cond_estimate(ell, rfull, k0, rinv, k0f, m_nested, &v, ws, st));
+                CQ_TRY(cond_estimate(ell, rfull, k0, rinv, k0f, m_nested, &v, ws, s2st));
                 raw[ell] = v;
             }
             double v = 1.0;
@@ -520,16 +561,22 @@ int dgeqpt_impl(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, i
         ctx->cond_m_pre = c;
         ctx->stage2_exact = 1;
     }
+    if (spec_q) {
+        CQ_CUDA(cudaEventRecord(ev_hi, shi), "stage-2 join");
+        CQ_CUDA(cudaStreamWaitEvent(st, ev_hi, 0), "stage-2 join wait");
+    }
     clk.mark(PH_RANK);
     *k_out = k;
     if (k == 0) {
+        CQ_TRY(join_spec());
         CQ_TRY(emit_pivots());
         finish_diag(0);
         return 0;
     }
 
     // ---- Q = M_pre[:, :k] R_pre^{-1}, in place into A[:, :k] ----------------
-    if (!(wave && fi == 0 && k == k0))
+    CQ_TRY(join_spec());
+    if (!(wave && fi == 0 && k == k0) && !(spec_q && k == k0f))
         CQ_TRY(trsm_right(m, k, mpre, ldp, nullptr, rfull, k0, A, lda, st, qsink, /*check_diag=*/false));
     clk.mark(PH_CHOL);
 
