@@ -357,7 +357,9 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (torch-generated C2-shaped matrix)",
             "config": cfg,
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e2e_t},
+                    "ms_per_step": e2e_t,
+                    "path": ("cqrrpt_gpu_dgeqpt_host, pinned host A/Q/R: A in 4 row chunks followed by the exact "
+                             "sketch, Q downloaded in 64-column blocks from the 128-column wavefront")},
             "roofline": roofline, "roofline_sketch": sk, "roofline_contractions": con,
             "phases_ms": dict(zip(names, [round(float(x), 4) for x in ph])),
             "k": k, "k0": k0, "gpu_launches": launches, "clocks": clk.summary(), "cpu_baseline": cpu}
