@@ -265,7 +265,8 @@ def main():
 
     # ---- e2e: host input -> device -> factor -> Q, R, J back to host, through
     # the public host entry point (cqrrpt_gpu_dgeqpt_host: pinned buffers, Q
-    # streamed back while the final TRSM runs) ------------------------------
+    # streamed back block by block: from the wavefront on one rank, during the
+    # final TRSM on several) --------------------------------------------------
     host_a = torch.empty((n, m), dtype=torch.float64).pin_memory()
     host_a.copy_(a0.t())
     k = res.k
@@ -359,7 +360,8 @@ def main():
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_t,
                     "path": ("cqrrpt_gpu_dgeqpt_host, pinned host A/Q/R: A in 4 row chunks followed by the exact "
-                             "sketch, Q downloaded in 64-column blocks from the 128-column wavefront")},
+                             "sketch, Q downloaded in 64-column blocks " +
+                             ("from the 128-column wavefront" if world == 1 else "during the final TRSM"))},
             "roofline": roofline, "roofline_sketch": sk, "roofline_contractions": con,
             "phases_ms": dict(zip(names, [round(float(x), 4) for x in ph])),
             "k": k, "k0": k0, "gpu_launches": launches, "clocks": clk.summary(), "cpu_baseline": cpu}
