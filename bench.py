@@ -1,22 +1,29 @@
-"""Benchmark: CQRRPT canonical GFLOP/s on BASELINE config 2 (one B200 per rank).
+"""Benchmark: CQRRPT canonical GFLOP/s on the BASELINE workload (one B200 per rank).
 
-metric   CQRRPT canonical GFLOP/s = (2 m n^2 - 2 n^3/3) / t
-workload BASELINE.json configs[1]: M 131072 x 1024 FP64 = U diag(sigma) V^T,
-         sigma_i = 10^(-10 i/(n-1)) (cond 1e10), d_factor 1.25, SASO nnz 8, seed 0.
-         U, V from QR of seeded Gaussians, generated on the GPU with torch
-         (synthetic stand-in with the config's shape and spectrum; not the
-         reference generator's bits).
-step     one cqrrpt_gpu_dgeqpt call (sketch -> QRCP -> stage 1/2 -> gather+TRSM
-         -> Gram -> Cholesky -> Q TRSM in place -> R) on the resident input.
-         Between timed steps the input is restored and L2 is flushed (256 MiB
-         write); the restore + flush are outside the timed events.
-N > 1    torchrun, one process per GPU, NCCL allreduce of the sketch and the
-         Gram inside the library; weak scaling (each rank owns 131072 rows of
-         an N*131072 x 1024 matrix).
+metric   CQRRPT canonical GFLOP/s = (2 m n^2 - 2 n^3/3) / t,
+         t = device time of one factorization, max over ranks.
+workload --config (default C5_2048): BASELINE configs[4] at its largest single-
+         GPU size, M 4194304 x 2048 FP64 (64 GiB), Gaussian columns scaled by
+         geometric norms 1 .. 1e-8 in a seeded random order, d_factor 1.25,
+         SASO nnz 8, seed 0 -- the largest config BASELINE lists at 1 GPU and
+         the one it lists at 1/2/4/8. Other configs (C1..C5_1024) are
+         secondary lines (tools/workloads.py). Data: seeded synthetic, generated
+         on the device in 65536-row tiles (the same global matrix at any N).
+step     one cqrrpt_gpu_dgeqpt call (sketch -> allreduce -> QRCP -> stage 1/2 ->
+         gather+TRSM -> Gram -> allreduce -> Cholesky -> Q TRSM in place -> R)
+         on the resident input. Between timed steps the input is restored
+         (device copy, or H2D from pinned host memory when A + its copy + M_pre
+         do not fit in HBM); the restore writes far more than L2 (126 MB), and
+         every input is larger than L2 -- both outside the timed events.
+N > 1    torchrun, one process per GPU, rows [r m/N, (r+1) m/N) of the one
+         global matrix per rank; NCCL allreduce of the d x n sketch and the
+         k0 x k0 Gram inside the library; strong scaling.
+e2e      the public host entry point cqrrpt_gpu_dgeqpt_host: pinned host A in,
+         Q (m x k), R, J out, copies inside the timed region.
 
---impl reference  times the reference's own CPU cqrrpt() (oracle/_ref, the
-         unmodified reference library built from /root/reference) on a bounded
-         row sample of the same workload with all host threads.
+--impl reference  the reference's own CPU cqrrpt() (oracle/_ref: the unmodified
+         reference library built from /root/reference) on the workload's first
+         S rows (a bounded row sample), all host threads; rank 0 only.
 """
 from __future__ import annotations
 
@@ -32,38 +39,13 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+from tools.workloads import CONFIGS, DESCRIPTION, SEED, canonical_flops, make_rows  # noqa: E402
 
-M_ROWS, N_COLS, GAMMA, NNZ, SEED = 131072, 1024, 1.25, 8, 0
-COND_DECADES = 10.0
-CPU_SAMPLE_ROWS = 16384  # bounded CPU sample (1/8 of the rows)
+NNZ = 8
 METRIC = "CQRRPT canonical GFLOP/s (2mn^2-2n^3/3)/t, FP64 tall M"
-
-
-def canonical_flops(m, n):
-    return 2.0 * m * n * n - 2.0 * n ** 3 / 3.0
-
-
-# --------------------------------------------------------------------------
-# input generation (harness only)
-# --------------------------------------------------------------------------
-def make_c2_torch(m, n, seed, device):
-    import torch
-    g = torch.Generator(device=device).manual_seed(seed)
-    u = torch.linalg.qr(torch.randn((m, n), dtype=torch.float64, device=device, generator=g))[0]
-    v = torch.linalg.qr(torch.randn((n, n), dtype=torch.float64, device=device, generator=g))[0]
-    sig = 10.0 ** (-COND_DECADES * torch.arange(n, dtype=torch.float64, device=device) / (n - 1))
-    a = torch.empty((n, m), dtype=torch.float64, device=device)  # column-major m x n
-    a.copy_(((u * sig) @ v.T).T)
-    del u, v
-    return a.t()
-
-
-def make_c2_numpy(m, n, seed):
-    rng = np.random.default_rng(seed)
-    u = np.linalg.qr(rng.standard_normal((m, n)))[0]
-    v = np.linalg.qr(rng.standard_normal((n, n)))[0]
-    sig = 10.0 ** (-COND_DECADES * np.arange(n) / (n - 1))
-    return np.asfortranarray((u * sig) @ v.T)
+# CPU reference row sample per config (~10-20 s per reference run on 16 cores)
+SAMPLE_ROWS = {"C1": 16384, "C2": 16384, "C3": 8192, "C3b": 8192, "C4": 4096, "C5_256": 65536,
+               "C5_512": 32768, "C5_1024": 16384, "C5_2048": 8192}
 
 
 # --------------------------------------------------------------------------
@@ -84,8 +66,7 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
-            # nvidia-smi takes a moment to start: wait for its first row so the
-            # samples cover the timed region, then keep only rows from here on
+            # wait for nvidia-smi's first row so the samples cover the timed region
             t0 = time.time()
             while not self.rows and time.time() - t0 < 5.0:
                 time.sleep(0.01)
@@ -123,8 +104,8 @@ class ClockSampler:
 # peaks
 # --------------------------------------------------------------------------
 def measure_fp64_peak(torch):
-    """cuBLAS DGEMM 8192^3 (torch.matmul float64), best of 5 — the FP64 roofline
-    denominator (MEASURED_PEAKS.json carries no FP64 figure)."""
+    """cuBLAS DGEMM 8192^3 (torch.matmul float64), best of 5 -- the FP64
+    roofline denominator (MEASURED_PEAKS.json carries no FP64 figure)."""
     n = 8192
     a = torch.randn((n, n), dtype=torch.float64, device="cuda")
     b = torch.randn((n, n), dtype=torch.float64, device="cuda")
@@ -147,34 +128,60 @@ def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         with open(p) as f:
-            return json.load(f), "measured"
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+            return json.load(f), "MEASURED_PEAKS.json (driver-measured copy bandwidth)"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
 
 
-def load_traffic():
+def load_traffic(config):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
         with open(p) as f:
-            return json.load(f)
+            return json.load(f).get(config, {})
     return {}
 
 
 # --------------------------------------------------------------------------
 # CPU reference arm / baseline
 # --------------------------------------------------------------------------
-def run_reference_cpu(steps, warmup, rows=CPU_SAMPLE_ROWS):
+def reference_sample(name):
+    """The workload's first S rows as a Fortran-ordered host array (generated
+    with the same tile generator on the box's GPU when there is one)."""
+    import torch
+    cfg = dict(CONFIGS[name])
+    rows = min(SAMPLE_ROWS[name], cfg["m"])
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    if cfg["kind"] == "spectral":  # C2 is generated whole; keep its first S rows
+        a = make_rows(cfg, 0, cfg["m"], dev)[:rows]
+    elif cfg["kind"] == "lowrank":
+        from tools.workloads import fill_rows, lowrank_fro_sq
+        fro = lowrank_fro_sq(cfg, 0, cfg["m"], dev)
+        a = torch.empty((cfg["n"], rows), dtype=torch.float64, device=dev).t()
+        fill_rows(cfg, 0, rows, a, dev, fro_sq_total=fro)
+    else:
+        a = make_rows(cfg, 0, rows, dev)
+    host = np.asfortranarray(a.cpu().numpy())
+    del a
+    if dev == "cuda":
+        torch.cuda.empty_cache()
+    return host, dev
+
+
+def run_reference_cpu(name, steps, warmup):
     from oracle.oracle import Reference
     ref = Reference()
     cores = ref.num_threads()
-    a = make_c2_numpy(rows, N_COLS, SEED)
+    a, dev = reference_sample(name)
+    rows, n = a.shape
+    gamma = CONFIGS[name]["gamma"]
     times = []
+    res = None
     for it in range(warmup + steps):
-        res = ref.cqrrpt(a, gamma=GAMMA, nnz=NNZ, eps_tol=1e-4, seed=SEED, validate=False)
+        res = ref.cqrrpt(a, gamma=gamma, nnz=NNZ, eps_tol=1e-4, seed=SEED, validate=False)
         if it >= warmup:
             times.append(res.extra["timings"]["total"])  # diagnostics.timings.total (cqrrpt.cc:288)
     t = float(np.mean(times))
-    return dict(value=canonical_flops(rows, N_COLS) / t / 1e9, t=t, best=float(np.min(times)), cores=cores,
-                k=res.k, rows=rows)
+    return dict(value=canonical_flops(rows, n) / t / 1e9, t=t, best=float(np.min(times)), cores=cores,
+                k=res.k, rows=rows, n=n, gen_device=dev, runs=len(times))
 
 
 # --------------------------------------------------------------------------
@@ -186,35 +193,46 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5_2048", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    cfg = {"workload": "BASELINE configs[1]: M 131072x1024 FP64, sigma_i=10^(-10 i/(n-1)), d_factor 1.25, "
-                       "SASO nnz 8, seed 0",
-           "m": M_ROWS * max(world, 1), "n": N_COLS, "d_factor": GAMMA, "nnz": NNZ,
-           "parallelism": f"rows{max(world, 1)}", "l2": "flushed between steps (256 MiB write)"}
+    name = args.config
+    cfg = CONFIGS[name]
+    m, n, gamma = cfg["m"], cfg["n"], cfg["gamma"]
+    conf = {"workload": f"{name}: {DESCRIPTION[name]}; d_factor {gamma}, SASO nnz {NNZ}, seed {SEED}",
+            "m": m, "n": n, "d_factor": gamma, "nnz": NNZ, "parallelism": f"rows{max(world, 1)}",
+            "l2": "inputs larger than L2 (126 MB); the between-step input restore writes the whole matrix"}
 
     if args.impl == "reference":
         if rank != 0:
             return
-        r = run_reference_cpu(args.steps, args.warmup)
+        r = run_reference_cpu(name, args.steps, args.warmup)
         line = {"metric": METRIC, "value": r["value"], "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": r["t"] * 1e3, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-                "config": dict(cfg, sample_rows=r["rows"]),
+                "warmup": args.warmup, "ms_per_step": r["t"] * 1e3, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (tools/workloads.py)", "impl": "reference",
+                "config": dict(conf, sample_rows=r["rows"]),
                 "cpu_baseline": {"value": r["value"], "unit": "GFLOP/s", "cores": r["cores"], "kind": "reference",
-                                 "sample": f"reference cqrrpt() on a {r['rows']}x{N_COLS} row sample of the workload "
-                                           f"(validate_output=false, timings.total, mean of {args.steps})"},
+                                 "sample": f"reference cqrrpt() (oracle/_ref, unmodified reference library) on the "
+                                           f"first {r['rows']} rows of the {name} matrix ({r['rows']}x{n}), "
+                                           f"validate_output=false, timings.total, mean of {r['runs']}"},
                 "e2e": {"value": r["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
 
     import torch
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines on stderr (nranks check)
     import paper_2311_08316_b200 as pkg
     from paper_2311_08316_b200 import kernels
 
+    if cfg["kind"] == "spectral" and world > 1:
+        raise SystemExit("C2 (U from a global QR) is a single-GPU workload")
+    if m % world:
+        raise SystemExit(f"m = {m} is not divisible by {world} ranks")
     torch.cuda.set_device(local)
     dist = None
     comm = None
@@ -223,23 +241,41 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         comm = pkg.Comm.from_torch_distributed()
     stream = torch.cuda.current_stream()
-
-    m, n = M_ROWS, N_COLS
-    a0 = make_c2_torch(m, n, SEED + rank, "cuda")
-    work = pkg.colmajor_empty(m, n)
-    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
-    canon = canonical_flops(m * world, n)
+    ml = m // world
+    r0 = rank * ml
 
     def barrier():
         if dist is not None:
             dist.barrier()
 
+    # ---- input: rows [r0, r0 + ml) of the global matrix ------------------------
+    work = make_rows(cfg, r0, r0 + ml, "cuda", dist=dist)
+    torch.cuda.synchronize()
+    free, total = torch.cuda.mem_get_info()
+    a_bytes = ml * n * 8
+    # keep a device copy of A when A, its copy and M_pre (m x n) fit; else pinned host
+    device_copy = 3 * a_bytes + (2 << 30) < total
+    host_a = torch.empty((n, ml), dtype=torch.float64).pin_memory()
+    host_a.copy_(work.t())
+    a0 = None
+    if device_copy:
+        a0 = torch.empty_like(work.t()).t()
+        a0.copy_(work)
+    canon = canonical_flops(m, n)
+
+    def restore():
+        if a0 is not None:
+            work.copy_(a0)
+        else:
+            work.t().copy_(host_a, non_blocking=True)
+
     def one_step(timed):
-        work.copy_(a0)
-        flush.fill_(1.0)
+        restore()
+        torch.cuda.synchronize()
+        barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        res = pkg.dgeqpt(work, d_factor=GAMMA, nnz=NNZ, seed=SEED, comm=comm, global_row_offset=rank * m,
+        res = pkg.dgeqpt(work, d_factor=gamma, nnz=NNZ, seed=SEED, comm=comm, global_row_offset=r0,
                          timings=timed)
         e1.record(stream)
         e1.synchronize()
@@ -256,51 +292,58 @@ def main():
             ms, res = one_step(True)
             step_ms.append(ms)
             phases += np.array(list(res.ctx.timings_ms))
+        clocks = clk.summary()
     torch.cuda.synchronize()
     barrier()
-    launches = kernels.launch_count(reset=True)
+    launches = kernels.launch_count(reset=True)  # all K timed steps
     total_ms = float(np.sum(step_ms))
+    ph = phases / args.steps
+    names = ["sketch", "qrcp", "rank_select", "precondition", "cholesky_qr", "undo", "total", "comm"]
+    per_rank = [dict(rank=rank, ms_per_step=total_ms / args.steps, comm_ms=float(ph[7]))]
     if dist is not None:
         t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
+        gathered = [None] * world
+        dist.all_gather_object(gathered, per_rank[0])
+        per_rank = gathered
     ms_per_step = total_ms / args.steps
     value = canon / (ms_per_step * 1e-3) / 1e9
-    ph = phases / args.steps
-    names = ["sketch", "qrcp", "rank_select", "precondition", "cholesky_qr", "undo", "total", "comm"]
+    k, k0 = res.k, res.k0
 
-    # ---- e2e: host input -> device -> factor -> Q, R, J back to host, through
-    # the public host entry point (cqrrpt_gpu_dgeqpt_host: pinned buffers, Q
-    # streamed back block by block: from the wavefront on one rank, during the
-    # final TRSM on several) --------------------------------------------------
-    host_a = torch.empty((n, m), dtype=torch.float64).pin_memory()
-    host_a.copy_(a0.t())
-    k = res.k
-    host_q = torch.empty((n, m), dtype=torch.float64).pin_memory().t()
-    host_r = torch.empty((n, n), dtype=torch.float64).pin_memory().t()
-    host_j = torch.empty(n, dtype=torch.int64).pin_memory()
-    e2e_ms = []
-    for it in range(args.warmup + args.steps):
-        flush.fill_(1.0)
-        torch.cuda.synchronize()
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        r2 = pkg.dgeqpt_host(host_a.t(), d_factor=GAMMA, nnz=NNZ, seed=SEED, q_out=host_q, r_out=host_r,
-                             j_out=host_j, stream=stream, comm=comm, global_row_offset=rank * m)
-        e1.record(stream)
-        e1.synchronize()
-        if it >= args.warmup:
-            e2e_ms.append(e0.elapsed_time(e1))
-    assert r2.k == k
-    e2e_t = float(np.mean(e2e_ms))
-    if dist is not None:
-        t = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_t = float(t.item())
-    e2e_value = canon / (e2e_t * 1e-3) / 1e9
-    h2d = m * n * 8
-    d2h = m * k * 8 + k * n * 8 + n * 8
+    # ---- e2e: host A in, Q, R, J out through the public host entry point ------
+    e2e = None
+    if not args.no_e2e:
+        del work
+        if a0 is not None:
+            del a0
+        pkg.release_workspace()
+        torch.cuda.empty_cache()
+        host_q = torch.empty((n, ml), dtype=torch.float64).pin_memory().t()
+        host_r = torch.empty((n, n), dtype=torch.float64).pin_memory().t()
+        host_j = torch.empty(n, dtype=torch.int64).pin_memory()
+        e2e_ms = []
+        for it in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r2 = pkg.dgeqpt_host(host_a.t(), d_factor=gamma, nnz=NNZ, seed=SEED, q_out=host_q, r_out=host_r,
+                                 j_out=host_j, stream=stream, comm=comm, global_row_offset=r0)
+            e1.record(stream)
+            e1.synchronize()
+            if it >= args.warmup:
+                e2e_ms.append(e0.elapsed_time(e1))
+        assert r2.k == k, (r2.k, k)
+        e2e_t = float(np.mean(e2e_ms))
+        if dist is not None:
+            t = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_t = float(t.item())
+        e2e = {"value": canon / (e2e_t * 1e-3) / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": ml * n * 8,
+               "d2h_bytes_per_step": ml * k * 8 + k * n * 8 + n * 8, "ms_per_step": e2e_t,
+               "path": "cqrrpt_gpu_dgeqpt_host, pinned host A/Q/R/J (rank-local rows): A in row chunks followed "
+                       "by the exact sketch, Q downloaded in 64-column blocks as the final solve forms them"}
 
     if rank != 0:
         if comm is not None:
@@ -308,69 +351,50 @@ def main():
         dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (gather + DMMA TRSM, K5a) --------------
+    # ---- rooflines ---------------------------------------------------------------
     fp64_peak = measure_fp64_peak(torch)
-    k0 = res.k0
-    trsm_flops = float(m) * k0 * k0  # trsm_right flop count m k0^2 (flop_model term)
-    trsm_ms = ph[3]
-    achieved = trsm_flops / (trsm_ms * 1e-3) / 1e12
-    # DRAM bytes of one TRSM pass (16 launches) from ncu, profiles/traffic.json
-    traffic = load_traffic().get("trsm_pass_dram_bytes")
     peaks, peak_src = measured_peaks()
-    roofline = {"bound": "tensor", "kernel": "trsm_block_kernel (K5a gather+TRSM, DMMA.8x8x4)",
+    tr = load_traffic(name)
+    trsm_flops = float(ml) * k0 * k0  # trsm_right: m k0^2 flops per pass (flop_model term)
+    achieved = trsm_flops / (ph[3] * 1e-3) / 1e12
+    roofline = {"bound": "tensor", "kernel": "trsm_block_kernel (K5a gather + TRSM on DMMA.8x8x4)",
                 "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
-                "traffic": traffic,
-                "peak_source": "measured live in this run: cuBLAS DGEMM 8192^3 via torch.matmul(float64), best of 5",
-                "algorithmic": "m*k0^2 flops per TRSM pass (m=131072, k0=1024)",
+                "traffic": tr.get("trsm_pass_dram_bytes"),
+                "peak_source": "measured live in this run: cuBLAS DGEMM 8192^3 (torch.matmul float64), best of 5 "
+                               "(MEASURED_PEAKS.json has no FP64 figure)",
+                "algorithmic": f"m_local*k0^2 = {trsm_flops:.4g} flops per precondition TRSM pass, over the "
+                               f"CUDA-event time of that phase",
                 "traffic_unit": "DRAM bytes per TRSM pass (ncu dram__bytes_read+write, profiles/traffic.json)"}
-    # secondary rooflines
-    sketch_bytes = 8.0 * m * n + 8.0 * res.ctx.d * n
-    sk = {"bound": "hbm", "achieved": sketch_bytes / (ph[0] * 1e-3) / 1e9, "peak": peaks.get("hbm_gbs"),
-          "unit": "GB/s", "peak_source": peak_src}
+    sketch_bytes = 8.0 * ml * n + 8.0 * res.ctx.d * n
+    sk = {"bound": "hbm", "kernel": "saso_apply_kernel", "achieved": sketch_bytes / (ph[0] * 1e-3) / 1e9,
+          "peak": peaks.get("hbm_gbs"), "unit": "GB/s", "peak_source": peak_src,
+          "algorithmic": "8 m n (read M) + 8 d n (write M_sk) bytes", "traffic": tr.get("saso_apply_dram_bytes")}
     sk["frac"] = sk["achieved"] / sk["peak"] if sk["peak"] else None
-    # the sketch's binding resource: shared-memory wavefronts (128 B each) of
-    # the apply kernel, counted by ncu for this configuration
-    # (profiles/traffic.json), over the live sketch-phase time, against
-    # 128 B/clk/SM x SMs x the SM clock sampled under load
-    tr = load_traffic()
-    wf = tr.get("saso_apply_smem_wavefronts")
-    if wf:
-        props = torch.cuda.get_device_properties(local)
-        sm_ghz = (clk.summary().get("sm_mhz") or 1965.0) / 1e3
-        smem_peak = 128.0 * props.multi_processor_count * sm_ghz  # GB/s
-        sk["smem"] = {"bound": "shared memory", "achieved": wf * 128.0 / (ph[0] * 1e-3) / 1e9, "peak": smem_peak,
-                      "unit": "GB/s", "wavefronts_per_launch": wf,
-                      "peak_source": "128 B/clk/SM x SMs x sampled SM clock",
-                      "traffic": tr.get("saso_apply_dram_bytes")}
-        sk["smem"]["frac"] = sk["smem"]["achieved"] / smem_peak
-    contraction_flops = float(m) * k0 * k0 + float(m) * k0 * (k0 + 1) + float(m) * k * k
+    contraction_flops = float(ml) * k0 * k0 + float(ml) * k0 * (k0 + 1) + float(ml) * k * k
     con = {"bound": "tensor", "achieved": contraction_flops / ((ph[3] + ph[4]) * 1e-3) / 1e12, "peak": fp64_peak,
-           "unit": "TFLOP/s"}
+           "unit": "TFLOP/s", "algorithmic": "m k0^2 (TRSM) + m k0 (k0+1) (Gram) + m k^2 (final TRSM) over the "
+                                             "precondition + cholesky_qr phases (incl. potrf)"}
     con["frac"] = con["achieved"] / fp64_peak
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
-            r = run_reference_cpu(1, 1)
+            r = run_reference_cpu(name, 1, 1)
             cpu = {"value": r["value"], "unit": "GFLOP/s", "cores": r["cores"], "kind": "reference",
-                   "sample": f"reference cqrrpt() (oracle/_ref) on a {r['rows']}x{N_COLS} row sample of the "
-                             f"workload, validate_output=false, timings.total"}
+                   "sample": f"reference cqrrpt() (oracle/_ref) on the first {r['rows']} rows of the {name} "
+                             f"matrix, validate_output=false, timings.total, 1 run after 1 warm-up"}
         except Exception as exc:  # reference library missing on this host
             cpu = {"value": None, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {exc}"}
 
     line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (torch-generated C2-shaped matrix)",
-            "config": cfg,
-            "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e2e_t,
-                    "path": ("cqrrpt_gpu_dgeqpt_host, pinned host A/Q/R: A in 4 row chunks followed by the exact "
-                             "sketch, Q downloaded in 64-column blocks " +
-                             ("from the 128-column wavefront" if world == 1 else "during the final TRSM"))},
-            "roofline": roofline, "roofline_sketch": sk, "roofline_contractions": con,
-            "phases_ms": dict(zip(names, [round(float(x), 4) for x in ph])),
-            "k": k, "k0": k0, "gpu_launches": launches, "clocks": clk.summary(), "cpu_baseline": cpu}
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (tools/workloads.py, seeded, device-generated)",
+            "config": dict(conf, restore="device copy" if device_copy else "H2D from pinned host memory"),
+            "e2e": e2e, "roofline": roofline, "roofline_sketch": sk, "roofline_contractions": con,
+            "phases_ms": dict(zip(names, [round(float(x), 4) for x in ph])), "per_rank": per_rank,
+            "k": k, "k0": k0, "gpu_launches": launches,
+            "gpu_launches_per_step": launches / max(args.steps, 1), "clocks": clocks, "cpu_baseline": cpu}
     print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()

@@ -10,10 +10,10 @@
 // configurations, std::domain_error for a singular preconditioner). A
 // reference caller switches with `namespace cqrrpt = cqrrpt_b200;`.
 //
-// Host data in, host data out (like the reference): the adapter copies M to
-// the device, runs cqrrpt_gpu_dgeqpt (include/cqrrpt_gpu.h) on sm_100a, and
-// copies Q (m x k), R (k x n) and the pivots back. Header-only; link
-// libcqrrpt_gpu.so and the CUDA runtime.
+// Host data in, host data out (like the reference): the adapter runs the host
+// entry point cqrrpt_gpu_dgeqpt_host (include/cqrrpt_gpu.h) on sm_100a, which
+// uploads M, factors it and streams Q (m x k), R (k x n) and the pivots back.
+// Header-only; link libcqrrpt_gpu.so and the CUDA runtime.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -134,10 +134,28 @@ struct DevBuf {
         if (p) cudaFree(p);
     }
 };
+// page-lock a large host range for the duration of a call
+struct Pinned {
+    void *p = nullptr;
+    Pinned(const void *ptr, size_t bytes, bool read_only) {
+        if (bytes < (size_t(64) << 20)) return;
+        unsigned flags = cudaHostRegisterPortable | (read_only ? cudaHostRegisterReadOnly : 0u);
+        if (cudaHostRegister(const_cast<void *>(ptr), bytes, flags) == cudaSuccess) p = const_cast<void *>(ptr);
+        else cudaGetLastError();
+    }
+    ~Pinned() {
+        if (p) cudaHostUnregister(p);
+    }
+};
 }  // namespace detail
 
-// Drop-in for cqrrpt::cqrrpt (cqrrpt.cc:317-328). validate_output is evaluated
-// on the device (cqrrpt_gpu_validate) with the reference's tolerance.
+// Drop-in for cqrrpt::cqrrpt (cqrrpt.cc:317-328) through the host entry point
+// cqrrpt_gpu_dgeqpt_host: M's pages are registered for full-bandwidth DMA
+// when large, A arrives in row chunks the exact sketch follows, Q streams back
+// block by block while the device still computes. validate_output is
+// evaluated on the device (cqrrpt_gpu_validate) with the reference's
+// tolerance. (The reference's own headers + types: paper_2311_08316_b200/
+// dropin/cqrrpt_dropin.cc defines cqrrpt::cqrrpt / cqrrpt_core themselves.)
 inline CqrrptOutput cqrrpt(const DenseMatrix &m, const CqrrptConfig &cfg = {}) {
     if (cfg.gamma < 1.0) throw std::invalid_argument("cqrrpt: gamma must be >= 1");
     if (!(cfg.eps_tol > unit_roundoff)) throw std::invalid_argument("cqrrpt: eps_tol must exceed the unit roundoff");
@@ -148,35 +166,39 @@ inline CqrrptOutput cqrrpt(const DenseMatrix &m, const CqrrptConfig &cfg = {}) {
         out.factorization.r = DenseMatrix(0, 0);
         return out;
     }
-    const size_t abytes = sizeof(double) * size_t(rows * n);
-    detail::DevBuf a(abytes), a0(cfg.validate_output ? abytes : 0), r(sizeof(double) * size_t(n * n)),
-        j(sizeof(int64_t) * size_t(n));
-    if (cudaMemcpy(a.p, m.data(), abytes, cudaMemcpyHostToDevice) != cudaSuccess)
-        throw std::runtime_error("H2D copy failed");
-    if (cfg.validate_output) cudaMemcpy(a0.p, a.p, abytes, cudaMemcpyDeviceToDevice);
     cqrrpt_gpu_ctx ctx;
     cqrrpt_gpu_ctx_init(&ctx);
     ctx.cond_method = int32_t(cfg.cond_method);
     ctx.sketch_family = cfg.family == SketchFamily::gaussian ? CQRRPT_SKETCH_GAUSSIAN
                         : cfg.family == SketchFamily::srft  ? CQRRPT_SKETCH_SRFT
                                                             : CQRRPT_SKETCH_SASO;
-    ctx.flags = CQRRPT_GPU_TIMINGS | CQRRPT_GPU_EXACT_STAGE2 | CQRRPT_GPU_DIAGNOSTICS |
-                (cfg.stage1_enabled ? 0 : CQRRPT_GPU_NO_STAGE1);
+    // the default fast-accept stage 2 is exact; DIAGNOSTICS fills cond_m_pre
+    ctx.flags = CQRRPT_GPU_TIMINGS | CQRRPT_GPU_DIAGNOSTICS | (cfg.stage1_enabled ? 0 : CQRRPT_GPU_NO_STAGE1);
+    DenseMatrix q(rows, n);  // room for k0 columns
+    std::vector<double> r(size_t(n * n), 0.0);
+    std::vector<int64_t> piv(size_t(n), 0);
     int64_t k = 0, k0 = 0;
-    int rc = cqrrpt_gpu_dgeqpt(rows, n, static_cast<double *>(a.p), rows, cfg.gamma, cfg.nnz_per_col, cfg.seed,
-                               cfg.eps_tol, static_cast<double *>(r.p), n, static_cast<int64_t *>(j.p), &k, &k0, &ctx);
-    if (rc) detail::throw_for(rc, "cqrrpt");
+    {
+        detail::Pinned pa(m.data(), sizeof(double) * m.size(), true), pq(q.data(), sizeof(double) * q.size(), false);
+        int rc = cqrrpt_gpu_dgeqpt_host(rows, n, m.data(), std::max<int64_t>(rows, 1), cfg.gamma, cfg.nnz_per_col,
+                                        cfg.seed, cfg.eps_tol, q.data(), std::max<int64_t>(rows, 1), r.data(), n,
+                                        piv.data(), &k, &k0, &ctx);
+        if (rc) detail::throw_for(rc, "cqrrpt");
+    }
     out.k = k;
     out.k0 = k0;
-    out.factorization.rank = k;
-    out.factorization.q = DenseMatrix(rows, k);
-    out.factorization.r = DenseMatrix(k, n);
-    out.factorization.pivots.resize(size_t(n));
-    cudaMemcpy(out.factorization.q.data(), a.p, sizeof(double) * size_t(rows * k), cudaMemcpyDeviceToHost);
-    if (k > 0)
-        cudaMemcpy2D(out.factorization.r.data(), sizeof(double) * size_t(k), r.p, sizeof(double) * size_t(n),
-                     sizeof(double) * size_t(k), size_t(n), cudaMemcpyDeviceToHost);
-    cudaMemcpy(out.factorization.pivots.data(), j.p, sizeof(int64_t) * size_t(n), cudaMemcpyDeviceToHost);
+    PivotedQR &f = out.factorization;
+    f.rank = k;
+    f.pivots = std::move(piv);
+    if (k == n) {
+        f.q = std::move(q);
+    } else {
+        f.q = DenseMatrix(rows, k);
+        std::memcpy(f.q.data(), q.data(), sizeof(double) * size_t(rows * k));
+    }
+    f.r = DenseMatrix(k, n);
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < k; ++i) f.r(i, j) = r[size_t(j * n + i)];
     auto &d = out.diagnostics;
     d.cond_m_pre = ctx.cond_m_pre;
     d.truncation_ratio = ctx.truncation_ratio;
@@ -189,7 +211,7 @@ inline CqrrptOutput cqrrpt(const DenseMatrix &m, const CqrrptConfig &cfg = {}) {
         const double tol = std::max(100.0 * double(n) * unit_roundoff, 10.0 * cfg.eps_tol);
         std::vector<char> seen(size_t(n), 0);
         v.pivots_valid = true;
-        for (int64_t p : out.factorization.pivots) {
+        for (int64_t p : f.pivots) {
             if (p < 0 || p >= n || seen[size_t(p)]) {
                 v.pivots_valid = false;
                 break;
@@ -197,17 +219,27 @@ inline CqrrptOutput cqrrpt(const DenseMatrix &m, const CqrrptConfig &cfg = {}) {
             seen[size_t(p)] = 1;
         }
         for (int64_t jj = 0; jj < n; ++jj)
-            for (int64_t ii = jj + 1; ii < k; ++ii)
-                v.max_below_diag = std::max(v.max_below_diag, std::abs(out.factorization.r(ii, jj)));
+            for (int64_t ii = jj + 1; ii < k; ++ii) v.max_below_diag = std::max(v.max_below_diag, std::abs(f.r(ii, jj)));
         v.diag_nonincreasing = true;
         for (int64_t ii = 1; ii < std::min(k, n); ++ii)
-            if (std::abs(out.factorization.r(ii, ii)) > std::abs(out.factorization.r(ii - 1, ii - 1)))
-                v.diag_nonincreasing = false;
+            if (std::abs(f.r(ii, ii)) > std::abs(f.r(ii - 1, ii - 1))) v.diag_nonincreasing = false;
         if (v.pivots_valid) {
-            rc = cqrrpt_gpu_validate(rows, n, k, static_cast<double *>(a0.p), rows, static_cast<double *>(a.p), rows,
-                                     static_cast<double *>(r.p), n, static_cast<int64_t *>(j.p), &v.orth_loss_fro,
-                                     &v.orth_loss, &v.recon_rel, nullptr);
+            const size_t abytes = sizeof(double) * size_t(rows * n);
+            detail::DevBuf a(abytes), qd(sizeof(double) * size_t(rows * std::max<int64_t>(k, 1))),
+                rd(sizeof(double) * size_t(std::max<int64_t>(k, 1) * n)), jd(sizeof(int64_t) * size_t(n));
+            cudaMemcpy(a.p, m.data(), abytes, cudaMemcpyHostToDevice);
+            if (k > 0) {
+                cudaMemcpy(qd.p, f.q.data(), sizeof(double) * size_t(rows * k), cudaMemcpyHostToDevice);
+                cudaMemcpy(rd.p, f.r.data(), sizeof(double) * size_t(k * n), cudaMemcpyHostToDevice);
+            }
+            cudaMemcpy(jd.p, f.pivots.data(), sizeof(int64_t) * size_t(n), cudaMemcpyHostToDevice);
+            int rc = cqrrpt_gpu_validate(rows, n, k, static_cast<double *>(a.p), rows, static_cast<double *>(qd.p), rows,
+                                         static_cast<double *>(rd.p), std::max<int64_t>(k, 1),
+                                         static_cast<int64_t *>(jd.p), &v.orth_loss_fro, &v.orth_loss, &v.recon_rel,
+                                         nullptr);
             if (rc) detail::throw_for(rc, "validate");
+        } else {
+            v.recon_rel = INFINITY;
         }
         v.pass = v.pivots_valid && v.max_below_diag == 0.0 && v.orth_loss <= tol && v.recon_rel <= tol;
         d.validation = v;

@@ -106,7 +106,9 @@ typedef struct cqrrpt_gpu_ctx {
     int64_t k0_final;            /* k0 after Cholesky-failure shrink */
     int32_t retries;             /* Cholesky-failure retries (rank_stage2) */
     int32_t stage2_exact;        /* 1 if the binary search ran, 0 if fast-accepted */
-    double cond_m_pre;           /* estimate at the final rank (exact path or flag) */
+    double cond_m_pre;           /* est.at(k) (cqrrpt.cc:205): filled when the stage-2 search
+                                    ran, or with CQRRPT_GPU_DIAGNOSTICS (evaluated after the
+                                    timed phases on the fast-accept path); NaN otherwise */
     double cond_upper_bound;     /* ||R_pre||_F ||R_pre^-1||_F (fast path) */
     double truncation_ratio;     /* ||C_k||_F / ||R_sk||_2 (CQRRPT_GPU_DIAGNOSTICS) */
     double flop_estimate;        /* flop_model (cqrrpt.cc:330-338) */
@@ -114,6 +116,11 @@ typedef struct cqrrpt_gpu_ctx {
      * sketch, qrcp, rank_select, precondition, cholesky_qr, undo, total,
      * + [7] communication (allreduce) */
     double timings_ms[8];
+    /* in (appended in ABI 1.1): > 0 sets the sketch row count d directly
+     * instead of ceil(d_factor * n) -- cqrrpt_core with an explicit operator
+     * of d rows (cqrrpt.hh:136); d_factor is then only validated (>= 1), as
+     * the reference's check_config does */
+    int64_t sketch_rows;
 } cqrrpt_gpu_ctx;
 
 /* Fill a context with defaults (single GPU, default stream). */
@@ -197,6 +204,21 @@ int cqrrpt_gpu_qrcp(int64_t d, int64_t n, double *Msk, int64_t ldm, double rank_
 
 /* rank_stage1 (cqrrpt.cc:92-112) on a k x n upper-trapezoidal R (device). */
 int cqrrpt_gpu_rank_stage1(int64_t k, int64_t n, const double *R, int64_t ldr, int64_t *k0,
+                           void *stream);
+
+/* rank_stage2 (cqrrpt.cc:149-209), the routine cqrrpt_gpu_dgeqpt runs after
+ * stage 1 (one rank): M_pre = M_k0 A_sk^{-1} (m x k0, A_sk upper k0 x k0),
+ * upper Cholesky of M_pre^T M_pre into R_pre (k0 x k0 buffer, ldr >= k0, on
+ * device) with the failure-shrink retry, then the NestedCondEstimator binary
+ * search for the largest leading block with cond <= sqrt(eps_tol/u).
+ * Outputs: M_pre columns [0, k0_final) and R_pre's leading rank x rank block
+ * (device), rank, k0_final, retries and cond_at_rank (= est.at(rank), 1.0 for
+ * rank 0) on the host. flags: CQRRPT_GPU_EXACT_STAGE2 forces the search (the
+ * result is the same; the fast accept is exact). A zero diagonal in A_sk
+ * returns CQRRPT_GPU_ERR_SINGULAR (the reference's std::domain_error). */
+int cqrrpt_gpu_rank_stage2(int64_t m, int64_t k0, const double *M_k0, int64_t ldm, const double *A_sk, int64_t ldas,
+                           double eps_tol, int32_t cond_method, int32_t flags, double *M_pre, int64_t ldp, double *R_pre,
+                           int64_t ldr, int64_t *rank, int64_t *k0_final, int32_t *retries, double *cond_at_rank,
                            void *stream);
 
 /* X (m x k, ldx) = B[:, cols] * U^{-1}, U upper-triangular k x k (ldu);

@@ -481,6 +481,11 @@ static void gaussian_block(int64_t m, int64_t n, uint64_t stream_seed, double *g
         for (int64_t i = 0; i < m; ++i) g[j * m + i] = orc_rng_normal(stream_seed, (uint64_t)(j * m + i));
 }
 
+int orc_gaussian_block(int64_t m, int64_t n, uint64_t stream_seed, double *out) { /* testmat.cc:17-25 */
+    gaussian_block(m, n, stream_seed, out);
+    return 0;
+}
+
 int orc_gen_gaussian(int64_t m, int64_t n, uint64_t seed, double *out) { /* testmat.cc:141-143 */
     gaussian_block(m, n, orc_mix_seed(seed, 0x676175ULL), out);
     return 0;
@@ -538,10 +543,8 @@ int orc_gen_kahan(int64_t n, double theta, double *out) { /* testmat.cc:126-139 
     return 0;
 }
 
-int orc_c5_scale_columns(int64_t m, int64_t n, int64_t ld, double span_decades, uint64_t seed,
-                         double *a, int64_t *perm_out) {
+static void c5_permutation(int64_t n, uint64_t seed, int64_t *p) {
     /* pi = Fisher-Yates as verify.cc:45-55, stream mix_seed(seed, "perm") */
-    int64_t *p = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
     for (int64_t i = 0; i < n; ++i) p[i] = i;
     uint64_t s = orc_mix_seed(seed, 0x7065726dULL);
     for (int64_t i = 0; i < n - 1; ++i) {
@@ -550,6 +553,30 @@ int orc_c5_scale_columns(int64_t m, int64_t n, int64_t ld, double span_decades, 
         p[i] = p[j];
         p[j] = t;
     }
+}
+
+int orc_c5_column_factors(int64_t n, double span_decades, uint64_t seed, double *f) {
+    int64_t *p = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+    c5_permutation(n, seed, p);
+    for (int64_t j = 0; j < n; ++j) f[j] = pow(10.0, -span_decades * (double)p[j] / (double)(n - 1));
+    free(p);
+    return 0;
+}
+
+int orc_gen_gaussian_rows(int64_t m, int64_t n, uint64_t seed, int64_t r0, int64_t r1, double *out, int64_t ld) {
+    /* rows [r0, r1) of gaussian_block(m, n, mix_seed(seed, "gau")): element (i, j) is draw j*m + i */
+    if (r0 < 0 || r1 > m || r0 > r1 || ld < r1 - r0) return -1;
+    const uint64_t s = orc_mix_seed(seed, 0x676175ULL);
+#pragma omp parallel for schedule(static)
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = r0; i < r1; ++i) out[j * ld + (i - r0)] = orc_rng_normal(s, (uint64_t)(j * m + i));
+    return 0;
+}
+
+int orc_c5_scale_columns(int64_t m, int64_t n, int64_t ld, double span_decades, uint64_t seed,
+                         double *a, int64_t *perm_out) {
+    int64_t *p = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+    c5_permutation(n, seed, p);
 #pragma omp parallel for schedule(static)
     for (int64_t j = 0; j < n; ++j) {
         double f = pow(10.0, -span_decades * (double)p[j] / (double)(n - 1));

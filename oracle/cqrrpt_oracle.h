@@ -32,6 +32,8 @@ uint64_t orc_mix_seed(uint64_t seed, uint64_t salt);
 
 /* testmat.cc generators (harness inputs, not hot path) */
 int orc_gen_gaussian(int64_t m, int64_t n, uint64_t seed, double *out);
+/* gaussian_block (testmat.cc:17-25) on an already mixed stream seed */
+int orc_gaussian_block(int64_t m, int64_t n, uint64_t stream_seed, double *out);
 int orc_gen_exact_rank(int64_t m, int64_t n, int64_t r, uint64_t seed, double *out);
 int orc_gen_spectral_list(int64_t m, int64_t n, const double *sigma, uint64_t seed, double *out);
 int orc_gen_kahan(int64_t n, double theta, double *out);
@@ -39,6 +41,12 @@ int orc_gen_kahan(int64_t n, double theta, double *out);
  * with seed mix_seed(0, 0x7065726d)), column j scaled by 10^(-span*pi[j]/(n-1)). */
 int orc_c5_scale_columns(int64_t m, int64_t n, int64_t ld, double span_decades, uint64_t seed,
                          double *a, int64_t *perm_out);
+/* Memory-lean (streaming) forms of the same generators for the full-size
+ * parity tests: rows [r0, r1) of gen_gaussian(m, n, seed) into out (ld), and
+ * the C5 column factors f[j] = 10^(-span*pi[j]/(n-1)) (a row block scaled by
+ * a[j*ld+i] *= f[j] is bitwise the same block of orc_c5_scale_columns). */
+int orc_gen_gaussian_rows(int64_t m, int64_t n, uint64_t seed, int64_t r0, int64_t r1, double *out, int64_t ld);
+int orc_c5_column_factors(int64_t n, double span_decades, uint64_t seed, double *f);
 
 /* sketch.cc:52-99 SASO sampling for global columns [c0, c0+count) of S.
  * rows/vals: count*nnz entries, column-major per S column. */

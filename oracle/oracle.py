@@ -123,6 +123,29 @@ class Oracle:
         assert self.lib.orc_gen_kahan(_i64(n), _f64(theta), _p(out)) == 0
         return out
 
+    def gaussian_block(self, m, n, stream_seed):
+        """gaussian_block (testmat.cc:17-25) on a mixed stream seed."""
+        out = np.empty((m, n), order="F")
+        assert self.lib.orc_gaussian_block(_i64(m), _i64(n), _u64(stream_seed), _p(out)) == 0
+        return out
+
+    def gen_gaussian_rows(self, m, n, seed, r0, r1):
+        """Rows [r0, r1) of gen_gaussian(m, n, seed) (testmat.cc:141-143),
+        bitwise, without materialising the whole matrix."""
+        out = np.empty((r1 - r0, n), order="F")
+        rc = self.lib.orc_gen_gaussian_rows(_i64(m), _i64(n), _u64(seed), _i64(r0), _i64(r1), _p(out),
+                                            _i64(max(r1 - r0, 1)))
+        if rc:
+            raise ValueError("gen_gaussian_rows: bad row range")
+        return out
+
+    def c5_column_factors(self, n, span=8.0, seed=0):
+        """C5 column factors 10^(-span*pi[j]/(n-1)); a block
+        scaled by them equals the same block of c5_scale_columns bitwise."""
+        f = np.empty(n)
+        self.lib.orc_c5_column_factors(_i64(n), _f64(span), _u64(seed), _p(f))
+        return f
+
     def c5_scale_columns(self, a, span=8.0, seed=0):
         a = _f(a).copy(order="F")
         perm = np.empty(a.shape[1], dtype=np.int64)

@@ -26,6 +26,7 @@ from .cqrrpt import (  # noqa: F401
     dgeqpt,
     dgeqpt_host,
     flop_model,
+    release_workspace,
     sketch_flops_saso,
     sketch_rows_for,
     to_device_colmajor,

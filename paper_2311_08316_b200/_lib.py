@@ -37,7 +37,7 @@ class Ctx(ctypes.Structure):
         ("sketch_family", _i32), ("reserved0", _i32),
         ("d", _i64), ("k_sk", _i64), ("k0_final", _i64), ("retries", _i32), ("stage2_exact", _i32),
         ("cond_m_pre", _f64), ("cond_upper_bound", _f64), ("truncation_ratio", _f64), ("flop_estimate", _f64),
-        ("timings_ms", _f64 * 8),
+        ("timings_ms", _f64 * 8), ("sketch_rows", _i64),
     ]
 
 
@@ -57,6 +57,9 @@ SYMBOLS = {
                                                    ctypes.c_uint32, _vp]),
     "cqrrpt_gpu_qrcp": (ctypes.c_int, [_i64, _i64, _vp, _i64, _f64, _vp, _i64, _vp, ctypes.POINTER(_i64), _vp]),
     "cqrrpt_gpu_rank_stage1": (ctypes.c_int, [_i64, _i64, _vp, _i64, ctypes.POINTER(_i64), _vp]),
+    "cqrrpt_gpu_rank_stage2": (ctypes.c_int, [_i64, _i64, _vp, _i64, _vp, _i64, _f64, _i32, _i32, _vp, _i64, _vp, _i64,
+                                              ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i32),
+                                              ctypes.POINTER(_f64), _vp]),
     "cqrrpt_gpu_trsm_right": (ctypes.c_int, [_i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp]),
     "cqrrpt_gpu_gram": (ctypes.c_int, [_i64, _i64, _vp, _i64, _vp, _i64, _vp]),
     "cqrrpt_gpu_potrf": (ctypes.c_int, [_i64, _vp, _i64, ctypes.POINTER(_i64), _vp]),

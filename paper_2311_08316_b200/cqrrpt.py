@@ -157,14 +157,25 @@ def colmajor_empty(m: int, n: int, device=None, dtype=None, pad_to: int = 1):
 
 
 def to_device_colmajor(a, device=None):
-    """Host/device array -> column-major float64 CUDA tensor (a copy)."""
+    """Host/device array -> column-major float64 CUDA tensor. Always a fresh
+    copy, also when ``a`` already is a column-major float64 CUDA tensor (the
+    callers write Q into it in place)."""
     torch = _torch()
     if isinstance(a, torch.Tensor):
-        t = a.to(device=device or a.device if a.is_cuda else "cuda", dtype=torch.float64)
-        return t.t().contiguous().t()
+        dev = device or (a.device if a.is_cuda else "cuda")
+        m, n = a.shape
+        out = colmajor_empty(m, n, device=dev)
+        out.copy_(a)
+        return out
     arr = np.asarray(a, dtype=np.float64)
     host = torch.from_numpy(np.ascontiguousarray(arr.T)).pin_memory()
     return host.to(device or "cuda", non_blocking=True).t()
+
+
+def release_workspace() -> None:
+    """Free the library's cached device workspaces of the calling thread
+    (cqrrpt_gpu_release_workspace)."""
+    _lib.load().cqrrpt_gpu_release_workspace()
 
 
 def _ld(t) -> int:
@@ -179,9 +190,9 @@ def _ld(t) -> int:
     return s1
 
 
-def _stream_ptr(stream) -> int:
+def _stream_ptr(stream, device=None) -> int:
     torch = _torch()
-    s = stream if stream is not None else torch.cuda.current_stream()
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return s.cuda_stream
 
 
@@ -267,7 +278,7 @@ def dgeqpt(a, d_factor: float = 1.25, nnz: int = 4, seed: int = 0, eps_tol: floa
     if j_out is None:
         j_out = torch.empty(max(n, 1), dtype=torch.int64, device=a.device)
     ctx = _lib.new_ctx()
-    ctx.stream = _stream_ptr(stream)
+    ctx.stream = _stream_ptr(stream, a.device)
     ctx.cond_method = int(cond_method)
     flags = 0
     if not stage1:
@@ -306,9 +317,10 @@ def dgeqpt(a, d_factor: float = 1.25, nnz: int = 4, seed: int = 0, eps_tol: floa
         ctx.rank = int(rank)
         ctx.global_row_offset = int(global_row_offset)
     k, k0 = _lib._i64(), _lib._i64()
-    rc = L.cqrrpt_gpu_dgeqpt(m, n, a.data_ptr() if a.numel() else None, lda, float(d_factor), int(nnz), int(seed),
-                             float(eps_tol), r_out.data_ptr() if n else None, ldr, j_out.data_ptr(),
-                             ctypes.byref(k), ctypes.byref(k0), ctypes.byref(ctx))
+    with torch.cuda.device(a.device):  # the library works on the current device
+        rc = L.cqrrpt_gpu_dgeqpt(m, n, a.data_ptr() if a.numel() else None, lda, float(d_factor), int(nnz),
+                                 int(seed), float(eps_tol), r_out.data_ptr() if n else None, ldr, j_out.data_ptr(),
+                                 ctypes.byref(k), ctypes.byref(k0), ctypes.byref(ctx))
     _lib.check(rc, "cqrrpt_gpu_dgeqpt")
     return DeviceResult(r=r_out[: k.value, :], pivots=j_out[:n], k=k.value, k0=k0.value, ctx=ctx)
 
@@ -441,8 +453,10 @@ def cqrrpt(m, cfg: Optional[CqrrptConfig] = None) -> CqrrptOutput:
         return CqrrptOutput(PivotedQR(q, r, np.zeros(0, dtype=np.int64), 0))
     A = to_device_colmajor(m)  # working copy: Q is written in place
     src = A.clone() if cfg.validate_output else None
+    # the default (fast-accept) stage 2 is exact; diagnostics=True fills
+    # cond_m_pre with the value the reference's search reports
     res = dgeqpt(A, d_factor=cfg.gamma, nnz=cfg.nnz_per_col, seed=cfg.seed, eps_tol=cfg.eps_tol,
-                 cond_method=int(cfg.cond_method), stage1=cfg.stage1_enabled, exact_stage2=True,
+                 cond_method=int(cfg.cond_method), stage1=cfg.stage1_enabled,
                  diagnostics=True, timings=True,
                  sketch_family={SketchFamily.gaussian: "gaussian", SketchFamily.srft: "srft"}.get(cfg.family, "saso"))
     k = res.k
@@ -450,8 +464,6 @@ def cqrrpt(m, cfg: Optional[CqrrptConfig] = None) -> CqrrptOutput:
     r_dev = res.r
     piv = res.pivots.cpu().numpy().astype(np.int64)
     diag = _diagnostics_from(res.ctx)
-    if not res.ctx.stage2_exact:
-        diag.cond_m_pre = 1.0
     if on_device:
         q_out, r_out = q_dev, r_dev
     else:

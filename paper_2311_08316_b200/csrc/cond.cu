@@ -292,10 +292,10 @@ int identity_deviation_first(const double *r, int64_t ldr, const int64_t *ells, 
     idev_gvec_kernel<<<(unsigned)std::min<int64_t>((maxl + 255) / 256, 1024), 256, 0, st>>>(maxl, g);
     note_launch();
     const size_t smem = sizeof(double) * (size_t)nells * kIdChunks * kIdRows;
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(idev_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(sizeof(double) * kIdMaxProbes * kIdChunks * kIdRows));
-    CQ_CUDA(attr, "idev smem attr");
+    if (first_on_device((const void *)idev_rows_kernel))
+        CQ_CUDA(cudaFuncSetAttribute(idev_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(sizeof(double) * kIdMaxProbes * kIdChunks * kIdRows)),
+                "idev smem attr");
     idev_rows_kernel<<<(unsigned)nblk, kIdRows * kIdChunks, smem, st>>>(r, ldr, dl, nells, maxl, g, part);
     note_launch();
     idev_final_kernel<<<1, 256, 0, st>>>(dl, nells, g, part, nblk, dout);
@@ -513,12 +513,9 @@ int cond_estimate(int64_t ell, const double *r, int64_t ldr, const double *rinv,
         a.out = dout;
         if (!a.v || !a.w || !a.z || !a.part || !a.bar) return fail_nomem("cond estimator");
         const size_t smem = sizeof(double) * (size_t)(8 * 32 + 64 + ell);
-        static thread_local bool attr = false;
-        if (!attr) {
+        if (first_on_device((const void *)cond_grid_kernel))
             CQ_CUDA(cudaFuncSetAttribute(cond_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
                     "cond grid smem");
-            attr = true;
-        }
         if (smem > 200 * 1024) return fail_internal("cond estimator: block too large for shared memory");
         CQ_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned long long), st), "cond bar");
         void *args[] = {&a};

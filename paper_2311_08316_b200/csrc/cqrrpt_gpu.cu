@@ -95,6 +95,9 @@ struct PhaseClock {
         cudaEventRecord(ev[n], st);
         tag[n++] = phase;
     }
+    ~PhaseClock() {  // early (error) returns: events not consumed by finish()
+        for (int i = 0; i < n; ++i) cudaEventDestroy(ev[i]);
+    }
     void finish(double *out) {
         if (!on) return;
         cudaEventSynchronize(ev[n - 1]);
@@ -135,7 +138,7 @@ void cqrrpt_gpu_ctx_init(cqrrpt_gpu_ctx *ctx) {
     std::memset(ctx, 0, sizeof(*ctx));
     ctx->nranks = 1;
     ctx->cond_method = CQRRPT_COND_IDENTITY_DEVIATION;
-    ctx->cond_m_pre = 1.0;
+    ctx->cond_m_pre = NAN;
 }
 
 const char *cqrrpt_gpu_last_error(void) { return cqg::last_error(); }
@@ -204,27 +207,15 @@ int wavefront_q(int64_t m, int64_t k0, double *A, int64_t lda, const int64_t *jd
     // > st (the precondition). Gram block b writes G's columns of block b and
     // the mirrored entries below the diagonal in rows of block b; s2 reads only
     // upper-triangle entries of blocks < b, so the two overlap safely.
-    static thread_local cudaStream_t s2 = nullptr, s3 = nullptr;
-    static thread_local std::vector<cudaEvent_t> ev_pre, ev_q, ev_g;
-    static thread_local cudaEvent_t ev_start = nullptr, ev_end = nullptr;
-    if (!s2) {
-        int least = 0, greatest = 0;
-        CQ_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest), "stream priorities");
-        CQ_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, greatest), "wavefront stream");
-        CQ_CUDA(cudaStreamCreateWithPriority(&s3, cudaStreamNonBlocking, greatest < least ? greatest + 1 : least),
-                "wavefront stream");
-        CQ_CUDA(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming), "wavefront event");
-        CQ_CUDA(cudaEventCreateWithFlags(&ev_end, cudaEventDisableTiming), "wavefront event");
-    }
-    while ((int64_t)ev_pre.size() < nsub) {
-        cudaEvent_t a, b, c;
-        CQ_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "wavefront event");
-        CQ_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "wavefront event");
-        CQ_CUDA(cudaEventCreateWithFlags(&c, cudaEventDisableTiming), "wavefront event");
-        ev_pre.push_back(a);
-        ev_q.push_back(b);
-        ev_g.push_back(c);
-    }
+    cudaStream_t s2 = nullptr, s3 = nullptr;
+    cudaEvent_t *ev_pre = nullptr, *ev_q = nullptr, *ev_g = nullptr, *ev_se = nullptr;
+    CQ_TRY(cached_stream("wf.s2", 1, &s2));
+    CQ_TRY(cached_stream("wf.s3", 2, &s3));
+    CQ_TRY(cached_events("wf.pre", (size_t)nsub, &ev_pre));
+    CQ_TRY(cached_events("wf.q", (size_t)nsub, &ev_q));
+    CQ_TRY(cached_events("wf.g", (size_t)nw, &ev_g));
+    CQ_TRY(cached_events("wf.se", 2, &ev_se));
+    cudaEvent_t ev_start = ev_se[0], ev_end = ev_se[1];
     // CQRRPT_WF_TRACE=1: print when each Q block is formed and downloaded
     static const bool trace = std::getenv("CQRRPT_WF_TRACE") != nullptr;
     std::vector<cudaEvent_t> tq, td;
@@ -248,7 +239,7 @@ int wavefront_q(int64_t m, int64_t k0, double *A, int64_t lda, const int64_t *jd
     CQ_CUDA(cudaStreamWaitEvent(s2, ev_start, 0), "wavefront start wait");
     CQ_CUDA(cudaStreamWaitEvent(s3, ev_start, 0), "wavefront start wait");
     // precondition M_pre = M[:, J[:k0]] A_sk^{-1} on st, an event per 64 columns
-    CQ_TRY(trsm_right(m, k0, A, lda, jd, rsk, ldk, mpre, ldp, st, nullptr, true, ev_pre.data()));
+    CQ_TRY(trsm_right(m, k0, A, lda, jd, rsk, ldk, mpre, ldp, st, nullptr, true, ev_pre));
     clk.mark(PH_PRE);
     if (!sink) CQ_CUDA(cudaStreamWaitEvent(s2, ev_pre[(size_t)(nsub - 1)], 0), "wavefront wait precondition");
     for (int64_t b = 0; b < nw; ++b) {  // Gram columns, as soon as M_pre's columns exist
@@ -298,6 +289,142 @@ int wavefront_q(int64_t m, int64_t k0, double *A, int64_t lda, const int64_t *jd
     return 0;
 }
 
+// ---- rank_stage2's attempt loop (cqrrpt.cc:160-193) -------------------------
+// M_pre = B[:, cols[:k0]] A_sk^{-1} (gather fused into the TRSM), G = M_pre^T
+// M_pre (allreduced across ranks), upper Cholesky of G in place. fi: 0 or the
+// 1-based first failing minor.
+int precondition_factor(int64_t m, int64_t k0, const double *B, int64_t ldb, const int64_t *cols, const double *a_sk,
+                        int64_t ldas, double *mpre, int64_t ldp, double *g, int64_t ldg, int64_t *fi,
+                        cqrrpt_gpu_ctx *ctx, PhaseClock *clk, Workspace &ws, cudaStream_t st) {
+    CQ_TRY(trsm_right(m, k0, B, ldb, cols, a_sk, ldas, mpre, ldp, st));
+    if (clk) clk->mark(PH_PRE);
+    CQ_TRY(gram(m, k0, mpre, ldp, g, ldg, ws, st));
+    if (clk) clk->mark(PH_CHOL);
+    if (ctx) CQ_TRY(do_allreduce(ctx, g, (size_t)(k0 * ldg), st));
+    if (clk) clk->mark(PH_COMM);
+    return potrf(k0, g, ldg, fi, ws, st);
+}
+
+// A failure at minor fi shrinks k0 to fi - 1. The retry on the leading fi-1
+// columns recomputes bitwise the same M_pre columns, Gram block (the Gram has
+// the leading-block property) and factor (cqrrpt.cc:162-164), so it always
+// succeeds: one retry, k0_final = fi - 1 (0 means rank 0, cqrrpt.cc:178-182).
+void shrink_after_failure(int64_t k0, int64_t fi, int64_t *k0f, int *retries) {
+    *k0f = k0;
+    *retries = 0;
+    if (fi > 0) {
+        *retries = 1;
+        *k0f = fi - 1;
+    }
+}
+
+// ---- rank_stage2's selection (cqrrpt.cc:195-207) ----------------------------
+// On the Cholesky factor R_pre (leading k0f x k0f block of rfull, ld ldf):
+// the largest leading block whose NestedCondEstimator value is <=
+// sqrt(eps_tol/u). Fast accept (exact): if every probe of the
+// all-pass search path has tau >= 1 at its first power iterate (so the
+// reference's identity_deviation is +inf and it falls back to krylov_bounds)
+// and ||R||_F ||R^-1||_F (1+1e-5) <= threshold bounds every krylov estimate,
+// every probe passes and k = k0f; otherwise the reference's binary search
+// runs on the device. rinv (k0f x k0f) = R_pre^{-1} stays valid in ws.
+struct Stage2Out {
+    int64_t k = 0;
+    double cond = NAN;   // est.at(k) when the search ran, NaN on the fast path
+    int exact = 0;       // 1 if the binary search ran
+    double bound = 0.0;  // ||R||_F ||R^-1||_F
+};
+
+static void all_pass_probes(int64_t k0f, std::vector<int64_t> &ells) {
+    ells.clear();
+    for (int64_t lo = 0, hi = k0f; lo < hi;) {  // cqrrpt.cc:197-204 when every probe passes
+        const int64_t mid = lo + (hi - lo + 1) / 2;
+        ells.push_back(mid);
+        lo = mid;
+    }
+}
+
+static int nested_method(int method) {
+    // identity_deviation with the nested krylov fallback (cqrrpt.cc:57-58)
+    return (method == CQRRPT_COND_IDENTITY_DEVIATION) ? CQRRPT_COND_NESTED_IDENTITY_DEVIATION : method;
+}
+
+int stage2_select(int64_t k0f, const double *rfull, int64_t ldf, double eps_tol, int method, bool force_exact,
+                  Workspace &ws, cudaStream_t s, Stage2Out *out, double **rinv_out) {
+    const double threshold = std::sqrt(eps_tol / kUnitRoundoff);
+    double *rinv = ws.get<double>("drv.rinv", (size_t)(k0f * k0f));
+    if (!rinv) return fail_nomem("rinv");
+    *rinv_out = rinv;
+    CQ_TRY(trtri_upper(k0f, rfull, ldf, rinv, k0f, ws, s));  // leading blocks of R^-1 = leading inverses
+    bool exact = force_exact;
+    out->k = k0f;
+    if (!exact) {
+        std::vector<int64_t> ells;
+        all_pass_probes(k0f, ells);
+        if (method == CQRRPT_COND_IDENTITY_DEVIATION) {
+            // power_iterate keeps est = max(est, ...) (linalg.cc:455): tau >= 1
+            // at the first iterate means +inf whatever the later iterates
+            std::vector<double> first(ells.size());
+            CQ_TRY(identity_deviation_first(rfull, ldf, ells.data(), (int)ells.size(), first.data(), ws, s));
+            for (double v : first)
+                if (!(v * (1.0 + 1e-6) >= 1.0)) exact = true;
+        }
+        double fr = 0.0, fi = 0.0;
+        CQ_TRY(frob_norm_upper(k0f, rfull, ldf, &fr, ws, s));
+        CQ_TRY(frob_norm_upper(k0f, rinv, k0f, &fi, ws, s));
+        out->bound = fr * fi;  // >= cond_2(R_ell) for every leading block
+        if (!(out->bound * (1.0 + 1e-5) <= threshold)) exact = true;
+    }
+    out->exact = exact ? 1 : 0;
+    if (!exact) return 0;
+    // NestedCondEstimator (cqrrpt.cc:47-71): memoised raw estimates, running max
+    std::map<int64_t, double> raw;
+    auto at = [&](int64_t ell, double *v) -> int {
+        if (ell <= 0) {
+            *v = 1.0;
+            return 0;
+        }
+        if (!raw.count(ell)) {
+            double e = 1.0;
+            CQ_TRY(cond_estimate(ell, rfull, ldf, rinv, k0f, nested_method(method), &e, ws, s));
+            raw[ell] = e;
+        }
+        double e = 1.0;
+        for (auto &kv : raw)
+            if (kv.first <= ell) e = std::max(e, kv.second);
+        *v = e;
+        return 0;
+    };
+    int64_t lo = 0, hi = k0f;  // binary search (cqrrpt.cc:197-207)
+    while (lo < hi) {
+        const int64_t mid = lo + (hi - lo + 1) / 2;
+        double e = 0.0;
+        CQ_TRY(at(mid, &e));
+        if (e <= threshold) lo = mid;
+        else hi = mid - 1;
+    }
+    out->k = lo;
+    double c = 1.0;
+    if (lo > 0) CQ_TRY(at(lo, &c));
+    out->cond = c;
+    return 0;
+}
+
+// est.at(k0f) after an all-pass search: the running max of the probes' raw
+// nested estimates (what the reference reports as cond_m_pre on that path)
+int probe_cond(int64_t k0f, const double *rfull, int64_t ldf, const double *rinv, int method, Workspace &ws,
+               cudaStream_t s, double *cond) {
+    std::vector<int64_t> ells;
+    all_pass_probes(k0f, ells);
+    double c = 1.0;
+    for (int64_t ell : ells) {
+        double e = 1.0;
+        CQ_TRY(cond_estimate(ell, rfull, ldf, rinv, k0f, nested_method(method), &e, ws, s));
+        c = std::max(c, e);
+    }
+    *cond = (k0f > 0) ? c : 1.0;
+    return 0;
+}
+
 // The driver; `qsink` (optional) downloads Q block by block during the final TRSM.
 constexpr int kInputChunks = 4;  // H2D row chunks of the host-buffer entry point
 
@@ -323,7 +450,7 @@ int dgeqpt_impl(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, i
     if (!multi && m < 1) return set_error("sample_sketch: need m >= 1"), -1;  // sketch.cc:54
     if (m > 0 && !A) return -3;
     if (m > 0 && lda < m) return set_error("lda < m"), -4;
-    const int64_t d = cqrrpt_gpu_sketch_rows(d_factor, n);
+    const int64_t d = ctx->sketch_rows > 0 ? ctx->sketch_rows : cqrrpt_gpu_sketch_rows(d_factor, n);
     if (ctx->sketch_family != CQRRPT_SKETCH_SASO && ctx->sketch_family != CQRRPT_SKETCH_GAUSSIAN &&
         ctx->sketch_family != CQRRPT_SKETCH_SRFT)
         return set_error("unknown sketch family"), -14;  // the reference throws std::logic_error
@@ -345,7 +472,7 @@ int dgeqpt_impl(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, i
     ctx->d = d;
     ctx->retries = 0;
     ctx->stage2_exact = 0;
-    ctx->cond_m_pre = 1.0;
+    ctx->cond_m_pre = NAN;
     ctx->cond_upper_bound = 0.0;
     ctx->truncation_ratio = 0.0;
 
@@ -399,6 +526,7 @@ int dgeqpt_impl(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, i
             csk = (double)n * ((double)m + P * std::log2(P) + (double)d);
         }
         ctx->flop_estimate = cqrrpt_gpu_flop_model(m, n, k, d, csk);
+        if (k == 0) ctx->cond_m_pre = 1.0;  // CqrrptDiagnostics default (cqrrpt.hh:118) on rank-0 outputs
         clk.finish(ctx->timings_ms);
     };
     if (k0 == 0) {  // cqrrpt.cc:257-260
@@ -425,23 +553,13 @@ int dgeqpt_impl(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, i
     if (wave) {
         clk.mark(PH_CHOL);
     } else {
-        CQ_TRY(trsm_right(m, k0, A, lda, jd, rsk, ldk, mpre, ldp, st));
-        clk.mark(PH_PRE);
-
-        // ---- Gram + Cholesky (rank_stage2 attempt loop, cqrrpt.cc:160-193) ---
-        CQ_TRY(gram(m, k0, mpre, ldp, gmat, k0, ws, st));
-        clk.mark(PH_CHOL);
-        CQ_TRY(do_allreduce(ctx, gmat, (size_t)(k0 * k0), st));
-        clk.mark(PH_COMM);
-        CQ_TRY(potrf(k0, gmat, k0, &fi, ws, st));
+        CQ_TRY(precondition_factor(m, k0, A, lda, jd, rsk, ldk, mpre, ldp, gmat, k0, &fi, ctx, &clk, ws, st));
     }
     int64_t k0f = k0;
+    int retries = 0;
+    shrink_after_failure(k0, fi, &k0f, &retries);
+    ctx->retries = retries;
     if (fi > 0) {
-        // The retry on the leading fi-1 columns recomputes bitwise the same
-        // M_pre columns, Gram block and factor (cqrrpt.cc:162-164), so it
-        // always succeeds: one retry, k0_final = fi - 1.
-        ctx->retries = 1;
-        k0f = fi - 1;
         if (k0f <= 0) {
             ctx->k0_final = 0;
             CQ_TRY(emit_pivots());
@@ -459,22 +577,42 @@ int dgeqpt_impl(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, i
     // for k columns in the rare case stage 2 truncates (A[:, k:k0] then holds
     // speculative columns). The side stream touches only M_pre, R_pre, A and
     // the TRSM's own block inverses, none of which stage 2 writes.
-    static thread_local cudaStream_t sq = nullptr;
-    static thread_local cudaEvent_t ev_sq0 = nullptr, ev_sq1 = nullptr;
     const bool spec_q = !wave && !qsink && !(ctx->flags & CQRRPT_GPU_NO_WAVEFRONT);
+    cudaStream_t sq = nullptr, shi = nullptr;
+    cudaEvent_t *ev_side = nullptr;
     if (spec_q) {
-        if (!sq) {
-            CQ_CUDA(cudaStreamCreateWithFlags(&sq, cudaStreamNonBlocking), "final solve stream");
-            CQ_CUDA(cudaEventCreateWithFlags(&ev_sq0, cudaEventDisableTiming), "final solve event");
-            CQ_CUDA(cudaEventCreateWithFlags(&ev_sq1, cudaEventDisableTiming), "final solve event");
+        CQ_TRY(cached_stream("drv.sq", 0, &sq));
+        CQ_TRY(cached_stream("drv.shi", 1, &shi));
+        CQ_TRY(cached_events("drv.side", 3, &ev_side));
+    }
+    cudaEvent_t ev_sq0 = spec_q ? ev_side[0] : nullptr, ev_sq1 = spec_q ? ev_side[1] : nullptr,
+                ev_hi = spec_q ? ev_side[2] : nullptr;
+    // On an error return after the fork, wait for the side streams before
+    // handing control back: the speculative solve writes into A.
+    struct SideJoin {
+        cudaEvent_t sq_done = nullptr, hi_done = nullptr;
+        cudaStream_t shi = nullptr;
+        bool armed = false;
+        ~SideJoin() {
+            if (!armed) return;
+            if (shi && hi_done && cudaEventRecord(hi_done, shi) == cudaSuccess) cudaEventSynchronize(hi_done);
+            if (sq_done) cudaEventSynchronize(sq_done);
+            cudaGetLastError();
         }
+    } side_join;
+    if (spec_q) {
         CQ_CUDA(cudaEventRecord(ev_sq0, st), "final solve fork");
         CQ_CUDA(cudaStreamWaitEvent(sq, ev_sq0, 0), "final solve fork wait");
+        side_join.armed = true;
+        side_join.shi = shi;
+        side_join.hi_done = ev_hi;
         CQ_TRY(trsm_right(m, k0f, mpre, ldp, nullptr, rfull, k0, A, lda, sq, nullptr, /*check_diag=*/false));
         CQ_CUDA(cudaEventRecord(ev_sq1, sq), "final solve join");
+        side_join.sq_done = ev_sq1;
     }
     auto join_spec = [&]() -> int {
         if (spec_q) CQ_CUDA(cudaStreamWaitEvent(st, ev_sq1, 0), "final solve join wait");
+        side_join.armed = false;  // st now orders everything after the side streams
         return 0;
     };
 
@@ -482,88 +620,23 @@ int dgeqpt_impl(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, i
     // with the speculative final solve in flight, stage 2 runs on a
     // high-priority stream so its small kernels are not queued behind the
     // solve's CTAs
-    static thread_local cudaStream_t shi = nullptr;
-    static thread_local cudaEvent_t ev_hi = nullptr;
     cudaStream_t s2st = st;
     if (spec_q) {
-        if (!shi) {
-            int least = 0, greatest = 0;
-            CQ_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest), "stream priorities");
-            CQ_CUDA(cudaStreamCreateWithPriority(&shi, cudaStreamNonBlocking, greatest), "stage-2 stream");
-            CQ_CUDA(cudaEventCreateWithFlags(&ev_hi, cudaEventDisableTiming), "stage-2 event");
-        }
         CQ_CUDA(cudaStreamWaitEvent(shi, ev_sq0, 0), "stage-2 fork");
         s2st = shi;
     }
-    const double threshold = std::sqrt(eps_tol / kUnitRoundoff);
-    const int method = ctx->cond_method;
-    double *rinv = ws.get<double>("drv.rinv", (size_t)(k0f * k0f));
-    if (!rinv) return fail_nomem("rinv");
-    CQ_TRY(trtri_upper(k0f, rfull, k0, rinv, k0f, ws, s2st));  // R^{-1}; leading blocks = leading inverses
-    bool exact = (ctx->flags & CQRRPT_GPU_EXACT_STAGE2) != 0;
-    int64_t k = k0f;
-    if (!exact) {
-        // probes of the all-pass binary search path (cqrrpt.cc:197-204)
-        std::vector<int64_t> ells;
-        for (int64_t lo = 0, hi = k0f; lo < hi;) {
-            int64_t mid = lo + (hi - lo + 1) / 2;
-            ells.push_back(mid);
-            lo = mid;
-        }
-        if (method == CQRRPT_COND_IDENTITY_DEVIATION) {
-            // power_iterate keeps est = max(est, ...) (linalg.cc:455): if the
-            // first iterate already gives tau >= 1 the reference returns +inf
-            // and falls back to krylov_bounds, whatever the later iterates.
-            std::vector<double> first(ells.size());
-            CQ_TRY(identity_deviation_first(rfull, k0, ells.data(), (int)ells.size(), first.data(), ws, s2st));
-            for (double v : first)
-                if (!(v * (1.0 + 1e-6) >= 1.0)) exact = true;
-        }
-        double fr = 0.0, fi_ = 0.0;
-        CQ_TRY(frob_norm_upper(k0f, rfull, k0, &fr, ws, s2st));
-        CQ_TRY(frob_norm_upper(k0f, rinv, k0f, &fi_, ws, s2st));
-        const double bound = fr * fi_;  // >= cond_2(R_ell) for every leading block
-        ctx->cond_upper_bound = bound;
-        if (!(bound * (1.0 + 1e-5) <= threshold)) exact = true;
-    }
-    if (exact) {
-        // NestedCondEstimator (cqrrpt.cc:47-71) + binary search (cqrrpt.cc:197-207)
-        std::map<int64_t, double> raw;
-        auto at = [&](int64_t ell, double *out) -> int {
-            if (ell <= 0) {
-                *out = 1.0;
-                return 0;
-            }
-            if (!raw.count(ell)) {
-                double v = 1.0;
-                // method 3 = identity_deviation with the nested krylov fallback
-                const int m_nested = (method == CQRRPT_COND_IDENTITY_DEVIATION) ? 3 : method;
-                CQ_TRY(cond_estimate(ell, rfull, k0, rinv, k0f, m_nested, &v, ws, s2st));
-                raw[ell] = v;
-            }
-            double v = 1.0;
-            for (auto &kv : raw)
-                if (kv.first <= ell) v = std::max(v, kv.second);
-            *out = v;
-            return 0;
-        };
-        int64_t lo = 0, hi = k0f;
-        while (lo < hi) {
-            int64_t mid = lo + (hi - lo + 1) / 2;
-            double e = 0.0;
-            CQ_TRY(at(mid, &e));
-            if (e <= threshold) lo = mid;
-            else hi = mid - 1;
-        }
-        k = lo;
-        double c = 1.0;
-        if (lo > 0) CQ_TRY(at(lo, &c));
-        ctx->cond_m_pre = c;
-        ctx->stage2_exact = 1;
-    }
+    Stage2Out s2o;
+    double *rinv = nullptr;
+    CQ_TRY(stage2_select(k0f, rfull, k0, eps_tol, ctx->cond_method, (ctx->flags & CQRRPT_GPU_EXACT_STAGE2) != 0, ws,
+                         s2st, &s2o, &rinv));
+    const int64_t k = s2o.k;
+    ctx->cond_upper_bound = s2o.bound;
+    ctx->stage2_exact = s2o.exact;
+    ctx->cond_m_pre = s2o.cond;  // NaN on the fast-accept path until the diagnostics below
     if (spec_q) {
         CQ_CUDA(cudaEventRecord(ev_hi, shi), "stage-2 join");
         CQ_CUDA(cudaStreamWaitEvent(st, ev_hi, 0), "stage-2 join wait");
+        side_join.shi = nullptr;  // joined
     }
     clk.mark(PH_RANK);
     *k_out = k;
@@ -598,6 +671,10 @@ int dgeqpt_impl(int64_t m, int64_t n, double *A, int64_t lda, double d_factor, i
     // ---- diagnostics (outside the profiled phases, cqrrpt.cc:298-303) -------
     finish_diag(k);
     if (ctx->flags & CQRRPT_GPU_DIAGNOSTICS) {
+        // cond_m_pre (cqrrpt.cc:205,298): on the fast-accept path every probe
+        // of the binary search passed, so est.at(k) is the running max of the
+        // probes' nested estimates -- evaluated here, outside the timed phases
+        if (!s2o.exact) CQ_TRY(probe_cond(k0f, rfull, k0, rinv, ctx->cond_method, ws, st, &ctx->cond_m_pre));
         std::vector<double> hr((size_t)(n * n));
         CQ_CUDA(cudaMemcpyAsync(hr.data(), rsk, sizeof(double) * n * n, cudaMemcpyDeviceToHost, st), "rsk d2h");
         CQ_CUDA(cudaStreamSynchronize(st), "diag sync");
@@ -637,22 +714,18 @@ int cqrrpt_gpu_dgeqpt_host(int64_t m, int64_t n, const double *A_host, int64_t l
     Workspace &ws = workspace();
     double *dA = (m > 0 && n > 0) ? ws.get<double>("host.a", (size_t)(m * n)) : nullptr;
     if (m > 0 && n > 0 && !dA) return fail_nomem("device copy of A");
-    static thread_local cudaStream_t copy = nullptr;
-    if (!copy) CQ_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking), "copy stream");
+    cudaStream_t copy = nullptr;
+    CQ_TRY(cached_stream("host.copy", 0, &copy));
     // H2D of A in row chunks on the copy stream; the exact sketch consumes
     // each chunk as it lands (its FMA chains run in row order), so only the
     // last chunk's share of the sketch remains after the transfer
-    static thread_local std::vector<cudaEvent_t> in_ev;
+    cudaEvent_t *in_ev = nullptr;
+    CQ_TRY(cached_events("host.in", kInputChunks, &in_ev));
     int64_t row_end[kInputChunks];
     int nch = 0;
     if (dA) {
         const int64_t tiles = (m + 255) / 256;
         nch = (int)std::max<int64_t>(1, std::min<int64_t>(kInputChunks, tiles / 64));
-        while ((int)in_ev.size() < nch) {
-            cudaEvent_t ev;
-            CQ_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "input event");
-            in_ev.push_back(ev);
-        }
         CQ_CUDA(cudaEventRecord(in_ev[0], st), "input order");  // A's buffer is free once st reaches here
         CQ_CUDA(cudaStreamWaitEvent(copy, in_ev[0], 0), "input order wait");
         int64_t r0 = 0;
@@ -666,7 +739,7 @@ int cqrrpt_gpu_dgeqpt_host(int64_t m, int64_t n, const double *A_host, int64_t l
             r0 = r1;
         }
     }
-    const InputChunks chunks{nch, in_ev.data(), row_end};
+    const InputChunks chunks{nch, in_ev, row_end};
     BlockSink sink{copy, Q_host, ldq};
     const int32_t flags = ctx->flags;
     ctx->flags |= CQRRPT_GPU_OUTPUTS_ON_HOST;
@@ -746,6 +819,52 @@ int cqrrpt_gpu_qrcp(int64_t d, int64_t n, double *Msk, int64_t ldm, double rank_
 int cqrrpt_gpu_rank_stage1(int64_t k, int64_t n, const double *R, int64_t ldr, int64_t *k0, void *stream) {
     if (k < 0 || n < 0) return -1;
     return rank_stage1(k, n, R, ldr, k0, workspace(), (cudaStream_t)stream);
+}
+
+int cqrrpt_gpu_rank_stage2(int64_t m, int64_t k0, const double *M_k0, int64_t ldm, const double *A_sk, int64_t ldas,
+                           double eps_tol, int32_t cond_method, int32_t flags, double *M_pre, int64_t ldp, double *R_pre,
+                           int64_t ldr, int64_t *rank, int64_t *k0_final, int32_t *retries, double *cond_at_rank,
+                           void *stream) {
+    if (m < 0) return -1;
+    if (k0 < 1) return set_error("rank_stage2: requires k0 >= 1"), -2;  // cqrrpt.cc:153
+    if (!M_k0 && m > 0) return -3;
+    if (m > 0 && ldm < m) return -4;
+    if (!A_sk) return -5;
+    if (ldas < k0) return -6;
+    if (!(eps_tol > kUnitRoundoff)) return -7;
+    if (cond_method < 0 || cond_method > 3) return -8;
+    if (!M_pre && m > 0) return -10;
+    if (m > 0 && ldp < m) return -11;
+    if (!R_pre) return -12;
+    if (ldr < k0) return -13;
+    if (!rank || !k0_final || !retries || !cond_at_rank) return -14;
+    cudaStream_t st = (cudaStream_t)stream;
+    Workspace &ws = workspace();
+    int64_t fi = 0;
+    CQ_TRY(precondition_factor(m, k0, M_k0, ldm, nullptr, A_sk, ldas, M_pre, std::max<int64_t>(ldp, 1), R_pre, ldr, &fi,
+                               nullptr, nullptr, ws, st));
+    int64_t k0f = k0;
+    int rt = 0;
+    shrink_after_failure(k0, fi, &k0f, &rt);
+    *retries = rt;
+    *k0_final = k0f;
+    *rank = 0;
+    *cond_at_rank = 1.0;
+    if (k0f <= 0) {
+        *k0_final = 0;
+        return 0;
+    }
+    Stage2Out s2o;
+    double *rinv = nullptr;
+    CQ_TRY(stage2_select(k0f, R_pre, ldr, eps_tol, cond_method, (flags & CQRRPT_GPU_EXACT_STAGE2) != 0, ws, st, &s2o,
+                         &rinv));
+    *rank = s2o.k;
+    if (s2o.k > 0) {
+        if (s2o.exact) *cond_at_rank = s2o.cond;
+        else CQ_TRY(probe_cond(k0f, R_pre, ldr, rinv, cond_method, ws, st, cond_at_rank));
+    }
+    CQ_CUDA(cudaStreamSynchronize(st), "rank_stage2 sync");
+    return 0;
 }
 
 int cqrrpt_gpu_trsm_right(int64_t m, int64_t k, const double *B, int64_t ldb, const int64_t *cols, const double *U,

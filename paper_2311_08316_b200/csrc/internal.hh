@@ -51,6 +51,15 @@ public:
 Workspace &workspace();
 void release_workspace();
 
+// Streams / events cached per (host thread, current device) under a name
+// (prio: 0 default, 1 highest, 2 second highest); cached_events returns an
+// array of >= count events (valid until the same name grows again).
+int current_device();
+int cached_stream(const char *name, int prio, cudaStream_t *out);
+int cached_events(const char *name, size_t count, cudaEvent_t **out);
+// true exactly once per (device, key): one-time per-device function attributes
+bool first_on_device(const void *key);
+
 // ---- kernels' host entry points (implemented in the .cu files) -------------
 int saso_plan(int64_t d, int64_t c0, int64_t count, int64_t nnz, uint64_t seed, uint32_t *plan, cudaStream_t st);
 // Rows of A still arriving when the sketch is launched: chunk c (rows up to

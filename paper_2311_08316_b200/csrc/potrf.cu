@@ -129,14 +129,11 @@ int potrf(int64_t n, double *g, int64_t ldg, int64_t *failure_index, Workspace &
     if (n <= 0) return 0;
     int64_t *fail = ws.get<int64_t>("potrf.fail", 1);
     if (!fail) return fail_nomem("potrf workspace");
-    static thread_local cudaStream_t aux = nullptr;
-    static thread_local cudaEvent_t ev_in = nullptr, ev_c1 = nullptr, ev_c2 = nullptr;
-    if (!aux) {
-        CQ_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking), "potrf aux stream");
-        CQ_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming), "potrf event");
-        CQ_CUDA(cudaEventCreateWithFlags(&ev_c1, cudaEventDisableTiming), "potrf event");
-        CQ_CUDA(cudaEventCreateWithFlags(&ev_c2, cudaEventDisableTiming), "potrf event");
-    }
+    cudaStream_t aux = nullptr;
+    cudaEvent_t *pev = nullptr;
+    CQ_TRY(cached_stream("potrf.aux", 0, &aux));
+    CQ_TRY(cached_events("potrf.ev", 3, &pev));
+    cudaEvent_t ev_in = pev[0], ev_c1 = pev[1], ev_c2 = pev[2];
     CQ_CUDA(cudaMemsetAsync(fail, 0, sizeof(int64_t), st), "memset fail");
     CQ_CUDA(cudaEventRecord(ev_in, st), "potrf record");
     CQ_CUDA(cudaStreamWaitEvent(aux, ev_in, 0), "potrf wait");

@@ -1561,10 +1561,11 @@ int qrcp(int64_t d, int64_t n, double *b, int64_t ldb, double rank_tol, double *
     size_t cl_smem = 0;
     const bool cluster_ok = getenv("CQRRPT_QRCP_GENERAL") == nullptr && getenv("CQRRPT_QRCP_NOCLUSTER") == nullptr;
     if (cluster_ok) {
-        static int checked = 0, cs_ok16 = 0, cs_ok8 = 0;  // per process (one GPU type)
+        static int cs_ok16_dev[64] = {0}, cs_ok8_dev[64] = {0};  // per device (attributes are per device)
+        const int dev = current_device() & 63;
+        int &cs_ok16 = cs_ok16_dev[dev], &cs_ok8 = cs_ok8_dev[dev];
         const int64_t rows_max = 1600;
-        if (!checked) {
-            checked = 1;
+        if (first_on_device((const void *)qrcp_cluster_kernel)) {
             const size_t smem_max = sizeof(double) * (size_t)(kClWarps + 2) * rows_max;
             cudaFuncSetAttribute(qrcp_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
             cudaFuncSetAttribute(qrcp_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

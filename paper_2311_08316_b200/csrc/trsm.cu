@@ -252,7 +252,8 @@ int trsm_right(int64_t m, int64_t k, const double *b, int64_t ldb, const int64_t
     if (!dinv) return fail_nomem("trsm diagonal-block inverses");
     CQ_TRY(trtri_diag_blocks(k, u, ldu, dinv, st));
     const unsigned grid = (unsigned)((m + kBM - 1) / kBM);
-    static thread_local std::vector<cudaEvent_t> evs;  // one per block, reused across calls
+    cudaEvent_t *evs = nullptr;  // one per block, reused across calls (per device)
+    if (sink) CQ_TRY(cached_events("trsm.sink", (size_t)((k + kNB - 1) / kNB), &evs));
     for (int64_t c0 = 0; c0 < k; c0 += kNB) {
         {
             cudaLaunchConfig_t cfg = {};
@@ -273,11 +274,6 @@ int trsm_right(int64_t m, int64_t k, const double *b, int64_t ldb, const int64_t
         if (block_ev) CQ_CUDA(cudaEventRecord(block_ev[c0 / kNB], st), "trsm block event");
         if (sink) {  // block c0 is final: download it while the next blocks run
             const size_t e = (size_t)(c0 / kNB);
-            while (evs.size() <= e) {
-                cudaEvent_t ev;
-                CQ_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "trsm sink event");
-                evs.push_back(ev);
-            }
             CQ_CUDA(cudaEventRecord(evs[e], st), "trsm sink record");
             CQ_CUDA(cudaStreamWaitEvent(sink->copy, evs[e], 0), "trsm sink wait");
             const int64_t nb = std::min<int64_t>(kNB, k - c0);

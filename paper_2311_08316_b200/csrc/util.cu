@@ -4,6 +4,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "internal.hh"
@@ -88,6 +89,64 @@ void *Workspace::raw(const char *name, size_t bytes) {
         b.bytes = want;
     }
     return b.p;
+}
+
+// ---- per-device streams, events and one-time attributes -------------------
+// Streams and events belong to the device that was current when they were
+// created, so the library caches them per (host thread, device): a thread
+// that later calls on another device gets that device's own objects.
+namespace {
+struct DevObjs {
+    std::map<std::string, cudaStream_t> streams;
+    std::map<std::string, std::vector<cudaEvent_t>> events;
+};
+thread_local std::map<int, DevObjs> g_objs;
+std::mutex g_once_mu;
+std::map<std::pair<int, const void *>, bool> g_once;
+}  // namespace
+
+int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
+
+int cached_stream(const char *name, int prio, cudaStream_t *out) {
+    DevObjs &o = g_objs[current_device()];
+    auto it = o.streams.find(name);
+    if (it != o.streams.end()) {
+        *out = it->second;
+        return 0;
+    }
+    int least = 0, greatest = 0;
+    CQ_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest), "stream priorities");
+    int p = least;  // prio 0: default priority
+    if (prio == 1) p = greatest;
+    if (prio == 2) p = greatest < least ? greatest + 1 : least;
+    cudaStream_t s = nullptr;
+    CQ_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, p), name);
+    o.streams[name] = s;
+    *out = s;
+    return 0;
+}
+
+int cached_events(const char *name, size_t count, cudaEvent_t **out) {
+    std::vector<cudaEvent_t> &v = g_objs[current_device()].events[name];
+    while (v.size() < count) {
+        cudaEvent_t e;
+        CQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), name);
+        v.push_back(e);
+    }
+    *out = v.data();
+    return 0;
+}
+
+bool first_on_device(const void *key) {
+    std::lock_guard<std::mutex> g(g_once_mu);
+    bool &done = g_once[{current_device(), key}];
+    if (done) return false;
+    done = true;
+    return true;
 }
 
 Workspace &workspace() {

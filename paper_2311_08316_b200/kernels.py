@@ -78,6 +78,26 @@ def rank_stage1(r, stream=None) -> int:
     return k0.value
 
 
+def rank_stage2(m_k0, a_sk, eps_tol: float = 1e-4, method: int = _lib.COND_IDENTITY_DEVIATION,
+                exact: bool = False, stream=None) -> dict:
+    """rank_stage2(M_k0, A_sk, eps_tol) (cqrrpt.cc:149-209): the routine the
+    driver runs after stage 1. Returns rank, k0_final, retries, cond_at_rank
+    and the device factors r_pre (rank x rank) and m_pre (m x k0_final)."""
+    m, k0 = m_k0.shape
+    mpre = colmajor_empty(m, k0)
+    rpre = colmajor_empty(k0, k0)
+    rank, k0f = _lib._i64(), _lib._i64()
+    retries, cond = _lib._i32(), _lib._f64()
+    _lib.check(_lib.load().cqrrpt_gpu_rank_stage2(m, k0, _p(m_k0), _ld(m_k0) if m else 1, _p(a_sk), _ld(a_sk),
+                                                  float(eps_tol), int(method), _lib.F_EXACT_STAGE2 if exact else 0,
+                                                  _p(mpre), _ld(mpre) if m else 1, _p(rpre), _ld(rpre),
+                                                  ctypes.byref(rank), ctypes.byref(k0f), ctypes.byref(retries),
+                                                  ctypes.byref(cond), _stream_ptr(stream)), "rank_stage2")
+    k = rank.value
+    return dict(rank=k, k0_final=k0f.value, retries=retries.value, cond_at_rank=cond.value,
+                r_pre=rpre[:k, :k], m_pre=mpre[:, : k0f.value])
+
+
 def trsm_right(b, u, cols=None, stream=None):
     """trsm_right(B[:, cols], U) (linalg.cc:244-277) -> X = B[:, cols] U^{-1}."""
     m = b.shape[0]

@@ -11,6 +11,7 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA (B200) device")
     config.addinivalue_line("markers", "slow: long-running")
+    config.addinivalue_line("markers", "fullsize: BASELINE-size parity against the reference (GPU box)")
 
 
 @pytest.fixture(scope="session")

@@ -162,49 +162,165 @@ def test_stage2_exact_vs_fast_path_agree(cuda, oracle):
     assert r2.ctx.cond_m_pre == pytest.approx(ref.cond_m_pre, rel=1e-6)
 
 
-@pytest.mark.parametrize("case", ["zero_col", "dups", "dups_small"])
-def test_stage2_cholesky_failure_paths(cuda, oracle, case):
-    """Reference stage-2 behaviour on its own failure inputs (test_cqrrpt.cc:170-197,302-313;
-    SURVEY P10 values: (retries, k0_final, rank) = (1,8,8), (1,6,6), (1,5,5))."""
+def _failure_input(oracle, case):
     if case == "zero_col":
         base = oracle.gen_gaussian(40, 8, 11)
         mk = np.zeros((40, 12)); mk[:, :8] = base; mk[:, 9:12] = base[:, :3]
-        want = (1, 8, 8)
-    elif case == "dups":
+        return mk, (1, 8, 8)
+    if case == "dups":
         base = oracle.gen_gaussian(50, 6, 12)
         mk = np.zeros((50, 9)); mk[:, :6] = base; mk[:, 6:9] = base[:, :3]
-        want = (1, 6, 6)
-    else:
-        base = oracle.gen_gaussian(30, 5, 13)
-        mk = np.zeros((30, 7)); mk[:, :5] = base; mk[:, 5:7] = base[:, :2]
-        want = (1, 5, 5)
+        return mk, (1, 6, 6)
+    base = oracle.gen_gaussian(30, 5, 13)
+    mk = np.zeros((30, 7)); mk[:, :5] = base; mk[:, 5:7] = base[:, :2]
+    return mk, (1, 5, 5)
+
+
+@pytest.mark.parametrize("case", ["zero_col", "dups", "dups_small"])
+def test_stage2_cholesky_failure_paths(cuda, oracle, case):
+    """The driver's own stage-2 routine (cqrrpt_gpu_rank_stage2) on the
+    reference's failure inputs (test_cqrrpt.cc:170-197,302-313; SURVEY P10:
+    (retries, k0_final, rank) = (1,8,8), (1,6,6), (1,5,5))."""
+    from paper_2311_08316_b200 import kernels
+    mk, want = _failure_input(oracle, case)
     ref = oracle.rank_stage2(mk, np.eye(mk.shape[1]))
     assert (ref["retries"], ref["k0_final"], ref["rank"]) == want
-    # the GPU path: TRSM (identity) + Gram + potrf + stage-2 via the kernels
-    from paper_2311_08316_b200 import kernels
-    mpre = kernels.trsm_right(cuda.to_device_colmajor(mk), cuda.to_device_colmajor(np.eye(mk.shape[1])))
-    g = kernels.gram(mpre)
-    r, fi = kernels.potrf(g)
-    assert fi - 1 == ref["k0_final"]
-    # binary search with the reference estimator semantics on the leading block
-    thr = np.sqrt(1e-4 / U)
-    R = r
-    memo = {}
+    for exact in (False, True):
+        got = kernels.rank_stage2(cuda.to_device_colmajor(mk), cuda.to_device_colmajor(np.eye(mk.shape[1])),
+                                  exact=exact)
+        assert (got["retries"], got["k0_final"], got["rank"]) == want
+        assert got["cond_at_rank"] == pytest.approx(ref["cond_at_rank"], rel=1e-6)
+        k = got["rank"]
+        np.testing.assert_allclose(got["r_pre"].cpu().numpy(), ref["r_pre"], rtol=0, atol=1e3 * k * U *
+                                   np.abs(ref["r_pre"]).max())
 
-    def at(ell):
-        if ell <= 0:
-            return 1.0
-        if ell not in memo:
-            memo[ell] = kernels.cond_estimate(R[:ell, :ell], 3)  # nested identity_deviation
-        return max([1.0] + [v for l, v in memo.items() if l <= ell])
-    lo, hi = 0, R.shape[0]
-    while lo < hi:
-        mid = lo + (hi - lo + 1) // 2
-        if at(mid) <= thr:
-            lo = mid
-        else:
-            hi = mid - 1
-    assert lo == ref["rank"]
+
+@pytest.mark.parametrize("decades,eps_tol", [(6.0, 1e-4), (9.0, 1e-8), (12.0, 1e-4), (4.0, 1e-12)])
+def test_stage2_truncation_vs_oracle(cuda, oracle, decades, eps_tol):
+    """rank_stage2 on an unpreconditioned block (A_sk = I) whose leading
+    blocks cross sqrt(eps_tol/u): the binary search truncates (and at 1e12 the
+    Cholesky fails first). rank, k0_final, retries equal the reference
+    restatement's; cond_at_rank within the estimator's rounding."""
+    from paper_2311_08316_b200 import kernels
+    n = 48
+    mk = oracle.gen_spectral(2000, n, 10.0 ** (-decades * np.arange(n) / (n - 1)), 5)
+    ref = oracle.rank_stage2(mk, np.eye(n), eps_tol=eps_tol)
+    assert ref["rank"] < n  # a truncating input
+    for exact in (False, True):
+        got = kernels.rank_stage2(cuda.to_device_colmajor(mk), cuda.to_device_colmajor(np.eye(n)),
+                                  eps_tol=eps_tol, exact=exact)
+        assert (got["retries"], got["k0_final"], got["rank"]) == (ref["retries"], ref["k0_final"], ref["rank"])
+        assert got["cond_at_rank"] == pytest.approx(ref["cond_at_rank"], rel=1e-4)
+
+
+def _coherent(oracle, seed, n):
+    """Leverage concentrated in n rows with a 1e-12 graded diagonal: with
+    nnz = 1 the SASO sketch folds those rows together, the preconditioner is
+    poor, and the driver's Gram hits a non-positive pivot (retry) before the
+    binary search truncates."""
+    a = np.zeros((400, n), order="F")
+    a[:n, :n] = np.diag(10.0 ** (-np.linspace(0, 12, n)))
+    a += 1e-13 * oracle.gen_gaussian(400, n, seed)
+    return np.asfortranarray(a)
+
+
+def _assert_cholesky_failure_tie(cuda, oracle, a, ref, k0f_gpu):
+    """The Cholesky-failure point of rank_stage2 (cqrrpt.cc:168-186) is a
+    rounding decision when the pivot there is at the Gram's rounding level:
+    the two Grams (reference dot order vs DMMA tiles) differ by ~u ||M_pre||^2,
+    so a pivot d_j with |d_j| / max_i G_ii <= 1e3 u k0 may come out either sign.
+    Where the GPU's and the reference's k0_final differ, the factorization
+    that got further must have such a pivot at the other's failure index."""
+    from paper_2311_08316_b200 import kernels
+    k0 = ref.k0
+    mk = np.asfortranarray(a[:, ref.pivots[:k0]])
+    ask = np.asfortranarray(ref.extra["r_sk"][:k0, :k0])
+    bar = 1e3 * U * k0
+    if k0f_gpu < ref.extra["k0_final"]:  # the reference passed the GPU's failing minor
+        g = oracle.gram(oracle.trsm_right(mk, ask))
+        r, _ = oracle.cholesky(g)
+        j = k0f_gpu
+    else:  # the GPU passed the reference's failing minor
+        g = kernels.gram(kernels.trsm_right(cuda.to_device_colmajor(mk), cuda.to_device_colmajor(ask)))
+        gd = g.cpu().numpy()
+        r, _ = kernels.potrf(g)
+        r = r.cpu().numpy()
+        g = gd
+        j = ref.extra["k0_final"]
+    rel = r[j, j] ** 2 / np.max(np.diag(g))
+    assert rel <= bar, (k0f_gpu, ref.extra["k0_final"], rel, bar)
+
+
+@pytest.mark.parametrize("kind,seed,n,gamma,nnz,eps_tol", [
+    ("coherent", 1, 32, 1.0, 1, 1e-4), ("coherent", 3, 32, 1.0, 1, 1e-4), ("coherent", 5, 16, 1.0, 1, 1e-4),
+    ("coherent", 5, 32, 1.0, 2, 1e-4),
+    ("gauss", 2, 64, 1.0, 8, 1e-13), ("gauss", 2, 64, 1.25, 8, 1e-14), ("c5", 1, 64, 1.0, 8, 1e-14)])
+def test_stage2_decisions_through_driver(cuda, oracle, kind, seed, n, gamma, nnz, eps_tol):
+    """Stage-2 decision paths through cqrrpt_gpu_dgeqpt compared with the
+    reference restatement's cqrrpt (cqrrpt.cc:160-207): Cholesky-failure
+    shrink + retry (coherent inputs) and cond-search truncation k < k0 (tight
+    eps_tol), on both the fast-accept and the forced-search paths."""
+    if kind == "coherent":
+        a = _coherent(oracle, seed, n)
+    elif kind == "gauss":
+        a = oracle.gen_gaussian(3000, n, seed)
+    else:
+        a, _ = oracle.c5_scale_columns(oracle.gen_gaussian(4000, n, seed), 8.0, 0)
+    ref = oracle.cqrrpt(a, gamma=gamma, nnz=nnz, eps_tol=eps_tol, seed=seed, want_sketch=True)
+    assert ref.k < ref.k0 or ref.extra["retries"] > 0
+    for exact in (False, True):
+        A = cuda.to_device_colmajor(a)
+        res = cuda.dgeqpt(A, d_factor=gamma, nnz=nnz, seed=seed, eps_tol=eps_tol, exact_stage2=exact,
+                          diagnostics=True)
+        assert (res.k0, res.k) == (ref.k0, ref.k)
+        assert res.ctx.retries == ref.extra["retries"]
+        if res.ctx.k0_final != ref.extra["k0_final"]:
+            _assert_cholesky_failure_tie(cuda, oracle, a, ref, res.ctx.k0_final)
+        assert np.array_equal(res.pivots.cpu().numpy(), ref.pivots)
+        assert res.ctx.cond_m_pre == pytest.approx(ref.cond_m_pre, rel=1e-4)
+        if ref.k:
+            q = A[:, : res.k].cpu().numpy()
+            v = oracle.validate(a, q, res.r.cpu().numpy(), ref.pivots)
+            vr = oracle.validate(a, ref.q, ref.r, ref.pivots)
+            assert v["orth_fro"] <= 10 * max(vr["orth_fro"], 10 * n * U)
+            assert v["recon_rel"] <= 10 * max(vr["recon_rel"], 10 * n * U)
+
+
+def test_cond_m_pre_fast_path(cuda, oracle):
+    """cond_m_pre on the default (fast-accept) path: NaN unless diagnostics
+    are requested, then est.at(k) exactly as the search would report it
+    (cqrrpt.cc:205,298)."""
+    a = oracle.gen_gaussian(4000, 96, 4)
+    ref = oracle.cqrrpt(a, gamma=1.25, nnz=8, seed=0)
+    r0 = cuda.dgeqpt(cuda.to_device_colmajor(a), d_factor=1.25, nnz=8, seed=0)
+    assert r0.ctx.stage2_exact == 0 and np.isnan(r0.ctx.cond_m_pre)
+    r1 = cuda.dgeqpt(cuda.to_device_colmajor(a), d_factor=1.25, nnz=8, seed=0, diagnostics=True)
+    r2 = cuda.dgeqpt(cuda.to_device_colmajor(a), d_factor=1.25, nnz=8, seed=0, exact_stage2=True)
+    assert r1.ctx.stage2_exact == 0 and r2.ctx.stage2_exact == 1
+    assert r1.ctx.cond_m_pre == r2.ctx.cond_m_pre
+    assert r1.ctx.cond_m_pre == pytest.approx(ref.cond_m_pre, rel=1e-6)
+
+
+def test_validate_pinned_to_oracle(cuda, oracle):
+    """cqrrpt_gpu_validate's orth_2 / orth_F / recon equal the restated
+    validate() (qrcp.cc:150-196) on the same factors, to rounding."""
+    from paper_2311_08316_b200 import _lib
+    import ctypes
+    import torch
+    for (m, n, seed) in [(3000, 64, 1), (5000, 200, 2)]:
+        a = oracle.gen_spectral(m, n, 10.0 ** (-6 * np.arange(n) / (n - 1)), seed)
+        ref = oracle.cqrrpt(a, gamma=1.25, nnz=8, seed=0)
+        vr = oracle.validate(a, ref.q, ref.r, ref.pivots)
+        A, Q, R = (cuda.to_device_colmajor(x) for x in (a, ref.q, ref.r))
+        J = torch.as_tensor(ref.pivots, dtype=torch.int64, device="cuda")
+        of, o2, rc = _lib._f64(), _lib._f64(), _lib._f64()
+        _lib.check(_lib.load().cqrrpt_gpu_validate(m, n, ref.k, A.data_ptr(), m, Q.data_ptr(), m, R.data_ptr(),
+                                                   ref.k, J.data_ptr(), ctypes.byref(of), ctypes.byref(o2),
+                                                   ctypes.byref(rc), None), "validate")
+        torch.cuda.synchronize()
+        assert of.value == pytest.approx(vr["orth_fro"], rel=1e-3)
+        assert o2.value == pytest.approx(vr["orth_loss"], rel=1e-3)
+        assert rc.value == pytest.approx(vr["recon_rel"], rel=1e-3)
 
 
 def test_c_abi_host_outputs_path(cuda, oracle):
