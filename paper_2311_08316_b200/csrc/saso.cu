@@ -259,8 +259,12 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
     constexpr int RB = kConsumers * A;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int64_t j0 = (int64_t)blockIdx.x * 32;
-    const int64_t r0 = (int64_t)blockIdx.y * RB;
+    // grid (row blocks, column groups): the row blocks of one column group
+    // are adjacent in launch order, so they are co-resident and march through
+    // the same tiles together -- A is read from HBM once, the other row
+    // blocks' copies hit L2
+    const int64_t j0 = (int64_t)blockIdx.y * 32;
+    const int64_t r0 = (int64_t)blockIdx.x * RB;
     const int64_t split = blockIdx.z;
     const int64_t t_begin = P.tile_hi ? P.tile_lo : split * P.tiles_per_split;
     const int64_t t_end = P.tile_hi ? P.tile_hi : cmin<int64_t>(t_begin + P.tiles_per_split, P.ntiles);
@@ -294,7 +298,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
         const double *a_tile = P.a + (j0 + pw) * P.lda + t_begin * kTileRows + lane;
         const uint32_t *g_ent = P.tent + t_begin * (int64_t)P.entw;
         const uint32_t *g_info =
-            reinterpret_cast<const uint32_t *>(P.tinfo + t_begin * P.nbs + (int64_t)blockIdx.y * kApplyWarps);
+            reinterpret_cast<const uint32_t *>(P.tinfo + t_begin * P.nbs + (int64_t)blockIdx.x * kApplyWarps);
         const int64_t full_tiles = P.m / kTileRows;  // tiles without rows past m
         const int pl = pw * 32 + lane;                // producer lane 0..127
         int stg = 0;
@@ -557,7 +561,7 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
     P.tile_lo = 0;
     P.tile_hi = 0;
     P.carry = 0;
-    dim3 grid((unsigned)cgroups, (unsigned)rblocks, (unsigned)nsplit);
+    dim3 grid((unsigned)rblocks, (unsigned)cgroups, (unsigned)nsplit);
     auto launch_A = [&](dim3 gr) -> int {
         switch (A) {
             case 1: return launch_apply<1>(P, gr, smem, st);
@@ -576,7 +580,7 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
             if (hi <= lo) continue;
             P.tile_lo = lo;
             P.tile_hi = hi;
-            if ((rc = launch_A(dim3((unsigned)cgroups, (unsigned)rblocks, 1)))) return rc;
+            if ((rc = launch_A(dim3((unsigned)rblocks, (unsigned)cgroups, 1)))) return rc;
             P.carry = 1;
             lo = hi;
         }
