@@ -154,7 +154,7 @@ def reference_sample(name):
         a = make_rows(cfg, 0, cfg["m"], dev)[:rows]
     elif cfg["kind"] == "lowrank":
         from tools.workloads import fill_rows, lowrank_fro_sq
-        fro = lowrank_fro_sq(cfg, 0, cfg["m"], dev)
+        fro = lowrank_fro_sq(cfg, dev)
         a = torch.empty((cfg["n"], rows), dtype=torch.float64, device=dev).t()
         fill_rows(cfg, 0, rows, a, dev, fro_sq_total=fro)
     else:

@@ -13,10 +13,15 @@ pytestmark = pytest.mark.gpu
 
 
 class ThreadAllreduce:
-    def __init__(self, nranks):
+    """Sum-allreduce between host-thread ranks; ``order`` is the rank order
+    the partial buffers are added in (NCCL's ring/tree order differs from a
+    single chain, which is what the tie rule is for)."""
+
+    def __init__(self, nranks, order=None):
         from paper_2311_08316_b200 import _lib
         self.L = _lib.load()
         self.n = nranks
+        self.order = list(order) if order is not None else list(range(nranks))
         self.bar = threading.Barrier(nranks)
         self.bufs = [None] * nranks
 
@@ -27,25 +32,28 @@ class ThreadAllreduce:
             L.cqrrpt_gpu_stream_sync(stream)
             self.bufs[rank] = ptr
             self.bar.wait()
-            if rank == 0:
-                for r in range(1, self.n):
+            first = self.order[0]
+            if rank == first:
+                for r in self.order[1:]:
                     assert L.cqrrpt_gpu_add(ptr, self.bufs[r], count, stream) == 0
                 L.cqrrpt_gpu_stream_sync(stream)
             self.bar.wait()
-            if rank != 0:
-                assert L.cqrrpt_gpu_copy(ptr, self.bufs[0], count * 8, stream) == 0
+            if rank != first:
+                assert L.cqrrpt_gpu_copy(ptr, self.bufs[first], count * 8, stream) == 0
             self.bar.wait()
         return ar
 
 
-@pytest.mark.parametrize("nranks", [2, 3])
-def test_threaded_ranks_match_single_gpu(cuda, oracle, nranks):
+@pytest.mark.parametrize("nranks,order", [(2, None), (3, None), (3, (2, 0, 1)), (4, (3, 2, 1, 0))])
+def test_threaded_ranks_match_single_gpu(cuda, oracle, nranks, order):
     import torch
     from paper_2311_08316_b200.distributed import shard_rows
+    from parity import assert_pivots_tie_rule, first_near_tie
     m, n = 9000, 96
     a = oracle.gen_gaussian(m, n, 17)
-    ref = oracle.cqrrpt(a, gamma=1.25, nnz=8, seed=0)
-    coll = ThreadAllreduce(nranks)
+    ref = oracle.cqrrpt(a, gamma=1.25, nnz=8, seed=0, want_sketch=True)
+    _, _, k_sk, gaps = oracle.qrcp(ref.extra["m_sk"], gaps=True)
+    coll = ThreadAllreduce(nranks, order)
     results = [None] * nranks
     errors = []
 
@@ -76,7 +84,10 @@ def test_threaded_ranks_match_single_gpu(cuda, oracle, nranks):
     for (_, _, r, p, k, k0) in results:
         assert np.array_equal(p, p0) and k == k_0 and k0 == k00
         assert np.array_equal(r, r0)  # replicated phases are bit-identical across ranks
-    assert np.array_equal(p0, ref.pivots) and k_0 == ref.k and k00 == ref.k0
+    # the allreduced sketch is summed in another order than the reference's
+    # single chain: J equal up to the first near-tie (tests/parity.py)
+    assert_pivots_tie_rule(p0, ref.pivots, first_near_tie(gaps, n, k_sk), k_sk)
+    assert k_0 == ref.k and k00 == ref.k0
     q = np.vstack([x[1] for x in sorted(results, key=lambda t: t[0])])
     v = oracle.validate(a, np.asfortranarray(q), r0, p0)
     vr = oracle.validate(a, ref.q, ref.r, ref.pivots)

@@ -97,10 +97,58 @@ def test_two_rank_gloo_decomposition_matches_single_process():
     # replicated decisions identical on both ranks and equal to the reference
     for (_, _, piv, k0, fi, r, _) in gathered:
         assert np.array_equal(piv, piv0) and k0 == k00 and fi == fi0 and np.array_equal(r, r0)
-    assert np.array_equal(piv0, ref.pivots)
+    from parity import assert_pivots_tie_rule, first_near_tie
+    _, _, k_sk, gaps = orc.qrcp(ref.extra["m_sk"], gaps=True)
+    assert_pivots_tie_rule(piv0, ref.pivots, first_near_tie(gaps, n, k_sk), k_sk)
     assert k00 == ref.k0 and fi0 == 0 and ref.k == k00
     err = np.linalg.norm(r0 - ref.r, axis=0) / np.linalg.norm(ref.r, axis=0)
     assert np.max(err) <= 1e-10
     # stacked local Q rows reproduce the global Q
     q_all = np.vstack([g[1] for g in sorted(gathered, key=lambda t: t[0])])
     assert np.max(np.abs(q_all - ref.q)) <= 1e-10
+
+
+def _bench_rows_worker(rank, world, port, q):
+    """bench.py's N-rank input: rank r generates rows [r m/N, (r+1) m/N) of the
+    one global matrix (tools/workloads.py tiles; C3's noise scale from the
+    all-reduced ||AB||_F^2)."""
+    import torch
+    import torch.distributed as dist
+    from tools.workloads import make_rows
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = {}
+        for cfg in (dict(m=4 * 65536, n=6, gamma=1.25, kind="graded"),
+                    dict(m=4 * 65536, n=6, gamma=1.25, kind="lowrank", rank=3, noise=1e-12)):
+            ml = cfg["m"] // world
+            a = make_rows(cfg, rank * ml, (rank + 1) * ml, "cpu", dist=dist)
+            gathered = [None] * world
+            dist.all_gather_object(gathered, a.numpy().copy())
+            out[cfg["kind"]] = np.vstack(gathered)
+        if rank == 0:
+            q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_bench_rows_are_one_global_matrix():
+    """The N-GPU bench factors the same matrix as the 1-GPU bench (strong
+    scaling): the ranks' row blocks stack to the single-rank matrix exactly."""
+    import torch.multiprocessing as mp
+    from tools.workloads import make_rows
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_rows_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    stacked = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for cfg in (dict(m=4 * 65536, n=6, gamma=1.25, kind="graded"),
+                dict(m=4 * 65536, n=6, gamma=1.25, kind="lowrank", rank=3, noise=1e-12)):
+        whole = make_rows(cfg, 0, cfg["m"], "cpu").numpy()
+        assert np.array_equal(stacked[cfg["kind"]], whole)

@@ -112,14 +112,33 @@ def fill_rows(cfg, r0, r1, out, device="cuda", seed=SEED, fro_sq_total=None):
     return out
 
 
-def lowrank_fro_sq(cfg, r0, r1, device="cuda", seed=SEED):
-    """||rows [r0, r1) of A B||_F^2 for C3 (sum over ranks for the whole)."""
+def lowrank_tile_sq(cfg, r0, r1, device="cuda", seed=SEED):
+    """{tile index: ||tile of A B||_F^2} for the 65536-row tiles that rows
+    [r0, r1) cover (r0, r1 tile-aligned or the matrix end). Summed in tile
+    order, these give a noise scale that does not depend on the rank count."""
     import torch
-    tmp = torch.empty((cfg["n"], r1 - r0), dtype=torch.float64, device=device).t()
-    fill_rows(cfg, r0, r1, tmp, device, seed, fro_sq_total=None)
-    s = float((tmp * tmp).sum().item())
-    del tmp
-    return s
+    out = {}
+    for t in range(r0 // TILE, (r1 + TILE - 1) // TILE):
+        a, b = t * TILE, min(cfg["m"], (t + 1) * TILE)
+        tmp = torch.empty((cfg["n"], b - a), dtype=torch.float64, device=device).t()
+        fill_rows(cfg, a, b, tmp, device, seed, fro_sq_total=None)
+        out[t] = float((tmp * tmp).sum().item())
+        del tmp
+    return out
+
+
+def lowrank_fro_sq(cfg, device="cuda", seed=SEED, dist=None, r0=0, r1=None):
+    """||A B||_F^2 of the whole C3 matrix: per-tile sums (this rank's rows,
+    all-gathered across ranks when ``dist`` is given) added in tile order."""
+    r1 = cfg["m"] if r1 is None else r1
+    parts = lowrank_tile_sq(cfg, r0, r1, device, seed)
+    if dist is not None:
+        gathered = [None] * dist.get_world_size()
+        dist.all_gather_object(gathered, parts)
+        parts = {}
+        for g in gathered:
+            parts.update(g)
+    return float(sum(parts[t] for t in sorted(parts)))
 
 
 def make_rows(cfg, r0, r1, device="cuda", seed=SEED, dist=None):
@@ -129,9 +148,7 @@ def make_rows(cfg, r0, r1, device="cuda", seed=SEED, dist=None):
     out = torch.empty((cfg["n"], r1 - r0), dtype=torch.float64, device=device).t()
     fro = None
     if cfg["kind"] == "lowrank":
-        fro = lowrank_fro_sq(cfg, r0, r1, device, seed)
-        if dist is not None:
-            t = torch.tensor([fro], dtype=torch.float64, device=device)
-            dist.all_reduce(t)
-            fro = float(t.item())
+        if dist is None and (r0, r1) != (0, cfg["m"]):
+            raise ValueError("C3 rows of part of the matrix need the whole ||AB||_F: pass dist, or r0=0, r1=m")
+        fro = lowrank_fro_sq(cfg, device, seed, dist, r0, r1)
     return fill_rows(cfg, r0, r1, out, device, seed, fro_sq_total=fro)
