@@ -13,6 +13,9 @@
 // 3-stage cp.async pipeline; the shared tiles are unpadded and XOR-swizzled
 // so all fragment loads and async fills are bank-conflict free, which keeps a
 // stage at 24 KB and allows 3 CTAs (12 warps) per SM.
+#include <cstdlib>
+#include <string>
+
 #include "common.cuh"
 #include "gemm.cuh"
 #include "internal.hh"
@@ -456,8 +459,21 @@ static int gram_slices(int64_t m, int64_t k, int64_t *rps_out, int64_t *nslices_
     return 0;
 }
 
+// Engine choice (CQRRPT_GPU_GRAM=dmma|ozaki overrides): the INT8 emulation
+// when cuBLASLt is loadable and the product is large enough to amortise its
+// residue passes, else the DMMA SYRK below.
 int gram(int64_t m, int64_t k, const double *x, int64_t ldx, double *gmat, int64_t ldg, Workspace &ws,
          cudaStream_t st) {
+    const char *env = getenv("CQRRPT_GPU_GRAM");
+    const bool force_dmma = env && std::string(env) == "dmma";
+    const bool force_oz = env && std::string(env) == "ozaki";
+    const bool oz = !force_dmma && (force_oz || (k >= 256 && m >= 65536)) && gram_ozaki_available();
+    if (oz) return gram_ozaki(m, k, x, ldx, gmat, ldg, ws, st);
+    return gram_dmma(m, k, x, ldx, gmat, ldg, ws, st);
+}
+
+int gram_dmma(int64_t m, int64_t k, const double *x, int64_t ldx, double *gmat, int64_t ldg, Workspace &ws,
+              cudaStream_t st) {
     if (k <= 0) return 0;
     constexpr int BM = 64, BN = 128;
     const int64_t tm = (k + BM - 1) / BM;

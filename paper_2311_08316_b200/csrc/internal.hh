@@ -98,6 +98,12 @@ int trsm_block(int64_t m, int64_t k, int64_t c0, const double *b, int64_t ldb, c
                int64_t ldu, const double *dinv_blk, double *x, int64_t ldx, cudaStream_t st);
 int gram(int64_t m, int64_t k, const double *x, int64_t ldx, double *g, int64_t ldg, Workspace &ws,
          cudaStream_t st);
+// the Gram on the INT8 tensor cores (Ozaki scheme II, ozaki.cu) and the DMMA one
+int gram_ozaki(int64_t m, int64_t k, const double *x, int64_t ldx, double *g, int64_t ldg, Workspace &ws,
+               cudaStream_t st);
+bool gram_ozaki_available();
+int gram_dmma(int64_t m, int64_t k, const double *x, int64_t ldx, double *g, int64_t ldg, Workspace &ws,
+              cudaStream_t st);
 // Column block [c0, c1) (rows 0..c1-1) of a Gram split over num_sms() slices
 // of m (min(.., m/512)): the same entries for any blocking. gram_col_tiles
 // appends the block's tile list; part holds gram_col_part_size(m, k, ntiles).
