@@ -50,6 +50,7 @@ public:
 };
 Workspace &workspace();
 void release_workspace();
+size_t ws_bytes(const char *name);  // bytes currently held under `name` (this thread, current device)
 
 // Streams / events cached per (host thread, current device) under a name
 // (prio: 0 default, 1 highest, 2 second highest); cached_events returns an

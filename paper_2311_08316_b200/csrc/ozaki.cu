@@ -46,6 +46,7 @@ constexpr int kMaxMod = 24;
 constexpr int kModList[kMaxMod] = {255, 254, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217,
                                    211, 199, 197, 193, 191, 181, 179, 173, 167, 163, 157, 151};
 constexpr int64_t kChunk = 131072;  // rows per int8 GEMM: 131072 * 127^2 < 2^31
+constexpr double kResidueBytes = 10e9;  // cap of the residue double buffer
 constexpr int kBeta = 53;           // bits kept per column (relative to its max): t < 2^53 is an exact double
 
 struct OzConst {
@@ -298,41 +299,63 @@ __global__ void oz_residue_kernel(int64_t m, int64_t k, const double *__restrict
                                   int64_t lstride) {
     const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // 4-row group
     const int64_t groups = ldr / 4;
-    const int64_t j = blockIdx.y;
-    if (q >= groups || j >= k) return;
-    const int s = sexp[j];
+    const int64_t j = blockIdx.y;  // j in [k, kp): zero padding columns
+    if (q >= groups) return;
+    const int s = (j < k) ? sexp[j] : 0;
     double t[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const int64_t i = q * 4 + u;
-        t[u] = (i < rows && r0 + i < m) ? trunc(ldexp(x[j * ldx + r0 + i], s)) : 0.0;
+        t[u] = (j < k && i < rows && r0 + i < m) ? trunc(ldexp(x[j * ldx + r0 + i], s)) : 0.0;
     }
-    // |t| < 2^53: the quotient estimate rint(t / p) is off by at most one,
-    // the fma remainder is exact, one +-p step makes it symmetric
+    // |t| < 2^53. q = t/p rounded to the nearest integer through the 1.5 2^52
+    // shifter (one DFMA + one DADD, no FRND), exact remainder by fma, the
+    // integer read from the shifted double's low word (no F2I), one
+    // symmetric fixup in int32 for the rare quotient that rounds the other way
+    const double kShift = 6755399441055744.0;  // 1.5 * 2^52
     const int nmod = c_oz.nmod;
 #pragma unroll
     for (int l = 0; l < kMaxMod; ++l) {
         if (l >= nmod) break;
         const double p = (double)c_oz.p[l], pi = c_oz.pinv[l];
+        const int pint = c_oz.p[l], hp = pint >> 1;
         char4 o;
         int8_t *ov = reinterpret_cast<int8_t *>(&o);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            double r = fma(-rint(t[u] * pi), p, t[u]);
-            if (r > 0.5 * p) r -= p;
-            if (r < -0.5 * p) r += p;  // p = 254: [-127, 127]; odd p: [-(p-1)/2, (p-1)/2]
-            ov[u] = (int8_t)(int)r;
+            const double qq = __dsub_rn(__fma_rn(t[u], pi, kShift), kShift);
+            const double r = __fma_rn(-qq, p, t[u]);  // exact
+            int ri = __double2loint(__dadd_rn(r, kShift));
+            ri = (ri > hp) ? ri - pint : ri;
+            ri = (ri < -hp) ? ri + pint : ri;  // p = 254: [-127, 127]; odd p: [-(p-1)/2, (p-1)/2]
+            ov[u] = (int8_t)ri;
         }
         *reinterpret_cast<char4 *>(out + l * lstride + j * ldr + q * 4) = o;
     }
 }
 
 // acc[l][e] = (acc[l][e] + c[l][e]) mod p_l, acc in [0, p_l)
-__global__ void oz_accum_kernel(int64_t nelem, const int32_t *__restrict__ c, int32_t *__restrict__ acc, int first) {
-    const int l = blockIdx.y;
-    const int p = c_oz.p[l];
-    const int32_t *cl = c + (int64_t)l * nelem;
-    int32_t *al = acc + (int64_t)l * nelem;
+// Product layout. FULL: one k x k block per modulus (region l, ld ldc).
+// SPLIT (the integer Gram is symmetric, so only 3 of the 2 x 2 half blocks
+// are multiplied): regions 2l + b = diagonal block b of modulus l, regions
+// 2 nmod + l = the upper off-diagonal block of modulus l; every region is
+// kh x kh (ld kh).
+struct OzLayout {
+    int split;
+    int64_t kh, region;  // SPLIT: half size and region size; FULL: region = ldc * k
+    int64_t ldc;
+};
+CQ_DEVI int region_mod(const OzLayout &L, int b, int nmod) {
+    return L.split ? (b < 2 * nmod ? (b >> 1) : b - 2 * nmod) : b;
+}
+
+// acc[b][e] = (acc[b][e] + c[b][e]) mod p, acc in [0, p)
+__global__ void oz_accum_kernel(OzLayout L, const int32_t *__restrict__ c, int32_t *__restrict__ acc, int first) {
+    const int b = blockIdx.y;
+    const int p = c_oz.p[region_mod(L, b, c_oz.nmod)];
+    const int64_t nelem = L.region;
+    const int32_t *cl = c + (int64_t)b * nelem;
+    int32_t *al = acc + (int64_t)b * nelem;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nelem; e += (int64_t)gridDim.x * blockDim.x) {
         int r = cl[e] % p;
         if (r < 0) r += p;
@@ -352,21 +375,36 @@ CQ_DEVI void two_sum(double a, double b, double &s, double &e) {
 }
 
 // Garner (symmetric digits) + double-double evaluation + 2^{-s_i-s_j}; G is k x k (ldg)
-__global__ void oz_crt_kernel(int64_t k, int64_t ldc, const int32_t *__restrict__ acc, int64_t nelem,
-                              const int *__restrict__ sexp, double *__restrict__ g, int64_t ldg) {
+__global__ void oz_crt_kernel(int64_t k, OzLayout L, const int32_t *__restrict__ acc, const int *__restrict__ sexp,
+                              double *__restrict__ g, int64_t ldg) {
     const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (q >= k * k) return;
     const int64_t i = q % k, j = q / k;
     // the integer Gram is exactly symmetric: read (min, max) so G is bitwise
-    // symmetric whatever the GEMM wrote
-    const int64_t e = (i <= j) ? j * ldc + i : i * ldc + j;
+    // symmetric whatever the GEMMs wrote
+    const int64_t ii = i < j ? i : j, jj = i < j ? j : i;
+    int64_t base, stride;  // element of modulus l at acc[base + l * stride]
+    if (!L.split) {
+        base = jj * L.ldc + ii;
+        stride = L.region;
+    } else {
+        const int64_t kh = L.kh;
+        const int bi = ii >= kh, bj = jj >= kh;
+        if (bi == bj) {  // diagonal block b: region 2l + b
+            base = (int64_t)bi * L.region + (jj - bj * kh) * kh + (ii - bi * kh);
+            stride = 2 * L.region;
+        } else {         // upper off-diagonal block: region 2 nmod + l
+            base = 2 * (int64_t)c_oz.nmod * L.region + (jj - kh) * kh + ii;
+            stride = L.region;
+        }
+    }
     const int nmod = c_oz.nmod;
     int v[kMaxMod];
     for (int l = 0; l < nmod; ++l) {
         const int p = c_oz.p[l];
         // t = (r_l - (v_0 + v_1 W_1 + ... + v_{l-1} W_{l-1})) / W_l  mod p_l, by Garner's
         // recurrence: t = (((r - v_0) inv_0 - v_1) inv_1 - ...) mod p
-        int t = acc[(int64_t)l * nelem + e];
+        int t = acc[base + (int64_t)l * stride];
         for (int q = 0; q < l; ++q) {
             t = (t - v[q]) % p;
             if (t < 0) t += p;
@@ -405,31 +443,35 @@ int gram_ozaki(int64_t m, int64_t k, const double *x, int64_t ldx, double *gmat,
     int beta = 0;
     const int nmod = choose_nmod(m, &beta);
     CQ_TRY(upload_constants(nmod));
-    const int64_t ldc = ((k + 3) / 4) * 4;  // int32 output rows (16-byte aligned columns)
-    const int64_t nelem = ldc * k;
-    // The residue double buffer, the int32 products and their residue sums come
-    // from the stream-ordered pool and go back to it when the Gram is done (no
-    // persistent 5-20 GB workspace next to A and M_pre). Chunks shrink to fit
-    // ~60% of the free memory; below 4096 rows the DMMA Gram takes over.
+    OzLayout L;
+    // the int8 GEMMs run on kp = k rounded up to 16 columns (zero residues in
+    // the padding), which every IMMA algorithm accepts
+    const int64_t kp = ((k + 15) / 16) * 16;
+    L.split = (kp >= 1024) ? 1 : 0;
+    L.kh = kp / 2;
+    L.ldc = L.split ? L.kh : kp;  // int32 output rows
+    L.region = L.split ? L.kh * L.kh : L.ldc * kp;
+    const int64_t nregions = L.split ? 3 * (int64_t)nmod : nmod;
+    const int64_t nelem = L.region * nregions / nmod;  // int32 entries per modulus
+    // Workspace (cached, grow-only like every other buffer): the residue
+    // double buffer is capped at kResidueBytes and at half of what is free
+    // beyond the buffers this Gram already holds; chunks shrink to fit, and
+    // below 4096 rows the DMMA Gram takes over.
     size_t free_b = 0, total_b = 0;
     CQ_CUDA(cudaMemGetInfo(&free_b, &total_b), "oz meminfo");
-    const double budget = 0.6 * (double)free_b - 2.0 * (double)nmod * (double)nelem * 4.0;
+    const double held = (double)ws_bytes("oz.res") + (double)ws_bytes("oz.c") + (double)ws_bytes("oz.acc");
+    const double budget = std::min(kResidueBytes, 0.5 * ((double)free_b + held) - 2.0 * nmod * (double)nelem * 4.0);
     int64_t chunk = std::min<int64_t>(kChunk, ((m + 15) / 16) * 16);
-    chunk = std::min<int64_t>(chunk, (int64_t)(budget / (2.0 * nmod * (double)k)) / 16 * 16);
+    chunk = std::min<int64_t>(chunk, (int64_t)(budget / (2.0 * nmod * (double)kp)) / 16 * 16);
     if (chunk < 4096 && chunk < m) return gram_dmma(m, k, x, ldx, gmat, ldg, ws, st);
-    const int64_t lstride = chunk * k;
+    const int64_t lstride = chunk * kp;
     int *sexp = ws.get<int>("oz.sexp", (size_t)k);
     void *ltws = ws.raw("oz.ltws", kLtWorkspace);
     if (!sexp || !ltws) return fail_nomem("ozaki gram workspace");
-    void *pool = nullptr;
-    const size_t res_b = (size_t)(2 * nmod * lstride), c_b = sizeof(int32_t) * (size_t)(nmod * nelem);
-    if (cudaMallocAsync(&pool, res_b + 2 * c_b + 512, st) != cudaSuccess) {
-        cudaGetLastError();
-        return gram_dmma(m, k, x, ldx, gmat, ldg, ws, st);
-    }
-    int8_t *res = static_cast<int8_t *>(pool);  // double buffer
-    int32_t *cbuf = reinterpret_cast<int32_t *>(static_cast<char *>(pool) + ((res_b + 255) & ~(size_t)255));
-    int32_t *acc = cbuf + ((nmod * nelem + 63) & ~(int64_t)63);
+    int8_t *res = ws.get<int8_t>("oz.res", (size_t)(2 * nmod * lstride));  // double buffer
+    int32_t *cbuf = ws.get<int32_t>("oz.c", (size_t)(nmod * nelem));
+    int32_t *acc = ws.get<int32_t>("oz.acc", (size_t)(nmod * nelem));
+    if (!res || !cbuf || !acc) return gram_dmma(m, k, x, ldx, gmat, ldg, ws, st);
     cudaStream_t aux = nullptr;
     cudaEvent_t *ev = nullptr;  // [0] start, [1..2] residues ready, [3..4] buffer free
     CQ_TRY(cached_stream("oz.aux", 0, &aux));
@@ -445,28 +487,36 @@ int gram_ozaki(int64_t m, int64_t k, const double *x, int64_t ldx, double *gmat,
     for (int64_t r0 = 0; r0 < m; r0 += chunk, ++c) {
         const int64_t rows = std::min<int64_t>(chunk, m - r0);
         const int64_t ldr = ((rows + 15) / 16) * 16;
+        const int64_t cls = ldr * kp;  // this chunk's residue stride between moduli (<= lstride)
         const int b = (int)(c & 1);
         int8_t *rb = res + (int64_t)b * nmod * lstride;
         if (c >= 2) CQ_CUDA(cudaStreamWaitEvent(aux, ev[3 + b], 0), "oz buffer wait");
-        dim3 grid((unsigned)((ldr / 4 + 255) / 256), (unsigned)k);
-        oz_residue_kernel<<<grid, 256, 0, aux>>>(m, k, x, ldx, r0, rows, ldr, sexp, rb, lstride);
+        dim3 grid((unsigned)((ldr / 4 + 255) / 256), (unsigned)kp);
+        oz_residue_kernel<<<grid, 256, 0, aux>>>(m, k, x, ldx, r0, rows, ldr, sexp, rb, cls);
         note_launch();
         CQ_TRY(check_launch("oz_residue_kernel"));
         CQ_CUDA(cudaEventRecord(ev[1 + b], aux), "oz residues ready");
         CQ_CUDA(cudaStreamWaitEvent(st, ev[1 + b], 0), "oz residues wait");
-        // one strided-batched int8 GEMM per chunk: batch = moduli
-        CQ_TRY(lt_gemm_tn(k, k, ldr, rb, ldr, rb, ldr, cbuf, ldc, nmod, lstride, nelem, ltws, st));
+        if (!L.split) {  // one strided-batched int8 GEMM per chunk: batch = moduli
+            CQ_TRY(lt_gemm_tn(kp, kp, ldr, rb, ldr, rb, ldr, cbuf, L.ldc, nmod, cls, L.region, ltws, st));
+        } else {
+            // diagonal half blocks of every modulus (batch 2 nmod: column half
+            // b of modulus l starts at (2l + b) kh ldr) and the upper
+            // off-diagonal half block (batch nmod)
+            const int64_t kh = L.kh;
+            CQ_TRY(lt_gemm_tn(kh, kh, ldr, rb, ldr, rb, ldr, cbuf, kh, 2 * nmod, kh * ldr, L.region, ltws, st));
+            CQ_TRY(lt_gemm_tn(kh, kh, ldr, rb, ldr, rb + kh * ldr, ldr, cbuf + 2 * nmod * L.region, kh, nmod, cls,
+                              L.region, ltws, st));
+        }
         CQ_CUDA(cudaEventRecord(ev[3 + b], st), "oz buffer free");
-        const unsigned gx = (unsigned)std::min<int64_t>((nelem + 255) / 256, 2048);
-        oz_accum_kernel<<<dim3(gx, (unsigned)nmod), 256, 0, st>>>(nelem, cbuf, acc, r0 == 0 ? 1 : 0);
+        const unsigned gx = (unsigned)std::min<int64_t>((L.region + 255) / 256, 2048);
+        oz_accum_kernel<<<dim3(gx, (unsigned)nregions), 256, 0, st>>>(L, cbuf, acc, r0 == 0 ? 1 : 0);
         note_launch();
         CQ_TRY(check_launch("oz_accum_kernel"));
     }
-    oz_crt_kernel<<<(unsigned)((k * k + 255) / 256), 256, 0, st>>>(k, ldc, acc, nelem, sexp, gmat, ldg);
+    oz_crt_kernel<<<(unsigned)((k * k + 255) / 256), 256, 0, st>>>(k, L, acc, sexp, gmat, ldg);
     note_launch();
-    CQ_TRY(check_launch("oz_crt_kernel"));
-    CQ_CUDA(cudaFreeAsync(pool, st), "oz pool free");
-    return 0;
+    return check_launch("oz_crt_kernel");
 }
 
 }  // namespace cqg

@@ -149,6 +149,13 @@ bool first_on_device(const void *key) {
     return true;
 }
 
+size_t ws_bytes(const char *name) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto it = g_ws.find({dev, name});
+    return it == g_ws.end() ? 0 : it->second.bytes;
+}
+
 Workspace &workspace() {
     static thread_local Workspace ws;
     return ws;
