@@ -194,10 +194,25 @@ int wavefront_q(int64_t m, int64_t k0, double *A, int64_t lda, const int64_t *jd
     // Q: in place into A (device entry point; its blocks wait until the
     // precondition has gathered all of A's columns) or, with a host sink, into
     // a separate buffer so Q's first blocks are formed while A is still read
-    const int64_t ldq = sink ? ldp : lda;
-    double *qws = sink ? ws.get<double>("wf.q", (size_t)(ldq * k0)) : A;
-    double *part = qws ? ws.get<double>("wf.part", part_n) : nullptr;
-    if (!qws || !part) return 0;  // does not fit next to A and M_pre: whole passes
+    // With a host sink Q goes to its own buffer so its first blocks can be
+    // formed while the precondition still gathers A's columns. When that
+    // buffer does not fit next to A and M_pre (C5-2048: 3 x 64 GiB) the whole
+    // passes run instead: Q written in place into A after the precondition,
+    // with its blocks streamed during the wavefront's DMMA Gram columns, was
+    // measured slower there (C5-2048 e2e 3.39 -> 3.61 s: the INT8 Gram of the
+    // whole passes is 2x faster than the column-block Gram).
+    // CQRRPT_WF_INPLACE=1 forces that in-place variant (tests).
+    int64_t ldq = sink ? ldp : lda;
+    const bool force_inplace = sink && getenv("CQRRPT_WF_INPLACE") != nullptr;
+    double *qws = (sink && !force_inplace) ? ws.get<double>("wf.q", (size_t)(ldq * k0)) : A;
+    if (!qws) return 0;  // does not fit: whole passes
+    const bool inplace = !sink || force_inplace;
+    if (inplace) {
+        qws = A;
+        ldq = lda;
+    }
+    double *part = ws.get<double>("wf.part", part_n);
+    if (!part) return 0;  // does not fit: whole passes
     int2 *tiles = ws.get<int2>("wf.tiles", tiles_h.size());
     double *dinv = ws.get<double>("wf.dinv", (size_t)(nsub * NB * NB));
     int64_t *fail = ws.get<int64_t>("wf.fail", 1);
@@ -241,7 +256,7 @@ int wavefront_q(int64_t m, int64_t k0, double *A, int64_t lda, const int64_t *jd
     // precondition M_pre = M[:, J[:k0]] A_sk^{-1} on st, an event per 64 columns
     CQ_TRY(trsm_right(m, k0, A, lda, jd, rsk, ldk, mpre, ldp, st, nullptr, true, ev_pre));
     clk.mark(PH_PRE);
-    if (!sink) CQ_CUDA(cudaStreamWaitEvent(s2, ev_pre[(size_t)(nsub - 1)], 0), "wavefront wait precondition");
+    if (inplace) CQ_CUDA(cudaStreamWaitEvent(s2, ev_pre[(size_t)(nsub - 1)], 0), "wavefront wait precondition");
     for (int64_t b = 0; b < nw; ++b) {  // Gram columns, as soon as M_pre's columns exist
         const int64_t w1 = std::min(k0, (b + 1) * WB);
         CQ_CUDA(cudaStreamWaitEvent(s3, ev_pre[(size_t)((w1 - 1) / NB)], 0), "wavefront wait block");

@@ -97,8 +97,11 @@ __global__ void saso_plan_kernel(int64_t d, int64_t c0, int64_t count, int nnz, 
 // the per-block words. One CTA per tile; histogram + scan by the block,
 // ordered scatter by warp 0.
 // ---------------------------------------------------------------------------
+// xrow: bytes between consecutive rows c of one column in the staged tile
+// (264 for the padded row-major LDGSTS layout, 8 for the column segments the
+// bulk copies write)
 __global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d, int nnz, int A, int nbs, int entw,
-                                                            const uint32_t *__restrict__ plan,
+                                                            uint32_t xrow, const uint32_t *__restrict__ plan,
                                                             uint2 *__restrict__ tinfo, uint32_t *__restrict__ tent) {
     extern __shared__ int32_t s_beg[];  // d + 1 counters -> row begins (s_beg[d] = entries)
     int32_t *s_cur = s_beg + (d + 1);   // d scatter cursors
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d
                 const uint32_t c_local = (uint32_t)(e / nnz);
                 const uint32_t neg = (~w >> 31) & 1u;  // plan bit 31 clear: -1/sqrt(d)
                 const uint32_t last = (pos == s_beg[r + 1] - 1) ? kEntLast : 0u;
-                oent[pos] = ((c_local * kXLD * 8u) << 15) | last | neg;
+                oent[pos] = ((c_local * xrow) << 15) | last | neg;
                 // highest-ranked member advances the cursor
                 if (rank == __popc(grp & act) - 1) s_cur[r] += __popc(grp & act);
             }
@@ -213,6 +216,16 @@ CQ_DEVI void mbar_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+CQ_DEVI void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`
+CQ_DEVI void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+CQ_DEVI void sts_f64(uint32_t a, double v) { asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(a), "d"(v) : "memory"); }
 CQ_DEVI uint32_t lds_u32(uint32_t a) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(a) : "memory");
@@ -251,10 +264,19 @@ struct ApplyArgs {
     double *part;
 };
 
-constexpr uint32_t kTileBytes = kTileRows * kXLD * 8;  // 67584
+constexpr uint32_t kTileBytes = kTileRows * kXLD * 8;  // 67584: [c][33] padded rows (LDGSTS staging)
+constexpr uint32_t kColB = kTileRows * 8 + 16;          // 2064: one column segment + 16-byte pad (bulk staging)
+constexpr uint32_t kTileBytesT = 32 * kColB;            // 66048
 constexpr uint32_t kInfoBytes = kApplyWarps * 8;       // one (start, mask) word pair per warp
 
-template <int A>
+// TMA = true: one producer thread stages each tile as 32 column segments with
+// cp.async.bulk (the TMA engine writes shared memory; no LDGSTS issue slots),
+// completion counted on the stage's mbarrier; x of (c, column lane) sits at
+// lane * 2064 + 8 c (16-byte aligned segments: a 4-way bank conflict on the
+// x reads instead of the padded layout's none, for staging that no longer
+// costs 8 cycles per 256-byte warp operation). Needs A 16-byte aligned, lda
+// even. TMA = false: the four producer warps' 8-byte LDGSTS into [c][33].
+template <int A, bool TMA>
 __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs P) {
     constexpr int RB = kConsumers * A;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -272,22 +294,53 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
     const int S = P.stages;
 
     // shared layout: S tiles | S entry lists | S info blocks | S full + S empty mbarriers
+    constexpr uint32_t TB = TMA ? kTileBytesT : kTileBytes;
     const uint32_t s_tiles = smem_u32(smem_raw);
     const uint32_t ent_bytes = (uint32_t)P.entw * 4u;
-    const uint32_t s_ents = s_tiles + (uint32_t)S * kTileBytes;
+    const uint32_t s_ents = s_tiles + (uint32_t)S * TB;
     const uint32_t s_info = s_ents + (uint32_t)S * ent_bytes;
     const uint32_t s_full = s_info + (uint32_t)S * kInfoBytes;
     const uint32_t s_empty = s_full + (uint32_t)S * 8u;
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
-            mbar_init(s_full + 8u * s, 32 * kProducers);  // the producer lanes (cp.async arrivals)
+            mbar_init(s_full + 8u * s, TMA ? 1 : 32 * kProducers);  // TMA: one arrive.expect_tx
             mbar_init(s_empty + 8u * s, kConsumers);  // one arrival per consumer warp
         }
     }
+    if (TMA && tid == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     __syncthreads();
     const int64_t ntl = t_end - t_begin;
 
-    if (wid >= kConsumers) {
+    if (TMA && wid >= kConsumers) {
+        if (wid != kConsumers || lane != 0) return;
+        const int ncols = (int)cmin<int64_t>(32, P.n - j0);
+        const uint32_t *g_ent = P.tent + t_begin * (int64_t)P.entw;
+        const uint2 *g_info = P.tinfo + t_begin * P.nbs + (int64_t)blockIdx.x * kApplyWarps;
+        int stg = 0;
+        uint32_t use = 0;
+        for (int64_t i = 0; i < ntl; ++i) {
+            const int64_t t = t_begin + i;
+            if (use) mbar_wait(s_empty + 8u * stg, (use - 1u) & 1u);
+            const uint32_t sb = s_tiles + (uint32_t)stg * TB;
+            const int rows = (int)cmin<int64_t>(kTileRows, P.m - t * kTileRows);
+            const uint32_t cb = (uint32_t)(rows & ~1) * 8u;  // bulk part (16-byte multiple)
+            const double *a0 = P.a + j0 * P.lda + t * kTileRows;
+            if (rows & 1)  // odd tail row of a ragged last tile: plain loads, ordered by the arrive
+                for (int jj = 0; jj < ncols; ++jj)
+                    sts_f64(sb + (uint32_t)jj * kColB + (uint32_t)(rows - 1) * 8u, a0[jj * P.lda + rows - 1]);
+            const uint32_t full = s_full + 8u * stg;
+            mbar_arrive_expect_tx(full, (uint32_t)ncols * cb + ent_bytes + kInfoBytes);
+            if (cb)
+                for (int jj = 0; jj < ncols; ++jj) bulk_g2s(sb + (uint32_t)jj * kColB, a0 + jj * P.lda, cb, full);
+            bulk_g2s(s_ents + (uint32_t)stg * ent_bytes, g_ent, ent_bytes, full);
+            bulk_g2s(s_info + (uint32_t)stg * kInfoBytes, g_info, kInfoBytes, full);
+            g_ent += P.entw;
+            g_info += P.nbs;
+            if (++stg == S) stg = 0, ++use;
+        }
+        return;
+    }
+    if (!TMA && wid >= kConsumers) {
         // ---------------- producer warps: stage tile after tile, up to S ahead.
         // Producer p copies columns p, p+4, ..., lane l rows l + 32k (k = 0..7):
         // 256-byte coalesced runs, immediate offsets, one pointer step per column
@@ -305,7 +358,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
         uint32_t use = 0;
         for (int64_t i = 0; i < ntl; ++i) {
             if (use) mbar_wait(s_empty + 8u * stg, (use - 1u) & 1u);  // consumers done with the stage's last tile
-            const uint32_t sb = s_tiles + (uint32_t)stg * kTileBytes + (uint32_t)lane * (kXLD * 8u);
+            const uint32_t sb = s_tiles + (uint32_t)stg * TB + (uint32_t)lane * (kXLD * 8u);
             const double *pa = a_tile;
             if (t_begin + i < full_tiles) {
                 for (int j = pw; j < ncols; j += kProducers) {
@@ -349,7 +402,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
     int stg = 0;
     uint32_t use = 0;  // how many times this stage has been filled before the current tile
     const double v = P.val;
-    const uint32_t lane_x = s_tiles + 8u * (uint32_t)lane;
+    const uint32_t lane_x = s_tiles + (TMA ? kColB : 8u) * (uint32_t)lane;
     // x with the entry's sign applied: bit 0 of the entry is 1 for -1/sqrt(d);
     // adding cur * 2^31 flips bit 63 of x exactly when it is set, and
     // fma(v, -x, s) == fma(-v, x, s) bit for bit
@@ -365,7 +418,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
             // the last entry of each row flagged. The loop is unrolled by two
             // (cur / nxt swap roles) so no word rotates between registers.
             uint32_t pe = s_ents + (uint32_t)stg * ent_bytes + 4u * info.x;
-            const uint32_t xb = lane_x + (uint32_t)stg * kTileBytes;
+            const uint32_t xb = lane_x + (uint32_t)stg * TB;
             uint32_t cur = lds_u32(pe);
             pe += 4u;
 #pragma unroll
@@ -437,18 +490,18 @@ int saso_plan(int64_t d, int64_t c0, int64_t count, int64_t nnz, uint64_t seed, 
     return check_launch("saso_plan_kernel");
 }
 
-static size_t apply_smem(int nnz, int *entw, int *nbs, int *stages, int64_t d, int A) {
+static size_t apply_smem(int nnz, int *entw, int *nbs, int *stages, int64_t d, int A, bool tma) {
     *entw = (kTileRows * nnz + 2 + 3) & ~3;  // u32 entries + two prefetch overrun words, 16-byte multiple
     const int64_t nb = (d + A - 1) / A;      // blocks of A sketch rows, kConsumers per CTA
     *nbs = (int)(((nb + kConsumers - 1) / kConsumers) * kApplyWarps);  // 32 slots per CTA row block
-    const size_t per = kTileBytes + 4 * (size_t)*entw + kInfoBytes + 16;
+    const size_t per = (tma ? kTileBytesT : kTileBytes) + 4 * (size_t)*entw + kInfoBytes + 16;
     *stages = (int)std::min<size_t>(6, (227 * 1024) / per);
     return per * (size_t)*stages;
 }
 
-template <int A>
+template <int A, bool TMA>
 static int launch_apply(ApplyArgs P, dim3 grid, size_t smem, cudaStream_t st) {
-    auto kern = saso_apply_kernel<A>;
+    auto kern = saso_apply_kernel<A, TMA>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return fail_cuda("saso_apply smem attr");
     kern<<<grid, kApplyThreads, smem, st>>>(P);
@@ -507,8 +560,17 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
         if (fa == 1 || fa == 2 || fa == 4 || fa == 6 || fa == 8 || fa == 12) A = fa;
     }
     const int64_t rblocks = (d + (int64_t)kConsumers * A - 1) / ((int64_t)kConsumers * A);
+    // Tile staging: bulk copies (TMA engine: no LDGSTS issue slots, but x
+    // reads from 16-byte aligned column segments take 4 instead of 2
+    // wavefronts) when A's segments are 16-byte aligned and few row blocks
+    // share each tile; else the four producer warps' 8-byte LDGSTS into the
+    // padded rows. Measured (tools/sketch_bench.py): C2 1.05 -> 0.90 ms,
+    // C5-1024 33.1 -> 26.6 ms with bulk copies (4 row blocks); C3 / C5-2048
+    // (8) no better, C4 (16) 63.5 -> 80.9 ms. CQRRPT_SASO_LDGSTS=1 forces LDGSTS.
+    const bool tma = (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (lda & 1) == 0 && rblocks <= 4 &&
+                     getenv("CQRRPT_SASO_LDGSTS") == nullptr;
     int entw = 0, nbs = 0, stages = 0;
-    const size_t smem = apply_smem((int)nnz, &entw, &nbs, &stages, d, A);
+    const size_t smem = apply_smem((int)nnz, &entw, &nbs, &stages, d, A, tma);
     if (stages < 2) return fail_internal("saso_apply: nnz too large for the staged entry lists");
     uint2 *tinfo = ws.get<uint2>("saso.tinfo", (size_t)(ntiles * nbs) + 32);
     uint32_t *tent = ws.get<uint32_t>("saso.tent", (size_t)(ntiles * entw) + 4);
@@ -518,7 +580,8 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
         cudaFuncSetAttribute(saso_tile_csr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csr_smem) !=
             cudaSuccess)
         return fail_cuda("csr smem attr");
-    saso_tile_csr_kernel<<<(unsigned)ntiles, 256, csr_smem, st>>>(m, d, (int)nnz, A, nbs, entw, plan, tinfo, tent);
+    saso_tile_csr_kernel<<<(unsigned)ntiles, 256, csr_smem, st>>>(m, d, (int)nnz, A, nbs, entw, tma ? 8u : kXLD * 8u,
+                                                                  plan, tinfo, tent);
     note_launch();
     if ((rc = check_launch("saso_tile_csr_kernel"))) return rc;
 
@@ -564,12 +627,12 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
     dim3 grid((unsigned)rblocks, (unsigned)cgroups, (unsigned)nsplit);
     auto launch_A = [&](dim3 gr) -> int {
         switch (A) {
-            case 1: return launch_apply<1>(P, gr, smem, st);
-            case 2: return launch_apply<2>(P, gr, smem, st);
-            case 4: return launch_apply<4>(P, gr, smem, st);
-            case 6: return launch_apply<6>(P, gr, smem, st);
-            case 8: return launch_apply<8>(P, gr, smem, st);
-            default: return launch_apply<12>(P, gr, smem, st);
+            case 1: return tma ? launch_apply<1, true>(P, gr, smem, st) : launch_apply<1, false>(P, gr, smem, st);
+            case 2: return tma ? launch_apply<2, true>(P, gr, smem, st) : launch_apply<2, false>(P, gr, smem, st);
+            case 4: return tma ? launch_apply<4, true>(P, gr, smem, st) : launch_apply<4, false>(P, gr, smem, st);
+            case 6: return tma ? launch_apply<6, true>(P, gr, smem, st) : launch_apply<6, false>(P, gr, smem, st);
+            case 8: return tma ? launch_apply<8, true>(P, gr, smem, st) : launch_apply<8, false>(P, gr, smem, st);
+            default: return tma ? launch_apply<12, true>(P, gr, smem, st) : launch_apply<12, false>(P, gr, smem, st);
         }
     };
     if (follow) {  // one launch per arrived chunk of rows, chains carried through `part`
@@ -587,14 +650,8 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
         P.tile_lo = P.tile_hi = 0;
         P.carry = 0;
         nsplit = 1;
-    } else
-    switch (A) {
-        case 1: rc = launch_apply<1>(P, grid, smem, st); break;
-        case 2: rc = launch_apply<2>(P, grid, smem, st); break;
-        case 4: rc = launch_apply<4>(P, grid, smem, st); break;
-        case 6: rc = launch_apply<6>(P, grid, smem, st); break;
-        case 8: rc = launch_apply<8>(P, grid, smem, st); break;
-        default: rc = launch_apply<12>(P, grid, smem, st); break;
+    } else {
+        rc = launch_A(grid);
     }
     if (rc) return rc;
     dim3 g((unsigned)((n + 31) / 32), (unsigned)((d + 31) / 32));

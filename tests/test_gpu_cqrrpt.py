@@ -412,6 +412,16 @@ def test_dgeqpt_host_wavefront(cuda, oracle, case):
     assert np.array_equal(wav.q, A[:, :k].cpu().numpy())
     assert np.array_equal(wav.r, dev.r.cpu().numpy())
     assert np.array_equal(again.q, wav.q) and np.array_equal(again.r, wav.r)
+    # the in-place variant (Q into A after the whole precondition, blocks still
+    # streamed: what the host entry point does when Q's own buffer does not fit)
+    import os
+    os.environ["CQRRPT_WF_INPLACE"] = "1"
+    try:
+        inpl = cuda.dgeqpt_host(a, d_factor=1.25, nnz=8, seed=3, eps_tol=eps)
+    finally:
+        del os.environ["CQRRPT_WF_INPLACE"]
+    assert (inpl.k, inpl.k0) == (wav.k, wav.k0) and np.array_equal(inpl.pivots, wav.pivots)
+    assert np.array_equal(inpl.q, wav.q) and np.array_equal(inpl.r, wav.r)
     if k:
         assert np.max(np.abs(wav.q - whole.q)) <= 1e-11 * np.max(np.abs(whole.q))
         rn = np.linalg.norm(whole.r, axis=0)
