@@ -45,7 +45,7 @@ NNZ = 8
 METRIC = "CQRRPT canonical GFLOP/s (2mn^2-2n^3/3)/t, FP64 tall M"
 # CPU reference row sample per config (~10-20 s per reference run on 16 cores)
 SAMPLE_ROWS = {"C1": 16384, "C2": 16384, "C3": 8192, "C3b": 8192, "C4": 4096, "C5_256": 65536,
-               "C5_512": 32768, "C5_1024": 16384, "C5_2048": 8192}
+               "C5_512": 32768, "C5_1024": 16384, "C5_2048": 4096}
 
 
 # --------------------------------------------------------------------------

@@ -540,7 +540,7 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
     const int sms = num_sms();
     int A = 12;
     if (!allow_split) {
-        const int cand[] = {12, 8, 6, 4, 2, 1};
+        const int cand[] = {16, 12, 8, 6, 4, 2, 1};
         double best = 1e300;
         for (int a : cand) {
             const int64_t rb = (int64_t)kConsumers * a;
@@ -557,7 +557,7 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
     }
     if (const char *ev = getenv("CQRRPT_SASO_A")) {  // experiments: force the row-block width
         const int fa = atoi(ev);
-        if (fa == 1 || fa == 2 || fa == 4 || fa == 6 || fa == 8 || fa == 12) A = fa;
+        if (fa == 1 || fa == 2 || fa == 4 || fa == 6 || fa == 8 || fa == 12 || fa == 16) A = fa;
     }
     const int64_t rblocks = (d + (int64_t)kConsumers * A - 1) / ((int64_t)kConsumers * A);
     // Tile staging: bulk copies (TMA engine: no LDGSTS issue slots, but x
@@ -567,8 +567,8 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
     // padded rows. Measured (tools/sketch_bench.py): C2 1.05 -> 0.90 ms,
     // C5-1024 33.1 -> 26.6 ms with bulk copies (4 row blocks); C3 / C5-2048
     // (8) no better, C4 (16) 63.5 -> 80.9 ms. CQRRPT_SASO_LDGSTS=1 forces LDGSTS.
-    const bool tma = (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (lda & 1) == 0 && rblocks <= 4 &&
-                     getenv("CQRRPT_SASO_LDGSTS") == nullptr;
+    const bool tma = (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (lda & 1) == 0 &&
+                     (rblocks <= 4 || getenv("CQRRPT_SASO_TMA") != nullptr) && getenv("CQRRPT_SASO_LDGSTS") == nullptr;
     int entw = 0, nbs = 0, stages = 0;
     const size_t smem = apply_smem((int)nnz, &entw, &nbs, &stages, d, A, tma);
     if (stages < 2) return fail_internal("saso_apply: nnz too large for the staged entry lists");
@@ -632,7 +632,8 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
             case 4: return tma ? launch_apply<4, true>(P, gr, smem, st) : launch_apply<4, false>(P, gr, smem, st);
             case 6: return tma ? launch_apply<6, true>(P, gr, smem, st) : launch_apply<6, false>(P, gr, smem, st);
             case 8: return tma ? launch_apply<8, true>(P, gr, smem, st) : launch_apply<8, false>(P, gr, smem, st);
-            default: return tma ? launch_apply<12, true>(P, gr, smem, st) : launch_apply<12, false>(P, gr, smem, st);
+            case 12: return tma ? launch_apply<12, true>(P, gr, smem, st) : launch_apply<12, false>(P, gr, smem, st);
+            default: return tma ? launch_apply<16, true>(P, gr, smem, st) : launch_apply<16, false>(P, gr, smem, st);
         }
     };
     if (follow) {  // one launch per arrived chunk of rows, chains carried through `part`
