@@ -307,37 +307,45 @@ int identity_deviation_first(const double *r, int64_t ldr, const int64_t *ells, 
 }
 
 // ---------------------------------------------------------------------------
-// Grid-wide estimator (the exact stage-2 path): the same power iterations and
-// control flow as cond_estimate_kernel, with each matvec spread over the grid
-// (cooperative launch). y = op x: CTA rows in 32-row chunks (lane = row,
-// warp = column residue mod 8, coalesced column segments); z = op^T y: warp
-// per column. Vectors live in global memory and are staged in shared memory
-// per half-iteration; norms are per-CTA partials summed in CTA order by every
-// CTA, so all CTAs take the same branches and the result is deterministic.
-// Three grid barriers per iteration.
+// Grouped estimator: several probes (leading blocks ell) at once, each on its
+// own group of CTAs (cooperative launch of sum of group sizes). The same
+// power iterations and control flow as cond_estimate_kernel, with each matvec
+// spread over the group: y = op x over 32-row chunks (lane = row, warp =
+// column residue mod 8, coalesced column segments), z = op^T y warp per
+// column. Vectors live in global memory and are staged in shared memory per
+// half-iteration; norms are per-CTA partials summed in CTA order by every
+// CTA of the group, so the group's CTAs take the same branches and the result
+// is deterministic. A probe's group size depends only on ell (group_size), so
+// an estimate does not depend on which other probes share the launch: the
+// binary search (one probe per launch) and the fast-accept diagnostics (all
+// probes in one launch) report bitwise the same values.
 // ---------------------------------------------------------------------------
 constexpr int kGridPowThreads = 256;
+constexpr int kMaxGroup = 16;
+
+static int group_size(int64_t ell) { return (int)std::max<int64_t>(1, std::min<int64_t>(kMaxGroup, (ell + 127) / 128)); }
 
 struct GridPow {
-    double *v, *w, *z;   // global vectors (length >= max(rows, cols))
-    double *part;        // per-CTA partial sums [gridDim.x]
+    double *v, *w, *z;   // group vectors (length >= max(rows, cols))
+    double *part;        // per-CTA partial sums [group size]
     unsigned long long *bar;
     unsigned long long nbar;
+    int gb, gn;          // this CTA's rank in its group, group size
     double *s_vec;       // shared staging (>= max(rows, cols))
     double *s_red;       // shared [8][32] + 32
 };
 
-CQ_DEVI void gp_sync(GridPow &g) { grid_barrier_mono(g.bar, (++g.nbar) * (unsigned long long)gridDim.x); }
+CQ_DEVI void gp_sync(GridPow &g) { grid_barrier_mono(g.bar, (++g.nbar) * (unsigned long long)g.gn); }
 
-// sum over CTAs of the partials, in CTA order (identical in every CTA)
+// sum over the group's CTAs of the partials, in CTA order (identical in every CTA)
 CQ_DEVI double gp_total(GridPow &g, double mine) {
     double *sr = g.s_red + 256;
     const double blk = block_sum(mine, sr);
-    if (threadIdx.x == 0) g.part[blockIdx.x] = blk;
+    if (threadIdx.x == 0) g.part[g.gb] = blk;
     gp_sync(g);
     double t = 0.0;
     if (threadIdx.x == 0) {
-        for (int b = 0; b < (int)gridDim.x; ++b) t += ld_cg(g.part + b);
+        for (int b = 0; b < g.gn; ++b) t += ld_cg(g.part + b);
         sr[0] = t;
     }
     __syncthreads();
@@ -353,7 +361,7 @@ CQ_DEVI double gp_forward(const PowOp &op, const double *src, double *dst, GridP
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t chunks = (op.rows + 31) / 32;
     double sq = 0.0;
-    for (int64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
+    for (int64_t ch = g.gb; ch < chunks; ch += g.gn) {
         const int64_t i = ch * 32 + lane;
         const int64_t jb = (op.kind == 0) ? 0 : ch * 32;  // upper: columns before the chunk are zero
         double acc = 0.0;
@@ -381,7 +389,7 @@ CQ_DEVI double gp_adjoint(const PowOp &op, const double *src, double *dst, GridP
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     double sq = 0.0;
-    for (int64_t j = blockIdx.x * (int64_t)nw + wid; j < op.cols; j += (int64_t)gridDim.x * nw) {
+    for (int64_t j = g.gb * (int64_t)nw + wid; j < op.cols; j += (int64_t)g.gn * nw) {
         const int64_t ie = (op.kind == 0) ? op.rows : j + 1;
         double s = 0.0;
         for (int64_t i = lane; i < ie; i += 32) s = fma(op_entry(op, i, j), g.s_vec[i], s);
@@ -394,18 +402,18 @@ CQ_DEVI double gp_adjoint(const PowOp &op, const double *src, double *dst, GridP
     return sq;
 }
 
-// power_iterate (linalg.cc:446-465) over the grid; same control flow as power_iterate_dev
+// power_iterate (linalg.cc:446-465) over the group; same control flow as power_iterate_dev
 CQ_DEVI double gp_power(const PowOp &op, GridPow &g, int *conv) {
     const int64_t n = op.cols;
     // deterministic_unit_vector (linalg.cc:434-442)
     double sq = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t i = g.gb * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)g.gn * blockDim.x) {
         const double x = normal_dev(0x5eedcafe01234567ULL, (uint64_t)i);
         g.v[i] = x;
         sq = fma(x, x, sq);
     }
     const double nrm = sqrt(gp_total(g, sq));
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t i = g.gb * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)g.gn * blockDim.x)
         g.v[i] = (nrm == 0.0) ? (i == 0 ? 1.0 : 0.0) : g.v[i] / nrm;
     gp_sync(g);
     double est = 0.0, prev = -1.0;
@@ -426,8 +434,7 @@ CQ_DEVI double gp_power(const PowOp &op, GridPow &g, int *conv) {
             *conv = 1;
             return est;
         }
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-             i += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t i = g.gb * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)g.gn * blockDim.x)
             g.v[i] = ld_cg(g.z + i) / nz;
         gp_sync(g);
     }
@@ -435,24 +442,33 @@ CQ_DEVI double gp_power(const PowOp &op, GridPow &g, int *conv) {
     return est;
 }
 
-struct CondGridArgs {
-    int64_t ell, ldr, ldi;
+struct CondGroupArgs {
+    int nprobes;
+    const int64_t *ells;      // [nprobes]
+    const int *first_cta;     // [nprobes + 1]: CTAs [first_cta[p], first_cta[p+1]) run probe p
+    int64_t ldr, ldi, vlen;   // vector stride per probe
     const double *r, *rinv;
     int method;
-    double *v, *w, *z, *part;
-    unsigned long long *bar;
-    double *out;
+    double *vec;              // [nprobes][3][vlen]
+    double *part;             // [total CTAs]
+    unsigned long long *bar;  // [nprobes] (zeroed)
+    double *out;              // [nprobes][2]
 };
 
-// methods 1..3 of cond_estimate_kernel, grid-wide (method 0 stays single-CTA)
-__global__ void __launch_bounds__(kGridPowThreads) cond_grid_kernel(CondGridArgs A) {
+// methods 1..3 of cond_estimate_kernel, one probe per CTA group
+__global__ void __launch_bounds__(kGridPowThreads) cond_group_kernel(CondGroupArgs A) {
     extern __shared__ double gsm[];
-    GridPow g{A.v, A.w, A.z, A.part, A.bar, 0, gsm + 8 * 32 + 64, gsm};
-    const int64_t ell = A.ell;
+    int p = 0;
+    while (p + 1 < A.nprobes && (int)blockIdx.x >= A.first_cta[p + 1]) ++p;
+    const int gb = (int)blockIdx.x - A.first_cta[p], gn = A.first_cta[p + 1] - A.first_cta[p];
+    double *vec = A.vec + (int64_t)p * 3 * A.vlen;
+    GridPow g{vec, vec + A.vlen, vec + 2 * A.vlen, A.part + A.first_cta[p], A.bar + p, 0, gb, gn,
+              gsm + 8 * 32 + 64, gsm};
+    const int64_t ell = A.ells[p];
     int conv = 1;
     double value = 1.0;
     bool need_krylov = (A.method == 1);
-    if (A.method == 2 || A.method == 3) {
+    if (ell > 0 && (A.method == 2 || A.method == 3)) {
         PowOp dev{A.r, A.ldr, ell, ell, 2};
         const double tau = gp_power(dev, g, &conv) * (1.0 + 1e-6);
         if (tau >= 1.0) {
@@ -463,7 +479,7 @@ __global__ void __launch_bounds__(kGridPowThreads) cond_grid_kernel(CondGridArgs
             value = vv < 1.0 ? 1.0 : vv;
         }
     }
-    if (need_krylov) {
+    if (ell > 0 && need_krylov) {
         int c1 = 1, c2 = 1;
         PowOp fwd{A.r, A.ldr, ell, ell, 1};
         const double hi = gp_power(fwd, g, &c1);
@@ -481,48 +497,87 @@ __global__ void __launch_bounds__(kGridPowThreads) cond_grid_kernel(CondGridArgs
         value = vv < 1.0 ? 1.0 : vv;
         conv = c1 && c2;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        A.out[0] = value;
-        A.out[1] = conv;
+    if (gb == 0 && threadIdx.x == 0) {
+        A.out[2 * p] = value;
+        A.out[2 * p + 1] = conv;
     }
+}
+
+int cond_estimate_batch(int nells, const int64_t *ells_host, const double *r, int64_t ldr, const double *rinv,
+                        int64_t ldi, int method, double *values_host, Workspace &ws, cudaStream_t st) {
+    if (nells <= 0) return 0;
+    if (method == 0) {  // diag ratio: a single pass each
+        for (int q = 0; q < nells; ++q) CQ_TRY(cond_estimate(ells_host[q], r, ldr, rinv, ldi, 0, values_host + q, ws, st));
+        return 0;
+    }
+    const int sms = num_sms();
+    if (first_on_device((const void *)cond_group_kernel))
+        CQ_CUDA(cudaFuncSetAttribute(cond_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+                "cond group smem");
+    int64_t maxl = 1;
+    for (int q = 0; q < nells; ++q) maxl = std::max<int64_t>(maxl, ells_host[q]);
+    const size_t smem = sizeof(double) * (size_t)(8 * 32 + 64 + maxl);
+    if (smem > 200 * 1024) return fail_internal("cond estimator: block too large for shared memory");
+    int per_sm = 0;
+    CQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cond_group_kernel, kGridPowThreads, smem),
+            "cond occupancy");
+    const int slots = std::max(1, per_sm) * sms;  // co-resident CTAs (cooperative launch)
+    double *vec = ws.get<double>("condg.vec", (size_t)(3 * maxl * nells));
+    double *outd = ws.get<double>("condg.out", (size_t)(2 * nells));
+    unsigned long long *bar = ws.get<unsigned long long>("condg.bar", (size_t)nells);
+    int64_t *dells = ws.get<int64_t>("condg.ells", (size_t)nells);
+    int *dfirst = ws.get<int>("condg.first", (size_t)nells + 1);
+    double *part = ws.get<double>("condg.part", (size_t)nells * kMaxGroup);
+    if (!vec || !outd || !bar || !dells || !dfirst || !part) return fail_nomem("cond estimator");
+    std::vector<int> first((size_t)nells + 1, 0);
+    std::vector<double> hout((size_t)(2 * nells));
+    // launches of as many whole probe groups as fit co-resident
+    for (int q0 = 0; q0 < nells;) {
+        int q1 = q0, ctas = 0;
+        while (q1 < nells && ctas + group_size(ells_host[q1]) <= slots) ctas += group_size(ells_host[q1++]);
+        if (q1 == q0) return fail_internal("cond estimator: group larger than the GPU");
+        const int np = q1 - q0;
+        first[0] = 0;
+        for (int q = 0; q < np; ++q) first[(size_t)q + 1] = first[(size_t)q] + group_size(ells_host[q0 + q]);
+        CQ_CUDA(cudaMemcpyAsync(dells, ells_host + q0, sizeof(int64_t) * np, cudaMemcpyHostToDevice, st), "ells");
+        CQ_CUDA(cudaMemcpyAsync(dfirst, first.data(), sizeof(int) * (np + 1), cudaMemcpyHostToDevice, st), "groups");
+        CQ_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned long long) * np, st), "cond bars");
+        CondGroupArgs a;
+        a.nprobes = np;
+        a.ells = dells;
+        a.first_cta = dfirst;
+        a.ldr = ldr;
+        a.ldi = ldi;
+        a.vlen = maxl;
+        a.r = r;
+        a.rinv = rinv;
+        a.method = method;
+        a.vec = vec;
+        a.part = part;
+        a.bar = bar;
+        a.out = outd;
+        void *args[] = {&a};
+        CQ_CUDA(cudaLaunchCooperativeKernel((void *)cond_group_kernel, dim3(first[(size_t)np]),
+                                            dim3(kGridPowThreads), args, smem, st),
+                "cond group launch");
+        note_launch();
+        CQ_CUDA(cudaMemcpyAsync(hout.data() + 2 * q0, outd, sizeof(double) * 2 * np, cudaMemcpyDeviceToHost, st),
+                "cond d2h");
+        CQ_CUDA(cudaStreamSynchronize(st), "cond sync");  // host arrays reused by the next launch
+        q0 = q1;
+    }
+    for (int q = 0; q < nells; ++q) values_host[q] = hout[(size_t)(2 * q)];
+    return 0;
 }
 
 int cond_estimate(int64_t ell, const double *r, int64_t ldr, const double *rinv, int64_t ldi, int method,
                   double *value_host, Workspace &ws, cudaStream_t st) {
+    if (method != 0 && ell > 0) return cond_estimate_batch(1, &ell, r, ldr, rinv, ldi, method, value_host, ws, st);
     double *dout = ws.get<double>("cond.out", 2);
-    if (method == 0 || ell < 256) {  // small blocks: one CTA runs every iteration
-        double *work = ws.get<double>("cond.work", (size_t)(3 * std::max<int64_t>(ell, 1)));
-        cond_estimate_kernel<<<1, kPowThreads, 0, st>>>(ell, r, ldr, rinv, ldi, method, work, dout);
-        note_launch();
-        CQ_TRY(check_launch("cond_estimate_kernel"));
-    } else {
-        const int sms = num_sms();
-        const int G = (int)std::max<int64_t>(1, std::min<int64_t>(sms, (ell + 31) / 32));
-        CondGridArgs a;
-        a.ell = ell;
-        a.ldr = ldr;
-        a.ldi = ldi;
-        a.r = r;
-        a.rinv = rinv;
-        a.method = method;
-        a.v = ws.get<double>("condg.v", (size_t)ell);
-        a.w = ws.get<double>("condg.w", (size_t)ell);
-        a.z = ws.get<double>("condg.z", (size_t)ell);
-        a.part = ws.get<double>("condg.part", (size_t)G);
-        a.bar = ws.get<unsigned long long>("condg.bar", 1);
-        a.out = dout;
-        if (!a.v || !a.w || !a.z || !a.part || !a.bar) return fail_nomem("cond estimator");
-        const size_t smem = sizeof(double) * (size_t)(8 * 32 + 64 + ell);
-        if (first_on_device((const void *)cond_grid_kernel))
-            CQ_CUDA(cudaFuncSetAttribute(cond_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
-                    "cond grid smem");
-        if (smem > 200 * 1024) return fail_internal("cond estimator: block too large for shared memory");
-        CQ_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned long long), st), "cond bar");
-        void *args[] = {&a};
-        CQ_CUDA(cudaLaunchCooperativeKernel((void *)cond_grid_kernel, dim3(G), dim3(kGridPowThreads), args, smem, st),
-                "cond grid launch");
-        note_launch();
-    }
+    double *work = ws.get<double>("cond.work", (size_t)(3 * std::max<int64_t>(ell, 1)));
+    cond_estimate_kernel<<<1, kPowThreads, 0, st>>>(ell, r, ldr, rinv, ldi, method, work, dout);
+    note_launch();
+    CQ_TRY(check_launch("cond_estimate_kernel"));
     CQ_CUDA(cudaMemcpyAsync(value_host, dout, sizeof(double), cudaMemcpyDeviceToHost, st), "cond d2h");
     CQ_CUDA(cudaStreamSynchronize(st), "cond sync");
     return 0;

@@ -430,12 +430,11 @@ int probe_cond(int64_t k0f, const double *rfull, int64_t ldf, const double *rinv
                cudaStream_t s, double *cond) {
     std::vector<int64_t> ells;
     all_pass_probes(k0f, ells);
+    std::vector<double> est(ells.size(), 1.0);
+    CQ_TRY(cond_estimate_batch((int)ells.size(), ells.data(), rfull, ldf, rinv, k0f, nested_method(method), est.data(),
+                               ws, s));
     double c = 1.0;
-    for (int64_t ell : ells) {
-        double e = 1.0;
-        CQ_TRY(cond_estimate(ell, rfull, ldf, rinv, k0f, nested_method(method), &e, ws, s));
-        c = std::max(c, e);
-    }
+    for (double e : est) c = std::max(c, e);
     *cond = (k0f > 0) ? c : 1.0;
     return 0;
 }

@@ -153,6 +153,9 @@ int identity_deviation_first(const double *r, int64_t ldr, const int64_t *ells, 
 // full reference cond_estimate on the leading ell block; rinv = explicit inverse (ld ldr) for krylov
 int cond_estimate(int64_t ell, const double *r, int64_t ldr, const double *rinv, int64_t ldi, int method,
                   double *value_host, Workspace &ws, cudaStream_t st);
+// several leading blocks at once (one CTA group per probe; same values as cond_estimate)
+int cond_estimate_batch(int nells, const int64_t *ells_host, const double *r, int64_t ldr, const double *rinv,
+                        int64_t ldi, int method, double *values_host, Workspace &ws, cudaStream_t st);
 int spectral_norm_estimate(int64_t m, int64_t n, const double *a, int64_t lda, double *value_host, Workspace &ws,
                            cudaStream_t st);
 

@@ -564,11 +564,13 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
     // reads from 16-byte aligned column segments take 4 instead of 2
     // wavefronts) when A's segments are 16-byte aligned and few row blocks
     // share each tile; else the four producer warps' 8-byte LDGSTS into the
-    // padded rows. Measured (tools/sketch_bench.py): C2 1.05 -> 0.90 ms,
-    // C5-1024 33.1 -> 26.6 ms with bulk copies (4 row blocks); C3 / C5-2048
-    // (8) no better, C4 (16) 63.5 -> 80.9 ms. CQRRPT_SASO_LDGSTS=1 forces LDGSTS.
+    // padded rows. Measured (tools/sketch_sweep.sh): bulk copies win up to 6
+    // row blocks (C2 1.04 -> 0.89 ms, C5-1024 33.1 -> 26.6 ms at 4; C3 5.13 ->
+    // 4.94 ms, C5-2048 84.0 -> 77.7 ms at 6 with A = 16) and lose at 12 (C4
+    // 55.2 -> 65.8 ms, C5-256 19.7 -> 22.2 ms). CQRRPT_SASO_LDGSTS=1 /
+    // CQRRPT_SASO_TMA=1 force either path.
     const bool tma = (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (lda & 1) == 0 &&
-                     (rblocks <= 4 || getenv("CQRRPT_SASO_TMA") != nullptr) && getenv("CQRRPT_SASO_LDGSTS") == nullptr;
+                     (rblocks <= 6 || getenv("CQRRPT_SASO_TMA") != nullptr) && getenv("CQRRPT_SASO_LDGSTS") == nullptr;
     int entw = 0, nbs = 0, stages = 0;
     const size_t smem = apply_smem((int)nnz, &entw, &nbs, &stages, d, A, tma);
     if (stages < 2) return fail_internal("saso_apply: nnz too large for the staged entry lists");

@@ -31,8 +31,11 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <stdexcept>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -72,7 +75,7 @@ int32_t family_code(SketchFamily f) {
 struct Pinned {
     void *p = nullptr;
     Pinned(const void *ptr, size_t bytes, bool read_only) {
-        if (bytes < (size_t(64) << 20)) return;
+        if (!ptr || bytes < (size_t(64) << 20)) return;
         unsigned flags = cudaHostRegisterPortable | (read_only ? cudaHostRegisterReadOnly : 0u);
         if (cudaHostRegister(const_cast<void *>(ptr), bytes, flags) == cudaSuccess) p = const_cast<void *>(ptr);
         else cudaGetLastError();  // already registered / not supported: pageable copies
@@ -81,6 +84,53 @@ struct Pinned {
         if (p) cudaHostUnregister(p);
     }
 };
+
+// Host transfer staging for the drop-in (CQRRPT_DROPIN_HOST = staged |
+// register | pageable; default staged): the caller's M and the returned Q
+// are ordinary pageable std::vector storage. "staged" keeps a grow-only
+// pinned buffer per process and copies M into it / Q out of it with all host
+// threads (page-locking the caller's buffers on every call costs more than
+// the copies); "register" page-locks the caller's buffers for the call;
+// "pageable" hands them to the copy engine as they are.
+struct Staging {
+    std::mutex mu;
+    void *p = nullptr;
+    size_t bytes = 0;
+    void *get(size_t want) {
+        if (want <= bytes) return p;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+        if (cudaHostAlloc(&p, want, cudaHostAllocPortable) != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+            return nullptr;
+        }
+        bytes = want;
+        return p;
+    }
+};
+Staging &staging() {
+    static Staging s;
+    return s;
+}
+void par_copy(void *dst, const void *src, size_t bytes) {
+    const size_t nt = std::max<size_t>(1, std::min<size_t>(std::thread::hardware_concurrency(), bytes >> 24));
+    std::vector<std::thread> th;
+    const size_t per = (bytes + nt - 1) / nt;
+    for (size_t t = 0; t < nt; ++t) {
+        const size_t b0 = t * per, b1 = std::min(bytes, b0 + per);
+        if (b0 < b1)
+            th.emplace_back([=] { std::memcpy(static_cast<char *>(dst) + b0, static_cast<const char *>(src) + b0, b1 - b0); });
+    }
+    for (auto &x : th) x.join();
+}
+int host_mode() {
+    const char *e = std::getenv("CQRRPT_DROPIN_HOST");
+    if (e && std::string(e) == "register") return 1;
+    if (e && std::string(e) == "pageable") return 2;
+    return 0;
+}
 
 struct DevBuf {
     void *p = nullptr;
@@ -193,23 +243,43 @@ CqrrptOutput run(const DenseMatrix &m, const CqrrptConfig &cfg, int32_t family, 
     // cond_m_pre and truncation_ratio as the reference reports them; the
     // default fast-accept stage 2 is exact, so no forced search
     ctx.flags = CQRRPT_GPU_TIMINGS | CQRRPT_GPU_DIAGNOSTICS | (cfg.stage1_enabled ? 0 : CQRRPT_GPU_NO_STAGE1);
-    DenseMatrix q(rows, n);  // room for k0 columns; trimmed to k below
     std::vector<double> r(size_t(n * n), 0.0);
     std::vector<int64_t> piv(size_t(n), 0);
     int64_t k = 0, k0 = 0;
-    {
-        Pinned pa(m.data(), sizeof(double) * m.size(), true), pq(q.data(), sizeof(double) * q.size(), false);
-        int rc = cqrrpt_gpu_dgeqpt_host(rows, n, m.data(), std::max<int64_t>(rows, 1), cfg.gamma, nnz, seed,
-                                        cfg.eps_tol, q.data(), std::max<int64_t>(rows, 1), r.data(), n, piv.data(),
-                                        &k, &k0, &ctx);
+    PivotedQR &f = out.factorization;
+    const size_t abytes = sizeof(double) * m.size();
+    const int mode = host_mode();
+    Staging &stg = staging();
+    std::unique_lock<std::mutex> lock(stg.mu, std::defer_lock);
+    double *pin = nullptr;
+    if (mode == 0) {
+        lock.lock();
+        pin = static_cast<double *>(stg.get(2 * abytes));  // [A | Q]
+    }
+    if (pin) {
+        par_copy(pin, m.data(), abytes);
+        double *qpin = pin + m.size();
+        int rc = cqrrpt_gpu_dgeqpt_host(rows, n, pin, std::max<int64_t>(rows, 1), cfg.gamma, nnz, seed, cfg.eps_tol,
+                                        qpin, std::max<int64_t>(rows, 1), r.data(), n, piv.data(), &k, &k0, &ctx);
         if (rc) raise(rc, "cqrrpt");
+        f.q = DenseMatrix(rows, k);
+        par_copy(f.q.data(), qpin, sizeof(double) * size_t(rows * k));
+    } else {
+        DenseMatrix q(rows, n);  // room for k0 columns; trimmed to k below
+        {
+            Pinned pa(mode == 1 ? m.data() : nullptr, mode == 1 ? abytes : 0, true),
+                pq(mode == 1 ? q.data() : nullptr, mode == 1 ? sizeof(double) * q.size() : 0, false);
+            int rc = cqrrpt_gpu_dgeqpt_host(rows, n, m.data(), std::max<int64_t>(rows, 1), cfg.gamma, nnz, seed,
+                                            cfg.eps_tol, q.data(), std::max<int64_t>(rows, 1), r.data(), n,
+                                            piv.data(), &k, &k0, &ctx);
+            if (rc) raise(rc, "cqrrpt");
+        }
+        f.q = (k == n) ? std::move(q) : q.leading_columns(k);
     }
     out.k0 = k0;
     out.k = k;
-    PivotedQR &f = out.factorization;
     f.rank = k;
     f.pivots = std::move(piv);
-    f.q = (k == n) ? std::move(q) : q.leading_columns(k);
     f.r = DenseMatrix(k, n);
     for (int64_t j = 0; j < n; ++j)
         for (int64_t i = 0; i < k; ++i) f.r(i, j) = r[size_t(j * n + i)];

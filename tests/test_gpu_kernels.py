@@ -96,17 +96,24 @@ def test_saso_sketch_deterministic(cuda, oracle):
     assert not np.array_equal(x, z)
 
 
-@pytest.mark.parametrize("A", [1, 2, 4, 6, 8, 12])
-def test_saso_sketch_every_row_block_width(cuda, oracle, monkeypatch, A):
+@pytest.mark.parametrize("path", ["LDGSTS", "TMA"])
+@pytest.mark.parametrize("A", [1, 2, 4, 6, 8, 12, 16])
+def test_saso_sketch_every_row_block_width(cuda, oracle, monkeypatch, A, path):
     """Every instantiation of the apply kernel (A accumulator rows per consumer
-    warp, forced by env var) against the reference's apply: several row
-    blocks, ragged last 256-row tile, ragged last column group."""
+    warp; LDGSTS or bulk-copy staging, forced by env var) against the
+    reference's apply: several row blocks, ragged last 256-row tile (even and
+    odd row counts: the bulk path loads an odd tail row by hand), ragged last
+    column group, a padded leading dimension."""
     from paper_2311_08316_b200 import kernels
     monkeypatch.setenv("CQRRPT_SASO_A", str(A))
-    m, n, d, nnz, seed = 5000, 45, 700, 8, 12
-    a = oracle.gen_gaussian(m, n, 31)
-    got = host(kernels.saso_sketch(dev(cuda, a), d, nnz, seed))
-    assert np.array_equal(got, oracle.saso_apply(d, a, nnz, seed))
+    monkeypatch.setenv("CQRRPT_SASO_" + path, "1")
+    n, d, nnz, seed = 45, 700, 8, 12
+    for m in (5000, 5001):
+        a = oracle.gen_gaussian(m, n, 31)
+        x = cuda.colmajor_empty(m, n, pad_to=2)  # even lda: eligible for bulk copies
+        x.copy_(dev(cuda, a))
+        got = host(kernels.saso_sketch(x, d, nnz, seed))
+        assert np.array_equal(got, oracle.saso_apply(d, a, nnz, seed)), m
 
 
 @pytest.mark.parametrize("nnz", [1, 2, 16])

@@ -76,7 +76,7 @@ def test_qrcp_repeatable_and_exact(cuda, oracle, noise, mode, d, n, monkeypatch)
         assert k == k_ref and np.array_equal(j, piv_ref) and np.array_equal(r, r_ref)
 
 
-@pytest.mark.parametrize("A", ["1", "2", "4", "6", "8", "12"])
+@pytest.mark.parametrize("A", ["1", "2", "4", "6", "8", "12", "16"])
 def test_saso_ring_repeatable_and_exact(cuda, oracle, noise, A, monkeypatch):
     from paper_2311_08316_b200 import kernels
     monkeypatch.setenv("CQRRPT_SASO_A", A)
