@@ -467,7 +467,9 @@ int gram(int64_t m, int64_t k, const double *x, int64_t ldx, double *gmat, int64
     const char *env = getenv("CQRRPT_GPU_GRAM");
     const bool force_dmma = env && std::string(env) == "dmma";
     const bool force_oz = env && std::string(env) == "ozaki";
-    const bool oz = !force_dmma && (force_oz || (k >= 256 && m >= 65536)) && gram_ozaki_available();
+    // below k = 1024 the int8 GEMMs (one 256 x 256 IMMA tile per modulus and
+    // column block) cannot fill the GPU: C5-256's Gram is faster on DMMA
+    const bool oz = !force_dmma && (force_oz || (k >= 1024 && m >= 65536)) && gram_ozaki_available();
     if (oz) return gram_ozaki(m, k, x, ldx, gmat, ldg, ws, st);
     return gram_dmma(m, k, x, ldx, gmat, ldg, ws, st);
 }

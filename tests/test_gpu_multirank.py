@@ -95,6 +95,63 @@ def test_threaded_ranks_match_single_gpu(cuda, oracle, nranks, order):
     assert v["recon_rel"] <= 10 * max(vr["recon_rel"], 1e-15)
 
 
+def test_threaded_ranks_int8_gram_size(cuda):
+    """Two ranks with 70000 rows each and n = 1024: each rank's Gram runs on
+    the INT8 engine (m_local >= 65536, k >= 1024) before the allreduce. J,
+    k0, k follow the single-GPU run under the tie rule (gaps from the
+    oracle's QRCP on the single-GPU sketch, which is the reference's sketch
+    bit for bit); Q and R to rounding."""
+    import torch
+    from parity import assert_pivots_tie_rule, first_near_tie
+    from paper_2311_08316_b200 import kernels
+    m, n, nranks = 140000, 1024, 2
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn((n, m), dtype=torch.float64, device="cuda", generator=g).t()
+    a *= (10.0 ** (-6.0 * torch.rand(n, dtype=torch.float64, device="cuda", generator=g)))[None, :]
+    single = a.clone()
+    ref = cuda.dgeqpt(single, d_factor=1.25, nnz=8, seed=0)
+    sk = kernels.saso_sketch(a, cuda.sketch_rows_for(1.25, n), 8, 0).cpu().numpy()
+    from oracle.oracle import Oracle
+    _, _, k_sk, gaps = Oracle().qrcp(sk, gaps=True)
+    coll = ThreadAllreduce(nranks)
+    results = [None] * nranks
+    errors = []
+
+    def run(rank):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            off = rank * (m // nranks)
+            with torch.cuda.stream(st):
+                A = a[off:off + m // nranks].clone()
+                st.synchronize()
+                res = cuda.dgeqpt(A, d_factor=1.25, nnz=8, seed=0, stream=st, allreduce=coll.for_rank(rank),
+                                  nranks=nranks, rank=rank, global_row_offset=off)
+                st.synchronize()
+                results[rank] = (A[:, : res.k].cpu().numpy(), res.r.cpu().numpy(), res.pivots.cpu().numpy(), res.k,
+                                 res.k0)
+        except Exception as exc:  # surfaced below
+            errors.append(repr(exc))
+            coll.bar.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errors, errors
+    q0, r0, p0, k_0, k00 = results[0]
+    assert np.array_equal(results[1][2], p0) and np.array_equal(results[1][1], r0)
+    assert (k_0, k00) == (ref.k, ref.k0)
+    assert_pivots_tie_rule(p0, ref.pivots.cpu().numpy(), first_near_tie(gaps, n, k_sk), k_sk)
+    q = np.vstack([results[0][0], results[1][0]])
+    qr_ref = single[:, : ref.k].cpu().numpy()
+    if np.array_equal(p0, ref.pivots.cpu().numpy()):
+        assert np.max(np.abs(q - qr_ref)) <= 1e-9
+        rr = ref.r.cpu().numpy()
+        assert np.max(np.abs(r0 - rr) / (np.abs(rr).max(axis=0) + 1e-300)) <= 1e-9
+
+
 def test_nccl_communicator_single_rank(cuda):
     """The NCCL path of the library (libnccl dlopen'ed, cqrrpt_gpu_comm_*):
     unique id -> init -> in-place sum-allreduce on device data -> destroy,
