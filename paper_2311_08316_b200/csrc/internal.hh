@@ -94,6 +94,13 @@ struct BlockSink {
 int trsm_right(int64_t m, int64_t k, const double *b, int64_t ldb, const int64_t *cols, const double *u,
                int64_t ldu, double *x, int64_t ldx, cudaStream_t st, const BlockSink *sink = nullptr,
                bool check_diag = true, const cudaEvent_t *block_ev = nullptr);
+// INT8 tensor-core engine of trsm_right (oztrsm.cu): right-looking 128-column
+// blocks, DMMA diagonal solves, tcgen05 kind::i8 emulated trailing updates.
+// dinv: the 64 x 64 diagonal-block inverses (trtri_diag_blocks).
+bool trsm_use_ozaki(int64_t m, int64_t k);
+int trsm_right_oz(int64_t m, int64_t k, const double *b, int64_t ldb, const int64_t *cols, const double *u,
+                  int64_t ldu, double *x, int64_t ldx, cudaStream_t st, const BlockSink *sink, const double *dinv,
+                  const cudaEvent_t *block_ev);
 // one 64-column block c0 of trsm_right (dinv_blk: inverse of U's diagonal block)
 int trsm_block(int64_t m, int64_t k, int64_t c0, const double *b, int64_t ldb, const int64_t *cols, const double *u,
                int64_t ldu, const double *dinv_blk, double *x, int64_t ldx, cudaStream_t st);
