@@ -34,8 +34,11 @@
 //            accumulators, double-buffered (2 x 8 x 32 = 512 TMEM columns);
 //   warps 2-5 epilogue: tcgen05.ld of the 8 groups (lane = row), FP64
 //            recombination, read-modify-write of T (coalesced column runs).
+#include <cuda.h>
+
 #include <climits>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -56,11 +59,16 @@ constexpr int kTileBBytes = kDig * kSliceB;  // 28672
 constexpr int kBStages = 3;
 constexpr int kEpiWarps = 8;               // 2 per TMEM lane quadrant, 16 columns each
 constexpr int kUpdThreads = 64 + 32 * kEpiWarps;  // producer, MMA, epilogue
-constexpr int kTmemCols = 512;             // 2 buffers x 8 groups x 32 columns
+constexpr int kTmemCols = 512;             // A digit slices (7 x 32) | accumulators (8 x 32)
+constexpr uint32_t kTmemAcc = 256;         // first accumulator column
 
+constexpr int kAStages = 2;                // digit slices staged on their way to TMEM
+constexpr int kCStages = 3;                // right-hand-side tiles (128 x 32 FP64)
+constexpr uint32_t kTileCBytes = kBM * kBN * 8;  // 32768, column c at c * 1024
 constexpr uint32_t kSmemA = 0;
-constexpr uint32_t kSmemB = kPanelBytes;
-constexpr uint32_t kSmemBar = kSmemB + kBStages * kTileBBytes;  // 200704
+constexpr uint32_t kSmemB = kAStages * kSliceA;
+constexpr uint32_t kSmemC = kSmemB + kBStages * kTileBBytes;
+constexpr uint32_t kSmemBar = kSmemC + kCStages * kTileCBytes;  // 217088
 constexpr uint32_t kUpdSmem = kSmemBar + 256;
 
 // byte offset of (row r, k kk) in a digit slice laid out as UMMA core matrices
@@ -191,7 +199,7 @@ CQ_DEVI void mb_wait(uint32_t bar, uint32_t parity) {
     for (uint32_t it = 0;; ++it) {
         asm volatile(
             "{\n.reg .pred p;\n"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
             "selp.u32 %0, 1, 0, p;\n}\n"
             : "=r"(ok)
             : "r"(bar), "r"(parity)
@@ -207,7 +215,7 @@ CQ_DEVI void mb_wait_warp(uint32_t bar, uint32_t parity) {
         uint32_t ok;
         asm volatile(
             "{\n.reg .pred p;\n"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
             "selp.u32 %0, 1, 0, p;\n}\n"
             : "=r"(ok)
             : "r"(bar), "r"(parity)
@@ -219,6 +227,19 @@ CQ_DEVI void mb_wait_warp(uint32_t bar, uint32_t parity) {
 CQ_DEVI void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+// 2-D tensor-map load (TMA) of a box at (x = row, y = column) into shared memory
+CQ_DEVI void tma_load_2d(uint32_t dst, const CUtensorMap *map, int x, int y, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+        : "memory");
+}
+CQ_DEVI void tma_store_2d(const CUtensorMap *map, int x, int y, uint32_t src) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(x), "r"(y), "r"(src)
                  : "memory");
 }
 CQ_DEVI void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
@@ -237,25 +258,34 @@ constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN
 CQ_DEVI uint32_t desc_lo(uint32_t addr) { return ((addr >> 4) & 0x3FFFu) | ((128u >> 4) << 16); }
 constexpr uint32_t kDescHi = (1024u >> 4) | (1u << 14);
 
-// D[tmem] (+)= A[smem] * B[smem]^T over the 4 K-steps (K = 128) of one digit
+// D[tmem] (+)= A[tmem] * B[smem]^T over the 4 K-steps (K = 128) of one digit
 // pair, int8 x int8 -> int32, issued by the single elected thread of the MMA
-// warp (its commits then track these MMAs). The K-step advances both start
-// addresses by 256 bytes (+16 in descriptor units).
+// warp (its commits then track these MMAs). A's K-step is 8 TMEM columns;
+// B's advances its start address by 256 bytes (+16 in descriptor units).
 template <uint32_t kIdescT, bool kFirst>
-CQ_DEVI void tc_mma_i8_k128(uint32_t dtmem, uint32_t alo, uint32_t blo) {
+CQ_DEVI void tc_mma_i8_k128(uint32_t dtmem, uint32_t atmem, uint32_t blo) {
     asm volatile(
-        "{\n.reg .pred q0, q1;\n.reg .b64 da, db;\n.reg .b32 a1, b1;\n"
+        "{\n.reg .pred q0, q1;\n.reg .b64 db;\n.reg .b32 a1, b1;\n"
         "setp.ne.b32 q0, %3, 0;\n"
         "setp.eq.b32 q1, %3, %3;\n"
-        "mov.b64 da, {%1, %4};\nmov.b64 db, {%2, %4};\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], da, db, %5, q0;\n"
-        "add.u32 a1, %1, 16;\nadd.u32 b1, %2, 16;\nmov.b64 da, {a1, %4};\nmov.b64 db, {b1, %4};\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], da, db, %5, q1;\n"
-        "add.u32 a1, %1, 32;\nadd.u32 b1, %2, 32;\nmov.b64 da, {a1, %4};\nmov.b64 db, {b1, %4};\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], da, db, %5, q1;\n"
-        "add.u32 a1, %1, 48;\nadd.u32 b1, %2, 48;\nmov.b64 da, {a1, %4};\nmov.b64 db, {b1, %4};\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], da, db, %5, q1;\n}\n" ::"r"(dtmem),
-        "r"(alo), "r"(blo), "n"(kFirst ? 0 : 1), "n"(kDescHi), "n"(kIdescT)
+        "mov.b64 db, {%2, %4};\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], db, %5, q0;\n"
+        "add.u32 a1, %1, 8;\nadd.u32 b1, %2, 16;\nmov.b64 db, {b1, %4};\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], db, %5, q1;\n"
+        "add.u32 a1, %1, 16;\nadd.u32 b1, %2, 32;\nmov.b64 db, {b1, %4};\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], db, %5, q1;\n"
+        "add.u32 a1, %1, 24;\nadd.u32 b1, %2, 48;\nmov.b64 db, {b1, %4};\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], db, %5, q1;\n}\n" ::"r"(dtmem),
+        "r"(atmem), "r"(blo), "n"(kFirst ? 0 : 1), "n"(kDescHi), "n"(kIdescT)
+        : "memory");
+}
+// smem (128 rows x 32 bytes, canonical layout) -> TMEM (128 lanes x 8 columns)
+CQ_DEVI void tc_cp_128x256b(uint32_t tmem_dst, uint32_t slo) {
+    asm volatile(
+        "{\n.reg .b64 sd;\n"
+        "mov.b64 sd, {%1, %2};\n"
+        "tcgen05.cp.cta_group::1.128x256b [%0], sd;\n}\n" ::"r"(tmem_dst),
+        "r"(slo), "n"(kDescHi)
         : "memory");
 }
 CQ_DEVI uint32_t elect_one() {
@@ -266,6 +296,14 @@ CQ_DEVI uint32_t elect_one() {
         "@px mov.s32 %0, 1;\n}\n"
         : "+r"(pred));
     return pred;
+}
+CQ_DEVI void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr)
+        : "memory");
 }
 CQ_DEVI void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
@@ -290,32 +328,46 @@ struct UpdArgs {
     const int64_t *cols_in;  // nullptr: column j of cin is j
     double *cout;
     int64_t ldout;
+    int dbg;  // experiments: 1 = epilogue releases without reading, 2 = no MMAs
 };
 
-__global__ void __launch_bounds__(kUpdThreads, 1) oz_update_kernel(UpdArgs P) {
+__global__ void __launch_bounds__(kUpdThreads, 1)
+    oz_update_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out, UpdArgs P) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t sbase = smem_u32(smem);
-    const uint32_t sA = sbase + kSmemA, sB = sbase + kSmemB;
+    const uint32_t sA = sbase + kSmemA, sB = sbase + kSmemB, sC = sbase + kSmemC;
     const uint32_t bar = sbase + kSmemBar;
-    const uint32_t a_full = bar, a_empty = bar + 8;
-    auto b_full = [&](int s) { return bar + 16 + 8u * s; };
-    auto b_empty = [&](int s) { return bar + 16 + 8u * (kBStages + s); };
-    auto acc_full = [&](int q) { return bar + 16 + 8u * (2 * kBStages + q); };
-    auto acc_empty = [&](int q) { return bar + 16 + 8u * (2 * kBStages + 2 + q); };
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + kSmemBar + 192);
+    // a_*: digit-slice staging ring (smem -> TMEM); b_*: U-slice N tiles;
+    // c_*: right-hand-side tiles; lo_full / hi_full: a tile's groups 0-3 /
+    // 4-7 accumulated; lo_free / hi_free: the epilogue has read them
+    auto a_full = [&](int s) { return bar + 8u * s; };
+    auto a_empty = [&](int s) { return bar + 8u * (kAStages + s); };
+    auto b_full = [&](int s) { return bar + 8u * (2 * kAStages + s); };
+    auto b_empty = [&](int s) { return bar + 8u * (2 * kAStages + kBStages + s); };
+    auto c_full = [&](int s) { return bar + 8u * (2 * kAStages + 2 * kBStages + s); };
+    auto c_empty = [&](int s) { return bar + 8u * (2 * kAStages + 2 * kBStages + kCStages + s); };
+    const uint32_t lo_full = bar + 8u * (2 * (kAStages + kBStages + kCStages));
+    const uint32_t hi_full = lo_full + 8, lo_free = lo_full + 16, hi_free = lo_full + 24;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + kSmemBar + 248);
 
     if (tid == 0) {
-        mb_init(a_full, 1);
-        mb_init(a_empty, 1);
+        for (int s = 0; s < kAStages; ++s) {
+            mb_init(a_full(s), 1);
+            mb_init(a_empty(s), 1);
+        }
         for (int s = 0; s < kBStages; ++s) {
             mb_init(b_full(s), 1);
             mb_init(b_empty(s), 1);
         }
-        for (int q = 0; q < 2; ++q) {
-            mb_init(acc_full(q), 1);
-            mb_init(acc_empty(q), kEpiWarps * 32);
+        for (int s = 0; s < kCStages; ++s) {
+            mb_init(c_full(s), 1);
+            mb_init(c_empty(s), 1);
         }
+        mb_init(lo_full, 1);
+        mb_init(hi_full, 1);
+        mb_init(lo_free, kEpiWarps * 32);
+        mb_init(hi_free, kEpiWarps * 32);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == 1) {
@@ -334,145 +386,236 @@ __global__ void __launch_bounds__(kUpdThreads, 1) oz_update_kernel(UpdArgs P) {
     constexpr uint32_t tmem = 0u;
 
     if (warp == 0) {
-        if (lane == 0) {  // ---------------- producer
-            int bs = 0;
-            uint32_t bfill = 0;
-            int pi = 0;
-            for (int p = blockIdx.x; p < P.npanels; p += gridDim.x, ++pi) {
-                if (pi) mb_wait(a_empty, (uint32_t)(pi - 1) & 1u);
-                mb_expect_tx(a_full, kPanelBytes);
+        if (lane == 0) {  // ---------------- producer (TMA bulk copies)
+            int as = 0, bs = 0, cs = 0;
+            uint32_t afill = 0, bfill = 0, cfill = 0;
+            for (int p = blockIdx.x; p < P.npanels; p += gridDim.x) {
                 const int8_t *ga = P.aslc + (int64_t)p * kPanelBytes;
-                for (int s = 0; s < kDig; ++s) bulk_g2s(sA + s * kSliceA, ga + s * kSliceA, kSliceA, a_full);
+                for (int s = 0; s < kDig; ++s) {
+                    if (afill) mb_wait(a_empty(as), (afill - 1u) & 1u);
+                    mb_expect_tx(a_full(as), kSliceA);
+                    bulk_g2s(sA + as * kSliceA, ga + s * kSliceA, kSliceA, a_full(as));
+                    if (++as == kAStages) as = 0, ++afill;
+                }
+                const int64_t r0 = (int64_t)p * kBM;
                 for (int nt = 0; nt < P.ntn; ++nt) {
                     if (bfill) mb_wait(b_empty(bs), (bfill - 1u) & 1u);
                     mb_expect_tx(b_full(bs), kTileBBytes);
                     bulk_g2s(sB + bs * kTileBBytes, P.bslc + (int64_t)nt * kTileBBytes, kTileBBytes, b_full(bs));
                     if (++bs == kBStages) bs = 0, ++bfill;
+                    // the tile's right-hand side: one bulk copy per column
+                    const int64_t j0 = (int64_t)nt * kBN;
+                    if (cfill) mb_wait(c_empty(cs), (cfill - 1u) & 1u);
+                    if (!P.cols_in) {  // one 128 x 32 box (rows / columns past the ends: zeros)
+                        mb_expect_tx(c_full(cs), kTileCBytes);
+                        tma_load_2d(sC + cs * kTileCBytes, &tm_in, (int)r0, (int)j0, c_full(cs));
+                    } else {  // gathered columns: one bulk copy per column
+                        const int64_t rows = P.m - r0 < kBM ? P.m - r0 : kBM;
+                        const uint32_t cbytes = (uint32_t)(rows & ~1ll) * 8u;  // 16-byte multiple
+                        const int ncj = (int)(P.ncols - j0 < kBN ? P.ncols - j0 : kBN);
+                        mb_expect_tx(c_full(cs), cbytes * (uint32_t)ncj);
+                        if (cbytes)
+                            for (int c = 0; c < ncj; ++c)
+                                bulk_g2s(sC + cs * kTileCBytes + c * (kBM * 8),
+                                         P.cin + __ldg(P.cols_in + j0 + c) * P.ldin + r0, cbytes, c_full(cs));
+                    }
+                    if (++cs == kCStages) cs = 0, ++cfill;
                 }
             }
         }
     } else if (warp == 1) {
-        {  // ---------------- MMA issuer (whole warp, warp-uniform loop)
-            int bs = 0;
-            uint32_t buse = 0;
-            uint32_t tc = 0;  // tiles issued: accumulator buffer tc & 1, its use tc >> 1
-            int pi = 0;
+        {  // ---------------- MMA issuer (whole warp waits; one elected thread issues)
+            int as = 0, bs = 0;
+            uint32_t ause = 0, buse = 0;
+            uint32_t tc = 0;  // tiles issued
             const uint32_t alo0 = desc_lo(sA);
-            for (int p = blockIdx.x; p < P.npanels; p += gridDim.x, ++pi) {
-                mb_wait_warp(a_full, (uint32_t)pi & 1u);
-                tc_fence_after();
-                for (int nt = 0; nt < P.ntn; ++nt) {
-                    mb_wait_warp(b_full(bs), buse & 1u);
-                    const int q = (int)(tc & 1u);
-                    if (tc >= 2u) mb_wait_warp(acc_empty(q), ((tc >> 1) - 1u) & 1u);
+            for (int p = blockIdx.x; p < P.npanels; p += gridDim.x) {
+                // the panel's digit slices: smem -> TMEM columns [0, 224),
+                // ordered after the previous panel's MMAs (same thread)
+                for (int s = 0; s < kDig; ++s) {
+                    mb_wait_warp(a_full(as), ause & 1u);
                     tc_fence_after();
-                    const uint32_t blo0 = desc_lo(sB + bs * kTileBBytes);
-                    const uint32_t d0 = tmem + (uint32_t)(q * kGroups * kBN);
-                    // digit pairs (s, t) with s + t = g, group by group
                     if (elect_one()) {
 #pragma unroll
-                    for (int g = 0; g < kGroups; ++g) {
-#pragma unroll
-                        for (int s = 0; s < kDig; ++s) {
-                            const int t = g - s;
-                            if (t < 0 || t >= kDig) continue;
-                            const uint32_t d = d0 + (uint32_t)(g * kBN);
-                            const uint32_t alo = alo0 + (uint32_t)(s * (kSliceA >> 4));
-                            const uint32_t blo = blo0 + (uint32_t)(t * (kSliceB >> 4));
-                            if (s == (g > kDig - 1 ? g - (kDig - 1) : 0))
-                                tc_mma_i8_k128<kIdesc, true>(d, alo, blo);
-                            else
-                                tc_mma_i8_k128<kIdesc, false>(d, alo, blo);
-                        }
-                    }
-                    tc_commit(b_empty(bs));
-                    tc_commit(acc_full(q));
+                        for (int ks = 0; ks < kW / 32; ++ks)
+                            tc_cp_128x256b(tmem + (uint32_t)(s * 32 + ks * 8),
+                                           alo0 + (uint32_t)((as * kSliceA + ks * 256) >> 4));
+                        tc_commit(a_empty(as));
                     }
                     __syncwarp();
-                    ++tc;
+                    if (++as == kAStages) as = 0, ++ause;
+                }
+                for (int nt = 0; nt < P.ntn; ++nt, ++tc) {
+                    mb_wait_warp(b_full(bs), buse & 1u);
+                    const uint32_t blo0 = desc_lo(sB + bs * kTileBBytes);
+                    constexpr uint32_t d0 = tmem + kTmemAcc;
+                    // groups 0-3 once the epilogue has read the previous tile's
+                    if (tc) mb_wait_warp(lo_free, (tc - 1u) & 1u);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        if (P.dbg != 2)
+#pragma unroll
+                            for (int g = 0; g < 4; ++g)
+#pragma unroll
+                                for (int s = 0; s < kDig; ++s) {
+                                    const int t = g - s;
+                                    if (t < 0 || t >= kDig) continue;
+                                    if (s == 0)
+                                        tc_mma_i8_k128<kIdesc, true>(d0 + g * kBN, tmem + s * 32,
+                                                                     blo0 + t * (kSliceB >> 4));
+                                    else
+                                        tc_mma_i8_k128<kIdesc, false>(d0 + g * kBN, tmem + s * 32,
+                                                                      blo0 + t * (kSliceB >> 4));
+                                }
+                        tc_commit(lo_full);
+                    }
+                    __syncwarp();
+                    if (tc) mb_wait_warp(hi_free, (tc - 1u) & 1u);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        if (P.dbg != 2)
+#pragma unroll
+                            for (int g = 4; g < kGroups; ++g)
+#pragma unroll
+                                for (int s = 0; s < kDig; ++s) {
+                                    const int t = g - s;
+                                    if (t < 0 || t >= kDig) continue;
+                                    if (s == (g > kDig - 1 ? g - (kDig - 1) : 0))
+                                        tc_mma_i8_k128<kIdesc, true>(d0 + g * kBN, tmem + s * 32,
+                                                                     blo0 + t * (kSliceB >> 4));
+                                    else
+                                        tc_mma_i8_k128<kIdesc, false>(d0 + g * kBN, tmem + s * 32,
+                                                                      blo0 + t * (kSliceB >> 4));
+                                }
+                        tc_commit(b_empty(bs));
+                        tc_commit(hi_full);
+                    }
+                    __syncwarp();
                     if (++bs == kBStages) bs = 0, ++buse;
                 }
-                if (elect_one()) tc_commit(a_empty);
-                __syncwarp();
             }
         }
     } else {  // ---------------- epilogue warps: lane quadrant warp % 4, 16 columns each
         const int quad = warp & 3, half = (warp - 2) >> 2;
         const int rloc = quad * 32 + lane;
-        const uint32_t taddr0 = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * 16);
+        const uint32_t taddr0 = tmem + kTmemAcc + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * 16);
         uint32_t tc = 0;
+        int cs = 0;
+        uint32_t cuse = 0;
         for (int p = blockIdx.x; p < P.npanels; p += gridDim.x) {
             const int64_t row = (int64_t)p * kBM + rloc;
             const bool valid = row < P.m;
-            const int64_t rowc = valid ? row : 0;  // rows past m load row 0 and store nothing
-            const double rs = P.rscale[row];       // rscale covers the padded panel
+            const double rs = P.rscale[row];  // rscale covers the padded panel
             for (int nt = 0; nt < P.ntn; ++nt, ++tc) {
                 const int64_t j0 = (int64_t)nt * kBN + half * 16;
                 const int64_t rem = P.ncols - j0;
                 const int nc = rem >= 16 ? 16 : (rem > 0 ? (int)rem : 0);
-                // this tile's right-hand side and column scales: loads in
-                // flight while the MMAs run
-                double cv[16], cs[16];
-                if (nc == 16) {
-                    if (P.cols_in) {
-#pragma unroll
-                        for (int c = 0; c < 16; ++c) cv[c] = P.cin[__ldg(P.cols_in + j0 + c) * P.ldin + rowc];
-                    } else {
-                        const double *pc = P.cin + j0 * P.ldin + rowc;
-#pragma unroll
-                        for (int c = 0; c < 16; ++c) cv[c] = pc[c * P.ldin];
-                    }
-#pragma unroll
-                    for (int c = 0; c < 16; ++c) cs[c] = __ldg(P.cscale + j0 + c);
-                } else {
-#pragma unroll
-                    for (int c = 0; c < 16; ++c) {
-                        cv[c] = 0.0;
-                        cs[c] = 0.0;
-                        if (c < nc) {
-                            const int64_t cj = P.cols_in ? __ldg(P.cols_in + j0 + c) : j0 + c;
-                            cv[c] = P.cin[cj * P.ldin + rowc];
-                            cs[c] = __ldg(P.cscale + j0 + c);
-                        }
-                    }
-                }
-                const int q = (int)(tc & 1u);
-                mb_wait(acc_full(q), (tc >> 1) & 1u);
+                double hs[16];
+                mb_wait(lo_full, tc & 1u);
                 tc_fence_after();
-                const uint32_t ta = taddr0 + (uint32_t)(q * kGroups * kBN);
-                double *po = P.cout + j0 * P.ldout + rowc;
+                // groups 0-3 -> hi (exact, |hi| < 2^50), then 4-7 -> lo;
+                // converted with the scales 2^-24 / 2^-56 folded into the magic
+                // constants and added (one rounding)
 #pragma unroll
                 for (int h = 0; h < 16; h += 8) {
-                    uint32_t v[kGroups][8];
+                    uint32_t v[4][8];
 #pragma unroll
-                    for (int g = 0; g < kGroups; ++g) tmem_ld8(ta + (uint32_t)(g * kBN + h), v[g]);
+                    for (int g = 0; g < 4; ++g) tmem_ld8(taddr0 + (uint32_t)(g * kBN + h), v[g]);
                     tmem_wait_ld();
 #pragma unroll
                     for (int c = 0; c < 8; ++c) {
-                        // exact integer recombination of groups 0-3 and 4-7
-                        // (|.| < 2^50), converted with the scales 2^-24 and
-                        // 2^-56 folded into the magic constants
                         const long long hi = (long long)(int)v[0][c] * 16777216ll + (long long)(int)v[1][c] * 65536ll +
                                              (long long)(int)v[2][c] * 256ll + (long long)(int)v[3][c];
-                        const long long lo = (long long)(int)v[4][c] * 16777216ll + (long long)(int)v[5][c] * 65536ll +
-                                             (long long)(int)v[6][c] * 256ll + (long long)(int)v[7][c];
-                        const double hs = __longlong_as_double(hi + 0x41B8000000000000ll) - 402653184.0;  // hi 2^-24
-                        const double ls = __longlong_as_double(lo + 0x3FB8000000000000ll) - 0.09375;      // lo 2^-56
-                        const double prod = hs + ls;
-                        if (valid && h + c < nc) po[(h + c) * P.ldout] = fma(-prod, rs * cs[h + c], cv[h + c]);
+                        hs[h + c] = __longlong_as_double(hi + 0x41B8000000000000ll) - 402653184.0;
                     }
                 }
                 tc_fence_before();
-                mb_arrive(acc_empty(q));
+                mb_arrive(lo_free);
+                mb_wait(hi_full, tc & 1u);
+                tc_fence_after();
+#pragma unroll
+                for (int h = 0; h < 16; h += 8) {
+                    uint32_t v[4][8];
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) tmem_ld8(taddr0 + (uint32_t)((g + 4) * kBN + h), v[g]);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const long long lo = (long long)(int)v[0][c] * 16777216ll + (long long)(int)v[1][c] * 65536ll +
+                                             (long long)(int)v[2][c] * 256ll + (long long)(int)v[3][c];
+                        hs[h + c] += __longlong_as_double(lo + 0x3FB8000000000000ll) - 0.09375;
+                    }
+                }
+                tc_fence_before();
+                mb_arrive(hi_free);
+                // out = T - prod 2^(e_i + f_j): T from the staged tile, the
+                // result written back in place and stored by one TMA store
+                mb_wait(c_full(cs), cuse & 1u);
+                {
+                    double *ct = reinterpret_cast<double *>(smem + kSmemC + cs * kTileCBytes) + half * 16 * kBM + rloc;
+                    const bool tail = P.cols_in && valid && (P.m & 1) && row == P.m - 1;  // not in the bulk copies
+#pragma unroll
+                    for (int c = 0; c < 16; ++c)
+                        if (c < nc) {
+                            const double t = tail ? P.cin[__ldg(P.cols_in + j0 + c) * P.ldin + row] : ct[c * kBM];
+                            ct[c * kBM] = fma(-hs[c], rs * __ldg(P.cscale + j0 + c), t);
+                        }
+                }
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                asm volatile("bar.sync 1, %0;\n" ::"n"(kEpiWarps * 32) : "memory");
+                if (warp == 2 && lane == 0) {
+                    // one store in flight: once the previous tile's store has
+                    // read its stage, that stage goes back to the producer
+                    tma_store_2d(&tm_out, (int)((int64_t)p * kBM), (int)(j0 - half * 16), sC + cs * kTileCBytes);
+                    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+                    asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+                    if (tc) mb_arrive(c_empty(cs == 0 ? kCStages - 1 : cs - 1));
+                }
+                if (++cs == kCStages) cs = 0, ++cuse;
             }
         }
     }
+    if (warp == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(kTmemCols) : "memory");
     }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// column-major m x n FP64 matrix, 128 x 32 boxes
+int make_map(CUtensorMap *map, const double *base, int64_t m, int64_t n, int64_t ld) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return fail_internal("cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)n};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 8u};
+    const cuuint32_t box[2] = {kBM, kBN};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail_internal("cuTensorMapEncodeTiled failed");
+    return 0;
 }
 
 int launch_update(const UpdArgs &P, cudaStream_t st) {
@@ -483,8 +626,12 @@ int launch_update(const UpdArgs &P, cudaStream_t st) {
                 "oz update smem attr");
         attr_dev = dev;
     }
+    alignas(64) CUtensorMap tm_in, tm_out;
+    std::memset(&tm_in, 0, sizeof(tm_in));
+    if (!P.cols_in) CQ_TRY(make_map(&tm_in, P.cin, P.m, P.ncols, P.ldin));
+    CQ_TRY(make_map(&tm_out, P.cout, P.m, P.ncols, P.ldout));
     const int grid = std::min(P.npanels, num_sms());
-    oz_update_kernel<<<grid, kUpdThreads, kUpdSmem, st>>>(P);
+    oz_update_kernel<<<grid, kUpdThreads, kUpdSmem, st>>>(tm_in, tm_out, P);
     note_launch();
     return check_launch("oz_update_kernel");
 }
@@ -570,6 +717,7 @@ int trsm_right_oz(int64_t m, int64_t k, const double *b, int64_t ldb, const int6
         }
         P.cout = x + b1 * ldx;
         P.ldout = ldx;
+        P.dbg = getenv("CQRRPT_OZ_DBG") ? atoi(getenv("CQRRPT_OZ_DBG")) : 0;
         CQ_TRY(launch_update(P, st));
     }
     return 0;

@@ -251,7 +251,11 @@ int trsm_right(int64_t m, int64_t k, const double *b, int64_t ldb, const int64_t
     double *dinv = workspace().get<double>("trsm.dinv", (size_t)(nblk * kNB * kNB));
     if (!dinv) return fail_nomem("trsm diagonal-block inverses");
     CQ_TRY(trtri_diag_blocks(k, u, ldu, dinv, st));
-    if (trsm_use_ozaki(m, k)) return trsm_right_oz(m, k, b, ldb, cols, u, ldu, x, ldx, st, sink, dinv, block_ev);
+    // the INT8 engine stages right-hand-side columns with 16-byte bulk copies
+    const bool aligned = ((reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(x)) & 15) == 0 &&
+                         ((ldb | ldx) & 1) == 0;
+    if (aligned && trsm_use_ozaki(m, k))
+        return trsm_right_oz(m, k, b, ldb, cols, u, ldu, x, ldx, st, sink, dinv, block_ev);
     const unsigned grid = (unsigned)((m + kBM - 1) / kBM);
     cudaEvent_t *evs = nullptr;  // one per block, reused across calls (per device)
     if (sink) CQ_TRY(cached_events("trsm.sink", (size_t)((k + kNB - 1) / kNB), &evs));
