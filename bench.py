@@ -357,14 +357,35 @@ def main():
     tr = load_traffic(name)
     trsm_flops = float(ml) * k0 * k0  # trsm_right: m k0^2 flops per pass (flop_model term)
     achieved = trsm_flops / (ph[3] * 1e-3) / 1e12
-    roofline = {"bound": "tensor", "kernel": "trsm_block_kernel (K5a gather + TRSM on DMMA.8x8x4)",
+    from paper_2311_08316_b200 import kernels as _k
+    engine = _k.trsm_engine(ml, k0)
+    kname = ("precondition TRSM pass: oz_update_kernel (exact INT8 emulation on tcgen05 kind::i8, TMEM "
+             "accumulators) for the trailing updates + trsm_block_kernel (DMMA) for the 128x128 diagonal blocks"
+             if engine == "int8" else "trsm_block_kernel (K5a gather + TRSM on DMMA.8x8x4)")
+    roofline = {"bound": "tensor", "kernel": kname,
                 "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
                 "traffic": tr.get("trsm_pass_dram_bytes"),
                 "peak_source": "measured live in this run: cuBLAS DGEMM 8192^3 (torch.matmul float64), best of 5 "
-                               "(MEASURED_PEAKS.json has no FP64 figure)",
+                               "(MEASURED_PEAKS.json has no FP64 figure); FP64-equivalent flops, so an INT8-emulated "
+                               "pass can exceed 1.0",
                 "algorithmic": f"m_local*k0^2 = {trsm_flops:.4g} flops per precondition TRSM pass, over the "
                                f"CUDA-event time of that phase",
                 "traffic_unit": "DRAM bytes per TRSM pass (ncu dram__bytes_read+write, profiles/traffic.json)"}
+    roofline_int8 = None
+    if engine == "int8":
+        # int8 MACs of the emulated trailing updates: 34 digit pairs per product,
+        # 128-column steps (csrc/oztrsm.cu); over the whole pass time (diagonal
+        # DMMA solves and digit slicing included), so a lower bound
+        ops = 0.0
+        for b0 in range(0, k0, 128):
+            b1 = min(k0, b0 + 128)
+            ops += 2.0 * 34 * (b1 - b0) * (k0 - b1) * ml
+        roofline_int8 = {"bound": "tensor", "kernel": "oz_update_kernel (tcgen05.mma kind::i8 M128 N32 K32)",
+                         "achieved": ops / (ph[3] * 1e-3) / 1e12, "peak": 4500.0, "unit": "TOPS",
+                         "peak_source": "B200 dense INT8 tensor nominal (4.5 POPS); not in MEASURED_PEAKS.json",
+                         "algorithmic": f"{ops:.4g} int8 ops per precondition pass (2 x 34 pairs x m x w x trailing "
+                                        f"columns per 128-column step) over the pass time"}
+        roofline_int8["frac"] = roofline_int8["achieved"] / roofline_int8["peak"]
     sketch_bytes = 8.0 * ml * n + 8.0 * res.ctx.d * n
     sk = {"bound": "hbm", "kernel": "saso_apply_kernel", "achieved": sketch_bytes / (ph[0] * 1e-3) / 1e9,
           "peak": peaks.get("hbm_gbs"), "unit": "GB/s", "peak_source": peak_src,
@@ -391,7 +412,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (tools/workloads.py, seeded, device-generated)",
             "config": dict(conf, restore="device copy" if device_copy else "H2D from pinned host memory"),
-            "e2e": e2e, "roofline": roofline, "roofline_sketch": sk, "roofline_contractions": con,
+            "e2e": e2e, "roofline": roofline, "roofline_int8": roofline_int8, "roofline_sketch": sk,
+            "roofline_contractions": con, "trsm_engine": engine,
             "phases_ms": dict(zip(names, [round(float(x), 4) for x in ph])), "per_rank": per_rank,
             "k": k, "k0": k0, "gpu_launches": launches,
             "gpu_launches_per_step": launches / max(args.steps, 1), "clocks": clocks, "cpu_baseline": cpu}

@@ -227,6 +227,13 @@ int cqrrpt_gpu_rank_stage2(int64_t m, int64_t k0, const double *M_k0, int64_t ld
 int cqrrpt_gpu_trsm_right(int64_t m, int64_t k, const double *B, int64_t ldb, const int64_t *cols,
                           const double *U, int64_t ldu, double *X, int64_t ldx, void *stream);
 
+/* Which engine cqrrpt_gpu_trsm_right (and the driver's two solves) uses for an
+ * m x k solve with 16-byte aligned operands and even leading dimensions: 0 =
+ * DMMA (FP64 tensor cores), 1 = the exact INT8 tensor-core emulation
+ * (tcgen05 kind::i8; from m >= 1048576 and k >= 1024, or CQRRPT_GPU_TRSM=oz |
+ * dmma). Diagnostic; no device work. */
+int cqrrpt_gpu_trsm_engine(int64_t m, int64_t k);
+
 /* G (k x k, ldg) = X^T X, bitwise symmetric; gram (linalg.cc:298-307). */
 int cqrrpt_gpu_gram(int64_t m, int64_t k, const double *X, int64_t ldx, double *G, int64_t ldg,
                     void *stream);

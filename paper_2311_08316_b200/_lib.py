@@ -61,6 +61,7 @@ SYMBOLS = {
                                               ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i32),
                                               ctypes.POINTER(_f64), _vp]),
     "cqrrpt_gpu_trsm_right": (ctypes.c_int, [_i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp]),
+    "cqrrpt_gpu_trsm_engine": (ctypes.c_int, [_i64, _i64]),
     "cqrrpt_gpu_gram": (ctypes.c_int, [_i64, _i64, _vp, _i64, _vp, _i64, _vp]),
     "cqrrpt_gpu_potrf": (ctypes.c_int, [_i64, _vp, _i64, ctypes.POINTER(_i64), _vp]),
     "cqrrpt_gpu_cond_estimate": (ctypes.c_int, [_i64, _vp, _i64, _i32, ctypes.POINTER(_f64), _vp]),

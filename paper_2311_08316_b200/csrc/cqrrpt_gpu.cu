@@ -409,6 +409,26 @@ int stage2_select(int64_t k0f, const double *rfull, int64_t ldf, double eps_tol,
         *v = e;
         return 0;
     };
+    // The search's all-pass prefix in one batched launch (the estimates do
+    // not depend on the batch): probes are memoised up to and including the
+    // first one whose running max fails -- exactly the probes the reference
+    // evaluates before its search turns; the rest of the search continues
+    // probe by probe.
+    {
+        std::vector<int64_t> ells;
+        all_pass_probes(k0f, ells);
+        if (ells.size() > 1) {
+            std::vector<double> est(ells.size(), 1.0);
+            CQ_TRY(cond_estimate_batch((int)ells.size(), ells.data(), rfull, ldf, rinv, k0f, nested_method(method),
+                                       est.data(), ws, s));
+            double run = 1.0;
+            for (size_t q = 0; q < ells.size(); ++q) {
+                raw[ells[q]] = est[q];
+                run = std::max(run, est[q]);
+                if (!(run <= threshold)) break;
+            }
+        }
+    }
     int64_t lo = 0, hi = k0f;  // binary search (cqrrpt.cc:197-207)
     while (lo < hi) {
         const int64_t mid = lo + (hi - lo + 1) / 2;
@@ -880,6 +900,8 @@ int cqrrpt_gpu_rank_stage2(int64_t m, int64_t k0, const double *M_k0, int64_t ld
     CQ_CUDA(cudaStreamSynchronize(st), "rank_stage2 sync");
     return 0;
 }
+
+int cqrrpt_gpu_trsm_engine(int64_t m, int64_t k) { return trsm_use_ozaki(m, k) ? 1 : 0; }
 
 int cqrrpt_gpu_trsm_right(int64_t m, int64_t k, const double *B, int64_t ldb, const int64_t *cols, const double *U,
                           int64_t ldu, double *X, int64_t ldx, void *stream) {

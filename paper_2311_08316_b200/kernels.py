@@ -109,6 +109,12 @@ def trsm_right(b, u, cols=None, stream=None):
     return x
 
 
+def trsm_engine(m, k):
+    """Engine of an m x k trsm_right: "dmma" (FP64 tensor cores) or "int8" (the
+    exact tcgen05 kind::i8 emulation, csrc/oztrsm.cu)."""
+    return "int8" if _lib.load().cqrrpt_gpu_trsm_engine(m, k) else "dmma"
+
+
 def gram(x, stream=None):
     """gram(M) (linalg.cc:298-307) -> k x k, bitwise symmetric."""
     m, k = x.shape

@@ -1,5 +1,5 @@
 """GPU parity of each CUDA kernel against the CPU oracle (oracle/cqrrpt_oracle.c,
-pinned bit-for-bit to the reference by tests/test_oracle_pin.py).
+pinned bit-for-bit to the reference by tests/test_oracle.py).
 
 Bars (stated per test): integer/index work bit-exact; FP64 work within the
 tolerance the reference's own tests use for that function.
