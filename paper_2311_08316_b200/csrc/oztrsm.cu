@@ -181,156 +181,6 @@ __global__ void oz_slice_cols_kernel(int64_t ncols, int w, const double *__restr
     }
 }
 
-
-// ---------------------------------------------------------------------------
-// Experimental (CQRRPT_OZ_FUSED_DIAG=1): the 128-column diagonal block fused
-//   X0 = T0 D0, T1 -= X0 U01, X1 = T1 D1 on DMMA (D0, D1: the 64 x 64
-//   diagonal-block inverses), plus the digit slices / row scales of X_b from
-// the same shared-memory tile. Persistent CTAs over 32-row tiles, D0 / U01 /
-// D1 resident, the next two tiles' loads in flight.
-// ---------------------------------------------------------------------------
-constexpr int kDR = 32;
-constexpr int kDLd = kW + 2;
-constexpr int kDBLd = 66;
-constexpr int kDThreads = 256;
-constexpr size_t kDiagSmem = sizeof(double) * (3 * 64 * kDBLd + 3 * (size_t)kDR * kDLd + 8 * kDR);
-
-__global__ void __launch_bounds__(kDThreads, 1)
-    oz_diag_kernel(int64_t m, int w, const double *__restrict__ src, int64_t lds, const int64_t *__restrict__ cols,
-                   const double *__restrict__ dinv, const double *__restrict__ u, int64_t ldu, double *__restrict__ x,
-                   int64_t ldx, int8_t *__restrict__ slices, double *__restrict__ rscale, int64_t ntiles) {
-    extern __shared__ __align__(16) double dsm[];
-    double *D0s = dsm, *Us = dsm + 64 * kDBLd, *D1s = dsm + 2 * 64 * kDBLd;
-    double *Tb = dsm + 3 * 64 * kDBLd;
-    double *Mx = Tb + 3 * kDR * kDLd;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int g = lane >> 2, t = lane & 3;
-    const int r_ld = lane, cg = warp;
-    for (int q = tid; q < 64 * 64; q += kDThreads) {
-        const int n = q >> 6, kq = q & 63;
-        D0s[n * kDBLd + kq] = __ldg(dinv + q);
-        D1s[n * kDBLd + kq] = w > 64 ? __ldg(dinv + 4096 + q) : 0.0;
-        Us[n * kDBLd + kq] = (64 + n < w) ? __ldg(u + (int64_t)(64 + n) * ldu + kq) : 0.0;
-    }
-    auto load_tile = [&](int64_t tile, int buf) {
-        const int64_t row = tile * kDR + r_ld;
-        const bool ok = row < m;
-        double *Ts = Tb + buf * kDR * kDLd;
-#pragma unroll 4
-        for (int j = 0; j < kW / 8; ++j) {
-            const int c = cg + 8 * j;
-            const bool in = ok && c < w;
-            const double *gp = in ? src + (cols ? __ldg(cols + c) : (int64_t)c) * lds + row : src;
-            cp_async8_zfill(Ts + r_ld * kDLd + c, gp, in ? 8 : 0);
-        }
-    };
-    int64_t tile = blockIdx.x;
-    int buf = 0;
-    if (tile < ntiles) load_tile(tile, 0);
-    cp_async_commit();
-    if (tile + gridDim.x < ntiles) load_tile(tile + gridDim.x, 1);
-    cp_async_commit();
-    for (; tile < ntiles; tile += gridDim.x, buf = (buf == 2 ? 0 : buf + 1)) {
-        if (tile + 2 * (int64_t)gridDim.x < ntiles) load_tile(tile + 2 * (int64_t)gridDim.x, buf == 0 ? 2 : buf - 1);
-        cp_async_commit();
-        cp_async_wait<2>();
-        __syncthreads();
-        double *Ts = Tb + buf * kDR * kDLd;
-        double ep[4][2];
-        auto tri_mul = [&](const double *Ds, int c_off) {
-#pragma unroll
-            for (int mi = 0; mi < 4; ++mi) ep[mi][0] = ep[mi][1] = 0.0;
-#pragma unroll 4
-            for (int kk = 0; kk < 64; kk += 4) {
-                if (kk > 8 * warp + 4) break;
-                const double bf = Ds[(warp * 8 + g) * kDBLd + kk + t];
-#pragma unroll
-                for (int mi = 0; mi < 4; ++mi)
-                    dmma884(ep[mi][0], ep[mi][1], Ts[(mi * 8 + g) * kDLd + c_off + kk + t], bf);
-            }
-        };
-        auto put = [&](int c_off) {
-#pragma unroll
-            for (int mi = 0; mi < 4; ++mi)
-                *reinterpret_cast<double2 *>(Ts + (mi * 8 + g) * kDLd + c_off + warp * 8 + 2 * t) =
-                    make_double2(ep[mi][0], ep[mi][1]);
-        };
-        tri_mul(D0s, 0);
-        __syncthreads();
-        put(0);
-        if (w > 64) {
-            __syncthreads();
-#pragma unroll
-            for (int mi = 0; mi < 4; ++mi) {
-                const double2 v = *reinterpret_cast<const double2 *>(Ts + (mi * 8 + g) * kDLd + 64 + warp * 8 + 2 * t);
-                ep[mi][0] = v.x;
-                ep[mi][1] = v.y;
-            }
-#pragma unroll 4
-            for (int kk = 0; kk < 64; kk += 4) {
-                const double bf = Us[(warp * 8 + g) * kDBLd + kk + t];
-#pragma unroll
-                for (int mi = 0; mi < 4; ++mi) dmma884(ep[mi][0], ep[mi][1], -Ts[(mi * 8 + g) * kDLd + kk + t], bf);
-            }
-            put(64);
-            __syncthreads();
-            tri_mul(D1s, 64);
-            __syncthreads();
-            put(64);
-        }
-        __syncthreads();
-        const int64_t row = tile * kDR + r_ld;
-        const bool valid = row < m;
-        if (valid)
-#pragma unroll 4
-            for (int j = 0; j < kW / 8; ++j) {
-                const int c = cg + 8 * j;
-                if (c < w) x[(int64_t)c * ldx + row] = Ts[r_ld * kDLd + c];
-            }
-        if (slices) {
-            double mx = 0.0;
-            bool bad = false;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const double a = fabs(Ts[r_ld * kDLd + cg * 16 + j]);
-                bad |= !(a <= 1.79769313486231570e308);
-                mx = fmax(mx, a);
-            }
-            Mx[cg * kDR + r_ld] = bad ? __longlong_as_double(0x7ff8000000000000ll) : mx;
-            __syncthreads();
-            mx = 0.0;
-            bad = false;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const double v = Mx[q * kDR + r_ld];
-                bad |= !(v == v);
-                mx = fmax(mx, v);
-            }
-            int e = 0;
-            if (mx > 0.0) frexp(mx, &e);
-            if (cg == 0) rscale[row] = bad ? __longlong_as_double(0x7ff8000000000000ll) : ldexp(1.0, e);
-            const int sh = 54 - e;
-            uint32_t wd[4][kDig];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-                for (int s2 = 0; s2 < kDig; ++s2) wd[q][s2] = 0u;
-            if (valid && !bad) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) digits7(Ts[r_ld * kDLd + cg * 16 + j], sh, wd[j >> 2], j & 3);
-            }
-            uint8_t *base = reinterpret_cast<uint8_t *>(slices) + (row / kBM) * (int64_t)kPanelBytes;
-            const int rp = (int)(row % kBM);
-#pragma unroll
-            for (int s2 = 0; s2 < kDig; ++s2)
-                *reinterpret_cast<uint4 *>(base + s2 * kSliceA + canon_off(rp, cg * 16)) =
-                    make_uint4(wd[0][s2], wd[1][s2], wd[2][s2], wd[3][s2]);
-        }
-        __syncthreads();
-    }
-    cp_async_wait<0>();
-}
-
 // ---------------------------------------------------------------------------
 // tcgen05 / mbarrier / bulk-copy primitives
 // ---------------------------------------------------------------------------
@@ -818,26 +668,6 @@ int trsm_right_oz(int64_t m, int64_t k, const double *b, int64_t ldb, const int6
     for (int64_t b0 = 0; b0 < k; b0 += kW) {
         const int64_t b1 = std::min(k, b0 + kW), w = b1 - b0;
         const bool first = b0 == 0;
-        const bool fused = getenv("CQRRPT_OZ_FUSED_DIAG") != nullptr;
-        if (fused) {
-            const double *sview = first ? (cols ? b : b + b0 * ldb) : x + b0 * ldx;
-            const int64_t lds = first ? ldb : ldx;
-            const int64_t *cview = (first && cols) ? cols + b0 : nullptr;
-            static thread_local int diag_attr_dev = -1;
-            if (diag_attr_dev != current_device()) {
-                CQ_CUDA(cudaFuncSetAttribute(oz_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)kDiagSmem),
-                        "oz diag smem attr");
-                diag_attr_dev = current_device();
-            }
-            const bool more = b1 < k;
-            const int64_t ntl = npanels * (kBM / kDR);
-            oz_diag_kernel<<<(unsigned)std::min<int64_t>(ntl, num_sms()), kDThreads, kDiagSmem, st>>>(
-                m, (int)w, sview, lds, cview, dinv + (b0 / NB) * NB * NB, u + b0 * ldu + b0, ldu, x + b0 * ldx, ldx,
-                more ? aslc : nullptr, more ? rexp : nullptr, ntl);
-            note_launch();
-            CQ_TRY(check_launch("oz_diag_kernel"));
-        }
         // X_b = T_b U_bb^{-1}: the DMMA block kernel on the view starting at b0
         // (T_b is the gathered input for the first block, else X's own
         // columns, updated in place by the previous steps)
@@ -845,7 +675,6 @@ int trsm_right_oz(int64_t m, int64_t k, const double *b, int64_t ldb, const int6
         const int64_t lds = first ? ldb : ldx;
         const int64_t *cview = (first && cols) ? cols + b0 : nullptr;
         for (int64_t c0 = 0; c0 < w; c0 += NB) {
-            if (!fused)
             CQ_TRY(trsm_block(m, k - b0, c0, sview, lds, cview, u + b0 * ldu + b0, ldu,
                               dinv + ((b0 + c0) / NB) * NB * NB, x + b0 * ldx, ldx, st));
             const int64_t cb = (b0 + c0) / NB;
@@ -864,11 +693,9 @@ int trsm_right_oz(int64_t m, int64_t k, const double *b, int64_t ldb, const int6
         // T_>b -= X_b U_b,>b on the INT8 tensor cores
         const int64_t ncols = k - b1;
         const int ntn = (int)((ncols + kBN - 1) / kBN);
-        if (!fused) {
-            oz_slice_rows_kernel<<<(unsigned)npanels, kBM, 0, st>>>(m, (int)w, x + b0 * ldx, ldx, aslc, rexp);
-            note_launch();
-            CQ_TRY(check_launch("oz_slice_rows_kernel"));
-        }
+        oz_slice_rows_kernel<<<(unsigned)npanels, kBM, 0, st>>>(m, (int)w, x + b0 * ldx, ldx, aslc, rexp);
+        note_launch();
+        CQ_TRY(check_launch("oz_slice_rows_kernel"));
         oz_slice_cols_kernel<<<(unsigned)((ntn * kBN + 127) / 128), 128, 0, st>>>(ncols, (int)w, u + b1 * ldu + b0,
                                                                                    ldu, bslc, cexp);
         note_launch();
