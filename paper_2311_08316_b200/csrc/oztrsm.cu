@@ -91,49 +91,63 @@ CQ_DEVI void digits7(double v, int sh, uint32_t (&w)[kDig], int byte) {
     }
 }
 
-// A operand: rows of X_b (m x w, column-major). CTA = one 128-row panel,
-// thread = row: exponent of the row max, then 7 digit slices in the canonical
-// layout (16-byte stores: 8 consecutive rows write one 128-byte core matrix).
-__global__ void __launch_bounds__(kBM) oz_slice_rows_kernel(int64_t m, int w, const double *__restrict__ x,
+// A operand: rows of X_b (m x w, column-major). CTA = 32 rows: the 32 x 128
+// tile is staged through shared memory with coalesced 256-byte column runs
+// (X_b is read once), then thread (row, 16-column chunk) forms the row
+// maximum's exponent (shared-memory reduction over the chunks) and the 7
+// digit slices of its chunk in the canonical layout (16-byte stores: 8
+// consecutive rows write one 128-byte core matrix).
+constexpr int kSR = 32;
+constexpr int kSLd = kW + 1;  // 129: conflict-free row reads
+__global__ void __launch_bounds__(256) oz_slice_rows_kernel(int64_t m, int w, const double *__restrict__ x,
                                                             int64_t ldx, int8_t *__restrict__ slices,
                                                             double *__restrict__ rscale) {
-    const int r = threadIdx.x;
-    const int64_t p = blockIdx.x, row = p * kBM + r;
+    __shared__ double ts[kSR * kSLd];
+    __shared__ double mx8[8 * kSR];
+    const int r = threadIdx.x & (kSR - 1), q = threadIdx.x >> 5;  // row, 16-column chunk
+    const int64_t row = (int64_t)blockIdx.x * kSR + r;
     const bool valid = row < m;
     const double *xr = x + (valid ? row : 0);
+#pragma unroll 4
+    for (int c = q; c < kW; c += 8) ts[r * kSLd + c] = (valid && c < w) ? xr[(int64_t)c * ldx] : 0.0;
+    __syncthreads();
     double mx = 0.0;
     bool bad = false;
-    if (valid)
-        for (int c = 0; c < w; ++c) {
-            const double a = fabs(xr[(int64_t)c * ldx]);
-            bad |= !(a <= 1.79769313486231570e308);
-            mx = fmax(mx, a);
-        }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const double a = fabs(ts[r * kSLd + q * 16 + j]);
+        bad |= !(a <= 1.79769313486231570e308);
+        mx = fmax(mx, a);
+    }
+    mx8[q * kSR + r] = bad ? __longlong_as_double(0x7ff8000000000000ll) : mx;
+    __syncthreads();
+    mx = 0.0;
+    bad = false;
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq) {
+        const double v = mx8[qq * kSR + r];
+        bad |= !(v == v);
+        mx = fmax(mx, v);
+    }
     int e = 0;
     if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
-    rscale[row] = bad ? __longlong_as_double(0x7ff8000000000000ll) : ldexp(1.0, e);
+    if (q == 0) rscale[row] = bad ? __longlong_as_double(0x7ff8000000000000ll) : ldexp(1.0, e);
     const int sh = 54 - e;
-    uint8_t *base = reinterpret_cast<uint8_t *>(slices) + p * (int64_t)kPanelBytes;
-#pragma unroll 1
-    for (int kc = 0; kc < kW / 16; ++kc) {
-        uint32_t wd[4][kDig];
+    uint32_t wd[4][kDig];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int s = 0; s < kDig; ++s) wd[q][s] = 0u;
-        if (valid && !bad) {
+        for (int s2 = 0; s2 < kDig; ++s2) wd[a][s2] = 0u;
+    if (valid && !bad) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int c = kc * 16 + j;
-                const double v = (c < w) ? xr[(int64_t)c * ldx] : 0.0;
-                digits7(v, sh, wd[j >> 2], j & 3);
-            }
-        }
-#pragma unroll
-        for (int s = 0; s < kDig; ++s)
-            *reinterpret_cast<uint4 *>(base + s * kSliceA + canon_off(r, kc * 16)) =
-                make_uint4(wd[0][s], wd[1][s], wd[2][s], wd[3][s]);
+        for (int j = 0; j < 16; ++j) digits7(ts[r * kSLd + q * 16 + j], sh, wd[j >> 2], j & 3);
     }
+    uint8_t *base = reinterpret_cast<uint8_t *>(slices) + (row / kBM) * (int64_t)kPanelBytes;
+    const int rp = (int)(row % kBM);
+#pragma unroll
+    for (int s2 = 0; s2 < kDig; ++s2)
+        *reinterpret_cast<uint4 *>(base + s2 * kSliceA + canon_off(rp, q * 16)) =
+            make_uint4(wd[0][s2], wd[1][s2], wd[2][s2], wd[3][s2]);
 }
 
 // B operand: columns j of U[b0 : b0 + w, c0 : c0 + N] (column-major U),
@@ -693,7 +707,8 @@ int trsm_right_oz(int64_t m, int64_t k, const double *b, int64_t ldb, const int6
         // T_>b -= X_b U_b,>b on the INT8 tensor cores
         const int64_t ncols = k - b1;
         const int ntn = (int)((ncols + kBN - 1) / kBN);
-        oz_slice_rows_kernel<<<(unsigned)npanels, kBM, 0, st>>>(m, (int)w, x + b0 * ldx, ldx, aslc, rexp);
+        oz_slice_rows_kernel<<<(unsigned)(npanels * (kBM / kSR)), 256, 0, st>>>(m, (int)w, x + b0 * ldx, ldx, aslc,
+                                                                              rexp);
         note_launch();
         CQ_TRY(check_launch("oz_slice_rows_kernel"));
         oz_slice_cols_kernel<<<(unsigned)((ntn * kBN + 127) / 128), 128, 0, st>>>(ncols, (int)w, u + b1 * ldu + b0,
