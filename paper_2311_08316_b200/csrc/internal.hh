@@ -103,7 +103,7 @@ int trsm_right_oz(int64_t m, int64_t k, const double *b, int64_t ldb, const int6
                   const cudaEvent_t *block_ev);
 // one 64-column block c0 of trsm_right (dinv_blk: inverse of U's diagonal block)
 int trsm_block(int64_t m, int64_t k, int64_t c0, const double *b, int64_t ldb, const int64_t *cols, const double *u,
-               int64_t ldu, const double *dinv_blk, double *x, int64_t ldx, cudaStream_t st);
+               int64_t ldu, const double *dinv_blk, double *x, int64_t ldx, cudaStream_t st, bool pdl = false);
 int gram(int64_t m, int64_t k, const double *x, int64_t ldx, double *g, int64_t ldg, Workspace &ws,
          cudaStream_t st);
 // the Gram on the INT8 tensor cores (Ozaki scheme II, ozaki.cu) and the DMMA one

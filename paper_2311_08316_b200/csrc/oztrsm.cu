@@ -690,7 +690,7 @@ int trsm_right_oz(int64_t m, int64_t k, const double *b, int64_t ldb, const int6
         const int64_t *cview = (first && cols) ? cols + b0 : nullptr;
         for (int64_t c0 = 0; c0 < w; c0 += NB) {
             CQ_TRY(trsm_block(m, k - b0, c0, sview, lds, cview, u + b0 * ldu + b0, ldu,
-                              dinv + ((b0 + c0) / NB) * NB * NB, x + b0 * ldx, ldx, st));
+                              dinv + ((b0 + c0) / NB) * NB * NB, x + b0 * ldx, ldx, st, /*pdl=*/c0 > 0 && !block_ev && !sink));
             const int64_t cb = (b0 + c0) / NB;
             if (block_ev) CQ_CUDA(cudaEventRecord(block_ev[cb], st), "oz trsm block event");
             if (sink) {

@@ -217,12 +217,28 @@ __global__ void diag_zero_check_kernel(int64_t k, const double *__restrict__ u, 
 }
 
 int trsm_block(int64_t m, int64_t k, int64_t c0, const double *b, int64_t ldb, const int64_t *cols, const double *u,
-               int64_t ldu, const double *dinv_blk, double *x, int64_t ldx, cudaStream_t st) {
+               int64_t ldu, const double *dinv_blk, double *x, int64_t ldx, cudaStream_t st, bool pdl) {
     if (m <= 0 || c0 >= k) return 0;
-    CQ_CUDA(cudaFuncSetAttribute(trsm_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrsmSmem),
-            "trsm smem attr");
-    trsm_block_kernel<<<(unsigned)((m + kBM - 1) / kBM), kThreads, kTrsmSmem, st>>>(m, k, c0, b, ldb, cols, u, ldu,
-                                                                                 dinv_blk, x, ldx);
+    static thread_local int attr_dev = -1;
+    if (attr_dev != current_device()) {
+        CQ_CUDA(cudaFuncSetAttribute(trsm_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrsmSmem),
+                "trsm smem attr");
+        attr_dev = current_device();
+    }
+    // pdl: programmatic dependent launch after a trsm_block of the same solve
+    // (the gather of this block's source columns overlaps its tail)
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3((unsigned)((m + kBM - 1) / kBM));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kTrsmSmem;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    CQ_CUDA(cudaLaunchKernelEx(&cfg, trsm_block_kernel, m, k, c0, b, ldb, cols, u, ldu, dinv_blk, x, ldx),
+            "trsm block launch");
     note_launch();
     return check_launch("trsm_block_kernel");
 }
