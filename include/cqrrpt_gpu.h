@@ -228,7 +228,8 @@ int cqrrpt_gpu_trsm_right(int64_t m, int64_t k, const double *B, int64_t ldb, co
                           const double *U, int64_t ldu, double *X, int64_t ldx, void *stream);
 
 /* Which engine cqrrpt_gpu_trsm_right (and the driver's two solves) uses for an
- * m x k solve with 16-byte aligned operands and even leading dimensions: 0 =
+ * m x k solve with even m, 16-byte aligned operands and even leading
+ * dimensions (else always DMMA): 0 =
  * DMMA (FP64 tensor cores), 1 = the exact INT8 tensor-core emulation
  * (tcgen05 kind::i8; from m >= 1048576 and k >= 1536, or CQRRPT_GPU_TRSM=oz |
  * dmma). Diagnostic; no device work. */

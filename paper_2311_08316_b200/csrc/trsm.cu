@@ -268,8 +268,11 @@ int trsm_right(int64_t m, int64_t k, const double *b, int64_t ldb, const int64_t
     if (!dinv) return fail_nomem("trsm diagonal-block inverses");
     CQ_TRY(trtri_diag_blocks(k, u, ldu, dinv, st));
     // the INT8 engine stages right-hand-side columns with 16-byte bulk copies
+    // and tensor-map boxes, whose row bound is applied at 16-byte granularity
+    // (measured: an odd m lets the store write row m): even m, even leading
+    // dimensions, 16-byte aligned bases
     const bool aligned = ((reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(x)) & 15) == 0 &&
-                         ((ldb | ldx) & 1) == 0;
+                         ((ldb | ldx | m) & 1) == 0;
     if (aligned && trsm_use_ozaki(m, k))
         return trsm_right_oz(m, k, b, ldb, cols, u, ldu, x, ldx, st, sink, dinv, block_ev);
     const unsigned grid = (unsigned)((m + kBM - 1) / kBM);

@@ -6,8 +6,6 @@ each 128-wide step's operands and the dropped digit pairs (<= 2^-61 of the
 FP64 GEMM's normwise bound), so the two engines agree column-wise to a few
 ulps of the solution and both satisfy the reference TRSM's residual bar.
 """
-import os
-
 import numpy as np
 import pytest
 
@@ -111,3 +109,30 @@ def test_dgeqpt_with_int8_engine_matches_dmma(cuda, oracle, engine):
     assert np.linalg.norm(qo.T @ qo - np.eye(ko)) <= 1e-13
     assert np.linalg.norm(a[:, jo] - qo @ ro) <= 1e-14 * np.linalg.norm(a)
     assert np.max(np.abs(ro - rd)) <= 1e3 * 512 * U * np.max(np.abs(rd))
+
+
+def test_int8_engine_odd_rows_even_leading_dimension(cuda, oracle, engine):
+    """m odd with even leading dimensions: TMA applies the row bound of a box
+    at 16-byte granularity, so the engine stands down for odd m (DMMA takes
+    the solve); the padding row below the matrix stays untouched."""
+    import torch
+    from paper_2311_08316_b200 import _lib, kernels
+    from paper_2311_08316_b200.kernels import _p
+    m, k, ld = 70001, 300, 70002
+    b = oracle.gen_gaussian(m, k + 3, 31)
+    u = _upper(oracle, k, 32)
+    cols = np.random.default_rng(2).permutation(k + 3)[:k].astype(np.int64)
+    bbuf = torch.zeros((k + 3, ld), dtype=torch.float64, device="cuda")
+    bbuf[:, :m] = torch.from_numpy(np.ascontiguousarray(b.T)).cuda()
+    xbuf = torch.full((k, ld), 7.0, dtype=torch.float64, device="cuda")
+    ud = dev(cuda, u)
+    tc = torch.as_tensor(cols, device="cuda")
+    engine("oz")
+    _lib.check(_lib.load().cqrrpt_gpu_trsm_right(m, k, _p(bbuf), ld, _p(tc), _p(ud), k, _p(xbuf), ld, None),
+               "trsm_right")
+    x = np.asfortranarray(xbuf.t()[:m].cpu().numpy())
+    assert np.all(xbuf[:, m].cpu().numpy() == 7.0)  # the padding row is not written
+    engine("dmma")
+    ref = host(kernels.trsm_right(dev(cuda, b), ud, cols=tc))
+    diff = np.linalg.norm(x - ref, axis=0) / np.linalg.norm(ref, axis=0)
+    assert np.max(diff) <= 1e3 * k * U
