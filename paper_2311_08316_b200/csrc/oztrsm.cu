@@ -17,23 +17,32 @@
 // integer, column j of U_b,>b by 2^(54 - f_j); each integer is split into 7
 // balanced base-256 digits (int8, most significant first). The products of
 // digit slices s, t with s + t = g <= 7 accumulate in int32 (exact: |acc| <=
-// 8 pairs * 128 * 2^14 = 2^24) into TMEM group g; the epilogue forms
-// sum_g acc_g 2^(-12-8g) in FP64 (smallest group first), scales by
-// 2^(e_i + f_j) and subtracts from T in FP64. Dropped pairs (g >= 8) and the
+// 8 pairs * 128 * 2^14 = 2^24) into TMEM group g; the drain recombines groups
+// 0-3 and 4-7 exactly in int64 (|.| < 2^50), converts each with the scale
+// 2^-24 / 2^-56 folded into a magic constant, adds them (one rounding) and
+// applies T - p 2^(e_i + f_j) with one more. Dropped pairs (g >= 8) and the
 // 54-bit rounding bound the error by ~2^-54 max|X_i,:| max|U_:,j| per term --
 // the FP64 GEMM's normwise bound (the parity tests compare with the DMMA
 // engine and the oracle).
 //
-// oz_update_kernel: persistent, one CTA per SM (200 KB shared memory):
-//   warp 0   producer: 1-D bulk copies (TMA engine) of the panel's digit
-//            slices (128 rows x 128 K x 7 = 112 KB, pre-tiled in the UMMA
-//            canonical K-major layout) and a 3-stage ring of N-tiles of U's
-//            slices (32 x 128 x 7 = 28 KB);
-//   warp 1   TMEM allocator + MMA issuer (one thread): per N tile 34 digit
-//            pairs x 4 K-steps of tcgen05.mma M128 N32 K32 into 8 group
-//            accumulators, double-buffered (2 x 8 x 32 = 512 TMEM columns);
-//   warps 2-5 epilogue: tcgen05.ld of the 8 groups (lane = row), FP64
-//            recombination, read-modify-write of T (coalesced column runs).
+// oz_update_kernel: persistent, one CTA per SM (212 KB shared memory, all 512
+// TMEM columns):
+//   warp 0    producer (TMA engine): the panel's 7 digit slices (128 rows x 128
+//             K each, pre-tiled in the UMMA canonical K-major layout) through a
+//             2-slice ring, a 3-stage ring of U's N tiles (32 x 128 x 7 = 28
+//             KB), and per tile the right-hand side (one 128 x 32 tensor-map
+//             box; per-column bulk copies for the gathered first step);
+//   warp 1    TMEM allocator + MMA issuer (one elected thread, operands in
+//             uniform registers): tcgen05.cp of the A slices into TMEM columns
+//             0..223 once per panel, then per N tile 34 digit pairs x 4 K-steps
+//             of tcgen05.mma M128 N32 K32 (A from TMEM, B from shared memory)
+//             into 8 group accumulators (columns 256..511); groups 0-3 and 4-7
+//             are committed and released separately, so a tile's first groups
+//             overlap the previous tile's drain;
+//   warps 2-9 drain + update: tcgen05.ld (lane = row, 16 columns per warp),
+//             the exact recombination, T - p 2^(e_i + f_j) in place in the
+//             staged tile, one TMA store per tile (one store in flight).
+// Even m only: TMA applies the box's row bound at 16-byte granularity.
 #include <cuda.h>
 
 #include <climits>
