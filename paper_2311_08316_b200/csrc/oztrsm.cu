@@ -320,6 +320,12 @@ CQ_DEVI uint32_t elect_one() {
         : "+r"(pred));
     return pred;
 }
+CQ_DEVI double lds_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a) : "memory");
+    return v;
+}
+CQ_DEVI void sts_f64(uint32_t a, double v) { asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(a), "d"(v) : "memory"); }
 CQ_DEVI void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
@@ -468,7 +474,6 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
                     if (tc) mb_wait_warp(lo_free, (tc - 1u) & 1u);
                     tc_fence_after();
                     if (elect_one()) {
-                        if (P.dbg != 2)
 #pragma unroll
                             for (int g = 0; g < 4; ++g)
 #pragma unroll
@@ -488,7 +493,6 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
                     if (tc) mb_wait_warp(hi_free, (tc - 1u) & 1u);
                     tc_fence_after();
                     if (elect_one()) {
-                        if (P.dbg != 2)
 #pragma unroll
                             for (int g = 4; g < kGroups; ++g)
 #pragma unroll
@@ -525,6 +529,13 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
                 const int64_t j0 = (int64_t)nt * kBN + half * 16;
                 const int64_t rem = P.ncols - j0;
                 const int nc = rem >= 16 ? 16 : (rem > 0 ? (int)rem : 0);
+                // this tile's scales 2^(e_i + f_j - 12), loaded before the wait
+                // (the scale array is padded to whole N tiles)
+                double wsc[16];
+#pragma unroll
+                for (int c = 0; c < 16; ++c) wsc[c] = __ldg(P.cscale + j0 + c);
+#pragma unroll
+                for (int c = 0; c < 16; ++c) wsc[c] *= rs;
                 double hs[16];
                 mb_wait(lo_full, tc & 1u);
                 tc_fence_after();
@@ -567,14 +578,19 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
                 // result written back in place and stored by one TMA store
                 mb_wait(c_full(cs), cuse & 1u);
                 {
-                    double *ct = reinterpret_cast<double *>(smem + kSmemC + cs * kTileCBytes) + half * 16 * kBM + rloc;
+                    // shared-memory addresses explicitly (no aliasing with the
+                    // global operands): 16 loads, 16 FMAs, 16 stores
+                    const uint32_t ct = sC + cs * kTileCBytes + (uint32_t)((half * 16 * kBM + rloc) * 8);
                     const bool tail = P.cols_in && valid && (P.m & 1) && row == P.m - 1;  // not in the bulk copies
+                    double t[16];
 #pragma unroll
-                    for (int c = 0; c < 16; ++c)
-                        if (c < nc) {
-                            const double t = tail ? P.cin[__ldg(P.cols_in + j0 + c) * P.ldin + row] : ct[c * kBM];
-                            ct[c * kBM] = fma(-hs[c], rs * __ldg(P.cscale + j0 + c), t);
-                        }
+                    for (int c = 0; c < 16; ++c) t[c] = lds_f64(ct + (uint32_t)(c * kBM * 8));
+                    if (tail)
+#pragma unroll
+                        for (int c = 0; c < 16; ++c)
+                            if (c < nc) t[c] = P.cin[__ldg(P.cols_in + j0 + c) * P.ldin + row];
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) sts_f64(ct + (uint32_t)(c * kBM * 8), fma(-hs[c], wsc[c], t[c]));
                 }
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 asm volatile("bar.sync 1, %0;\n" ::"n"(kEpiWarps * 32) : "memory");
@@ -736,7 +752,6 @@ int trsm_right_oz(int64_t m, int64_t k, const double *b, int64_t ldb, const int6
         }
         P.cout = x + b1 * ldx;
         P.ldout = ldx;
-        P.dbg = getenv("CQRRPT_OZ_DBG") ? atoi(getenv("CQRRPT_OZ_DBG")) : 0;
         CQ_TRY(launch_update(P, st));
     }
     return 0;
