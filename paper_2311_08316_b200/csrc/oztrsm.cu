@@ -349,7 +349,6 @@ struct UpdArgs {
     const int64_t *cols_in;  // nullptr: column j of cin is j
     double *cout;
     int64_t ldout;
-    int dbg;  // experiments: 1 = epilogue releases without reading, 2 = no MMAs
 };
 
 __global__ void __launch_bounds__(kUpdThreads, 1)
