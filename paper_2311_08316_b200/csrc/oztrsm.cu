@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
         }
         for (int s = 0; s < kCStages; ++s) {
             mb_init(c_full(s), 1);
-            mb_init(c_empty(s), 1);
+            mb_init(c_empty(s), 2);  // one store per 16-column half
         }
         mb_init(lo_full, 1);
         mb_init(hi_full, 1);
@@ -592,11 +592,13 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
                     for (int c = 0; c < 16; ++c) sts_f64(ct + (uint32_t)(c * kBM * 8), fma(-hs[c], wsc[c], t[c]));
                 }
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                asm volatile("bar.sync 1, %0;\n" ::"n"(kEpiWarps * 32) : "memory");
-                if (warp == 2 && lane == 0) {
-                    // one store in flight: once the previous tile's store has
-                    // read its stage, that stage goes back to the producer
-                    tma_store_2d(&tm_out, (int)((int64_t)p * kBM), (int)(j0 - half * 16), sC + cs * kTileCBytes);
+                // each 16-column half (its 4 warps) is stored on its own: a
+                // named barrier per half, one TMA store (box 128 x 16) each
+                asm volatile("bar.sync %0, %1;\n" ::"r"(1 + half), "n"(kEpiWarps * 16) : "memory");
+                if ((warp & 3) == 2 && lane == 0) {
+                    // one store in flight per half: once the previous tile's
+                    // store has read its stage, that stage goes back to the producer
+                    tma_store_2d(&tm_out, (int)((int64_t)p * kBM), (int)j0, sC + cs * kTileCBytes + (uint32_t)(half * 16 * kBM * 8));
                     asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
                     asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
                     if (tc) mb_arrive(c_empty(cs == 0 ? kCStages - 1 : cs - 1));
@@ -605,7 +607,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
             }
         }
     }
-    if (warp == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+    if (warp >= 2 && (warp & 3) == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -634,12 +636,12 @@ EncodeTiledFn encode_fn() {
 }
 
 // column-major m x n FP64 matrix, 128 x 32 boxes
-int make_map(CUtensorMap *map, const double *base, int64_t m, int64_t n, int64_t ld) {
+int make_map(CUtensorMap *map, const double *base, int64_t m, int64_t n, int64_t ld, uint32_t box_cols = kBN) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return fail_internal("cuTensorMapEncodeTiled unavailable");
     const cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)n};
     const cuuint64_t strides[1] = {(cuuint64_t)ld * 8u};
-    const cuuint32_t box[2] = {kBM, kBN};
+    const cuuint32_t box[2] = {kBM, box_cols};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -659,7 +661,7 @@ int launch_update(const UpdArgs &P, cudaStream_t st) {
     alignas(64) CUtensorMap tm_in, tm_out;
     std::memset(&tm_in, 0, sizeof(tm_in));
     if (!P.cols_in) CQ_TRY(make_map(&tm_in, P.cin, P.m, P.ncols, P.ldin));
-    CQ_TRY(make_map(&tm_out, P.cout, P.m, P.ncols, P.ldout));
+    CQ_TRY(make_map(&tm_out, P.cout, P.m, P.ncols, P.ldout, kBN / 2));
     const int grid = std::min(P.npanels, num_sms());
     oz_update_kernel<<<grid, kUpdThreads, kUpdSmem, st>>>(tm_in, tm_out, P);
     note_launch();
