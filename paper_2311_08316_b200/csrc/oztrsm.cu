@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
         }
         for (int s = 0; s < kCStages; ++s) {
             mb_init(c_full(s), 1);
-            mb_init(c_empty(s), 2);  // one store per 16-column half
+            mb_init(c_empty(s), kEpiWarps);  // one store per epilogue warp
         }
         mb_init(lo_full, 1);
         mb_init(hi_full, 1);
@@ -426,18 +426,13 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
                     // the tile's right-hand side: one bulk copy per column
                     const int64_t j0 = (int64_t)nt * kBN;
                     if (cfill) mb_wait(c_empty(cs), (cfill - 1u) & 1u);
-                    if (!P.cols_in) {  // one 128 x 32 box (rows / columns past the ends: zeros)
+                    if (!P.cols_in) {  // 8 boxes of 32 rows x 16 columns, one per epilogue warp (zeros past the ends)
                         mb_expect_tx(c_full(cs), kTileCBytes);
-                        tma_load_2d(sC + cs * kTileCBytes, &tm_in, (int)r0, (int)j0, c_full(cs));
-                    } else {  // gathered columns: one bulk copy per column
-                        const int64_t rows = P.m - r0 < kBM ? P.m - r0 : kBM;
-                        const uint32_t cbytes = (uint32_t)(rows & ~1ll) * 8u;  // 16-byte multiple
-                        const int ncj = (int)(P.ncols - j0 < kBN ? P.ncols - j0 : kBN);
-                        mb_expect_tx(c_full(cs), cbytes * (uint32_t)ncj);
-                        if (cbytes)
-                            for (int c = 0; c < ncj; ++c)
-                                bulk_g2s(sC + cs * kTileCBytes + c * (kBM * 8),
-                                         P.cin + __ldg(P.cols_in + j0 + c) * P.ldin + r0, cbytes, c_full(cs));
+                        for (int sb = 0; sb < 8; ++sb)
+                            tma_load_2d(sC + cs * kTileCBytes + (uint32_t)sb * 4096u, &tm_in, (int)(r0 + (sb & 3) * 32),
+                                        (int)(j0 + (sb >> 2) * 16), c_full(cs));
+                    } else {  // gathered columns: the epilogue reads them from global memory
+                        mb_arrive(c_full(cs));
                     }
                     if (++cs == kCStages) cs = 0, ++cfill;
                 }
@@ -577,28 +572,30 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
                 // result written back in place and stored by one TMA store
                 mb_wait(c_full(cs), cuse & 1u);
                 {
-                    // shared-memory addresses explicitly (no aliasing with the
-                    // global operands): 16 loads, 16 FMAs, 16 stores
-                    const uint32_t ct = sC + cs * kTileCBytes + (uint32_t)((half * 16 * kBM + rloc) * 8);
-                    const bool tail = P.cols_in && valid && (P.m & 1) && row == P.m - 1;  // not in the bulk copies
+                    // this warp's 32 x 16 box of the staged tile (column c at
+                    // c * 256 bytes), shared-memory addresses explicitly: 16
+                    // loads, 16 FMAs, 16 stores; the gathered first step reads
+                    // its right-hand side from global memory instead
+                    const uint32_t ct = sC + cs * kTileCBytes + (uint32_t)((half * 4 + quad) * 4096 + lane * 8);
                     double t[16];
+                    if (!P.cols_in) {
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) t[c] = lds_f64(ct + (uint32_t)(c * kBM * 8));
-                    if (tail)
+                        for (int c = 0; c < 16; ++c) t[c] = lds_f64(ct + (uint32_t)(c * 256));
+                    } else {
 #pragma unroll
                         for (int c = 0; c < 16; ++c)
-                            if (c < nc) t[c] = P.cin[__ldg(P.cols_in + j0 + c) * P.ldin + row];
+                            t[c] = (valid && c < nc) ? P.cin[__ldg(P.cols_in + j0 + c) * P.ldin + row] : 0.0;
+                    }
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) sts_f64(ct + (uint32_t)(c * kBM * 8), fma(-hs[c], wsc[c], t[c]));
+                    for (int c = 0; c < 16; ++c) sts_f64(ct + (uint32_t)(c * 256), fma(-hs[c], wsc[c], t[c]));
                 }
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                // each 16-column half (its 4 warps) is stored on its own: a
-                // named barrier per half, one TMA store (box 128 x 16) each
-                asm volatile("bar.sync %0, %1;\n" ::"r"(1 + half), "n"(kEpiWarps * 16) : "memory");
-                if ((warp & 3) == 2 && lane == 0) {
-                    // one store in flight per half: once the previous tile's
-                    // store has read its stage, that stage goes back to the producer
-                    tma_store_2d(&tm_out, (int)((int64_t)p * kBM), (int)j0, sC + cs * kTileCBytes + (uint32_t)(half * 16 * kBM * 8));
+                __syncwarp();
+                if (lane == 0) {
+                    // one store in flight per warp: once the previous tile's
+                    // store has read its box, that stage gets this warp's release
+                    tma_store_2d(&tm_out, (int)((int64_t)p * kBM + quad * 32), (int)j0,
+                                 sC + cs * kTileCBytes + (uint32_t)((half * 4 + quad) * 4096));
                     asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
                     asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
                     if (tc) mb_arrive(c_empty(cs == 0 ? kCStages - 1 : cs - 1));
@@ -607,7 +604,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
             }
         }
     }
-    if (warp >= 2 && (warp & 3) == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+    if (warp >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -641,7 +638,7 @@ int make_map(CUtensorMap *map, const double *base, int64_t m, int64_t n, int64_t
     if (!fn) return fail_internal("cuTensorMapEncodeTiled unavailable");
     const cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)n};
     const cuuint64_t strides[1] = {(cuuint64_t)ld * 8u};
-    const cuuint32_t box[2] = {kBM, box_cols};
+    const cuuint32_t box[2] = {32, box_cols};  // one epilogue warp's rows
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -660,8 +657,8 @@ int launch_update(const UpdArgs &P, cudaStream_t st) {
     }
     alignas(64) CUtensorMap tm_in, tm_out;
     std::memset(&tm_in, 0, sizeof(tm_in));
-    if (!P.cols_in) CQ_TRY(make_map(&tm_in, P.cin, P.m, P.ncols, P.ldin));
-    CQ_TRY(make_map(&tm_out, P.cout, P.m, P.ncols, P.ldout, kBN / 2));
+    if (!P.cols_in) CQ_TRY(make_map(&tm_in, P.cin, P.m, P.ncols, P.ldin, kBN / 2));
+    CQ_TRY(make_map(&tm_out, P.cout, P.m, P.ncols, P.ldout, kBN / 2));  // 32 x 16 boxes
     const int grid = std::min(P.npanels, num_sms());
     oz_update_kernel<<<grid, kUpdThreads, kUpdSmem, st>>>(tm_in, tm_out, P);
     note_launch();
