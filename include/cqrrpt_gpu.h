@@ -231,7 +231,7 @@ int cqrrpt_gpu_trsm_right(int64_t m, int64_t k, const double *B, int64_t ldb, co
  * m x k solve with even m, 16-byte aligned operands and even leading
  * dimensions (else always DMMA): 0 =
  * DMMA (FP64 tensor cores), 1 = the exact INT8 tensor-core emulation
- * (tcgen05 kind::i8; from m >= 1048576 and k >= 1536, or CQRRPT_GPU_TRSM=oz |
+ * (tcgen05 kind::i8; from m >= 131072 and k >= 768, or CQRRPT_GPU_TRSM=oz |
  * dmma). Diagnostic; no device work. */
 int cqrrpt_gpu_trsm_engine(int64_t m, int64_t k);
 

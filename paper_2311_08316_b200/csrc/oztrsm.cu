@@ -668,15 +668,16 @@ int launch_update(const UpdArgs &P, cudaStream_t st) {
 }  // namespace
 
 // Engine choice for trsm_right: CQRRPT_GPU_TRSM=oz | dmma forces one; by
-// default the INT8 engine from m >= 1048576 rows and k >= 1536 columns, where
-// it measured faster than the DMMA engine (m = 1M, k = 2048: 123 vs 131 ms;
-// C4 precondition 462 vs 513 ms, C5-2048 490 vs 521 ms); at C5-1024 (k = 1024)
-// it was 3% slower (139.5 vs 135.3 ms).
+// default the INT8 engine from m >= 131072 rows and k >= 768 columns, where it
+// measured faster than the DMMA engine (tools/oz_probe.py, one B200: 131072 x
+// 1024 4.37 vs 4.53 ms, 524288 x 768 9.89 vs 10.10, 262144 x 2048 26.3 vs
+// 33.4, 2097152 x 1024 63.4 vs 68.0, 1048576 x 2048 107 vs 131); at k = 512
+// it was slower (1048576 x 512: 10.3 vs 9.5 ms).
 bool trsm_use_ozaki(int64_t m, int64_t k) {
     const char *env = getenv("CQRRPT_GPU_TRSM");
     if (env && env[0] == 'd') return false;
     if (env && env[0] == 'o') return k > 0 && m > 0;
-    return m >= 1048576 && k >= 1536;
+    return m >= 131072 && k >= 768;
 }
 
 int trsm_right_oz(int64_t m, int64_t k, const double *b, int64_t ldb, const int64_t *cols, const double *u,
