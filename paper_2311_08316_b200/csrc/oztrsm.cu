@@ -386,8 +386,8 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
         }
         mb_init(lo_full, 1);
         mb_init(hi_full, 1);
-        mb_init(lo_free, kEpiWarps * 32);
-        mb_init(hi_free, kEpiWarps * 32);
+        mb_init(lo_free, kEpiWarps);  // one arrival per drain warp
+        mb_init(hi_free, kEpiWarps);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == 1) {
@@ -550,7 +550,8 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
                     }
                 }
                 tc_fence_before();
-                mb_arrive(lo_free);
+                __syncwarp();
+                if (lane == 0) mb_arrive(lo_free);
                 mb_wait(hi_full, tc & 1u);
                 tc_fence_after();
 #pragma unroll
@@ -567,7 +568,8 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
                     }
                 }
                 tc_fence_before();
-                mb_arrive(hi_free);
+                __syncwarp();
+                if (lane == 0) mb_arrive(hi_free);
                 // out = T - prod 2^(e_i + f_j): T from the staged tile, the
                 // result written back in place and stored by one TMA store
                 mb_wait(c_full(cs), cuse & 1u);
