@@ -88,3 +88,19 @@ def test_no_cpu_fallback_without_device():
     import numpy as np
     with pytest.raises(RuntimeError):
         pkg.cqrrpt(np.ones((10, 3)), pkg.CqrrptConfig())
+
+
+def test_trsm_engine_choice(monkeypatch):
+    """cqrrpt_gpu_trsm_engine (a host-only query): the INT8 tensor-core engine
+    from m >= 131072 rows and k >= 768 columns, DMMA below; CQRRPT_GPU_TRSM
+    forces either."""
+    from paper_2311_08316_b200 import kernels
+    monkeypatch.delenv("CQRRPT_GPU_TRSM", raising=False)
+    assert kernels.trsm_engine(4194304, 2048) == "int8"  # C5-2048
+    assert kernels.trsm_engine(131072, 1024) == "int8"   # C2
+    assert kernels.trsm_engine(4194304, 512) == "dmma"   # k = 512: DMMA measured faster
+    assert kernels.trsm_engine(16384, 256) == "dmma"     # C1
+    monkeypatch.setenv("CQRRPT_GPU_TRSM", "dmma")
+    assert kernels.trsm_engine(4194304, 2048) == "dmma"
+    monkeypatch.setenv("CQRRPT_GPU_TRSM", "oz")
+    assert kernels.trsm_engine(1000, 300) == "int8"
