@@ -25,23 +25,32 @@
 // the FP64 GEMM's normwise bound (the parity tests compare with the DMMA
 // engine and the oracle).
 //
-// oz_update_kernel: persistent, one CTA per SM (212 KB shared memory, all 512
+// oz_update_kernel: persistent, one CTA per SM (216 KB shared memory, all 512
 // TMEM columns):
 //   warp 0    producer (TMA engine): the panel's 7 digit slices (128 rows x 128
 //             K each, pre-tiled in the UMMA canonical K-major layout) through a
-//             2-slice ring, a 3-stage ring of U's N tiles (32 x 128 x 7 = 28
-//             KB), and per tile the right-hand side (one 128 x 32 tensor-map
-//             box; per-column bulk copies for the gathered first step);
+//             2-slice ring, a 2-stage ring of U's N tiles (32 x 128 x 7 = 28
+//             KB), and per tile the right-hand side into a 4-stage ring (eight
+//             32 x 16 tensor-map boxes, one per drain warp; the gathered first
+//             step is read from global memory by the drain warps instead);
 //   warp 1    TMEM allocator + MMA issuer (one elected thread, operands in
 //             uniform registers): tcgen05.cp of the A slices into TMEM columns
-//             0..223 once per panel, then per N tile 34 digit pairs x 4 K-steps
-//             of tcgen05.mma M128 N32 K32 (A from TMEM, B from shared memory)
-//             into 8 group accumulators (columns 256..511); groups 0-3 and 4-7
-//             are committed and released separately, so a tile's first groups
-//             overlap the previous tile's drain;
-//   warps 2-9 drain + update: tcgen05.ld (lane = row, 16 columns per warp),
-//             the exact recombination, T - p 2^(e_i + f_j) in place in the
-//             staged tile, one TMA store per tile (one store in flight).
+//             0..223 once per panel, then per N tile and K-step ONE
+//             tcgen05.mma per digit slice s of X covering all its partner
+//             slices t of U at once: U's slices are consecutive 32-row blocks
+//             of the canonical layout, so B = slices t0.. with N = 32 * count
+//             and D = group s + t0 lands every pair (s, t) in group s + t.
+//             44 MMAs of N = 32..128 per tile instead of 136 of N = 32: the
+//             128 x 32-byte A operand is read once per slice and K-step, not
+//             once per pair (at N = 32 the A read, not the math, set the
+//             rate). Groups 0-3 and 4-7 are committed and released
+//             separately, so a tile's first groups overlap the previous
+//             tile's drain;
+//   warps 2-17 drain + update, two sets of 8 taking alternate tiles (the
+//             second set drains tile t + 1 while the first still updates and
+//             stores tile t): tcgen05.ld (lane = row, 16 columns per warp), the
+//             exact recombination, T - p 2^(e_i + f_j) in place in the staged
+//             tile, the warp's own TMA store of its 32 x 16 box.
 // Even m only: TMA applies the box's row bound at 16-byte granularity.
 #include <cuda.h>
 
@@ -65,14 +74,14 @@ constexpr int kSliceA = kBM * kW;          // 16384 B per digit slice of a panel
 constexpr int kSliceB = kBN * kW;          // 4096 B per digit slice of an N tile
 constexpr int kPanelBytes = kDig * kSliceA;  // 114688
 constexpr int kTileBBytes = kDig * kSliceB;  // 28672
-constexpr int kBStages = 3;
-constexpr int kEpiWarps = 8;               // 2 per TMEM lane quadrant, 16 columns each
-constexpr int kUpdThreads = 64 + 32 * kEpiWarps;  // producer, MMA, epilogue
+constexpr int kBStages = 2;
+constexpr int kEpiWarps = 8;               // per drain set: 2 per TMEM lane quadrant, 16 columns each
+constexpr int kMaxSets = 2;                // drain sets (alternating tiles)
 constexpr int kTmemCols = 512;             // A digit slices (7 x 32) | accumulators (8 x 32)
 constexpr uint32_t kTmemAcc = 256;         // first accumulator column
 
 constexpr int kAStages = 2;                // digit slices staged on their way to TMEM
-constexpr int kCStages = 3;                // right-hand-side tiles (128 x 32 FP64)
+constexpr int kCStages = 4;                // right-hand-side tiles (128 x 32 FP64)
 constexpr uint32_t kTileCBytes = kBM * kBN * 8;  // 32768, column c at c * 1024
 constexpr uint32_t kSmemA = 0;
 constexpr uint32_t kSmemB = kAStages * kSliceA;
@@ -271,9 +280,10 @@ CQ_DEVI void tc_commit(uint32_t bar) {  // by the MMA-issuing thread
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
                  : "memory");
 }
-// instruction descriptor: s32 accumulate, s8 x s8, both K-major, N = 32, M = 128
-constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
-                            ((uint32_t)(kBM >> 4) << 24);
+// instruction descriptor: s32 accumulate, s8 x s8, both K-major, N columns, M = 128
+__host__ __device__ constexpr uint32_t idesc_n(int n) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
+}
 
 // Shared-memory matrix descriptor (no swizzle, K-major core matrices): low
 // word = start address >> 4 | (LBO = 128) >> 4 << 16, high word = (SBO =
@@ -351,7 +361,8 @@ struct UpdArgs {
     int64_t ldout;
 };
 
-__global__ void __launch_bounds__(kUpdThreads, 1)
+template <int kSets>
+__global__ void __launch_bounds__(64 + 32 * kEpiWarps * kSets, 1)
     oz_update_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out, UpdArgs P) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -367,8 +378,11 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
     auto b_empty = [&](int s) { return bar + 8u * (2 * kAStages + kBStages + s); };
     auto c_full = [&](int s) { return bar + 8u * (2 * kAStages + 2 * kBStages + s); };
     auto c_empty = [&](int s) { return bar + 8u * (2 * kAStages + 2 * kBStages + kCStages + s); };
-    const uint32_t lo_full = bar + 8u * (2 * (kAStages + kBStages + kCStages));
-    const uint32_t hi_full = lo_full + 8, lo_free = lo_full + 16, hi_free = lo_full + 24;
+    // lo_full / hi_full: one barrier per drain set (a set waits for every
+    // kSets-th tile, so its waits must not see the other sets' phases)
+    const uint32_t lo_full0 = bar + 8u * (2 * (kAStages + kBStages + kCStages));
+    const uint32_t hi_full0 = lo_full0 + 8u * kMaxSets;
+    const uint32_t lo_free = hi_full0 + 8u * kMaxSets, hi_free = lo_free + 8;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + kSmemBar + 248);
 
     if (tid == 0) {
@@ -384,8 +398,10 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
             mb_init(c_full(s), 1);
             mb_init(c_empty(s), kEpiWarps);  // one store per epilogue warp
         }
-        mb_init(lo_full, 1);
-        mb_init(hi_full, 1);
+        for (int s = 0; s < kMaxSets; ++s) {
+            mb_init(lo_full0 + 8u * s, 1);
+            mb_init(hi_full0 + 8u * s, 1);
+        }
         mb_init(lo_free, kEpiWarps);  // one arrival per drain warp
         mb_init(hi_free, kEpiWarps);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -468,142 +484,153 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
                     if (tc) mb_wait_warp(lo_free, (tc - 1u) & 1u);
                     tc_fence_after();
                     if (elect_one()) {
-#pragma unroll
-                            for (int g = 0; g < 4; ++g)
-#pragma unroll
-                                for (int s = 0; s < kDig; ++s) {
-                                    const int t = g - s;
-                                    if (t < 0 || t >= kDig) continue;
-                                    if (s == 0)
-                                        tc_mma_i8_k128<kIdesc, true>(d0 + g * kBN, tmem + s * 32,
-                                                                     blo0 + t * (kSliceB >> 4));
-                                    else
-                                        tc_mma_i8_k128<kIdesc, false>(d0 + g * kBN, tmem + s * 32,
-                                                                      blo0 + t * (kSliceB >> 4));
-                                }
-                        tc_commit(lo_full);
+                        // Digit slice s of X against slices t = 0 .. 3 - s of U in ONE
+                        // MMA per K-step: U's slices are consecutive 32-row blocks of
+                        // the canonical layout, so N = 32 (4 - s) columns starting at
+                        // group s are the products for groups s .. 3 (the A operand is
+                        // read once per slice and K-step, not once per digit pair)
+                        tc_mma_i8_k128<idesc_n(128), true>(d0 + 0 * kBN, tmem + 0 * 32, blo0);
+                        tc_mma_i8_k128<idesc_n(96), false>(d0 + 1 * kBN, tmem + 1 * 32, blo0);
+                        tc_mma_i8_k128<idesc_n(64), false>(d0 + 2 * kBN, tmem + 2 * 32, blo0);
+                        tc_mma_i8_k128<idesc_n(32), false>(d0 + 3 * kBN, tmem + 3 * 32, blo0);
+                        tc_commit(lo_full0 + 8u * (tc % kSets));
                     }
                     __syncwarp();
                     if (tc) mb_wait_warp(hi_free, (tc - 1u) & 1u);
                     tc_fence_after();
                     if (elect_one()) {
-#pragma unroll
-                            for (int g = 4; g < kGroups; ++g)
-#pragma unroll
-                                for (int s = 0; s < kDig; ++s) {
-                                    const int t = g - s;
-                                    if (t < 0 || t >= kDig) continue;
-                                    if (s == (g > kDig - 1 ? g - (kDig - 1) : 0))
-                                        tc_mma_i8_k128<kIdesc, true>(d0 + g * kBN, tmem + s * 32,
-                                                                     blo0 + t * (kSliceB >> 4));
-                                    else
-                                        tc_mma_i8_k128<kIdesc, false>(d0 + g * kBN, tmem + s * 32,
-                                                                      blo0 + t * (kSliceB >> 4));
-                                }
+                        // groups 4-7: slice s against t = max(4 - s, 0) .. min(7 - s, 6),
+                        // landing in groups max(4, s) ..; slice 1 goes first because it
+                        // covers all four groups (its first K-step overwrites them)
+                        constexpr uint32_t sl = kSliceB >> 4;
+                        tc_mma_i8_k128<idesc_n(128), true>(d0 + 4 * kBN, tmem + 1 * 32, blo0 + 3 * sl);
+                        tc_mma_i8_k128<idesc_n(96), false>(d0 + 4 * kBN, tmem + 0 * 32, blo0 + 4 * sl);
+                        tc_mma_i8_k128<idesc_n(128), false>(d0 + 4 * kBN, tmem + 2 * 32, blo0 + 2 * sl);
+                        tc_mma_i8_k128<idesc_n(128), false>(d0 + 4 * kBN, tmem + 3 * 32, blo0 + 1 * sl);
+                        tc_mma_i8_k128<idesc_n(128), false>(d0 + 4 * kBN, tmem + 4 * 32, blo0);
+                        tc_mma_i8_k128<idesc_n(96), false>(d0 + 5 * kBN, tmem + 5 * 32, blo0);
+                        tc_mma_i8_k128<idesc_n(64), false>(d0 + 6 * kBN, tmem + 6 * 32, blo0);
                         tc_commit(b_empty(bs));
-                        tc_commit(hi_full);
+                        tc_commit(hi_full0 + 8u * (tc % kSets));
                     }
                     __syncwarp();
                     if (++bs == kBStages) bs = 0, ++buse;
                 }
             }
         }
-    } else {  // ---------------- epilogue warps: lane quadrant warp % 4, 16 columns each
-        const int quad = warp & 3, half = (warp - 2) >> 2;
+    } else {  // ---------------- drain warps: set (warp - 2) / 8 takes tiles set, set + kSets, ...;
+              // lane quadrant warp % 4, 16 columns each
+        const int quad = warp & 3, half = ((warp - 2) >> 2) & 1, set = (warp - 2) >> 3;
         const int rloc = quad * 32 + lane;
         const uint32_t taddr0 = tmem + kTmemAcc + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * 16);
-        uint32_t tc = 0;
-        int cs = 0;
-        uint32_t cuse = 0;
-        for (int p = blockIdx.x; p < P.npanels; p += gridDim.x) {
-            const int64_t row = (int64_t)p * kBM + rloc;
-            const bool valid = row < P.m;
-            const double rs = P.rscale[row];  // rscale covers the padded panel
-            for (int nt = 0; nt < P.ntn; ++nt, ++tc) {
-                const int64_t j0 = (int64_t)nt * kBN + half * 16;
-                const int64_t rem = P.ncols - j0;
-                const int nc = rem >= 16 ? 16 : (rem > 0 ? (int)rem : 0);
-                // this tile's scales 2^(e_i + f_j - 12), loaded before the wait
-                // (the scale array is padded to whole N tiles)
-                double wsc[16];
+        const uint32_t lo_full = lo_full0 + 8u * set, hi_full = hi_full0 + 8u * set;
+        // tiles of this CTA in issue order: panel blockIdx.x + pcur * gridDim.x, N tile nt
+        // (the host bounds npanels * ntn / gridDim.x below 2^31)
+        const int npan = P.npanels > (int)blockIdx.x ? (P.npanels - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+        const int ntiles = npan * P.ntn;
+        int pi = -1;  // panel index (of this CTA) whose row scale is loaded
+        double rs = 0.0;
+        int64_t row = 0;
+        bool valid = false;
+        for (int tc = set; tc < ntiles; tc += kSets) {
+            const int pcur = tc / P.ntn;
+            const int nt = tc - pcur * P.ntn;
+            const int64_t p = (int64_t)blockIdx.x + (int64_t)pcur * gridDim.x;
+            if (pcur != pi) {
+                pi = pcur;
+                row = p * kBM + rloc;
+                valid = row < P.m;
+                rs = P.rscale[row];  // rscale covers the padded panel
+            }
+            const uint32_t par = (uint32_t)(tc / kSets) & 1u;
+            const int cs = (int)(tc % kCStages);
+            const uint32_t cpar = (uint32_t)(tc / kCStages) & 1u;
+            const int64_t j0 = (int64_t)nt * kBN + half * 16;
+            const int64_t rem = P.ncols - j0;
+            const int nc = rem >= 16 ? 16 : (rem > 0 ? (int)rem : 0);
+            double hs[16];
+            mb_wait(lo_full, par);
+            tc_fence_after();
+            // groups 0-3 -> hi (exact, |hi| < 2^50), then 4-7 -> lo;
+            // converted with the scales 2^-24 / 2^-56 folded into the magic
+            // constants and added (one rounding)
 #pragma unroll
-                for (int c = 0; c < 16; ++c) wsc[c] = __ldg(P.cscale + j0 + c);
+            for (int h = 0; h < 16; h += 8) {
+                uint32_t v[4][8];
 #pragma unroll
-                for (int c = 0; c < 16; ++c) wsc[c] *= rs;
-                double hs[16];
-                mb_wait(lo_full, tc & 1u);
-                tc_fence_after();
-                // groups 0-3 -> hi (exact, |hi| < 2^50), then 4-7 -> lo;
-                // converted with the scales 2^-24 / 2^-56 folded into the magic
-                // constants and added (one rounding)
+                for (int g = 0; g < 4; ++g) tmem_ld8(taddr0 + (uint32_t)(g * kBN + h), v[g]);
+                tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const long long hi = (long long)(int)v[0][c] * 16777216ll + (long long)(int)v[1][c] * 65536ll +
+                                         (long long)(int)v[2][c] * 256ll + (long long)(int)v[3][c];
+                    hs[h + c] = __longlong_as_double(hi + 0x41B8000000000000ll) - 402653184.0;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mb_arrive(lo_free);
+            mb_wait(hi_full, par);
+            tc_fence_after();
+#pragma unroll
+            for (int h = 0; h < 16; h += 8) {
+                uint32_t v[4][8];
+#pragma unroll
+                for (int g = 0; g < 4; ++g) tmem_ld8(taddr0 + (uint32_t)((g + 4) * kBN + h), v[g]);
+                tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const long long lo = (long long)(int)v[0][c] * 16777216ll + (long long)(int)v[1][c] * 65536ll +
+                                         (long long)(int)v[2][c] * 256ll + (long long)(int)v[3][c];
+                    hs[h + c] += __longlong_as_double(lo + 0x3FB8000000000000ll) - 0.09375;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mb_arrive(hi_free);
+            // out = T - prod 2^(e_i + f_j): T from the staged tile, the result
+            // written back in place and stored by this warp's own TMA store.
+            // The accumulators are released by now, so this part overlaps the
+            // other set's drain of the next tile.
+            mb_wait(c_full(cs), cpar);
+            {
+                // this warp's 32 x 16 box of the staged tile (column c at
+                // c * 256 bytes), shared-memory addresses explicitly, 8 columns
+                // at a time: loads, FMAs with the scale 2^(e_i + f_j - 12)
+                // (the scale array is padded to whole N tiles), stores; the
+                // gathered first step reads its right-hand side from global
+                // memory instead
+                const uint32_t ct = sC + cs * kTileCBytes + (uint32_t)((half * 4 + quad) * 4096 + lane * 8);
 #pragma unroll
                 for (int h = 0; h < 16; h += 8) {
-                    uint32_t v[4][8];
+                    double wsc[8], t[8];
 #pragma unroll
-                    for (int g = 0; g < 4; ++g) tmem_ld8(taddr0 + (uint32_t)(g * kBN + h), v[g]);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const long long hi = (long long)(int)v[0][c] * 16777216ll + (long long)(int)v[1][c] * 65536ll +
-                                             (long long)(int)v[2][c] * 256ll + (long long)(int)v[3][c];
-                        hs[h + c] = __longlong_as_double(hi + 0x41B8000000000000ll) - 402653184.0;
-                    }
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mb_arrive(lo_free);
-                mb_wait(hi_full, tc & 1u);
-                tc_fence_after();
-#pragma unroll
-                for (int h = 0; h < 16; h += 8) {
-                    uint32_t v[4][8];
-#pragma unroll
-                    for (int g = 0; g < 4; ++g) tmem_ld8(taddr0 + (uint32_t)((g + 4) * kBN + h), v[g]);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const long long lo = (long long)(int)v[0][c] * 16777216ll + (long long)(int)v[1][c] * 65536ll +
-                                             (long long)(int)v[2][c] * 256ll + (long long)(int)v[3][c];
-                        hs[h + c] += __longlong_as_double(lo + 0x3FB8000000000000ll) - 0.09375;
-                    }
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mb_arrive(hi_free);
-                // out = T - prod 2^(e_i + f_j): T from the staged tile, the
-                // result written back in place and stored by one TMA store
-                mb_wait(c_full(cs), cuse & 1u);
-                {
-                    // this warp's 32 x 16 box of the staged tile (column c at
-                    // c * 256 bytes), shared-memory addresses explicitly: 16
-                    // loads, 16 FMAs, 16 stores; the gathered first step reads
-                    // its right-hand side from global memory instead
-                    const uint32_t ct = sC + cs * kTileCBytes + (uint32_t)((half * 4 + quad) * 4096 + lane * 8);
-                    double t[16];
+                    for (int c = 0; c < 8; ++c) wsc[c] = __ldg(P.cscale + j0 + h + c);
                     if (!P.cols_in) {
 #pragma unroll
-                        for (int c = 0; c < 16; ++c) t[c] = lds_f64(ct + (uint32_t)(c * 256));
+                        for (int c = 0; c < 8; ++c) t[c] = lds_f64(ct + (uint32_t)((h + c) * 256));
                     } else {
 #pragma unroll
-                        for (int c = 0; c < 16; ++c)
-                            t[c] = (valid && c < nc) ? P.cin[__ldg(P.cols_in + j0 + c) * P.ldin + row] : 0.0;
+                        for (int c = 0; c < 8; ++c)
+                            t[c] = (valid && h + c < nc) ? P.cin[__ldg(P.cols_in + j0 + h + c) * P.ldin + row] : 0.0;
                     }
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) sts_f64(ct + (uint32_t)(c * 256), fma(-hs[c], wsc[c], t[c]));
+                    for (int c = 0; c < 8; ++c)
+                        sts_f64(ct + (uint32_t)((h + c) * 256), fma(-hs[h + c], wsc[c] * rs, t[c]));
                 }
-                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                __syncwarp();
-                if (lane == 0) {
-                    // one store in flight per warp: once the previous tile's
-                    // store has read its box, that stage gets this warp's release
-                    tma_store_2d(&tm_out, (int)((int64_t)p * kBM + quad * 32), (int)j0,
-                                 sC + cs * kTileCBytes + (uint32_t)((half * 4 + quad) * 4096));
-                    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-                    asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
-                    if (tc) mb_arrive(c_empty(cs == 0 ? kCStages - 1 : cs - 1));
-                }
-                if (++cs == kCStages) cs = 0, ++cuse;
             }
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                // the stage gets this warp's release once the store has read
+                // its box (the wait is off the accumulators' critical path)
+                tma_store_2d(&tm_out, (int)(p * kBM + quad * 32), (int)j0,
+                             sC + cs * kTileCBytes + (uint32_t)((half * 4 + quad) * 4096));
+                asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                mb_arrive(c_empty(cs));
+            }
+            __syncwarp();
         }
     }
     if (warp >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
@@ -653,7 +680,9 @@ int launch_update(const UpdArgs &P, cudaStream_t st) {
     static thread_local int attr_dev = -1;
     const int dev = current_device();
     if (attr_dev != dev) {
-        CQ_CUDA(cudaFuncSetAttribute(oz_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem),
+        CQ_CUDA(cudaFuncSetAttribute(oz_update_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem),
+                "oz update smem attr");
+        CQ_CUDA(cudaFuncSetAttribute(oz_update_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem),
                 "oz update smem attr");
         attr_dev = dev;
     }
@@ -662,7 +691,13 @@ int launch_update(const UpdArgs &P, cudaStream_t st) {
     if (!P.cols_in) CQ_TRY(make_map(&tm_in, P.cin, P.m, P.ncols, P.ldin, kBN / 2));
     CQ_TRY(make_map(&tm_out, P.cout, P.m, P.ncols, P.ldout, kBN / 2));  // 32 x 16 boxes
     const int grid = std::min(P.npanels, num_sms());
-    oz_update_kernel<<<grid, kUpdThreads, kUpdSmem, st>>>(tm_in, tm_out, P);
+    if (((int64_t)P.npanels / grid + 1) * P.ntn > INT_MAX / 2) return fail_internal("oz update: too many tiles per CTA");
+    // drain sets: 2 by default (CQRRPT_OZ_SETS=1 keeps a single set of 8 drain warps)
+    const char *es = getenv("CQRRPT_OZ_SETS");
+    if (es && es[0] == '1')
+        oz_update_kernel<1><<<grid, 64 + 32 * kEpiWarps, kUpdSmem, st>>>(tm_in, tm_out, P);
+    else
+        oz_update_kernel<2><<<grid, 64 + 64 * kEpiWarps, kUpdSmem, st>>>(tm_in, tm_out, P);
     note_launch();
     return check_launch("oz_update_kernel");
 }

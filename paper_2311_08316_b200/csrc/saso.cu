@@ -44,6 +44,7 @@
 // nnz = 8 times the HBM bytes of A, against ~5.5x more shared-memory than HBM
 // bandwidth: this kernel cannot reach the HBM roofline whatever its issue
 // efficiency.
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 
@@ -100,7 +101,8 @@ __global__ void saso_plan_kernel(int64_t d, int64_t c0, int64_t count, int nnz, 
 // xrow: bytes between consecutive rows c of one column in the staged tile
 // (264 for the padded row-major LDGSTS layout, 8 for the column segments the
 // bulk copies write)
-__global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d, int nnz, int A, int nbs, int entw,
+// S: row slots per consumer warp (32 / W lanes-per-row groups of W columns)
+__global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d, int nnz, int A, int S, int nbs, int entw,
                                                             uint32_t xrow, const uint32_t *__restrict__ plan,
                                                             uint2 *__restrict__ tinfo, uint32_t *__restrict__ tent) {
     extern __shared__ int32_t s_beg[];  // d + 1 counters -> row begins (s_beg[d] = entries)
@@ -150,9 +152,9 @@ __global__ void __launch_bounds__(256) saso_tile_csr_kernel(int64_t m, int64_t d
     __syncthreads();
     // block words: (first entry, rows of the block that have entries)
     uint2 *oinfo = tinfo + tile * (int64_t)nbs;
-    for (int sl = threadIdx.x; sl < nbs; sl += blockDim.x) {  // slot = CTA row block * 32 + warp
-        const int w = sl % kApplyWarps;
-        const int64_t rb = ((int64_t)(sl / kApplyWarps) * kConsumers + w) * A;
+    for (int sl = threadIdx.x; sl < nbs; sl += blockDim.x) {  // slot = (CTA row block * 32 + warp) * S + sub-slot
+        const int h = sl % S, w = (sl / S) % kApplyWarps;
+        const int64_t rb = (((int64_t)(sl / (S * kApplyWarps)) * kConsumers + w) * S + h) * A;
         uint2 word = make_uint2((uint32_t)nent, 0u);
         if (w < kConsumers && rb < d) {
             uint32_t mask = 0;
@@ -264,10 +266,12 @@ struct ApplyArgs {
     double *part;
 };
 
-constexpr uint32_t kTileBytes = kTileRows * kXLD * 8;  // 67584: [c][33] padded rows (LDGSTS staging)
 constexpr uint32_t kColB = kTileRows * 8 + 16;          // 2064: one column segment + 16-byte pad (bulk staging)
 constexpr uint32_t kTileBytesT = 32 * kColB;            // 66048
-constexpr uint32_t kInfoBytes = kApplyWarps * 8;       // one (start, mask) word pair per warp
+// LDGSTS staging: [c][W + 1] padded rows (W = 32: 67584 bytes); one (start,
+// mask) word pair per warp and row slot
+__host__ __device__ constexpr uint32_t tile_bytes(int W) { return kTileRows * (uint32_t)(W + 1) * 8u; }
+__host__ __device__ constexpr uint32_t info_bytes(int W) { return kApplyWarps * (uint32_t)(32 / W) * 8u; }
 
 // TMA = true: one producer thread stages each tile as 32 column segments with
 // cp.async.bulk (the TMA engine writes shared memory; no LDGSTS issue slots),
@@ -276,16 +280,27 @@ constexpr uint32_t kInfoBytes = kApplyWarps * 8;       // one (start, mask) word
 // x reads instead of the padded layout's none, for staging that no longer
 // costs 8 cycles per 256-byte warp operation). Needs A 16-byte aligned, lda
 // even. TMA = false: the four producer warps' 8-byte LDGSTS into [c][33].
-template <int A, bool TMA>
+//
+// W < 32 (narrow n: too few 32-column groups to fill the GPU, and each CTA's
+// staging of its whole column group is the bound): a CTA takes W columns, and
+// a consumer warp S = 32 / W row slots at once -- lanes [h W, (h + 1) W) walk
+// the entry lists of the A rows of slot h over the same W columns. The slots
+// of a warp diverge (different list lengths); every chain is still the
+// reference's, so the result is bit-identical. LDGSTS staging only.
+template <int A, bool TMA, int W>
 __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs P) {
-    constexpr int RB = kConsumers * A;
+    static_assert(!TMA || W == 32, "bulk staging takes whole 32-column groups");
+    constexpr int SL = 32 / W;  // row slots per consumer warp
+    constexpr int RB = kConsumers * SL * A;
+    constexpr uint32_t kInfoBytes = info_bytes(W);
+    constexpr uint32_t kXLDB = (uint32_t)(W + 1) * 8u;  // staged row stride in bytes
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     // grid (row blocks, column groups): the row blocks of one column group
     // are adjacent in launch order, so they are co-resident and march through
     // the same tiles together -- A is read from HBM once, the other row
     // blocks' copies hit L2
-    const int64_t j0 = (int64_t)blockIdx.y * 32;
+    const int64_t j0 = (int64_t)blockIdx.y * W;
     const int64_t r0 = (int64_t)blockIdx.x * RB;
     const int64_t split = blockIdx.z;
     const int64_t t_begin = P.tile_hi ? P.tile_lo : split * P.tiles_per_split;
@@ -294,7 +309,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
     const int S = P.stages;
 
     // shared layout: S tiles | S entry lists | S info blocks | S full + S empty mbarriers
-    constexpr uint32_t TB = TMA ? kTileBytesT : kTileBytes;
+    constexpr uint32_t TB = TMA ? kTileBytesT : tile_bytes(W);
     const uint32_t s_tiles = smem_u32(smem_raw);
     const uint32_t ent_bytes = (uint32_t)P.entw * 4u;
     const uint32_t s_ents = s_tiles + (uint32_t)S * TB;
@@ -315,7 +330,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
         if (wid != kConsumers || lane != 0) return;
         const int ncols = (int)cmin<int64_t>(32, P.n - j0);
         const uint32_t *g_ent = P.tent + t_begin * (int64_t)P.entw;
-        const uint2 *g_info = P.tinfo + t_begin * P.nbs + (int64_t)blockIdx.x * kApplyWarps;
+        const uint2 *g_info = P.tinfo + t_begin * P.nbs + (int64_t)blockIdx.x * (kApplyWarps * SL);
         int stg = 0;
         uint32_t use = 0;
         for (int64_t i = 0; i < ntl; ++i) {
@@ -345,26 +360,26 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
         // Producer p copies columns p, p+4, ..., lane l rows l + 32k (k = 0..7):
         // 256-byte coalesced runs, immediate offsets, one pointer step per column
         const int pw = wid - kConsumers;
-        const int ncols = (int)cmin<int64_t>(32, P.n - j0);
+        const int ncols = (int)cmin<int64_t>(W, P.n - j0);
         const int64_t lda4 = kProducers * P.lda;
         const int nent16 = P.entw / 4;
         const double *a_tile = P.a + (j0 + pw) * P.lda + t_begin * kTileRows + lane;
         const uint32_t *g_ent = P.tent + t_begin * (int64_t)P.entw;
         const uint32_t *g_info =
-            reinterpret_cast<const uint32_t *>(P.tinfo + t_begin * P.nbs + (int64_t)blockIdx.x * kApplyWarps);
+            reinterpret_cast<const uint32_t *>(P.tinfo + t_begin * P.nbs + (int64_t)blockIdx.x * (kApplyWarps * SL));
         const int64_t full_tiles = P.m / kTileRows;  // tiles without rows past m
         const int pl = pw * 32 + lane;                // producer lane 0..127
         int stg = 0;
         uint32_t use = 0;
         for (int64_t i = 0; i < ntl; ++i) {
             if (use) mbar_wait(s_empty + 8u * stg, (use - 1u) & 1u);  // consumers done with the stage's last tile
-            const uint32_t sb = s_tiles + (uint32_t)stg * TB + (uint32_t)lane * (kXLD * 8u);
+            const uint32_t sb = s_tiles + (uint32_t)stg * TB + (uint32_t)lane * kXLDB;
             const double *pa = a_tile;
             if (t_begin + i < full_tiles) {
                 for (int j = pw; j < ncols; j += kProducers) {
 #pragma unroll
                     for (int k = 0; k < kTileRows / 32; ++k)
-                        cp_async8_s(sb + 8u * (uint32_t)j + (uint32_t)(k * 32 * kXLD * 8), pa + 32 * k);
+                        cp_async8_s(sb + 8u * (uint32_t)j + (uint32_t)k * (32u * kXLDB), pa + 32 * k);
                     pa += lda4;
                 }
             } else {  // the ragged last tile
@@ -373,7 +388,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
 #pragma unroll
                     for (int k = 0; k < kTileRows / 32; ++k)
                         if (lane + 32 * k < rem)
-                            cp_async8_s(sb + 8u * (uint32_t)j + (uint32_t)(k * 32 * kXLD * 8), pa + 32 * k);
+                            cp_async8_s(sb + 8u * (uint32_t)j + (uint32_t)k * (32u * kXLDB), pa + 32 * k);
                     pa += lda4;
                 }
             }
@@ -390,19 +405,22 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
     }
 
     // ---------------- consumer warps
+    const int slot = wid * SL + lane / W, cl = lane % W;  // row slot of the CTA, column of the group
+    const int wr0 = slot * A;
+    const int64_t col = j0 + cl;
     double acc[A];
 #pragma unroll
     for (int q = 0; q < A; ++q) acc[q] = 0.0;
-    if (P.carry && j0 + lane < P.n) {  // carried chains continue bit for bit (one split)
-        const double *pp = P.part + (r0 + wid * A) * P.n + j0 + lane;
+    if (P.carry && col < P.n) {  // carried chains continue bit for bit (one split)
+        const double *pp = P.part + (r0 + wr0) * P.n + col;
 #pragma unroll
         for (int q = 0; q < A; ++q)
-            if (wid * A + q < rows_here) acc[q] = pp[(int64_t)q * P.n];
+            if (wr0 + q < rows_here) acc[q] = pp[(int64_t)q * P.n];
     }
     int stg = 0;
     uint32_t use = 0;  // how many times this stage has been filled before the current tile
     const double v = P.val;
-    const uint32_t lane_x = s_tiles + (TMA ? kColB : 8u) * (uint32_t)lane;
+    const uint32_t lane_x = s_tiles + (TMA ? kColB : 8u) * (uint32_t)cl;
     // x with the entry's sign applied: bit 0 of the entry is 1 for -1/sqrt(d);
     // adding cur * 2^31 flips bit 63 of x exactly when it is set, and
     // fma(v, -x, s) == fma(-v, x, s) bit for bit
@@ -411,8 +429,9 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
     };
     for (int64_t i = 0; i < ntl; ++i) {
         mbar_wait(s_full + 8u * stg, use & 1u);
-        const uint2 info = lds_u32x2(s_info + (uint32_t)stg * kInfoBytes + 8u * (uint32_t)wid);
-        const uint32_t mask = __reduce_or_sync(0xffffffffu, info.y);  // warp-uniform
+        const uint2 info = lds_u32x2(s_info + (uint32_t)stg * kInfoBytes + 8u * (uint32_t)slot);
+        // one slot per warp: warp-uniform; several: the slots of a warp diverge
+        const uint32_t mask = SL == 1 ? __reduce_or_sync(0xffffffffu, info.y) : info.y;
         if (mask) {
             // The warp's entries: rows ascending, c ascending within a row,
             // the last entry of each row flagged. The loop is unrolled by two
@@ -447,8 +466,6 @@ __global__ void __launch_bounds__(kApplyThreads, 1) saso_apply_kernel(ApplyArgs 
         if (++stg == S) stg = 0, ++use;
     }
     // write the partial: part[split][r][j]
-    const int wr0 = wid * A;
-    const int64_t col = j0 + lane;
     if (col < P.n) {
         double *pp = P.part + split * P.d * P.n;
 #pragma unroll
@@ -490,18 +507,19 @@ int saso_plan(int64_t d, int64_t c0, int64_t count, int64_t nnz, uint64_t seed, 
     return check_launch("saso_plan_kernel");
 }
 
-static size_t apply_smem(int nnz, int *entw, int *nbs, int *stages, int64_t d, int A, bool tma) {
+static size_t apply_smem(int nnz, int *entw, int *nbs, int *stages, int64_t d, int A, bool tma, int W) {
+    const int S = 32 / W;                    // row slots per consumer warp
     *entw = (kTileRows * nnz + 2 + 3) & ~3;  // u32 entries + two prefetch overrun words, 16-byte multiple
-    const int64_t nb = (d + A - 1) / A;      // blocks of A sketch rows, kConsumers per CTA
-    *nbs = (int)(((nb + kConsumers - 1) / kConsumers) * kApplyWarps);  // 32 slots per CTA row block
-    const size_t per = (tma ? kTileBytesT : kTileBytes) + 4 * (size_t)*entw + kInfoBytes + 16;
+    const int64_t nb = (d + (int64_t)A * S - 1) / ((int64_t)A * S);  // consumer warps needed, kConsumers per CTA
+    *nbs = (int)(((nb + kConsumers - 1) / kConsumers) * kApplyWarps * S);  // 32 S slots per CTA row block
+    const size_t per = (tma ? kTileBytesT : tile_bytes(W)) + 4 * (size_t)*entw + info_bytes(W) + 16;
     *stages = (int)std::min<size_t>(6, (227 * 1024) / per);
     return per * (size_t)*stages;
 }
 
-template <int A, bool TMA>
+template <int A, bool TMA, int W = 32>
 static int launch_apply(ApplyArgs P, dim3 grid, size_t smem, cudaStream_t st) {
-    auto kern = saso_apply_kernel<A, TMA>;
+    auto kern = saso_apply_kernel<A, TMA, W>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return fail_cuda("saso_apply smem attr");
     kern<<<grid, kApplyThreads, smem, st>>>(P);
@@ -536,22 +554,39 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
     // issue slots (per consumer warp ~30 per tile and ~5 per row, ~7.5 per
     // entry, ~500 for the producer warps, over 4 schedulers); minimise
     // waves * that.
-    const int64_t cgroups = (n + 31) / 32;
     const int sms = num_sms();
-    int A = 12;
+    // Narrow n (at most 512 columns: fewer than 16 column groups of 32, each
+    // CTA's LDGSTS staging of its whole column group is the bound, 8 cycles
+    // per 256-byte warp copy = 64 W cycles per tile): W = 16 or 8 columns per
+    // CTA, a consumer warp walks 32 / W row slots at once (divergent, its
+    // iterations ~ the longest of the slots' Poisson entry lists).
+    int A = 12, W = 32;
     if (!allow_split) {
-        const int cand[] = {16, 12, 8, 6, 4, 2, 1};
+        const int candA[] = {16, 12, 8, 6, 4, 2, 1};
+        const int candW[] = {32, 16, 8};
+        const double lam = (double)kTileRows * (double)nnz / (double)d;  // entries per sketch row and tile
         double best = 1e300;
-        for (int a : cand) {
-            const int64_t rb = (int64_t)kConsumers * a;
-            const int64_t ctas = cgroups * ((d + rb - 1) / rb);
-            const double ents = (double)kTileRows * (double)nnz * (double)std::min<int64_t>(rb, d) / (double)d;
-            const double smem_c = 528.0 + 3.0 * ents + (double)kTileRows * (double)nnz / 32.0;
-            const double issue_c = (kConsumers * (30.0 + 5.0 * a) + 7.5 * ents + 500.0) / 4.0;
-            const double cost = (double)((ctas + sms - 1) / sms) * std::max(smem_c, issue_c);
-            if (cost < best * 0.999) {
-                best = cost;
-                A = a;
+        for (int w : candW) {
+            if (w < 32 && n > 512) continue;
+            const int S = 32 / w;
+            const double spread = S == 1 ? 0.0 : (S == 2 ? 0.56 : 1.03);  // E[max of S] - mean, in sigmas
+            for (int a : candA) {
+                if (w < 32 && a != 1 && a != 2 && a != 4 && a != 8) continue;  // instantiated widths
+                const int64_t rb = (int64_t)kConsumers * S * a;
+                const int64_t ctas = ((n + w - 1) / w) * ((d + rb - 1) / rb);
+                const double ents = (double)kTileRows * (double)nnz * (double)std::min<int64_t>(rb, d) / (double)d;
+                // warp iterations of the CTA per tile: one entry each (S = 1) or one entry per slot
+                const double iters =
+                    S == 1 ? ents : (double)std::min<int64_t>(rb, d) / S * (lam + spread * std::sqrt(lam));
+                const double smem_c = 16.5 * w + 3.0 * iters + (double)kTileRows * (double)nnz / 32.0;
+                const double issue_c = (kConsumers * (30.0 + 5.0 * a) + 7.5 * iters + 500.0 * w / 32.0) / 4.0;
+                const double stage_c = n <= 512 ? 64.0 * w : 0.0;  // LDGSTS issue (wide n: the choice of A is unchanged)
+                const double cost = (double)((ctas + sms - 1) / sms) * std::max(std::max(smem_c, issue_c), stage_c);
+                if (cost < best * 0.999) {
+                    best = cost;
+                    A = a;
+                    W = w;
+                }
             }
         }
     }
@@ -559,7 +594,14 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
         const int fa = atoi(ev);
         if (fa == 1 || fa == 2 || fa == 4 || fa == 6 || fa == 8 || fa == 12 || fa == 16) A = fa;
     }
-    const int64_t rblocks = (d + (int64_t)kConsumers * A - 1) / ((int64_t)kConsumers * A);
+    if (const char *ev = getenv("CQRRPT_SASO_W")) {  // experiments / tests: force the column-group width
+        const int fw = atoi(ev);
+        if (fw == 8 || fw == 16 || fw == 32) W = fw;
+    }
+    if (W < 32 && A != 1 && A != 2 && A != 4 && A != 8) A = A > 8 ? 8 : (A == 6 ? 4 : A);
+    const int SL = 32 / W;
+    const int64_t cgroups = (n + W - 1) / W;
+    const int64_t rblocks = (d + (int64_t)kConsumers * SL * A - 1) / ((int64_t)kConsumers * SL * A);
     // Tile staging: bulk copies (TMA engine: no LDGSTS issue slots, but x
     // reads from 16-byte aligned column segments take 4 instead of 2
     // wavefronts) when A's segments are 16-byte aligned and few row blocks
@@ -569,10 +611,10 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
     // 4.94 ms, C5-2048 84.0 -> 77.7 ms at 6 with A = 16) and lose at 12 (C4
     // 55.2 -> 65.8 ms, C5-256 19.7 -> 22.2 ms). CQRRPT_SASO_LDGSTS=1 /
     // CQRRPT_SASO_TMA=1 force either path.
-    const bool tma = (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (lda & 1) == 0 &&
+    const bool tma = W == 32 && (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (lda & 1) == 0 &&
                      (rblocks <= 6 || getenv("CQRRPT_SASO_TMA") != nullptr) && getenv("CQRRPT_SASO_LDGSTS") == nullptr;
     int entw = 0, nbs = 0, stages = 0;
-    const size_t smem = apply_smem((int)nnz, &entw, &nbs, &stages, d, A, tma);
+    const size_t smem = apply_smem((int)nnz, &entw, &nbs, &stages, d, A, tma, W);
     if (stages < 2) return fail_internal("saso_apply: nnz too large for the staged entry lists");
     uint2 *tinfo = ws.get<uint2>("saso.tinfo", (size_t)(ntiles * nbs) + 32);
     uint32_t *tent = ws.get<uint32_t>("saso.tent", (size_t)(ntiles * entw) + 4);
@@ -582,7 +624,7 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
         cudaFuncSetAttribute(saso_tile_csr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csr_smem) !=
             cudaSuccess)
         return fail_cuda("csr smem attr");
-    saso_tile_csr_kernel<<<(unsigned)ntiles, 256, csr_smem, st>>>(m, d, (int)nnz, A, nbs, entw, tma ? 8u : kXLD * 8u,
+    saso_tile_csr_kernel<<<(unsigned)ntiles, 256, csr_smem, st>>>(m, d, (int)nnz, A, SL, nbs, entw, tma ? 8u : (uint32_t)(W + 1) * 8u,
                                                                   plan, tinfo, tent);
     note_launch();
     if ((rc = check_launch("saso_tile_csr_kernel"))) return rc;
@@ -628,6 +670,22 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
     P.carry = 0;
     dim3 grid((unsigned)rblocks, (unsigned)cgroups, (unsigned)nsplit);
     auto launch_A = [&](dim3 gr) -> int {
+        if (W == 16) {
+            switch (A) {
+                case 1: return launch_apply<1, false, 16>(P, gr, smem, st);
+                case 2: return launch_apply<2, false, 16>(P, gr, smem, st);
+                case 4: return launch_apply<4, false, 16>(P, gr, smem, st);
+                default: return launch_apply<8, false, 16>(P, gr, smem, st);
+            }
+        }
+        if (W == 8) {
+            switch (A) {
+                case 1: return launch_apply<1, false, 8>(P, gr, smem, st);
+                case 2: return launch_apply<2, false, 8>(P, gr, smem, st);
+                case 4: return launch_apply<4, false, 8>(P, gr, smem, st);
+                default: return launch_apply<8, false, 8>(P, gr, smem, st);
+            }
+        }
         switch (A) {
             case 1: return tma ? launch_apply<1, true>(P, gr, smem, st) : launch_apply<1, false>(P, gr, smem, st);
             case 2: return tma ? launch_apply<2, true>(P, gr, smem, st) : launch_apply<2, false>(P, gr, smem, st);

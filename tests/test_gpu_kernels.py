@@ -116,6 +116,40 @@ def test_saso_sketch_every_row_block_width(cuda, oracle, monkeypatch, A, path):
         assert np.array_equal(got, oracle.saso_apply(d, a, nnz, seed)), m
 
 
+@pytest.mark.parametrize("W", [8, 16])
+@pytest.mark.parametrize("A", [1, 2, 4, 8])
+def test_saso_sketch_narrow_column_groups(cuda, oracle, monkeypatch, A, W):
+    """Narrow column groups (W columns per CTA, 32 / W row slots per consumer
+    warp whose entry walks diverge; chosen by default for n <= 512) against
+    the reference's apply, bit for bit: several row blocks, ragged last tile
+    and last column group, padded leading dimension, an offset shard, and the
+    chained launches of the chunked host path."""
+    from paper_2311_08316_b200 import kernels
+    monkeypatch.setenv("CQRRPT_SASO_A", str(A))
+    monkeypatch.setenv("CQRRPT_SASO_W", str(W))
+    n, d, nnz, seed = 45, 700, 8, 12
+    for m in (5000, 5001):
+        a = oracle.gen_gaussian(m, n, 31)
+        x = cuda.colmajor_empty(m, n, pad_to=2)
+        x.copy_(dev(cuda, a))
+        got = host(kernels.saso_sketch(x, d, nnz, seed))
+        assert np.array_equal(got, oracle.saso_apply(d, a, nnz, seed)), m
+    # few sketch rows (one partial row block), nnz = 2
+    a = oracle.gen_gaussian(3000, 19, 5)
+    got = host(kernels.saso_sketch(dev(cuda, a), 24, 2, 3))
+    assert np.array_equal(got, oracle.saso_apply(24, a, 2, 3))
+
+
+def test_saso_sketch_narrow_default_choice(cuda, oracle):
+    """The default choice at a C5-256-like shape (n <= 512: narrow column
+    groups) is bit-identical to the reference's apply."""
+    from paper_2311_08316_b200 import kernels
+    m, n, d = 40000, 256, 320
+    a = oracle.gen_gaussian(m, n, 9)
+    got = host(kernels.saso_sketch(dev(cuda, a), d, 8, 0))
+    assert np.array_equal(got, oracle.saso_apply(d, a, 8, 0))
+
+
 @pytest.mark.parametrize("nnz", [1, 2, 16])
 def test_saso_sketch_nnz(cuda, oracle, nnz):
     """Other nonzeros per column (entry-list sizes per tile), bit-identical."""

@@ -1,6 +1,6 @@
 """Device time of the exact SASO sketch (K1 plan + CSR + K2 apply + reduce)
 on BASELINE shapes; HBM roofline fraction of the algorithmic bytes
-8 m n + 8 d n. usage: python tools/sketch_bench.py [C2 C4 C5_256 ...]"""
+8 m n + 8 d n. usage: python tools/sketch_bench.py [C2 C4 C5_256 m,n,d ...]"""
 import json
 import os
 import sys
@@ -16,9 +16,12 @@ HBM = 6553.6
 
 def main(names):
     for name in names:
-        cfg = CONFIGS[name]
-        m, n = cfg["m"], cfg["n"]
-        d = -(-int(cfg["gamma"] * n * 4) // 4) if False else int(-(-cfg["gamma"] * n // 1))
+        if "," in name:  # an explicit shape m,n,d
+            m, n, d = (int(v) for v in name.split(","))
+        else:
+            cfg = CONFIGS[name]
+            m, n = cfg["m"], cfg["n"]
+            d = int(-(-cfg["gamma"] * n // 1))
         a = torch.randn((n, m), dtype=torch.float64, device="cuda").t()
         for _ in range(2):
             kernels.saso_sketch(a, d, 8, 0)
