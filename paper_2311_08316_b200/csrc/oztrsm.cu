@@ -69,25 +69,28 @@ constexpr int kW = 128;                    // column block = K of each update
 constexpr int kDig = 7;                    // base-256 digits per value
 constexpr int kGroups = 8;                 // digit-pair groups g = s + t <= 7
 constexpr int kBM = 128;                   // panel rows = MMA M = TMEM lanes
-constexpr int kBN = 32;                    // N tile
+constexpr int kBN = 16;                    // N tile
 constexpr int kSliceA = kBM * kW;          // 16384 B per digit slice of a panel
-constexpr int kSliceB = kBN * kW;          // 4096 B per digit slice of an N tile
+constexpr int kSliceB = kBN * kW;          // 2048 B per digit slice of an N tile
 constexpr int kPanelBytes = kDig * kSliceA;  // 114688
-constexpr int kTileBBytes = kDig * kSliceB;  // 28672
-constexpr int kBStages = 2;
-constexpr int kEpiWarps = 8;               // per drain set: 2 per TMEM lane quadrant, 16 columns each
-constexpr int kMaxSets = 2;                // drain sets (alternating tiles)
-constexpr int kTmemCols = 512;             // A digit slices (7 x 32) | accumulators (8 x 32)
+constexpr int kTileBBytes = kDig * kSliceB;  // 14336 in global memory
+constexpr int kTileBSmem = (kDig + 1) * kSliceB;  // staged with an all-zero 8th slice (group 7 of digit 0)
+constexpr int kBufs = 2;                   // accumulator buffers (tile parity)
+constexpr int kSets = 4;                   // drain sets (tile index mod 4; buffer = set mod 2)
+constexpr int kEpiWarps = 4;               // per drain set: one per TMEM lane quadrant, 16 columns
+constexpr int kUpdThreads = 64 + 32 * kEpiWarps * kSets;  // producer, MMA, drain sets
+constexpr int kTmemCols = 512;             // A digit slices (7 x 32) | 2 x accumulators (8 x 16)
 constexpr uint32_t kTmemAcc = 256;         // first accumulator column
+constexpr uint32_t kAccCols = kGroups * kBN;  // 128 columns per buffer
 
 constexpr int kAStages = 2;                // digit slices staged on their way to TMEM
-constexpr int kCStages = 4;                // right-hand-side tiles (128 x 32 FP64)
-constexpr uint32_t kTileCBytes = kBM * kBN * 8;  // 32768, column c at c * 1024
+constexpr uint32_t kTileCBytes = kBM * kBN * 8;  // 16384: quadrant q's 32 x 16 box at q * 4096, column c at c * 256
 constexpr uint32_t kSmemA = 0;
 constexpr uint32_t kSmemB = kAStages * kSliceA;
-constexpr uint32_t kSmemC = kSmemB + kBStages * kTileBBytes;
-constexpr uint32_t kSmemBar = kSmemC + kCStages * kTileCBytes;  // 217088
-constexpr uint32_t kUpdSmem = kSmemBar + 256;
+// ring depths: kBStages staged U tiles (16 KB), kCStages right-hand-side tiles (16 KB)
+__host__ __device__ constexpr uint32_t upd_smem(int bst, int cst) {
+    return kSmemB + (uint32_t)bst * kTileBSmem + (uint32_t)cst * kTileCBytes + 512u;
+}
 
 // byte offset of (row r, k kk) in a digit slice laid out as UMMA core matrices
 // (8 rows x 16 bytes, K-major, no swizzle): LBO = 128 (next 16 K), SBO = 1024
@@ -361,29 +364,30 @@ struct UpdArgs {
     int64_t ldout;
 };
 
-template <int kSets>
-__global__ void __launch_bounds__(64 + 32 * kEpiWarps * kSets, 1)
+template <int kBStages, int kCStages>
+__global__ void __launch_bounds__(kUpdThreads, 1)
     oz_update_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out, UpdArgs P) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t sbase = smem_u32(smem);
+    constexpr uint32_t kSmemC = kSmemB + kBStages * kTileBSmem;
+    constexpr uint32_t kSmemBar = kSmemC + kCStages * kTileCBytes;
     const uint32_t sA = sbase + kSmemA, sB = sbase + kSmemB, sC = sbase + kSmemC;
     const uint32_t bar = sbase + kSmemBar;
     // a_*: digit-slice staging ring (smem -> TMEM); b_*: U-slice N tiles;
-    // c_*: right-hand-side tiles; lo_full / hi_full: a tile's groups 0-3 /
-    // 4-7 accumulated; lo_free / hi_free: the epilogue has read them
+    // c_*: right-hand-side tiles; acc_full / acc_free (one pair per drain
+    // set, so every barrier's phases are one set's consecutive tiles): the
+    // set's tile accumulated / its accumulator buffer read
     auto a_full = [&](int s) { return bar + 8u * s; };
     auto a_empty = [&](int s) { return bar + 8u * (kAStages + s); };
     auto b_full = [&](int s) { return bar + 8u * (2 * kAStages + s); };
     auto b_empty = [&](int s) { return bar + 8u * (2 * kAStages + kBStages + s); };
     auto c_full = [&](int s) { return bar + 8u * (2 * kAStages + 2 * kBStages + s); };
     auto c_empty = [&](int s) { return bar + 8u * (2 * kAStages + 2 * kBStages + kCStages + s); };
-    // lo_full / hi_full: one barrier per drain set (a set waits for every
-    // kSets-th tile, so its waits must not see the other sets' phases)
-    const uint32_t lo_full0 = bar + 8u * (2 * (kAStages + kBStages + kCStages));
-    const uint32_t hi_full0 = lo_full0 + 8u * kMaxSets;
-    const uint32_t lo_free = hi_full0 + 8u * kMaxSets, hi_free = lo_free + 8;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + kSmemBar + 248);
+    auto acc_full = [&](uint32_t s) { return bar + 8u * (2 * (kAStages + kBStages + kCStages) + s); };
+    auto acc_free = [&](uint32_t s) { return bar + 8u * (2 * (kAStages + kBStages + kCStages) + kSets + s); };
+    static_assert(8 * (2 * (kAStages + kBStages + kCStages) + 2 * kSets) <= 504, "barrier block");
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + kSmemBar + 504);
 
     if (tid == 0) {
         for (int s = 0; s < kAStages; ++s) {
@@ -396,16 +400,20 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps * kSets, 1)
         }
         for (int s = 0; s < kCStages; ++s) {
             mb_init(c_full(s), 1);
-            mb_init(c_empty(s), kEpiWarps);  // one store per epilogue warp
+            mb_init(c_empty(s), kEpiWarps);  // one store per drain warp
         }
-        for (int s = 0; s < kMaxSets; ++s) {
-            mb_init(lo_full0 + 8u * s, 1);
-            mb_init(hi_full0 + 8u * s, 1);
+        for (int s = 0; s < kSets; ++s) {
+            mb_init(acc_full(s), 1);
+            mb_init(acc_free(s), kEpiWarps);  // one arrival per drain warp of the set
         }
-        mb_init(lo_free, kEpiWarps);  // one arrival per drain warp
-        mb_init(hi_free, kEpiWarps);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
+    // the all-zero 8th slice of every staged U tile (the bulk copies write the first 7)
+    for (int i = tid; i < kBStages * (kSliceB / 16); i += kUpdThreads) {
+        const int st = i / (kSliceB / 16), o = i % (kSliceB / 16);
+        *reinterpret_cast<uint4 *>(smem + kSmemB + st * kTileBSmem + kDig * kSliceB + o * 16) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
                      "n"(kTmemCols)
@@ -437,17 +445,16 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps * kSets, 1)
                 for (int nt = 0; nt < P.ntn; ++nt) {
                     if (bfill) mb_wait(b_empty(bs), (bfill - 1u) & 1u);
                     mb_expect_tx(b_full(bs), kTileBBytes);
-                    bulk_g2s(sB + bs * kTileBBytes, P.bslc + (int64_t)nt * kTileBBytes, kTileBBytes, b_full(bs));
+                    bulk_g2s(sB + bs * kTileBSmem, P.bslc + (int64_t)nt * kTileBBytes, kTileBBytes, b_full(bs));
                     if (++bs == kBStages) bs = 0, ++bfill;
-                    // the tile's right-hand side: one bulk copy per column
                     const int64_t j0 = (int64_t)nt * kBN;
                     if (cfill) mb_wait(c_empty(cs), (cfill - 1u) & 1u);
-                    if (!P.cols_in) {  // 8 boxes of 32 rows x 16 columns, one per epilogue warp (zeros past the ends)
+                    if (!P.cols_in) {  // 4 boxes of 32 rows x 16 columns, one per drain warp (zeros past the ends)
                         mb_expect_tx(c_full(cs), kTileCBytes);
-                        for (int sb = 0; sb < 8; ++sb)
-                            tma_load_2d(sC + cs * kTileCBytes + (uint32_t)sb * 4096u, &tm_in, (int)(r0 + (sb & 3) * 32),
-                                        (int)(j0 + (sb >> 2) * 16), c_full(cs));
-                    } else {  // gathered columns: the epilogue reads them from global memory
+                        for (int q = 0; q < 4; ++q)
+                            tma_load_2d(sC + cs * kTileCBytes + (uint32_t)q * 4096u, &tm_in, (int)(r0 + q * 32), (int)j0,
+                                        c_full(cs));
+                    } else {  // gathered columns: the drain warps read them from global memory
                         mb_arrive(c_full(cs));
                     }
                     if (++cs == kCStages) cs = 0, ++cfill;
@@ -478,52 +485,39 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps * kSets, 1)
                 }
                 for (int nt = 0; nt < P.ntn; ++nt, ++tc) {
                     mb_wait_warp(b_full(bs), buse & 1u);
-                    const uint32_t blo0 = desc_lo(sB + bs * kTileBBytes);
-                    constexpr uint32_t d0 = tmem + kTmemAcc;
-                    // groups 0-3 once the epilogue has read the previous tile's
-                    if (tc) mb_wait_warp(lo_free, (tc - 1u) & 1u);
+                    const uint32_t blo0 = desc_lo(sB + bs * kTileBSmem);
+                    const uint32_t buf = tc & 1u, set = tc & 3u;
+                    const uint32_t d0 = tmem + kTmemAcc + buf * kAccCols;
+                    // this buffer's previous tile (tc - 2, drained by set (tc - 2) % 4) has been read
+                    if (tc >= 2) mb_wait_warp(acc_free((tc - 2u) & 3u), ((tc - 2u) >> 2) & 1u);
                     tc_fence_after();
                     if (elect_one()) {
-                        // Digit slice s of X against slices t = 0 .. 3 - s of U in ONE
-                        // MMA per K-step: U's slices are consecutive 32-row blocks of
-                        // the canonical layout, so N = 32 (4 - s) columns starting at
-                        // group s are the products for groups s .. 3 (the A operand is
-                        // read once per slice and K-step, not once per digit pair)
+                        // Digit slice s of X against ALL its partner slices t = 0 ..
+                        // min(6, 7 - s) of U in one MMA per K-step: U's slices are
+                        // consecutive 16-row blocks of the canonical layout, so N =
+                        // 16 (count) columns starting at group s land pair (s, t) in
+                        // group s + t. Slice 0 runs over the zero 8th slice too: its
+                        // first K-step overwrites all 8 groups, the rest accumulate.
                         tc_mma_i8_k128<idesc_n(128), true>(d0 + 0 * kBN, tmem + 0 * 32, blo0);
-                        tc_mma_i8_k128<idesc_n(96), false>(d0 + 1 * kBN, tmem + 1 * 32, blo0);
-                        tc_mma_i8_k128<idesc_n(64), false>(d0 + 2 * kBN, tmem + 2 * 32, blo0);
-                        tc_mma_i8_k128<idesc_n(32), false>(d0 + 3 * kBN, tmem + 3 * 32, blo0);
-                        tc_commit(lo_full0 + 8u * (tc % kSets));
-                    }
-                    __syncwarp();
-                    if (tc) mb_wait_warp(hi_free, (tc - 1u) & 1u);
-                    tc_fence_after();
-                    if (elect_one()) {
-                        // groups 4-7: slice s against t = max(4 - s, 0) .. min(7 - s, 6),
-                        // landing in groups max(4, s) ..; slice 1 goes first because it
-                        // covers all four groups (its first K-step overwrites them)
-                        constexpr uint32_t sl = kSliceB >> 4;
-                        tc_mma_i8_k128<idesc_n(128), true>(d0 + 4 * kBN, tmem + 1 * 32, blo0 + 3 * sl);
-                        tc_mma_i8_k128<idesc_n(96), false>(d0 + 4 * kBN, tmem + 0 * 32, blo0 + 4 * sl);
-                        tc_mma_i8_k128<idesc_n(128), false>(d0 + 4 * kBN, tmem + 2 * 32, blo0 + 2 * sl);
-                        tc_mma_i8_k128<idesc_n(128), false>(d0 + 4 * kBN, tmem + 3 * 32, blo0 + 1 * sl);
-                        tc_mma_i8_k128<idesc_n(128), false>(d0 + 4 * kBN, tmem + 4 * 32, blo0);
-                        tc_mma_i8_k128<idesc_n(96), false>(d0 + 5 * kBN, tmem + 5 * 32, blo0);
-                        tc_mma_i8_k128<idesc_n(64), false>(d0 + 6 * kBN, tmem + 6 * 32, blo0);
+                        tc_mma_i8_k128<idesc_n(112), false>(d0 + 1 * kBN, tmem + 1 * 32, blo0);
+                        tc_mma_i8_k128<idesc_n(96), false>(d0 + 2 * kBN, tmem + 2 * 32, blo0);
+                        tc_mma_i8_k128<idesc_n(80), false>(d0 + 3 * kBN, tmem + 3 * 32, blo0);
+                        tc_mma_i8_k128<idesc_n(64), false>(d0 + 4 * kBN, tmem + 4 * 32, blo0);
+                        tc_mma_i8_k128<idesc_n(48), false>(d0 + 5 * kBN, tmem + 5 * 32, blo0);
+                        tc_mma_i8_k128<idesc_n(32), false>(d0 + 6 * kBN, tmem + 6 * 32, blo0);
                         tc_commit(b_empty(bs));
-                        tc_commit(hi_full0 + 8u * (tc % kSets));
+                        tc_commit(acc_full(set));
                     }
                     __syncwarp();
                     if (++bs == kBStages) bs = 0, ++buse;
                 }
             }
         }
-    } else {  // ---------------- drain warps: set (warp - 2) / 8 takes tiles set, set + kSets, ...;
-              // lane quadrant warp % 4, 16 columns each
-        const int quad = warp & 3, half = ((warp - 2) >> 2) & 1, set = (warp - 2) >> 3;
+    } else {  // ---------------- drain warps: set (warp - 2) / 4 takes tiles set, set + 4, ...
+              // (accumulator buffer = set % 2); lane quadrant warp % 4, all 16 columns
+        const int quad = warp & 3, set = (warp - 2) >> 2;
         const int rloc = quad * 32 + lane;
-        const uint32_t taddr0 = tmem + kTmemAcc + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * 16);
-        const uint32_t lo_full = lo_full0 + 8u * set, hi_full = hi_full0 + 8u * set;
+        const uint32_t taddr0 = tmem + kTmemAcc + (uint32_t)(set & 1) * kAccCols + ((uint32_t)(quad * 32) << 16);
         // tiles of this CTA in issue order: panel blockIdx.x + pcur * gridDim.x, N tile nt
         // (the host bounds npanels * ntn / gridDim.x below 2^31)
         const int npan = P.npanels > (int)blockIdx.x ? (P.npanels - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
@@ -543,19 +537,19 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps * kSets, 1)
                 rs = P.rscale[row];  // rscale covers the padded panel
             }
             const uint32_t par = (uint32_t)(tc / kSets) & 1u;
-            const int cs = (int)(tc % kCStages);
+            const int cs = tc % kCStages;
             const uint32_t cpar = (uint32_t)(tc / kCStages) & 1u;
-            const int64_t j0 = (int64_t)nt * kBN + half * 16;
+            const int64_t j0 = (int64_t)nt * kBN;
             const int64_t rem = P.ncols - j0;
-            const int nc = rem >= 16 ? 16 : (rem > 0 ? (int)rem : 0);
-            double hs[16];
-            mb_wait(lo_full, par);
+            const int nc = rem >= kBN ? kBN : (rem > 0 ? (int)rem : 0);
+            double hs[kBN];
+            mb_wait(acc_full(set), par);
             tc_fence_after();
-            // groups 0-3 -> hi (exact, |hi| < 2^50), then 4-7 -> lo;
+            // groups 0-3 -> hi (exact, |hi| < 2^50), groups 4-7 -> lo;
             // converted with the scales 2^-24 / 2^-56 folded into the magic
             // constants and added (one rounding)
 #pragma unroll
-            for (int h = 0; h < 16; h += 8) {
+            for (int h = 0; h < kBN; h += 8) {
                 uint32_t v[4][8];
 #pragma unroll
                 for (int g = 0; g < 4; ++g) tmem_ld8(taddr0 + (uint32_t)(g * kBN + h), v[g]);
@@ -566,18 +560,14 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps * kSets, 1)
                                          (long long)(int)v[2][c] * 256ll + (long long)(int)v[3][c];
                     hs[h + c] = __longlong_as_double(hi + 0x41B8000000000000ll) - 402653184.0;
                 }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mb_arrive(lo_free);
-            mb_wait(hi_full, par);
-            tc_fence_after();
-#pragma unroll
-            for (int h = 0; h < 16; h += 8) {
-                uint32_t v[4][8];
 #pragma unroll
                 for (int g = 0; g < 4; ++g) tmem_ld8(taddr0 + (uint32_t)((g + 4) * kBN + h), v[g]);
                 tmem_wait_ld();
+                if (h + 8 == kBN) {  // every column of the buffer is in registers: release it
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mb_arrive(acc_free(set));
+                }
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                     const long long lo = (long long)(int)v[0][c] * 16777216ll + (long long)(int)v[1][c] * 65536ll +
@@ -585,13 +575,9 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps * kSets, 1)
                     hs[h + c] += __longlong_as_double(lo + 0x3FB8000000000000ll) - 0.09375;
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mb_arrive(hi_free);
             // out = T - prod 2^(e_i + f_j): T from the staged tile, the result
-            // written back in place and stored by this warp's own TMA store.
-            // The accumulators are released by now, so this part overlaps the
-            // other set's drain of the next tile.
+            // written back in place and stored by this warp's own TMA store
+            // (the other set drains the next tile meanwhile)
             mb_wait(c_full(cs), cpar);
             {
                 // this warp's 32 x 16 box of the staged tile (column c at
@@ -600,9 +586,9 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps * kSets, 1)
                 // (the scale array is padded to whole N tiles), stores; the
                 // gathered first step reads its right-hand side from global
                 // memory instead
-                const uint32_t ct = sC + cs * kTileCBytes + (uint32_t)((half * 4 + quad) * 4096 + lane * 8);
+                const uint32_t ct = sC + cs * kTileCBytes + (uint32_t)(quad * 4096 + lane * 8);
 #pragma unroll
-                for (int h = 0; h < 16; h += 8) {
+                for (int h = 0; h < kBN; h += 8) {
                     double wsc[8], t[8];
 #pragma unroll
                     for (int c = 0; c < 8; ++c) wsc[c] = __ldg(P.cscale + j0 + h + c);
@@ -622,10 +608,8 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps * kSets, 1)
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             __syncwarp();
             if (lane == 0) {
-                // the stage gets this warp's release once the store has read
-                // its box (the wait is off the accumulators' critical path)
-                tma_store_2d(&tm_out, (int)(p * kBM + quad * 32), (int)j0,
-                             sC + cs * kTileCBytes + (uint32_t)((half * 4 + quad) * 4096));
+                // the stage gets this warp's release once the store has read its box
+                tma_store_2d(&tm_out, (int)(p * kBM + quad * 32), (int)j0, sC + cs * kTileCBytes + (uint32_t)(quad * 4096));
                 asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
                 asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
                 mb_arrive(c_empty(cs));
@@ -677,27 +661,27 @@ int make_map(CUtensorMap *map, const double *base, int64_t m, int64_t n, int64_t
 }
 
 int launch_update(const UpdArgs &P, cudaStream_t st) {
-    static thread_local int attr_dev = -1;
-    const int dev = current_device();
-    if (attr_dev != dev) {
-        CQ_CUDA(cudaFuncSetAttribute(oz_update_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem),
-                "oz update smem attr");
-        CQ_CUDA(cudaFuncSetAttribute(oz_update_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem),
-                "oz update smem attr");
-        attr_dev = dev;
-    }
     alignas(64) CUtensorMap tm_in, tm_out;
     std::memset(&tm_in, 0, sizeof(tm_in));
-    if (!P.cols_in) CQ_TRY(make_map(&tm_in, P.cin, P.m, P.ncols, P.ldin, kBN / 2));
-    CQ_TRY(make_map(&tm_out, P.cout, P.m, P.ncols, P.ldout, kBN / 2));  // 32 x 16 boxes
+    if (!P.cols_in) CQ_TRY(make_map(&tm_in, P.cin, P.m, P.ncols, P.ldin));
+    CQ_TRY(make_map(&tm_out, P.cout, P.m, P.ncols, P.ldout));  // 32 x 16 boxes
     const int grid = std::min(P.npanels, num_sms());
     if (((int64_t)P.npanels / grid + 1) * P.ntn > INT_MAX / 2) return fail_internal("oz update: too many tiles per CTA");
-    // drain sets: 2 by default (CQRRPT_OZ_SETS=1 keeps a single set of 8 drain warps)
-    const char *es = getenv("CQRRPT_OZ_SETS");
-    if (es && es[0] == '1')
-        oz_update_kernel<1><<<grid, 64 + 32 * kEpiWarps, kUpdSmem, st>>>(tm_in, tm_out, P);
-    else
-        oz_update_kernel<2><<<grid, 64 + 64 * kEpiWarps, kUpdSmem, st>>>(tm_in, tm_out, P);
+    const char *sv = getenv("CQRRPT_OZ_STAGES");  // experiments: ring depths "B,C"
+    const int variant = sv ? atoi(sv) : 48;
+#define OZ_LAUNCH(BST, CST)                                                                                          \
+    do {                                                                                                             \
+        auto kern = oz_update_kernel<BST, CST>;                                                                      \
+        CQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem(BST, CST)),    \
+                "oz update smem attr");                                                                              \
+        kern<<<grid, kUpdThreads, upd_smem(BST, CST), st>>>(tm_in, tm_out, P);                                       \
+    } while (0)
+    switch (variant) {
+        case 38: OZ_LAUNCH(3, 8); break;
+        case 66: OZ_LAUNCH(6, 6); break;
+        default: OZ_LAUNCH(4, 8); break;
+    }
+#undef OZ_LAUNCH
     note_launch();
     return check_launch("oz_update_kernel");
 }
