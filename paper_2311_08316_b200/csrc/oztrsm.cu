@@ -25,32 +25,31 @@
 // the FP64 GEMM's normwise bound (the parity tests compare with the DMMA
 // engine and the oracle).
 //
-// oz_update_kernel: persistent, one CTA per SM (216 KB shared memory, all 512
-// TMEM columns):
+// oz_update_kernel: persistent, one CTA per SM (225 KB shared memory, all 512
+// TMEM columns), tiles of 128 rows x 16 columns:
 //   warp 0    producer (TMA engine): the panel's 7 digit slices (128 rows x 128
 //             K each, pre-tiled in the UMMA canonical K-major layout) through a
-//             2-slice ring, a 2-stage ring of U's N tiles (32 x 128 x 7 = 28
-//             KB), and per tile the right-hand side into a 4-stage ring (eight
-//             32 x 16 tensor-map boxes, one per drain warp; the gathered first
-//             step is read from global memory by the drain warps instead);
+//             2-slice ring, a ring of U's N tiles (16 x 128 x 7 = 14 KB, staged
+//             with an all-zero 8th slice), and per tile the right-hand side
+//             into a ring of 16 KB stages (eight 32 x 8 tensor-map boxes, one
+//             per drain warp; the gathered first step is read from global
+//             memory by the drain warps instead);
 //   warp 1    TMEM allocator + MMA issuer (one elected thread, operands in
 //             uniform registers): tcgen05.cp of the A slices into TMEM columns
 //             0..223 once per panel, then per N tile and K-step ONE
 //             tcgen05.mma per digit slice s of X covering all its partner
-//             slices t of U at once: U's slices are consecutive 32-row blocks
-//             of the canonical layout, so B = slices t0.. with N = 32 * count
-//             and D = group s + t0 lands every pair (s, t) in group s + t.
-//             44 MMAs of N = 32..128 per tile instead of 136 of N = 32: the
-//             128 x 32-byte A operand is read once per slice and K-step, not
-//             once per pair (at N = 32 the A read, not the math, set the
-//             rate). Groups 0-3 and 4-7 are committed and released
-//             separately, so a tile's first groups overlap the previous
-//             tile's drain;
-//   warps 2-17 drain + update, two sets of 8 taking alternate tiles (the
-//             second set drains tile t + 1 while the first still updates and
-//             stores tile t): tcgen05.ld (lane = row, 16 columns per warp), the
-//             exact recombination, T - p 2^(e_i + f_j) in place in the staged
-//             tile, the warp's own TMA store of its 32 x 16 box.
+//             slices t of U at once: U's slices are consecutive 16-row blocks
+//             of the canonical layout, so B = slices 0.. with N = 16 * count
+//             and D = group s lands every pair (s, t) in group s + t (28 MMAs
+//             of N = 32..128 per tile). Two accumulator buffers (columns
+//             256..383, 384..511) alternate between tiles, so a tile's MMAs
+//             run while the previous tile is drained;
+//   warps 2-17 drain + update, two sets of 8 (set = accumulator buffer = tile
+//             parity): tcgen05.ld of all 8 groups of the warp's 32 rows x 8
+//             columns in one batch, the buffer released at once (this
+//             hand-off is the tile period's critical path), then the exact
+//             recombination, T - p 2^(e_i + f_j) in place in the staged tile,
+//             the warp's own TMA store of its 32 x 8 box.
 // Even m only: TMA applies the box's row bound at 16-byte granularity.
 #include <cuda.h>
 
@@ -75,16 +74,16 @@ constexpr int kSliceB = kBN * kW;          // 2048 B per digit slice of an N til
 constexpr int kPanelBytes = kDig * kSliceA;  // 114688
 constexpr int kTileBBytes = kDig * kSliceB;  // 14336 in global memory
 constexpr int kTileBSmem = (kDig + 1) * kSliceB;  // staged with an all-zero 8th slice (group 7 of digit 0)
-constexpr int kBufs = 2;                   // accumulator buffers (tile parity)
-constexpr int kSets = 4;                   // drain sets (tile index mod 4; buffer = set mod 2)
-constexpr int kEpiWarps = 4;               // per drain set: one per TMEM lane quadrant, 16 columns
+constexpr int kSets = 2;                   // accumulator buffers = drain sets (tile parity)
+constexpr int kEpiWarps = 8;               // per drain set: two per TMEM lane quadrant, 8 columns each
+constexpr int kDC = kBN / 2;               // columns per drain warp
 constexpr int kUpdThreads = 64 + 32 * kEpiWarps * kSets;  // producer, MMA, drain sets
 constexpr int kTmemCols = 512;             // A digit slices (7 x 32) | 2 x accumulators (8 x 16)
 constexpr uint32_t kTmemAcc = 256;         // first accumulator column
 constexpr uint32_t kAccCols = kGroups * kBN;  // 128 columns per buffer
 
 constexpr int kAStages = 2;                // digit slices staged on their way to TMEM
-constexpr uint32_t kTileCBytes = kBM * kBN * 8;  // 16384: quadrant q's 32 x 16 box at q * 4096, column c at c * 256
+constexpr uint32_t kTileCBytes = kBM * kBN * 8;  // 16384: box (half h, quadrant q) = 32 rows x 8 columns at (4 h + q) * 2048, column c at c * 256
 constexpr uint32_t kSmemA = 0;
 constexpr uint32_t kSmemB = kAStages * kSliceA;
 // ring depths: kBStages staged U tiles (16 KB), kCStages right-hand-side tiles (16 KB)
@@ -375,9 +374,8 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
     const uint32_t sA = sbase + kSmemA, sB = sbase + kSmemB, sC = sbase + kSmemC;
     const uint32_t bar = sbase + kSmemBar;
     // a_*: digit-slice staging ring (smem -> TMEM); b_*: U-slice N tiles;
-    // c_*: right-hand-side tiles; acc_full / acc_free (one pair per drain
-    // set, so every barrier's phases are one set's consecutive tiles): the
-    // set's tile accumulated / its accumulator buffer read
+    // c_*: right-hand-side tiles; acc_full / acc_free: accumulator buffer
+    // (tile parity) accumulated / read by its drain set
     auto a_full = [&](int s) { return bar + 8u * s; };
     auto a_empty = [&](int s) { return bar + 8u * (kAStages + s); };
     auto b_full = [&](int s) { return bar + 8u * (2 * kAStages + s); };
@@ -449,11 +447,11 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
                     if (++bs == kBStages) bs = 0, ++bfill;
                     const int64_t j0 = (int64_t)nt * kBN;
                     if (cfill) mb_wait(c_empty(cs), (cfill - 1u) & 1u);
-                    if (!P.cols_in) {  // 4 boxes of 32 rows x 16 columns, one per drain warp (zeros past the ends)
+                    if (!P.cols_in) {  // 8 boxes of 32 rows x 8 columns, one per drain warp (zeros past the ends)
                         mb_expect_tx(c_full(cs), kTileCBytes);
-                        for (int q = 0; q < 4; ++q)
-                            tma_load_2d(sC + cs * kTileCBytes + (uint32_t)q * 4096u, &tm_in, (int)(r0 + q * 32), (int)j0,
-                                        c_full(cs));
+                        for (int sb = 0; sb < 8; ++sb)
+                            tma_load_2d(sC + cs * kTileCBytes + (uint32_t)sb * 2048u, &tm_in, (int)(r0 + (sb & 3) * 32),
+                                        (int)(j0 + (sb >> 2) * kDC), c_full(cs));
                     } else {  // gathered columns: the drain warps read them from global memory
                         mb_arrive(c_full(cs));
                     }
@@ -486,10 +484,10 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
                 for (int nt = 0; nt < P.ntn; ++nt, ++tc) {
                     mb_wait_warp(b_full(bs), buse & 1u);
                     const uint32_t blo0 = desc_lo(sB + bs * kTileBSmem);
-                    const uint32_t buf = tc & 1u, set = tc & 3u;
+                    const uint32_t buf = tc & 1u;
                     const uint32_t d0 = tmem + kTmemAcc + buf * kAccCols;
-                    // this buffer's previous tile (tc - 2, drained by set (tc - 2) % 4) has been read
-                    if (tc >= 2) mb_wait_warp(acc_free((tc - 2u) & 3u), ((tc - 2u) >> 2) & 1u);
+                    // this buffer's previous tile (tc - 2) has been read by its drain set
+                    if (tc >= 2) mb_wait_warp(acc_free(buf), ((tc >> 1) - 1u) & 1u);
                     tc_fence_after();
                     if (elect_one()) {
                         // Digit slice s of X against ALL its partner slices t = 0 ..
@@ -506,18 +504,19 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
                         tc_mma_i8_k128<idesc_n(48), false>(d0 + 5 * kBN, tmem + 5 * 32, blo0);
                         tc_mma_i8_k128<idesc_n(32), false>(d0 + 6 * kBN, tmem + 6 * 32, blo0);
                         tc_commit(b_empty(bs));
-                        tc_commit(acc_full(set));
+                        tc_commit(acc_full(buf));
                     }
                     __syncwarp();
                     if (++bs == kBStages) bs = 0, ++buse;
                 }
             }
         }
-    } else {  // ---------------- drain warps: set (warp - 2) / 4 takes tiles set, set + 4, ...
-              // (accumulator buffer = set % 2); lane quadrant warp % 4, all 16 columns
-        const int quad = warp & 3, set = (warp - 2) >> 2;
+    } else {  // ---------------- drain warps: set (warp - 2) / 8 takes tiles set, set + 2, ...
+              // (accumulator buffer = set); lane quadrant warp % 4, 8 columns each
+        const int quad = warp & 3, half = ((warp - 2) >> 2) & 1, set = (warp - 2) >> 3;
         const int rloc = quad * 32 + lane;
-        const uint32_t taddr0 = tmem + kTmemAcc + (uint32_t)(set & 1) * kAccCols + ((uint32_t)(quad * 32) << 16);
+        const uint32_t taddr0 =
+            tmem + kTmemAcc + (uint32_t)set * kAccCols + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * kDC);
         // tiles of this CTA in issue order: panel blockIdx.x + pcur * gridDim.x, N tile nt
         // (the host bounds npanels * ntn / gridDim.x below 2^31)
         const int npan = P.npanels > (int)blockIdx.x ? (P.npanels - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
@@ -539,77 +538,61 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
             const uint32_t par = (uint32_t)(tc / kSets) & 1u;
             const int cs = tc % kCStages;
             const uint32_t cpar = (uint32_t)(tc / kCStages) & 1u;
-            const int64_t j0 = (int64_t)nt * kBN;
+            const int64_t j0 = (int64_t)nt * kBN + half * kDC;
             const int64_t rem = P.ncols - j0;
-            const int nc = rem >= kBN ? kBN : (rem > 0 ? (int)rem : 0);
-            double hs[kBN];
+            const int nc = rem >= kDC ? kDC : (rem > 0 ? (int)rem : 0);
             mb_wait(acc_full(set), par);
             tc_fence_after();
+            // all 8 groups of this warp's 8 columns in one batch of TMEM loads,
+            // then the buffer is released (the hand-off is the tile period's
+            // critical path; the arithmetic comes after it)
+            uint32_t v[kGroups][kDC];
+#pragma unroll
+            for (int g = 0; g < kGroups; ++g) tmem_ld8(taddr0 + (uint32_t)(g * kBN), v[g]);
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mb_arrive(acc_free(set));
             // groups 0-3 -> hi (exact, |hi| < 2^50), groups 4-7 -> lo;
             // converted with the scales 2^-24 / 2^-56 folded into the magic
             // constants and added (one rounding)
+            double hs[kDC];
 #pragma unroll
-            for (int h = 0; h < kBN; h += 8) {
-                uint32_t v[4][8];
-#pragma unroll
-                for (int g = 0; g < 4; ++g) tmem_ld8(taddr0 + (uint32_t)(g * kBN + h), v[g]);
-                tmem_wait_ld();
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const long long hi = (long long)(int)v[0][c] * 16777216ll + (long long)(int)v[1][c] * 65536ll +
-                                         (long long)(int)v[2][c] * 256ll + (long long)(int)v[3][c];
-                    hs[h + c] = __longlong_as_double(hi + 0x41B8000000000000ll) - 402653184.0;
-                }
-#pragma unroll
-                for (int g = 0; g < 4; ++g) tmem_ld8(taddr0 + (uint32_t)((g + 4) * kBN + h), v[g]);
-                tmem_wait_ld();
-                if (h + 8 == kBN) {  // every column of the buffer is in registers: release it
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mb_arrive(acc_free(set));
-                }
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const long long lo = (long long)(int)v[0][c] * 16777216ll + (long long)(int)v[1][c] * 65536ll +
-                                         (long long)(int)v[2][c] * 256ll + (long long)(int)v[3][c];
-                    hs[h + c] += __longlong_as_double(lo + 0x3FB8000000000000ll) - 0.09375;
-                }
+            for (int c = 0; c < kDC; ++c) {
+                const long long hi = (long long)(int)v[0][c] * 16777216ll + (long long)(int)v[1][c] * 65536ll +
+                                     (long long)(int)v[2][c] * 256ll + (long long)(int)v[3][c];
+                const long long lo = (long long)(int)v[4][c] * 16777216ll + (long long)(int)v[5][c] * 65536ll +
+                                     (long long)(int)v[6][c] * 256ll + (long long)(int)v[7][c];
+                hs[c] = (__longlong_as_double(hi + 0x41B8000000000000ll) - 402653184.0) +
+                        (__longlong_as_double(lo + 0x3FB8000000000000ll) - 0.09375);
             }
             // out = T - prod 2^(e_i + f_j): T from the staged tile, the result
             // written back in place and stored by this warp's own TMA store
             // (the other set drains the next tile meanwhile)
+            double wsc[kDC], t[kDC];
+#pragma unroll
+            for (int c = 0; c < kDC; ++c) wsc[c] = __ldg(P.cscale + j0 + c);  // padded to whole N tiles
             mb_wait(c_full(cs), cpar);
-            {
-                // this warp's 32 x 16 box of the staged tile (column c at
-                // c * 256 bytes), shared-memory addresses explicitly, 8 columns
-                // at a time: loads, FMAs with the scale 2^(e_i + f_j - 12)
-                // (the scale array is padded to whole N tiles), stores; the
-                // gathered first step reads its right-hand side from global
-                // memory instead
-                const uint32_t ct = sC + cs * kTileCBytes + (uint32_t)(quad * 4096 + lane * 8);
+            // this warp's 32 x 8 box of the staged tile (column c at c * 256
+            // bytes), shared-memory addresses explicitly; the gathered first
+            // step reads its right-hand side from global memory instead
+            const uint32_t ct = sC + cs * kTileCBytes + (uint32_t)((half * 4 + quad) * 2048 + lane * 8);
+            if (!P.cols_in) {
 #pragma unroll
-                for (int h = 0; h < kBN; h += 8) {
-                    double wsc[8], t[8];
+                for (int c = 0; c < kDC; ++c) t[c] = lds_f64(ct + (uint32_t)(c * 256));
+            } else {
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) wsc[c] = __ldg(P.cscale + j0 + h + c);
-                    if (!P.cols_in) {
-#pragma unroll
-                        for (int c = 0; c < 8; ++c) t[c] = lds_f64(ct + (uint32_t)((h + c) * 256));
-                    } else {
-#pragma unroll
-                        for (int c = 0; c < 8; ++c)
-                            t[c] = (valid && h + c < nc) ? P.cin[__ldg(P.cols_in + j0 + h + c) * P.ldin + row] : 0.0;
-                    }
-#pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        sts_f64(ct + (uint32_t)((h + c) * 256), fma(-hs[h + c], wsc[c] * rs, t[c]));
-                }
+                for (int c = 0; c < kDC; ++c)
+                    t[c] = (valid && c < nc) ? P.cin[__ldg(P.cols_in + j0 + c) * P.ldin + row] : 0.0;
             }
+#pragma unroll
+            for (int c = 0; c < kDC; ++c) sts_f64(ct + (uint32_t)(c * 256), fma(-hs[c], wsc[c] * rs, t[c]));
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             __syncwarp();
             if (lane == 0) {
                 // the stage gets this warp's release once the store has read its box
-                tma_store_2d(&tm_out, (int)(p * kBM + quad * 32), (int)j0, sC + cs * kTileCBytes + (uint32_t)(quad * 4096));
+                tma_store_2d(&tm_out, (int)(p * kBM + quad * 32), (int)j0,
+                             sC + cs * kTileCBytes + (uint32_t)((half * 4 + quad) * 2048));
                 asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
                 asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
                 mb_arrive(c_empty(cs));
@@ -663,8 +646,8 @@ int make_map(CUtensorMap *map, const double *base, int64_t m, int64_t n, int64_t
 int launch_update(const UpdArgs &P, cudaStream_t st) {
     alignas(64) CUtensorMap tm_in, tm_out;
     std::memset(&tm_in, 0, sizeof(tm_in));
-    if (!P.cols_in) CQ_TRY(make_map(&tm_in, P.cin, P.m, P.ncols, P.ldin));
-    CQ_TRY(make_map(&tm_out, P.cout, P.m, P.ncols, P.ldout));  // 32 x 16 boxes
+    if (!P.cols_in) CQ_TRY(make_map(&tm_in, P.cin, P.m, P.ncols, P.ldin, kDC));
+    CQ_TRY(make_map(&tm_out, P.cout, P.m, P.ncols, P.ldout, kDC));  // 32 x 8 boxes
     const int grid = std::min(P.npanels, num_sms());
     if (((int64_t)P.npanels / grid + 1) * P.ntn > INT_MAX / 2) return fail_internal("oz update: too many tiles per CTA");
     const char *sv = getenv("CQRRPT_OZ_STAGES");  // experiments: ring depths "B,C"
