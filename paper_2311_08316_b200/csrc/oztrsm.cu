@@ -87,9 +87,8 @@ constexpr uint32_t kTileCBytes = kBM * kBN * 8;  // 16384: box (half h, quadrant
 constexpr uint32_t kSmemA = 0;
 constexpr uint32_t kSmemB = kAStages * kSliceA;
 // ring depths: kBStages staged U tiles (16 KB), kCStages right-hand-side tiles (16 KB)
-constexpr uint32_t kScaleBytes = 16384;    // the step's column scales (up to 2048 columns) staged in shared memory
 __host__ __device__ constexpr uint32_t upd_smem(int bst, int cst) {
-    return kSmemB + (uint32_t)bst * kTileBSmem + (uint32_t)cst * kTileCBytes + 512u + kScaleBytes;
+    return kSmemB + (uint32_t)bst * kTileBSmem + (uint32_t)cst * kTileCBytes + 512u;
 }
 
 // byte offset of (row r, k kk) in a digit slice laid out as UMMA core matrices
@@ -362,7 +361,6 @@ struct UpdArgs {
     const int64_t *cols_in;  // nullptr: column j of cin is j
     double *cout;
     int64_t ldout;
-    int dbg;  // experiment (CQRRPT_OZ_DBG=1): the producer skips the U-tile loads (wrong results, timing only)
 };
 
 template <int kBStages, int kCStages>
@@ -408,11 +406,6 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    // the step's column scales, when they fit (else the drain warps read them from global memory)
-    const bool cs_smem = (uint32_t)P.ntn * kBN * 8u <= kScaleBytes;
-    const uint32_t sS = bar + 512u;
-    if (cs_smem)
-        for (int i = tid; i < P.ntn * kBN; i += kUpdThreads) sts_f64(sS + 8u * (uint32_t)i, P.cscale[i]);
     // the all-zero 8th slice of every staged U tile (the bulk copies write the first 7)
     for (int i = tid; i < kBStages * (kSliceB / 16); i += kUpdThreads) {
         const int st = i / (kSliceB / 16), o = i % (kSliceB / 16);
@@ -449,12 +442,8 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
                 const int64_t r0 = (int64_t)p * kBM;
                 for (int nt = 0; nt < P.ntn; ++nt) {
                     if (bfill) mb_wait(b_empty(bs), (bfill - 1u) & 1u);
-                    if (P.dbg) {
-                        mb_arrive(b_full(bs));
-                    } else {
-                        mb_expect_tx(b_full(bs), kTileBBytes);
-                        bulk_g2s(sB + bs * kTileBSmem, P.bslc + (int64_t)nt * kTileBBytes, kTileBBytes, b_full(bs));
-                    }
+                    mb_expect_tx(b_full(bs), kTileBBytes);
+                    bulk_g2s(sB + bs * kTileBSmem, P.bslc + (int64_t)nt * kTileBBytes, kTileBBytes, b_full(bs));
                     if (++bs == kBStages) bs = 0, ++bfill;
                     const int64_t j0 = (int64_t)nt * kBN;
                     if (cfill) mb_wait(c_empty(cs), (cfill - 1u) & 1u);
@@ -582,8 +571,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
             // (the other set drains the next tile meanwhile)
             double wsc[kDC], t[kDC];
 #pragma unroll
-            for (int c = 0; c < kDC; ++c)  // padded to whole N tiles
-                wsc[c] = cs_smem ? lds_f64(sS + 8u * (uint32_t)(j0 + c)) : __ldg(P.cscale + j0 + c);
+            for (int c = 0; c < kDC; ++c) wsc[c] = __ldg(P.cscale + j0 + c);  // padded to whole N tiles
             mb_wait(c_full(cs), cpar);
             // this warp's 32 x 8 box of the staged tile (column c at c * 256
             // bytes), shared-memory addresses explicitly; the gathered first
@@ -663,7 +651,7 @@ int launch_update(const UpdArgs &P, cudaStream_t st) {
     const int grid = std::min(P.npanels, num_sms());
     if (((int64_t)P.npanels / grid + 1) * P.ntn > INT_MAX / 2) return fail_internal("oz update: too many tiles per CTA");
     const char *sv = getenv("CQRRPT_OZ_STAGES");  // experiments: ring depths "B,C"
-    const int variant = sv ? atoi(sv) : 38;
+    const int variant = sv ? atoi(sv) : 48;
 #define OZ_LAUNCH(BST, CST)                                                                                          \
     do {                                                                                                             \
         auto kern = oz_update_kernel<BST, CST>;                                                                      \
@@ -672,9 +660,9 @@ int launch_update(const UpdArgs &P, cudaStream_t st) {
         kern<<<grid, kUpdThreads, upd_smem(BST, CST), st>>>(tm_in, tm_out, P);                                       \
     } while (0)
     switch (variant) {
-        case 47: OZ_LAUNCH(4, 7); break;
-        case 56: OZ_LAUNCH(5, 6); break;
-        default: OZ_LAUNCH(3, 8); break;
+        case 38: OZ_LAUNCH(3, 8); break;
+        case 66: OZ_LAUNCH(6, 6); break;
+        default: OZ_LAUNCH(4, 8); break;
     }
 #undef OZ_LAUNCH
     note_launch();
@@ -767,8 +755,6 @@ int trsm_right_oz(int64_t m, int64_t k, const double *b, int64_t ldb, const int6
         }
         P.cout = x + b1 * ldx;
         P.ldout = ldx;
-        const char *dbg = getenv("CQRRPT_OZ_DBG");
-        P.dbg = dbg ? atoi(dbg) : 0;
         CQ_TRY(launch_update(P, st));
     }
     return 0;
