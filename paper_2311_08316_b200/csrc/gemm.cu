@@ -467,9 +467,11 @@ int gram(int64_t m, int64_t k, const double *x, int64_t ldx, double *gmat, int64
     const char *env = getenv("CQRRPT_GPU_GRAM");
     const bool force_dmma = env && std::string(env) == "dmma";
     const bool force_oz = env && std::string(env) == "ozaki";
-    // below k = 1024 the int8 GEMMs (one 256 x 256 IMMA tile per modulus and
-    // column block) cannot fill the GPU: C5-256's Gram is faster on DMMA
-    const bool oz = !force_dmma && (force_oz || (k >= 1024 && m >= 65536)) && gram_ozaki_available();
+    // at narrow k the int8 GEMMs (one 256 x 256 IMMA tile per modulus and
+    // column block) cannot fill the GPU: C5-256's Gram is faster on DMMA (26.8
+    // vs 33.2 ms for Gram + potrf + Q), C5-512's on INT8 (75.1 vs 81.3 ms)
+    const bool big = (k >= 1024 && m >= 65536) || (k >= 512 && m >= 1048576);
+    const bool oz = !force_dmma && (force_oz || big) && gram_ozaki_available();
     if (oz) return gram_ozaki(m, k, x, ldx, gmat, ldg, ws, st);
     return gram_dmma(m, k, x, ldx, gmat, ldg, ws, st);
 }
