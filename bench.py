@@ -380,7 +380,7 @@ def main():
         for b0 in range(0, k0, 128):
             b1 = min(k0, b0 + 128)
             ops += 2.0 * 34 * (b1 - b0) * (k0 - b1) * ml
-        roofline_int8 = {"bound": "tensor", "kernel": "oz_update_kernel (tcgen05.mma kind::i8 M128 N32 K32)",
+        roofline_int8 = {"bound": "tensor", "kernel": "oz_update_kernel (tcgen05.mma kind::i8, M128 K32, N = 32..128: one MMA per digit slice and K-step)",
                          "achieved": ops / (ph[3] * 1e-3) / 1e12, "peak": 4500.0, "unit": "TOPS",
                          "peak_source": "B200 dense INT8 tensor nominal (4.5 POPS); not in MEASURED_PEAKS.json",
                          "algorithmic": f"{ops:.4g} int8 ops per precondition pass (2 x 34 pairs x m x w x trailing "
