@@ -571,7 +571,7 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
             const int S = 32 / w;
             const double spread = S == 1 ? 0.0 : (S == 2 ? 0.56 : 1.03);  // E[max of S] - mean, in sigmas
             for (int a : candA) {
-                if (w < 32 && a != 1 && a != 2 && a != 4 && a != 8) continue;  // instantiated widths
+                if (w < 32 && a == 6) continue;  // not instantiated
                 const int64_t rb = (int64_t)kConsumers * S * a;
                 const int64_t ctas = ((n + w - 1) / w) * ((d + rb - 1) / rb);
                 const double ents = (double)kTileRows * (double)nnz * (double)std::min<int64_t>(rb, d) / (double)d;
@@ -598,7 +598,7 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
         const int fw = atoi(ev);
         if (fw == 8 || fw == 16 || fw == 32) W = fw;
     }
-    if (W < 32 && A != 1 && A != 2 && A != 4 && A != 8) A = A > 8 ? 8 : (A == 6 ? 4 : A);
+    if (W < 32 && A == 6) A = 4;  // not instantiated
     const int SL = 32 / W;
     const int64_t cgroups = (n + W - 1) / W;
     const int64_t rblocks = (d + (int64_t)kConsumers * SL * A - 1) / ((int64_t)kConsumers * SL * A);
@@ -675,7 +675,9 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
                 case 1: return launch_apply<1, false, 16>(P, gr, smem, st);
                 case 2: return launch_apply<2, false, 16>(P, gr, smem, st);
                 case 4: return launch_apply<4, false, 16>(P, gr, smem, st);
-                default: return launch_apply<8, false, 16>(P, gr, smem, st);
+                case 8: return launch_apply<8, false, 16>(P, gr, smem, st);
+                case 12: return launch_apply<12, false, 16>(P, gr, smem, st);
+                default: return launch_apply<16, false, 16>(P, gr, smem, st);
             }
         }
         if (W == 8) {
@@ -683,7 +685,9 @@ int saso_sketch(int64_t m, int64_t n, const double *a, int64_t lda, int64_t d, i
                 case 1: return launch_apply<1, false, 8>(P, gr, smem, st);
                 case 2: return launch_apply<2, false, 8>(P, gr, smem, st);
                 case 4: return launch_apply<4, false, 8>(P, gr, smem, st);
-                default: return launch_apply<8, false, 8>(P, gr, smem, st);
+                case 8: return launch_apply<8, false, 8>(P, gr, smem, st);
+                case 12: return launch_apply<12, false, 8>(P, gr, smem, st);
+                default: return launch_apply<16, false, 8>(P, gr, smem, st);
             }
         }
         switch (A) {

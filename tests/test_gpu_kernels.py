@@ -117,7 +117,7 @@ def test_saso_sketch_every_row_block_width(cuda, oracle, monkeypatch, A, path):
 
 
 @pytest.mark.parametrize("W", [8, 16])
-@pytest.mark.parametrize("A", [1, 2, 4, 8])
+@pytest.mark.parametrize("A", [1, 2, 4, 8, 12, 16])
 def test_saso_sketch_narrow_column_groups(cuda, oracle, monkeypatch, A, W):
     """Narrow column groups (W columns per CTA, 32 / W row slots per consumer
     warp whose entry walks diverge; chosen by default for n <= 512) against
