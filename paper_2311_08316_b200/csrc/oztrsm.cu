@@ -650,7 +650,7 @@ int launch_update(const UpdArgs &P, cudaStream_t st) {
     CQ_TRY(make_map(&tm_out, P.cout, P.m, P.ncols, P.ldout, kDC));  // 32 x 8 boxes
     const int grid = std::min(P.npanels, num_sms());
     if (((int64_t)P.npanels / grid + 1) * P.ntn > INT_MAX / 2) return fail_internal("oz update: too many tiles per CTA");
-    const char *sv = getenv("CQRRPT_OZ_STAGES");  // experiments: ring depths "B,C"
+    const char *sv = getenv("CQRRPT_OZ_STAGES");  // experiments: ring depths "BC" (48 default, 38, 66)
     const int variant = sv ? atoi(sv) : 48;
 #define OZ_LAUNCH(BST, CST)                                                                                          \
     do {                                                                                                             \
