@@ -41,7 +41,11 @@
 //             slices t of U at once: U's slices are consecutive 16-row blocks
 //             of the canonical layout, so B = slices 0.. with N = 16 * count
 //             and D = group s lands every pair (s, t) in group s + t (28 MMAs
-//             of N = 32..128 per tile). Two accumulator buffers (columns
+//             of N = 32..128 per tile, issued K-step by K-step in chunks of 7
+//             that are committed to a chunk barrier with at most two chunks in
+//             flight: the issuing thread sleeps on the barrier instead of
+//             sitting throttled on the tensor pipe, which starved the drain
+//             warps of its scheduler). Two accumulator buffers (columns
 //             256..383, 384..511) alternate between tiles, so a tile's MMAs
 //             run while the previous tile is drained;
 //   warps 2-17 drain + update, two sets of 8 (set = accumulator buffer = tile
@@ -314,6 +318,17 @@ CQ_DEVI void tc_mma_i8_k128(uint32_t dtmem, uint32_t atmem, uint32_t blo) {
         "r"(atmem), "r"(blo), "n"(kFirst ? 0 : 1), "n"(kDescHi), "n"(kIdescT)
         : "memory");
 }
+// one K-step (K = 32) of the same; accumulate = 0 overwrites D
+template <uint32_t kIdescT>
+CQ_DEVI void tc_mma_i8_k32(uint32_t dtmem, uint32_t atmem, uint32_t blo, uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred q0;\n.reg .b64 db;\n"
+        "setp.ne.b32 q0, %3, 0;\n"
+        "mov.b64 db, {%2, %4};\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], db, %5, q0;\n}\n" ::"r"(dtmem),
+        "r"(atmem), "r"(blo), "r"(accumulate), "n"(kDescHi), "n"(kIdescT)
+        : "memory");
+}
 // smem (128 rows x 32 bytes, canonical layout) -> TMEM (128 lanes x 8 columns)
 CQ_DEVI void tc_cp_128x256b(uint32_t tmem_dst, uint32_t slo) {
     asm volatile(
@@ -384,7 +399,8 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
     auto c_empty = [&](int s) { return bar + 8u * (2 * kAStages + 2 * kBStages + kCStages + s); };
     auto acc_full = [&](uint32_t s) { return bar + 8u * (2 * (kAStages + kBStages + kCStages) + s); };
     auto acc_free = [&](uint32_t s) { return bar + 8u * (2 * (kAStages + kBStages + kCStages) + kSets + s); };
-    static_assert(8 * (2 * (kAStages + kBStages + kCStages) + 2 * kSets) <= 504, "barrier block");
+    const uint32_t chunk_bar = bar + 8u * (2 * (kAStages + kBStages + kCStages) + 2 * kSets);  // two barriers
+    static_assert(8 * (2 * (kAStages + kBStages + kCStages) + 2 * kSets + 2) <= 504, "barrier block");
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + kSmemBar + 504);
 
     if (tid == 0) {
@@ -404,6 +420,8 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
             mb_init(acc_full(s), 1);
             mb_init(acc_free(s), kEpiWarps);  // one arrival per drain warp of the set
         }
+        mb_init(chunk_bar, 1);
+        mb_init(chunk_bar + 8u, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     // the all-zero 8th slice of every staged U tile (the bulk copies write the first 7)
@@ -464,6 +482,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
             int as = 0, bs = 0;
             uint32_t ause = 0, buse = 0;
             uint32_t tc = 0;  // tiles issued
+            uint32_t nchunk = 0;  // MMA chunks committed before this tile
             const uint32_t alo0 = desc_lo(sA);
             for (int p = blockIdx.x; p < P.npanels; p += gridDim.x) {
                 // the panel's digit slices: smem -> TMEM columns [0, 224),
@@ -496,17 +515,32 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
                         // 16 (count) columns starting at group s land pair (s, t) in
                         // group s + t. Slice 0 runs over the zero 8th slice too: its
                         // first K-step overwrites all 8 groups, the rest accumulate.
-                        tc_mma_i8_k128<idesc_n(128), true>(d0 + 0 * kBN, tmem + 0 * 32, blo0);
-                        tc_mma_i8_k128<idesc_n(112), false>(d0 + 1 * kBN, tmem + 1 * 32, blo0);
-                        tc_mma_i8_k128<idesc_n(96), false>(d0 + 2 * kBN, tmem + 2 * 32, blo0);
-                        tc_mma_i8_k128<idesc_n(80), false>(d0 + 3 * kBN, tmem + 3 * 32, blo0);
-                        tc_mma_i8_k128<idesc_n(64), false>(d0 + 4 * kBN, tmem + 4 * 32, blo0);
-                        tc_mma_i8_k128<idesc_n(48), false>(d0 + 5 * kBN, tmem + 5 * 32, blo0);
-                        tc_mma_i8_k128<idesc_n(32), false>(d0 + 6 * kBN, tmem + 6 * 32, blo0);
+                        // K-step-major chunks of 7 MMAs, each committed to a chunk
+                        // barrier (chunk c uses barrier c % 2, whose previous arrival
+                        // was chunk c - 2); at most two chunks are in flight, so the
+                        // issuing thread sleeps on a barrier instead of sitting
+                        // throttled on the tensor pipe, which starved the drain warps
+                        // of its scheduler (lane quadrant 1) and delayed their release
+                        // of the accumulator buffer by a whole tile's issue time
+#pragma unroll
+                        for (int ks = 0; ks < kW / 32; ++ks) {
+                            const uint32_t cb = chunk_bar + 8u * ((nchunk + ks) & 1u);
+                            if (nchunk + ks >= 2) mb_wait(cb, (((nchunk + ks) >> 1) - 1u) & 1u);
+                            const uint32_t ao = tmem + 8u * ks, bo = blo0 + 16u * ks;
+                            tc_mma_i8_k32<idesc_n(128)>(d0 + 0 * kBN, ao + 0 * 32, bo, ks ? 1u : 0u);
+                            tc_mma_i8_k32<idesc_n(112)>(d0 + 1 * kBN, ao + 1 * 32, bo, 1u);
+                            tc_mma_i8_k32<idesc_n(96)>(d0 + 2 * kBN, ao + 2 * 32, bo, 1u);
+                            tc_mma_i8_k32<idesc_n(80)>(d0 + 3 * kBN, ao + 3 * 32, bo, 1u);
+                            tc_mma_i8_k32<idesc_n(64)>(d0 + 4 * kBN, ao + 4 * 32, bo, 1u);
+                            tc_mma_i8_k32<idesc_n(48)>(d0 + 5 * kBN, ao + 5 * 32, bo, 1u);
+                            tc_mma_i8_k32<idesc_n(32)>(d0 + 6 * kBN, ao + 6 * 32, bo, 1u);
+                            tc_commit(cb);
+                        }
                         tc_commit(b_empty(bs));
                         tc_commit(acc_full(buf));
                     }
                     __syncwarp();
+                    nchunk += kW / 32;
                     if (++bs == kBStages) bs = 0, ++buse;
                 }
             }
