@@ -96,8 +96,22 @@ class ClockSampler:
             for nm, v in zip(names, r[4:8]):
                 if v.strip().lower() == "active":
                     reasons.add(nm)
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+        # the timed region alternates factorization steps with idle-clock input
+        # restores, so the median sits at the idle clock; also report the lowest
+        # sample, the samples taken while the power cap was active, and the draw
+        capped = [num(r[0]) for r in self.rows if len(r) > 7 and r[7].strip().lower() == "active"]
+        capped = [v for v in capped if v is not None]
+        power = [v for v in (num(r[2]) for r in self.rows if len(r) > 2) if v is not None]
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+                "reasons": sorted(reasons), "samples": len(self.rows),
+                "sm_min_mhz": min(sm) if sm else None,
+                "sm_mhz_power_capped": float(np.median(capped)) if capped else None,
+                "power_w_max": max(power) if power else None}
 
 
 # --------------------------------------------------------------------------
